@@ -1,0 +1,151 @@
+/*
+ * texpr_b200.h — C ABI of libtexpr_b200.so, the B200 (sm_100a) execution
+ * library behind the compiled-graph hot path of the texpr expression compiler
+ * (arXiv 1605.02688, "Theano").
+ *
+ * The reference has no native boundary: its VM calls op.perform() on NumPy
+ * arrays (pkg/src/texpr/runtime.py:326-349 -> ops/*.py perform).  Each entry
+ * point below replaces one of those perform() families; the Python VM
+ * (paper_1605_02688_b200/vm.py) binds them with ctypes.
+ *
+ * Conventions
+ *  - Every function returns int: 0 = TX_OK, otherwise a TX_E_* code; the
+ *    message is read with tx_last_error() (thread-local).  Nothing aborts or
+ *    throws across the ABI.
+ *  - Device memory is owned by the caller (PyTorch allocations used as plain
+ *    buffers).  The library owns only NVRTC modules, CUDA graphs, events,
+ *    streams it created, and NCCL communicators; each has a *_destroy.
+ *  - Tensors are passed as tx_tensor: data pointer, dtype code, rank, shape,
+ *    strides in ELEMENTS (0 = broadcast).  Rank <= 8 (reference graph.py:23).
+ *  - All launches take an explicit cudaStream_t (passed as void*).  A handle
+ *    may be used by one host thread at a time (mirrors the per-function lock,
+ *    reference runtime.py:301, :371-373).
+ */
+#ifndef TEXPR_B200_H
+#define TEXPR_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TX_MAX_RANK 8
+#define TX_ABI_VERSION 1
+
+/* dtype codes — the closed set of reference dtypes.py:16-21 */
+enum { TX_F32 = 0, TX_F64 = 1, TX_I32 = 2, TX_I64 = 3, TX_BOOL = 4 };
+
+/* status codes */
+enum {
+  TX_OK = 0,
+  TX_E_ARG = 1,        /* bad argument / unsupported layout            */
+  TX_E_CUDA = 2,       /* CUDA runtime or driver error                 */
+  TX_E_NVRTC = 3,      /* NVRTC compilation failed (log in message)    */
+  TX_E_NCCL = 4,       /* NCCL error                                   */
+  TX_E_UNSUPPORTED = 5,/* dtype / shape combination not implemented    */
+  TX_E_NODEVICE = 6,   /* no CUDA device / driver                      */
+  TX_E_ZERODIV = 7     /* integer division by zero inside a kernel     */
+};
+
+typedef struct tx_tensor {
+  void* data;
+  int32_t dtype;
+  int32_t ndim;
+  int64_t shape[TX_MAX_RANK];
+  int64_t strides[TX_MAX_RANK]; /* in elements */
+} tx_tensor;
+
+/* ---------------------------------------------------------------- runtime */
+int tx_version(void);
+const char* tx_last_error(void);
+/* Select the device; fails with TX_E_NODEVICE when no driver/GPU exists. */
+int tx_init(int device);
+int tx_device_info(int* sm_count, int* cc_major, int* cc_minor, int64_t* total_mem);
+
+int tx_stream_create(void** stream);
+int tx_stream_destroy(void* stream);
+int tx_stream_sync(void* stream);
+int tx_event_create(void** ev);
+int tx_event_destroy(void* ev);
+int tx_event_record(void* ev, void* stream);
+int tx_stream_wait_event(void* stream, void* ev);
+int tx_event_elapsed_ms(void* start, void* stop, float* ms);
+/* kind: 0 H2D, 1 D2H, 2 D2D (all async on stream) */
+int tx_memcpy_async(void* dst, const void* src, size_t bytes, int kind, void* stream);
+int tx_memset_async(void* dst, int value, size_t bytes, void* stream);
+int tx_host_register(void* ptr, size_t bytes);
+int tx_host_unregister(void* ptr);
+
+/* Capture every launch issued on `stream` between begin/end into one CUDA
+ * graph (replaces the per-node Python walk, runtime.py:428-446). */
+int tx_graph_begin(void* stream);
+int tx_graph_end(void* stream, void** graph_exec);
+int tx_graph_launch(void* graph_exec, void* stream);
+int tx_graph_destroy(void* graph_exec);
+
+/* Strided copy dst <- src (same dtype, broadcast src allowed).  Used for
+ * update commits and outputs that alias storage. */
+int tx_copy(const tx_tensor* src, tx_tensor* dst, void* stream);
+
+/* ------------------------------------------- fused elementwise (NVRTC)
+ * Replaces Elemwise.perform / CompositeElemwise._perform_chunked/_plain
+ * (reference ops/elemwise.py:314-326, :538-597).
+ * `source` is a complete CUDA translation unit produced by the Python code
+ * generator from the hand-written template (csrc/ew_template.cuh); it must
+ * define extern "C" kernels tx_ew_flat and tx_ew_strided.  Compiled for
+ * sm_100a without fast-math (-fmad=false, IEEE div/sqrt, no FTZ).  Handles are
+ * cached by the caller; tx_ew_destroy unloads. */
+int tx_ew_compile(const char* source, const char* name, void** kernel);
+/* Compile-only check (no device needed): returns the cubin size. */
+int tx_ew_check(const char* source, const char* name, size_t* cubin_bytes);
+/* ops: n_out outputs first, then n_in inputs.  Inputs broadcast to the
+ * output shape (all outputs share one shape).  err_flag: optional device int
+ * set to 1 on integer division by zero. */
+int tx_ew_launch(void* kernel, int n_out, int n_in, const tx_tensor* ops, int* err_flag, void* stream);
+int tx_ew_destroy(void* kernel);
+
+/* ------------------------------------------------------------ reductions
+ * Replaces Sum/Max/ArgmaxOnehot.perform (reference ops/reductions.py:87-188)
+ * and adds an index argmax.  axes_mask bit i = reduce dim i. */
+enum { TX_SUM = 0, TX_MAX = 1, TX_ARGMAX_ONEHOT = 2, TX_ARGMAX_INDEX = 3 };
+int tx_reduce_workspace(int op, const tx_tensor* x, uint32_t axes_mask, size_t* bytes);
+int tx_reduce(int op, const tx_tensor* x, uint32_t axes_mask, tx_tensor* y,
+              void* workspace, size_t workspace_bytes, void* stream);
+
+/* ------------------------------------------------------------------ GEMM
+ * Replaces Dot.perform -> np.dot -> OpenBLAS sgemm (reference
+ * ops/linalg.py:42-62).  C[M,N] = A[M,K] . B[K,N]; operand transposes are
+ * expressed by strides.  fp32 uses tcgen05/TMEM TF32 tensor cores fed by TMA
+ * when the layout allows; skinny or float64 problems use CUDA-core kernels. */
+enum {
+  TX_GEMM_AUTO = 0,    /* tcgen05 TF32 where eligible                    */
+  TX_GEMM_SIMT = 1,    /* force CUDA-core fp32/fp64 (exact fp32 products) */
+  TX_GEMM_TC = 2       /* force tcgen05 (error if the layout is ineligible) */
+};
+/* Optional fused epilogue applied to the accumulator before the store. */
+enum { TX_EPI_NONE = 0, TX_EPI_BIAS = 1, TX_EPI_BIAS_TANH = 2, TX_EPI_MUL_1MSQR = 3 };
+typedef struct tx_epilogue {
+  int32_t kind;
+  tx_tensor aux; /* BIAS*: bias row [N]; MUL_1MSQR: h [M,N] (C = acc*(1-h^2)) */
+} tx_epilogue;
+int tx_gemm_workspace(const tx_tensor* A, const tx_tensor* B, const tx_tensor* C, int mode,
+                      size_t* bytes);
+int tx_gemm(const tx_tensor* A, const tx_tensor* B, tx_tensor* C, const tx_epilogue* epi,
+            int mode, void* workspace, size_t workspace_bytes, void* stream);
+/* Which path tx_gemm would take (0 simt, 1 skinny, 2 tcgen05). */
+int tx_gemm_path(const tx_tensor* A, const tx_tensor* B, const tx_tensor* C, int mode, int* path);
+
+/* ------------------------------------------------------------------ NCCL
+ * Gradient sync for data-parallel updates (new; Platoon-style synchronous
+ * DP).  libnccl.so.2 is dlopen'ed (the one torch loaded). */
+int tx_nccl_unique_id(char out[128]);
+int tx_nccl_init(int nranks, int rank, const char uid[128], void** comm);
+int tx_nccl_allreduce_sum(void* comm, void* buf, size_t count, int dtype, void* stream);
+int tx_nccl_destroy(void* comm);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TEXPR_B200_H */

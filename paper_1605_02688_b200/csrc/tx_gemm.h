@@ -1,0 +1,67 @@
+// Internal GEMM problem description shared by the GEMM translation units.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "tx_common.h"
+
+namespace tx {
+
+// Fused epilogue, evaluated per output element with IEEE round-to-nearest
+// intrinsics (no FMA contraction) so that it rounds exactly like the unfused
+// elementwise nodes it replaces (add(b, dot) -> tanh, mul(dot, 1 - sqr(h))).
+template <class T>
+struct Epi {
+  int kind = TX_EPI_NONE;
+  const T* aux = nullptr;
+  int64_t s0 = 0, s1 = 0;  // aux strides (bias: s1 only)
+  __device__ __forceinline__ T apply(T acc, int64_t m, int64_t n) const;
+};
+
+template <>
+__device__ __forceinline__ float Epi<float>::apply(float acc, int64_t m, int64_t n) const {
+  switch (kind) {
+    case TX_EPI_BIAS: return __fadd_rn(aux[n * s1], acc);
+    case TX_EPI_BIAS_TANH: return tanhf(__fadd_rn(aux[n * s1], acc));
+    case TX_EPI_MUL_1MSQR: {
+      float h = aux[m * s0 + n * s1];
+      return __fmul_rn(acc, __fsub_rn(1.0f, __fmul_rn(h, h)));
+    }
+  }
+  return acc;
+}
+
+template <>
+__device__ __forceinline__ double Epi<double>::apply(double acc, int64_t m, int64_t n) const {
+  switch (kind) {
+    case TX_EPI_BIAS: return __dadd_rn(aux[n * s1], acc);
+    case TX_EPI_BIAS_TANH: return tanh(__dadd_rn(aux[n * s1], acc));
+    case TX_EPI_MUL_1MSQR: {
+      double h = aux[m * s0 + n * s1];
+      return __dmul_rn(acc, __dsub_rn(1.0, __dmul_rn(h, h)));
+    }
+  }
+  return acc;
+}
+
+struct G {
+  int dtype;
+  const void* A;
+  const void* B;
+  void* C;
+  int64_t M, N, K;
+  int64_t sam, sak, sbk, sbn, scm, scn;
+  Epi<float> epi_f;
+  Epi<double> epi_d;
+};
+
+enum { PATH_SIMT = 0, PATH_SKINNY = 1, PATH_TC = 2 };
+enum { SK_ROWDOT = 0, SK_OUTER = 1, SK_KRED = 2 };
+
+int gemm_simt(const G& g, cudaStream_t st);
+int gemm_skinny(const G& g, int kind, void* ws, size_t wsb, cudaStream_t st);
+int kred_splits(int64_t M, int64_t K);
+// tcgen05 path: returns TX_E_UNSUPPORTED if the layout is ineligible
+int gemm_tc_eligible(const G& g);
+int gemm_tc(const G& g, cudaStream_t st);
+
+}  // namespace tx

@@ -1,0 +1,366 @@
+// tcgen05 / TMEM / TMA TF32 GEMM for sm_100a.
+//
+// Replaces np.dot -> OpenBLAS sgemm for large float32 problems (reference
+// pkg/src/texpr/ops/linalg.py:42-62).  C[M,N] = A[M,K] . B[K,N] (+ epilogue).
+//
+// Structure (persistent, warp-specialised, one CTA per SM):
+//   warp 0      TMA producer: one elected lane streams A/B K-slices into a
+//               4-stage shared-memory ring (128 B swizzle), completion tracked
+//               by mbarrier transaction counts.
+//   warp 1      TMEM owner + MMA issuer: allocates 512 TMEM columns (two
+//               128x256 fp32 accumulators), one lane issues
+//               tcgen05.mma.cta_group::1.kind::tf32 (128x256x8 per instruction)
+//               and tcgen05.commit's smem slots back to the producer and full
+//               accumulators to the epilogue.
+//   warps 2-5   epilogue: tcgen05.ld 32x32b rows out of TMEM, fused epilogue
+//               (bias / bias+tanh / *(1-h^2)), 128-bit global stores; the
+//               second accumulator lets tile i+1's MMAs overlap tile i's
+//               epilogue.
+// Operand transposes (DimShuffle views) are not copied: a K-contiguous
+// operand uses the K-major UMMA descriptor, an M/N-contiguous one the
+// MN-major descriptor (legal for TF32), with the matching TMA box shape.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <mutex>
+
+#include "tx_common.h"
+#include "tx_gemm.h"
+
+namespace tx {
+namespace {
+
+constexpr int BM = 128;
+constexpr int BN = 256;
+constexpr int BK = 32;  // 32 fp32 = 128 B = one swizzle span
+constexpr int STAGES = 4;
+constexpr int A_BYTES = BM * BK * 4;  // 16 KB
+constexpr int B_BYTES = BN * BK * 4;  // 32 KB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int NUM_THREADS = 192;
+constexpr int TMEM_COLS = 512;
+constexpr int GROUP_M = 16;
+constexpr size_t SMEM_BYTES = 1024 /*align slack*/ + (size_t)STAGES * STAGE_BYTES + 256 /*barriers*/;
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(su32(b)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          su32(dst)),
+      "l"((uint64_t)map), "r"(su32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// UMMA shared-memory descriptor, SWIZZLE_128B (sm100 "version 1" layout).
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+__device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+struct TcParams {
+  float* C;
+  int64_t ldc;
+  int M, N, K;
+  int a_mn, b_mn;  // 1 = operand is MN-major in memory
+  int num_m, num_n, num_tiles;
+  Epi<float> epi;
+};
+
+__device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int& mb, int& nb) {
+  const int per_group = GROUP_M * num_n;
+  const int g = t / per_group;
+  const int first = g * GROUP_M;
+  const int gsz = min(num_m - first, GROUP_M);
+  const int r = t - g * per_group;
+  mb = first + r % gsz;
+  nb = r / gsz;
+}
+
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                   const TcParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = (uint64_t*)(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }
+    for (int b = 0; b < 2; ++b) { mbar_init(tfull + b, 1); mbar_init(tempty + b, 4); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
+                 "r"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int num_kb = (p.K + BK - 1) / BK;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&mapA) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&mapB) : "memory");
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+        int mb, nb;
+        tile_coords(t, p.num_m, p.num_n, mb, nb);
+        const int m0 = mb * BM, n0 = nb * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(empty + stage, phase ^ 1);
+          uint8_t* sa = smem + stage * STAGE_BYTES;
+          uint8_t* sb = sa + A_BYTES;
+          mbar_expect_tx(full + stage, STAGE_BYTES);
+          const int k0 = kb * BK;
+          if (p.a_mn) {
+#pragma unroll
+            for (int j = 0; j < BM / 32; ++j) tma_load_2d(sa + j * 4096, &mapA, full + stage, m0 + 32 * j, k0);
+          } else {
+            tma_load_2d(sa, &mapA, full + stage, k0, m0);
+          }
+          if (p.b_mn) {
+#pragma unroll
+            for (int j = 0; j < BN / 32; ++j) tma_load_2d(sb + j * 4096, &mapB, full + stage, n0 + 32 * j, k0);
+          } else {
+            tma_load_2d(sb, &mapB, full + stage, k0, n0);
+          }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)p.a_mn << 15) |
+                           ((uint32_t)p.b_mn << 16) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+    // descriptor geometry per operand layout
+    const uint32_t a_lbo = p.a_mn ? 4096u : 16u, a_step = p.a_mn ? 1024u : 32u;
+    const uint32_t b_lbo = p.b_mn ? 4096u : 16u, b_step = p.b_mn ? 1024u : 32u;
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0;
+    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
+      const int buf = it & 1;
+      const uint32_t use = (uint32_t)(it >> 1);
+      mbar_wait(tempty + buf, (use & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t tmem_d = tmem_base + (uint32_t)(buf * BN);
+      for (int kb = 0; kb < num_kb; ++kb) {
+        mbar_wait(full + stage, phase);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t sa = su32(smem + stage * STAGE_BYTES);
+          const uint32_t sb = sa + A_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            const uint64_t da = sdesc(sa + kk * a_step, a_lbo, 1024);
+            const uint64_t db = sdesc(sb + kk * b_step, b_lbo, 1024);
+            umma_tf32(tmem_d, da, db, idesc, (kb | kk) != 0);
+          }
+          umma_commit(empty + stage);
+        }
+        __syncwarp();
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+      if (lane == 0) umma_commit(tfull + buf);
+      __syncwarp();
+    }
+  } else {
+    // epilogue warps 2..5 -> TMEM lane quarter (warp % 4)
+    const int q = warp & 3;
+    int it = 0;
+    const bool vec_ok = (p.ldc % 4 == 0) && (((uintptr_t)p.C & 15) == 0);
+    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
+      int mb, nb;
+      tile_coords(t, p.num_m, p.num_n, mb, nb);
+      const int buf = it & 1;
+      const uint32_t use = (uint32_t)(it >> 1);
+      mbar_wait(tfull + buf, use & 1);
+      tc_fence_after();
+      const int row = mb * BM + q * 32 + lane;
+      const uint32_t taddr = tmem_base + (uint32_t)(buf * BN) + ((uint32_t)(q * 32) << 16);
+      float* crow = p.C + (int64_t)row * p.ldc;
+      for (int c = 0; c < BN; c += 16) {
+        float v[16];
+        tmem_ld16(taddr + c, v);
+        const int n = nb * BN + c;
+        if (row < p.M && n < p.N) {
+          if (p.epi.kind != TX_EPI_NONE) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] = p.epi.apply(v[i], row, n + i);
+          }
+          if (vec_ok && n + 16 <= p.N) {
+#pragma unroll
+            for (int i = 0; i < 16; i += 4)
+              *reinterpret_cast<float4*>(crow + n + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+          } else {
+            for (int i = 0; i < 16 && n + i < p.N; ++i) crow[n + i] = v[i];
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty + buf);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS)
+                 : "memory");
+  }
+}
+
+// ----------------------------------------------------------------- host side
+typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                             const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                             CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeFn g_encode = nullptr;
+static std::once_flag g_once;
+static bool g_attr_set = false;
+
+static EncodeFn encode_fn() {
+  std::call_once(g_once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode = (EncodeFn)p;
+  });
+  return g_encode;
+}
+
+// inner-contiguous 2D map: dims {inner, outer}, outer stride in elements
+static int make_map(CUtensorMap* m, const void* base, int64_t inner, int64_t outer, int64_t ostride, int box_inner,
+                    int box_outer) {
+  EncodeFn enc = encode_fn();
+  TX_CHECK(enc, TX_E_NODEVICE, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  cuuint64_t strides[1] = {(cuuint64_t)(ostride * 4)};
+  cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_TFLOAT32, 2, const_cast<void*>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(TX_E_CUDA, "cuTensorMapEncodeTiled failed (code " + std::to_string((int)r) + ")");
+  return TX_OK;
+}
+
+}  // namespace
+
+int gemm_tc_eligible(const G& g) {
+  if (g.dtype != TX_F32) return TX_E_UNSUPPORTED;
+  if (g.M < 64 || g.N < 64 || g.K < 16) return TX_E_UNSUPPORTED;
+  if (g.M > INT32_MAX || g.N > INT32_MAX || g.K > INT32_MAX) return TX_E_UNSUPPORTED;
+  if (g.scn != 1) return TX_E_UNSUPPORTED;
+  if (((uintptr_t)g.A & 15) || ((uintptr_t)g.B & 15)) return TX_E_UNSUPPORTED;
+  bool a_k = g.sak == 1 && g.sam % 4 == 0 && g.sam >= g.K;
+  bool a_m = g.sam == 1 && g.sak % 4 == 0 && g.sak >= g.M;
+  bool b_k = g.sbk == 1 && g.sbn % 4 == 0 && g.sbn >= g.K;
+  bool b_n = g.sbn == 1 && g.sbk % 4 == 0 && g.sbk >= g.N;
+  if (!(a_k || a_m) || !(b_k || b_n)) return TX_E_UNSUPPORTED;
+  return TX_OK;
+}
+
+int gemm_tc(const G& g, cudaStream_t st) {
+  int rc = gemm_tc_eligible(g);
+  if (rc) return fail(rc, "tx_gemm: operand layout not eligible for the tcgen05 path");
+  const bool a_mn = !(g.sak == 1 && g.sam % 4 == 0 && g.sam >= g.K);
+  const bool b_mn = (g.sbn == 1 && g.sbk % 4 == 0 && g.sbk >= g.N);
+  CUtensorMap ma, mb;
+  if (a_mn) rc = make_map(&ma, g.A, g.M, g.K, g.sak, 32, 32);
+  else rc = make_map(&ma, g.A, g.K, g.M, g.sam, 32, BM);
+  if (rc) return rc;
+  if (b_mn) rc = make_map(&mb, g.B, g.N, g.K, g.sbk, 32, 32);
+  else rc = make_map(&mb, g.B, g.K, g.N, g.sbn, 32, BN);
+  if (rc) return rc;
+  TcParams p;
+  p.C = (float*)g.C;
+  p.ldc = g.scm;
+  p.M = (int)g.M;
+  p.N = (int)g.N;
+  p.K = (int)g.K;
+  p.a_mn = a_mn;
+  p.b_mn = b_mn;
+  p.num_m = (int)((g.M + BM - 1) / BM);
+  p.num_n = (int)((g.N + BN - 1) / BN);
+  p.num_tiles = p.num_m * p.num_n;
+  p.epi = g.epi_f;
+  if (!g_attr_set) {
+    TX_CUDA(cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES));
+    g_attr_set = true;
+  }
+  int grid = p.num_tiles < sm_count() ? p.num_tiles : sm_count();
+  tc_gemm_kernel<<<grid, NUM_THREADS, SMEM_BYTES, st>>>(ma, mb, p);
+  TX_CUDA(cudaGetLastError());
+  return TX_OK;
+}
+
+}  // namespace tx

@@ -1,0 +1,598 @@
+// CAReduce on sm_100a: sum / max / first-max one-hot / first-max index over an
+// arbitrary axis set of a strided tensor.
+//
+// Replaces np.add.reduce / np.maximum.reduce / np.argmax+put_along_axis in
+// reference pkg/src/texpr/ops/reductions.py:91-101, :119-129, :166-179.
+//
+// The (kept dims) x (reduced dims) problem is collapsed to the cheapest form:
+//   ROW    reduced elements contiguous per output ("axis 1" / all axes):
+//          CTA-per-row (or per row-slice), 128-bit loads, warp-shuffle tree,
+//          optional split of long rows across CTAs with a deterministic
+//          second pass (no atomics: results are run-to-run identical).
+//   COL    kept elements contiguous ("axis 0"): each thread owns 4 adjacent
+//          columns (one 128-bit load per row), rows split across grid.y into
+//          partials combined in fixed order by a finalize kernel.
+//   GEN    anything else: one thread per output, div/mod addressing.
+// max / argmax are bit-exact with NumPy: NaN propagates (and counts as the
+// maximum for argmax), and the first maximal element wins ties.
+#include <cuda_runtime.h>
+
+#include <cfloat>
+#include <climits>
+#include <cstring>
+
+#include "tx_common.h"
+
+namespace tx {
+namespace {
+
+constexpr int kThreads = 256;
+
+template <class T> __device__ __forceinline__ bool isnan_(T v) { return false; }
+template <> __device__ __forceinline__ bool isnan_<float>(float v) { return v != v; }
+template <> __device__ __forceinline__ bool isnan_<double>(double v) { return v != v; }
+
+template <class T> __device__ __forceinline__ T lowest();
+template <> __device__ __forceinline__ float lowest<float>() { return -INFINITY; }
+template <> __device__ __forceinline__ double lowest<double>() { return -INFINITY; }
+template <> __device__ __forceinline__ int lowest<int>() { return INT_MIN; }
+template <> __device__ __forceinline__ long long lowest<long long>() { return LLONG_MIN; }
+template <> __device__ __forceinline__ unsigned char lowest<unsigned char>() { return 0; }
+
+// Accumulator state for one reduction op.  idx is the flat index over the
+// reduced dims (only meaningful for the argmax ops).
+template <class T, int OP>
+struct Acc {
+  T v;
+  long long i;
+  __device__ __forceinline__ void init() {
+    if (OP == TX_SUM) v = T(0); else v = lowest<T>();
+    i = LLONG_MAX;
+  }
+  __device__ __forceinline__ void push(T x, long long idx) {
+    if (OP == TX_SUM) {
+      v = v + x;
+    } else if (OP == TX_MAX) {
+      // NaN-propagating max (np.maximum semantics)
+      if (isnan_<T>(v)) return;
+      if (isnan_<T>(x) || x > v) v = x;
+    } else {
+      // first-max with NaN as maximal; callers push in increasing idx order
+      // within a thread, merges use merge() which compares indices.
+      merge_pair(x, idx);
+    }
+  }
+  __device__ __forceinline__ void merge_pair(T x, long long idx) {
+    bool xn = isnan_<T>(x), vn = isnan_<T>(v);
+    bool take;
+    if (vn && xn) take = idx < i;
+    else if (vn) take = false;
+    else if (xn) take = true;
+    else if (x > v) take = true;
+    else if (x < v) take = false;
+    else take = idx < i;
+    if (i == LLONG_MAX) take = true;
+    if (take) { v = x; i = idx; }
+  }
+  __device__ __forceinline__ void merge(const Acc& o) {
+    if (OP == TX_SUM) v = v + o.v;
+    else if (OP == TX_MAX) push(o.v, 0);
+    else if (o.i != LLONG_MAX) merge_pair(o.v, o.i);
+  }
+};
+
+template <class T, int OP>
+__device__ __forceinline__ Acc<T, OP> shfl_down(const Acc<T, OP>& a, int off) {
+  Acc<T, OP> r;
+  r.v = __shfl_down_sync(0xffffffffu, a.v, off);
+  r.i = __shfl_down_sync(0xffffffffu, a.i, off);
+  return r;
+}
+
+template <class T, int OP>
+__device__ __forceinline__ Acc<T, OP> block_reduce(Acc<T, OP> a) {
+  __shared__ T sv[kThreads / 32];
+  __shared__ long long si[kThreads / 32];
+  for (int off = 16; off > 0; off >>= 1) a.merge(shfl_down(a, off));
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) { sv[warp] = a.v; si[warp] = a.i; }
+  __syncthreads();
+  if (warp == 0) {
+    Acc<T, OP> b;
+    b.init();
+    if (lane < (int)(blockDim.x >> 5)) { b.v = sv[lane]; b.i = si[lane]; }
+    for (int off = 16; off > 0; off >>= 1) b.merge(shfl_down(b, off));
+    a = b;
+  }
+  return a;  // valid in thread 0
+}
+
+template <class T> struct Vec4 {};
+template <> struct Vec4<float> { using type = float4; };
+template <> struct Vec4<int> { using type = int4; };
+
+// ------------------------------------------------------------------ ROW
+// rows x R, row r at x + r*rs, contiguous within the row.  grid = (splits, rows).
+// splits == 1: write the final result; else write partials [rows][splits].
+template <class T, int OP>
+__global__ void __launch_bounds__(kThreads) row_kernel(const T* __restrict__ x, int64_t rows, int64_t R, int64_t rs,
+                                                      int splits, T* __restrict__ out, long long* __restrict__ out_idx,
+                                                      T* __restrict__ pv, long long* __restrict__ pi) {
+  const int64_t row = blockIdx.y + (int64_t)blockIdx.z * gridDim.y;
+  if (row >= rows) return;
+  const int64_t chunk = (R + splits - 1) / splits;
+  const int64_t lo = (int64_t)blockIdx.x * chunk;
+  const int64_t hi = min(R, lo + chunk);
+  const T* p = x + row * rs;
+  Acc<T, OP> a;
+  a.init();
+  if constexpr (sizeof(T) == 4 && (OP == TX_SUM || OP == TX_MAX) && !std::is_same<T, unsigned char>::value) {
+    // 128-bit path when the slice start is 16 B aligned
+    int64_t head = lo;
+    const int64_t mis = ((uintptr_t)(p + lo) & 15) / sizeof(T);
+    int64_t vstart = lo + (mis ? (4 - mis) : 0);
+    if (vstart > hi) vstart = hi;
+    for (int64_t k = lo + threadIdx.x; k < vstart; k += blockDim.x) a.push(p[k], k);
+    const int64_t nv = (hi - vstart) / 4;
+    using V = typename Vec4<T>::type;
+    const V* pv4 = reinterpret_cast<const V*>(p + vstart);
+    int64_t k = threadIdx.x;
+    for (; k + 3 * (int64_t)blockDim.x < nv; k += 4 * (int64_t)blockDim.x) {
+      V q0 = __ldcs(pv4 + k), q1 = __ldcs(pv4 + k + blockDim.x);
+      V q2 = __ldcs(pv4 + k + 2 * blockDim.x), q3 = __ldcs(pv4 + k + 3 * blockDim.x);
+      a.push(q0.x, 0); a.push(q0.y, 0); a.push(q0.z, 0); a.push(q0.w, 0);
+      a.push(q1.x, 0); a.push(q1.y, 0); a.push(q1.z, 0); a.push(q1.w, 0);
+      a.push(q2.x, 0); a.push(q2.y, 0); a.push(q2.z, 0); a.push(q2.w, 0);
+      a.push(q3.x, 0); a.push(q3.y, 0); a.push(q3.z, 0); a.push(q3.w, 0);
+    }
+    for (; k < nv; k += blockDim.x) {
+      V q = __ldcs(pv4 + k);
+      a.push(q.x, 0); a.push(q.y, 0); a.push(q.z, 0); a.push(q.w, 0);
+    }
+    for (int64_t t = vstart + nv * 4 + threadIdx.x; t < hi; t += blockDim.x) a.push(p[t], t);
+    (void)head;
+  } else if constexpr (sizeof(T) == 4 && (OP == TX_ARGMAX_INDEX || OP == TX_ARGMAX_ONEHOT)) {
+    const bool al = (((uintptr_t)(p + lo)) & 15) == 0;
+    if (al) {
+      using V = typename Vec4<T>::type;
+      const int64_t nv = (hi - lo) / 4;
+      const V* pv4 = reinterpret_cast<const V*>(p + lo);
+      for (int64_t k = threadIdx.x; k < nv; k += blockDim.x) {
+        V q = __ldcs(pv4 + k);
+        int64_t b = lo + 4 * k;
+        a.merge_pair(q.x, b); a.merge_pair(q.y, b + 1); a.merge_pair(q.z, b + 2); a.merge_pair(q.w, b + 3);
+      }
+      for (int64_t t = lo + nv * 4 + threadIdx.x; t < hi; t += blockDim.x) a.merge_pair(p[t], t);
+    } else {
+      for (int64_t k = lo + threadIdx.x; k < hi; k += blockDim.x) a.merge_pair(p[k], k);
+    }
+  } else {
+    for (int64_t k = lo + threadIdx.x; k < hi; k += blockDim.x) {
+      if (OP == TX_SUM || OP == TX_MAX) a.push(p[k], k); else a.merge_pair(p[k], k);
+    }
+  }
+  a = block_reduce<T, OP>(a);
+  if (threadIdx.x == 0) {
+    if (splits == 1) {
+      if (OP == TX_SUM || OP == TX_MAX) out[row] = a.v; else out_idx[row] = a.i;
+    } else {
+      pv[row * splits + blockIdx.x] = a.v;
+      pi[row * splits + blockIdx.x] = a.i;
+    }
+  }
+}
+
+// warp-per-row variant for short rows (softmax-sized [B, 10] tensors)
+template <class T, int OP>
+__global__ void __launch_bounds__(kThreads) row_warp_kernel(const T* __restrict__ x, int64_t rows, int64_t R, int64_t rs,
+                                                           int64_t es, T* __restrict__ out, long long* __restrict__ out_idx) {
+  const int64_t row = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const T* p = x + row * rs;
+  Acc<T, OP> a;
+  a.init();
+  for (int64_t k = lane; k < R; k += 32) {
+    if (OP == TX_SUM || OP == TX_MAX) a.push(p[k * es], k); else a.merge_pair(p[k * es], k);
+  }
+  for (int off = 16; off > 0; off >>= 1) a.merge(shfl_down(a, off));
+  if (lane == 0) {
+    if (OP == TX_SUM || OP == TX_MAX) out[row] = a.v; else out_idx[row] = a.i;
+  }
+}
+
+template <class T, int OP>
+__global__ void finalize_splits(int64_t rows, int splits, const T* __restrict__ pv, const long long* __restrict__ pi,
+                                T* __restrict__ out, long long* __restrict__ out_idx) {
+  int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (row >= rows) return;
+  Acc<T, OP> a;
+  a.init();
+  for (int s = 0; s < splits; ++s) {
+    Acc<T, OP> b;
+    b.v = pv[row * splits + s];
+    b.i = pi[row * splits + s];
+    a.merge(b);
+  }
+  if (OP == TX_SUM || OP == TX_MAX) out[row] = a.v; else out_idx[row] = a.i;
+}
+
+// ------------------------------------------------------------------ COL
+// R rows x K columns, element (r, c) at x + r*rs + c (kept dim contiguous).
+// grid.x covers columns (4 per thread), grid.y splits rows.
+template <class T, int OP>
+__global__ void __launch_bounds__(kThreads) col_kernel(const T* __restrict__ x, int64_t R, int64_t K, int64_t rs,
+                                                      int splits, bool vec, T* __restrict__ out,
+                                                      long long* __restrict__ out_idx, T* __restrict__ pv,
+                                                      long long* __restrict__ pi) {
+  const int64_t c0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (c0 >= K) return;
+  const int64_t chunk = (R + splits - 1) / splits;
+  const int64_t lo = (int64_t)blockIdx.y * chunk;
+  const int64_t hi = min(R, lo + chunk);
+  Acc<T, OP> a[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) a[j].init();
+  const int nc = (int)min((int64_t)4, K - c0);
+  if constexpr (sizeof(T) == 4 && !std::is_same<T, unsigned char>::value) {
+    if (vec && nc == 4) {
+      using V = typename Vec4<T>::type;
+      int64_t r = lo;
+      for (; r + 3 < hi; r += 4) {
+        V q0 = __ldcs(reinterpret_cast<const V*>(x + r * rs + c0));
+        V q1 = __ldcs(reinterpret_cast<const V*>(x + (r + 1) * rs + c0));
+        V q2 = __ldcs(reinterpret_cast<const V*>(x + (r + 2) * rs + c0));
+        V q3 = __ldcs(reinterpret_cast<const V*>(x + (r + 3) * rs + c0));
+        a[0].push(q0.x, r); a[1].push(q0.y, r); a[2].push(q0.z, r); a[3].push(q0.w, r);
+        a[0].push(q1.x, r + 1); a[1].push(q1.y, r + 1); a[2].push(q1.z, r + 1); a[3].push(q1.w, r + 1);
+        a[0].push(q2.x, r + 2); a[1].push(q2.y, r + 2); a[2].push(q2.z, r + 2); a[3].push(q2.w, r + 2);
+        a[0].push(q3.x, r + 3); a[1].push(q3.y, r + 3); a[2].push(q3.z, r + 3); a[3].push(q3.w, r + 3);
+      }
+      for (; r < hi; ++r) {
+        V q = __ldcs(reinterpret_cast<const V*>(x + r * rs + c0));
+        a[0].push(q.x, r); a[1].push(q.y, r); a[2].push(q.z, r); a[3].push(q.w, r);
+      }
+      goto done;
+    }
+  }
+  for (int64_t r = lo; r < hi; ++r)
+    for (int j = 0; j < nc; ++j) a[j].push(x[r * rs + c0 + j], r);
+done:
+  for (int j = 0; j < nc; ++j) {
+    const int64_t c = c0 + j;
+    if (splits == 1) {
+      if (OP == TX_SUM || OP == TX_MAX) out[c] = a[j].v; else out_idx[c] = a[j].i;
+    } else {
+      pv[(int64_t)blockIdx.y * K + c] = a[j].v;
+      pi[(int64_t)blockIdx.y * K + c] = a[j].i;
+    }
+  }
+}
+
+template <class T, int OP>
+__global__ void finalize_cols(int64_t K, int splits, const T* __restrict__ pv, const long long* __restrict__ pi,
+                              T* __restrict__ out, long long* __restrict__ out_idx) {
+  int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= K) return;
+  Acc<T, OP> a;
+  a.init();
+  for (int s = 0; s < splits; ++s) {
+    Acc<T, OP> b;
+    b.v = pv[(int64_t)s * K + c];
+    b.i = pi[(int64_t)s * K + c];
+    a.merge(b);
+  }
+  if (OP == TX_SUM || OP == TX_MAX) out[c] = a.v; else out_idx[c] = a.i;
+}
+
+// ------------------------------------------------------------------ GEN
+struct GenMeta {
+  int nk, nr;
+  int64_t kshape[TX_MAX_RANK], kstride[TX_MAX_RANK];
+  int64_t rshape[TX_MAX_RANK], rstride[TX_MAX_RANK];
+};
+
+template <class T, int OP>
+__global__ void gen_kernel(const T* __restrict__ x, int64_t K, int64_t R, GenMeta m, T* __restrict__ out,
+                           long long* __restrict__ out_idx) {
+  int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (o >= K) return;
+  int64_t base = 0, t = o;
+  for (int d = m.nk - 1; d >= 0; --d) { base += (t % m.kshape[d]) * m.kstride[d]; t /= m.kshape[d]; }
+  Acc<T, OP> a;
+  a.init();
+  for (int64_t r = 0; r < R; ++r) {
+    int64_t off = 0, u = r;
+    for (int d = m.nr - 1; d >= 0; --d) { off += (u % m.rshape[d]) * m.rstride[d]; u /= m.rshape[d]; }
+    if (OP == TX_SUM || OP == TX_MAX) a.push(x[base + off], r); else a.merge_pair(x[base + off], r);
+  }
+  if (OP == TX_SUM || OP == TX_MAX) out[o] = a.v; else out_idx[o] = a.i;
+}
+
+// one-hot materialisation: y has x's shape; element is 1 where its flat
+// reduced index equals idx[flat kept index].
+template <class T>
+__global__ void onehot_kernel(T* __restrict__ y, int64_t n, GenMeta m, const long long* __restrict__ idx) {
+  // m.kshape/kstride hold y's FULL shape and a per-dim role: kstride[d] = 1 kept, 0 reduced
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t t = e, ki = 0, ri = 0, kmul = 1, rmul = 1, off = 0;
+    for (int d = m.nk - 1; d >= 0; --d) {
+      int64_t c = t % m.kshape[d];
+      t /= m.kshape[d];
+      off += c * m.rstride[d];
+      if (m.kstride[d]) { ki += c * kmul; kmul *= m.kshape[d]; }
+      else { ri += c * rmul; rmul *= m.kshape[d]; }
+    }
+    y[off] = (ri == idx[ki]) ? T(1) : T(0);
+  }
+}
+
+template <class T>
+__global__ void onehot_rows(T* __restrict__ y, int64_t rows, int64_t R, const long long* __restrict__ idx) {
+  // y contiguous [rows, R]
+  const int64_t n = rows * R;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = e / R;
+    __stcs(y + e, (e - r * R) == idx[r] ? T(1) : T(0));
+  }
+}
+
+template <class T>
+__global__ void onehot_cols(T* __restrict__ y, int64_t R, int64_t K, const long long* __restrict__ idx) {
+  // y contiguous [R, K]; idx per column
+  const int64_t n = R * K;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = e / K;
+    __stcs(y + e, r == idx[e - r * K] ? T(1) : T(0));
+  }
+}
+
+// ------------------------------------------------------------------ planning
+enum Form { ROW, ROWWARP, COL, GEN };
+
+struct Plan {
+  Form form;
+  int64_t K = 1, R = 1;   // outputs, reduced elements
+  int64_t ks = 0, rs = 0; // collapsed single-dim strides (ROW: row stride; COL: row stride)
+  int64_t es = 1;         // ROWWARP element stride
+  int splits = 1;
+  GenMeta gm;
+  size_t ws_partial = 0, ws_idx = 0;
+};
+
+// merge a list of (extent, stride) dims in order when row-major compatible
+static int merge_dims(int n, int64_t* sh, int64_t* st) {
+  int o = 0;
+  for (int i = 0; i < n; ++i) {
+    if (sh[i] == 1) continue;
+    if (o > 0 && st[o - 1] == st[i] * sh[i]) {
+      sh[o - 1] *= sh[i];
+      st[o - 1] = st[i];
+      continue;
+    }
+    sh[o] = sh[i];
+    st[o] = st[i];
+    ++o;
+  }
+  return o;
+}
+
+static void make_plan(int op, const tx_tensor& x, uint32_t mask, int itemsz, Plan* p) {
+  int64_t ksh[TX_MAX_RANK], kst[TX_MAX_RANK], rsh[TX_MAX_RANK], rst[TX_MAX_RANK];
+  int nk = 0, nr = 0;
+  for (int d = 0; d < x.ndim; ++d) {
+    if (mask & (1u << d)) { rsh[nr] = x.shape[d]; rst[nr] = x.strides[d]; ++nr; }
+    else { ksh[nk] = x.shape[d]; kst[nk] = x.strides[d]; ++nk; }
+  }
+  int64_t K = 1, R = 1;
+  for (int i = 0; i < nk; ++i) K *= ksh[i];
+  for (int i = 0; i < nr; ++i) R *= rsh[i];
+  p->K = K;
+  p->R = R;
+  // keep an uncollapsed copy for GEN
+  p->gm.nk = nk;
+  p->gm.nr = nr;
+  for (int i = 0; i < nk; ++i) { p->gm.kshape[i] = ksh[i]; p->gm.kstride[i] = kst[i]; }
+  for (int i = 0; i < nr; ++i) { p->gm.rshape[i] = rsh[i]; p->gm.rstride[i] = rst[i]; }
+  int mk = merge_dims(nk, ksh, kst);
+  int mr = merge_dims(nr, rsh, rst);
+  const int sms = sm_count();
+  if (mk <= 1 && mr <= 1) {
+    int64_t kstride = mk == 1 ? kst[0] : 0;
+    int64_t rstride = mr == 1 ? rst[0] : 1;
+    if (R == 1 || rstride == 1) {
+      if (R <= 512 && K >= 8) {
+        p->form = ROWWARP;
+        p->ks = kstride;
+        p->es = 1;
+      } else {
+        p->form = ROW;
+        p->ks = kstride;
+        // split long rows so that at least ~4 CTAs per SM exist
+        int64_t want = (int64_t)sms * 4;
+        int64_t splits = 1;
+        if (K < want) {
+          splits = (want + K - 1) / K;
+          int64_t maxs = R / 4096;
+          if (splits > maxs) splits = maxs;
+          if (splits < 1) splits = 1;
+        }
+        p->splits = (int)splits;
+      }
+    } else if (kstride == 1 || K == 1) {
+      if (K == 1) {
+        // strided full reduce: treat as warp rows with element stride
+        p->form = ROWWARP;
+        p->ks = 0;
+        p->es = rstride;
+      } else {
+        p->form = COL;
+        p->rs = rstride;
+        int64_t colblocks = (K + 4 * kThreads - 1) / (4 * kThreads);
+        int64_t want = (int64_t)sms * 8;
+        int64_t splits = (want + colblocks - 1) / colblocks;
+        int64_t maxs = R / 64;
+        if (splits > maxs) splits = maxs;
+        if (splits > 65535) splits = 65535;
+        if (splits < 1) splits = 1;
+        p->splits = (int)splits;
+      }
+    } else if (R <= 512) {
+      p->form = ROWWARP;
+      p->ks = kstride;
+      p->es = rstride;
+    } else {
+      p->form = GEN;
+    }
+  } else {
+    p->form = GEN;
+  }
+  if (p->splits > 1) p->ws_partial = (size_t)p->splits * (size_t)p->K * (itemsz + 8);
+  if (op == TX_ARGMAX_ONEHOT) p->ws_idx = (size_t)p->K * 8;
+}
+
+static size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
+
+template <class T, int OP>
+static int run(const tx_tensor& x, uint32_t mask, tx_tensor& y, char* ws, size_t ws_bytes, cudaStream_t st) {
+  Plan p;
+  make_plan(OP, x, mask, (int)sizeof(T), &p);
+  TX_CHECK(align256(p.ws_partial) + p.ws_idx <= ws_bytes || (p.ws_partial == 0 && p.ws_idx == 0), TX_E_ARG,
+           "tx_reduce: workspace too small");
+  const int sms = sm_count();
+  T* out = (T*)y.data;
+  long long* out_idx = (long long*)y.data;
+  long long* onehot_idx = nullptr;
+  if (OP == TX_ARGMAX_ONEHOT) {
+    onehot_idx = (long long*)(ws + align256(p.ws_partial));
+    out_idx = onehot_idx;
+  }
+  // the output of SUM / MAX / ARGMAX_INDEX is written densely in kept-dim C order;
+  // require y contiguous for those (the VM allocates it so).
+  if (OP != TX_ARGMAX_ONEHOT) TX_CHECK(is_contiguous(y), TX_E_ARG, "tx_reduce: output must be contiguous");
+  T* pv = (T*)ws;
+  long long* pi = (long long*)(ws + (size_t)p.splits * p.K * sizeof(T));
+  if (p.splits > 1) pi = (long long*)(ws + (((size_t)p.splits * p.K * sizeof(T) + 7) & ~(size_t)7));
+  if (p.K == 0) return TX_OK;
+  if (p.R == 0) {
+    TX_CHECK(OP == TX_SUM, TX_E_ARG, "zero-size array to reduction operation maximum which has no identity");
+    TX_CUDA(cudaMemsetAsync(y.data, 0, (size_t)p.K * sizeof(T), st));
+    return TX_OK;
+  }
+  const T* xp = (const T*)x.data;
+  switch (p.form) {
+    case ROW: {
+      int64_t rows = p.K;
+      unsigned gy = (unsigned)(rows < 65535 ? rows : 65535);
+      unsigned gz = (unsigned)((rows + gy - 1) / gy);
+      dim3 grid((unsigned)p.splits, gy, gz);
+      row_kernel<T, OP><<<grid, kThreads, 0, st>>>(xp, rows, p.R, p.ks, p.splits, out, out_idx, pv, pi);
+      if (p.splits > 1)
+        finalize_splits<T, OP><<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(rows, p.splits, pv, pi, out, out_idx);
+      break;
+    }
+    case ROWWARP: {
+      int64_t rows = p.K;
+      unsigned blocks = (unsigned)((rows + (kThreads / 32) - 1) / (kThreads / 32));
+      row_warp_kernel<T, OP><<<blocks, kThreads, 0, st>>>(xp, rows, p.R, p.ks, p.es, out, out_idx);
+      break;
+    }
+    case COL: {
+      bool vec = ((uintptr_t)xp & 15) == 0 && (p.rs % 4) == 0;
+      unsigned gx = (unsigned)((p.K + 4 * kThreads - 1) / (4 * kThreads));
+      dim3 grid(gx, (unsigned)p.splits);
+      col_kernel<T, OP><<<grid, kThreads, 0, st>>>(xp, p.R, p.K, p.rs, p.splits, vec, out, out_idx, pv, pi);
+      if (p.splits > 1)
+        finalize_cols<T, OP><<<(unsigned)((p.K + 255) / 256), 256, 0, st>>>(p.K, p.splits, pv, pi, out, out_idx);
+      break;
+    }
+    case GEN: {
+      gen_kernel<T, OP><<<(unsigned)((p.K + 127) / 128), 128, 0, st>>>(xp, p.K, p.R, p.gm, out, out_idx);
+      break;
+    }
+  }
+  TX_CUDA(cudaGetLastError());
+  if (OP == TX_ARGMAX_ONEHOT) {
+    T* yp = (T*)y.data;
+    int64_t n = numel(y);
+    int64_t blocks = (n + 255) / 256;
+    if (blocks > (int64_t)sms * 16) blocks = (int64_t)sms * 16;
+    // fast forms when y is contiguous and the reduced dims are a trailing / leading block
+    bool ycont = is_contiguous(y);
+    int first_r = -1, last_r = -1, nred = 0;
+    for (int d = 0; d < x.ndim; ++d)
+      if (mask & (1u << d)) { if (first_r < 0) first_r = d; last_r = d; ++nred; }
+    bool block_contig = nred > 0 && (last_r - first_r + 1) == nred;
+    if (ycont && block_contig && last_r == x.ndim - 1) {
+      onehot_rows<T><<<(unsigned)blocks, 256, 0, st>>>(yp, p.K, p.R, onehot_idx);
+    } else if (ycont && block_contig && first_r == 0) {
+      onehot_cols<T><<<(unsigned)blocks, 256, 0, st>>>(yp, p.R, p.K, onehot_idx);
+    } else {
+      GenMeta m;
+      m.nk = y.ndim;
+      for (int d = 0; d < y.ndim; ++d) {
+        m.kshape[d] = y.shape[d];
+        m.kstride[d] = (mask & (1u << d)) ? 0 : 1;
+        m.rstride[d] = y.strides[d];
+      }
+      onehot_kernel<T><<<(unsigned)blocks, 256, 0, st>>>(yp, n, m, onehot_idx);
+    }
+    TX_CUDA(cudaGetLastError());
+  }
+  return TX_OK;
+}
+
+template <class T>
+static int dispatch_op(int op, const tx_tensor& x, uint32_t mask, tx_tensor& y, char* ws, size_t wsb, cudaStream_t st) {
+  switch (op) {
+    case TX_SUM: return run<T, TX_SUM>(x, mask, y, ws, wsb, st);
+    case TX_MAX: return run<T, TX_MAX>(x, mask, y, ws, wsb, st);
+    case TX_ARGMAX_ONEHOT: return run<T, TX_ARGMAX_ONEHOT>(x, mask, y, ws, wsb, st);
+    case TX_ARGMAX_INDEX: return run<T, TX_ARGMAX_INDEX>(x, mask, y, ws, wsb, st);
+  }
+  return fail(TX_E_ARG, "tx_reduce: unknown op");
+}
+
+}  // namespace
+
+int reduce_launch(int op, const tx_tensor& x, uint32_t mask, tx_tensor& y, void* ws, size_t wsb, cudaStream_t st) {
+  switch (x.dtype) {
+    case TX_F32: return dispatch_op<float>(op, x, mask, y, (char*)ws, wsb, st);
+    case TX_F64: return dispatch_op<double>(op, x, mask, y, (char*)ws, wsb, st);
+    case TX_I32: return dispatch_op<int>(op, x, mask, y, (char*)ws, wsb, st);
+    case TX_I64: return dispatch_op<long long>(op, x, mask, y, (char*)ws, wsb, st);
+    case TX_BOOL:
+      // numpy add.reduce into a bool buffer is logical OR == max over {0,1}
+      return dispatch_op<unsigned char>(op == TX_SUM ? TX_MAX : op, x, mask, y, (char*)ws, wsb, st);
+  }
+  return fail(TX_E_UNSUPPORTED, "tx_reduce: dtype");
+}
+
+}  // namespace tx
+
+using namespace tx;
+
+extern "C" {
+
+int tx_reduce_workspace(int op, const tx_tensor* x, uint32_t mask, size_t* bytes) {
+  TX_CHECK(x && bytes, TX_E_ARG, "tx_reduce_workspace: null argument");
+  Plan p;
+  int isz = itemsize(x->dtype);
+  make_plan(op, *x, mask, isz < 4 ? 4 : isz, &p);
+  *bytes = (p.ws_partial || p.ws_idx) ? align256(p.ws_partial) + p.ws_idx + 256 : 0;
+  return TX_OK;
+}
+
+int tx_reduce(int op, const tx_tensor* x, uint32_t mask, tx_tensor* y, void* ws, size_t wsb, void* stream) {
+  TX_CHECK(x && y, TX_E_ARG, "tx_reduce: null tensor");
+  TX_CHECK(x->ndim <= TX_MAX_RANK, TX_E_ARG, "tx_reduce: rank");
+  if (mask == 0) {  // empty axis tuple: identity copy (reference ops/reductions.py:94-95)
+    if (op == TX_ARGMAX_ONEHOT) {
+      TX_CHECK(false, TX_E_UNSUPPORTED, "argmax_onehot over no axes is lowered as a fill");
+    }
+    return tx_copy(x, y, stream);
+  }
+  return reduce_launch(op, *x, mask, *y, ws, wsb, (cudaStream_t)stream);
+}
+
+}  // extern "C"

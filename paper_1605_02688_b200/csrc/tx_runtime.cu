@@ -1,0 +1,220 @@
+// Runtime plumbing of libtexpr_b200: errors, device, streams, events, CUDA
+// graph capture (the VM's replacement for the reference's per-node Python
+// loop, runtime.py:428-446), async copies and a strided copy kernel.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "tx_common.h"
+
+namespace tx {
+
+static thread_local std::string g_last_error;
+static int g_sm_count = 0;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+int sm_count() {
+  if (g_sm_count == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sm_count, cudaDevAttrMultiProcessorCount, dev);
+    if (g_sm_count <= 0) g_sm_count = 148;
+  }
+  return g_sm_count;
+}
+
+void collapse(int ndim, const int64_t* shape, int nops, const int64_t (*strides)[TX_MAX_RANK], Space* out) {
+  // drop extent-1 dims
+  int64_t sh[TX_MAX_RANK];
+  int64_t st[32][TX_MAX_RANK];
+  int nd = 0;
+  for (int d = 0; d < ndim; ++d) {
+    if (shape[d] == 1) continue;
+    sh[nd] = shape[d];
+    for (int k = 0; k < nops; ++k) st[k][nd] = strides[k][d];
+    ++nd;
+  }
+  // merge dim d into d+1 (row-major) when every operand has stride[d] == stride[d+1]*shape[d+1]
+  int od = 0;
+  for (int d = 0; d < nd; ++d) {
+    if (od > 0) {
+      bool ok = true;
+      for (int k = 0; k < nops; ++k)
+        if (out->strides[k][od - 1] != st[k][d] * sh[d]) { ok = false; break; }
+      if (ok) {
+        out->shape[od - 1] *= sh[d];
+        for (int k = 0; k < nops; ++k) out->strides[k][od - 1] = st[k][d];
+        continue;
+      }
+    }
+    out->shape[od] = sh[d];
+    for (int k = 0; k < nops; ++k) out->strides[k][od] = st[k][d];
+    ++od;
+  }
+  out->ndim = od;
+}
+
+// ---------------------------------------------------------------- copy kernel
+struct CopyMeta {
+  int64_t v[3 * TX_MAX_RANK];
+};
+
+template <typename T>
+__global__ void strided_copy_kernel_p(const T* __restrict__ src, T* __restrict__ dst, int64_t n, int nd,
+                                      CopyMeta m) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = i, so = 0, dof = 0;
+    for (int d = nd - 1; d >= 0; --d) {
+      int64_t e = m.v[d];
+      int64_t c = r % e;
+      r /= e;
+      so += c * m.v[nd + d];
+      dof += c * m.v[2 * nd + d];
+    }
+    dst[dof] = src[so];
+  }
+}
+
+template <typename T>
+static int launch_copy(const tx_tensor* s, tx_tensor* d, cudaStream_t st) {
+  int64_t strides[2][TX_MAX_RANK];
+  int nd = d->ndim;
+  for (int i = 0; i < nd; ++i) {
+    int j = i - (nd - s->ndim);
+    strides[0][i] = (j >= 0 && s->shape[j] != 1) ? s->strides[j] : 0;
+    strides[1][i] = d->strides[i];
+  }
+  Space sp;
+  collapse(nd, d->shape, 2, strides, &sp);
+  int64_t n = numel(*d);
+  if (n == 0) return TX_OK;
+  CopyMeta m;
+  for (int i = 0; i < sp.ndim; ++i) {
+    m.v[i] = sp.shape[i];
+    m.v[sp.ndim + i] = sp.strides[0][i];
+    m.v[2 * sp.ndim + i] = sp.strides[1][i];
+  }
+  if (sp.ndim == 0) {  // scalar
+    m.v[0] = 1; m.v[1] = 0; m.v[2] = 0; sp.ndim = 1;
+  }
+  int threads = 256;
+  int64_t blocks = (n + threads - 1) / threads;
+  int64_t cap = (int64_t)sm_count() * 8;
+  if (blocks > cap) blocks = cap;
+  strided_copy_kernel_p<T><<<(unsigned)blocks, threads, 0, st>>>((const T*)s->data, (T*)d->data, n, sp.ndim, m);
+  TX_CUDA(cudaGetLastError());
+  return TX_OK;
+}
+
+}  // namespace tx
+
+using namespace tx;
+
+extern "C" {
+
+int tx_version(void) { return TX_ABI_VERSION; }
+
+const char* tx_last_error(void) { return g_last_error.c_str(); }
+
+int tx_init(int device) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0)
+    return fail(TX_E_NODEVICE, std::string("no CUDA device: ") + (e != cudaSuccess ? cudaGetErrorString(e) : "count=0"));
+  TX_CHECK(device >= 0 && device < n, TX_E_ARG, "device index out of range");
+  TX_CUDA(cudaSetDevice(device));
+  TX_CUDA(cudaFree(0));  // create the primary context
+  g_sm_count = 0;
+  sm_count();
+  return TX_OK;
+}
+
+int tx_device_info(int* sms, int* major, int* minor, int64_t* total_mem) {
+  int dev = 0;
+  TX_CUDA(cudaGetDevice(&dev));
+  cudaDeviceProp p;
+  TX_CUDA(cudaGetDeviceProperties(&p, dev));
+  if (sms) *sms = p.multiProcessorCount;
+  if (major) *major = p.major;
+  if (minor) *minor = p.minor;
+  if (total_mem) *total_mem = (int64_t)p.totalGlobalMem;
+  return TX_OK;
+}
+
+int tx_stream_create(void** s) {
+  cudaStream_t st;
+  TX_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  *s = st;
+  return TX_OK;
+}
+int tx_stream_destroy(void* s) { TX_CUDA(cudaStreamDestroy((cudaStream_t)s)); return TX_OK; }
+int tx_stream_sync(void* s) { TX_CUDA(cudaStreamSynchronize((cudaStream_t)s)); return TX_OK; }
+int tx_event_create(void** ev) {
+  cudaEvent_t e;
+  TX_CUDA(cudaEventCreate(&e));
+  *ev = e;
+  return TX_OK;
+}
+int tx_event_destroy(void* ev) { TX_CUDA(cudaEventDestroy((cudaEvent_t)ev)); return TX_OK; }
+int tx_event_record(void* ev, void* s) { TX_CUDA(cudaEventRecord((cudaEvent_t)ev, (cudaStream_t)s)); return TX_OK; }
+int tx_stream_wait_event(void* s, void* ev) {
+  TX_CUDA(cudaStreamWaitEvent((cudaStream_t)s, (cudaEvent_t)ev, 0));
+  return TX_OK;
+}
+int tx_event_elapsed_ms(void* a, void* b, float* ms) {
+  TX_CUDA(cudaEventElapsedTime(ms, (cudaEvent_t)a, (cudaEvent_t)b));
+  return TX_OK;
+}
+int tx_memcpy_async(void* dst, const void* src, size_t bytes, int kind, void* s) {
+  cudaMemcpyKind k = kind == 0 ? cudaMemcpyHostToDevice : kind == 1 ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+  if (bytes == 0) return TX_OK;
+  TX_CUDA(cudaMemcpyAsync(dst, src, bytes, k, (cudaStream_t)s));
+  return TX_OK;
+}
+int tx_memset_async(void* dst, int value, size_t bytes, void* s) {
+  if (bytes == 0) return TX_OK;
+  TX_CUDA(cudaMemsetAsync(dst, value, bytes, (cudaStream_t)s));
+  return TX_OK;
+}
+int tx_host_register(void* p, size_t bytes) {
+  TX_CUDA(cudaHostRegister(p, bytes, cudaHostRegisterDefault));
+  return TX_OK;
+}
+int tx_host_unregister(void* p) { TX_CUDA(cudaHostUnregister(p)); return TX_OK; }
+
+int tx_graph_begin(void* s) {
+  TX_CUDA(cudaStreamBeginCapture((cudaStream_t)s, cudaStreamCaptureModeThreadLocal));
+  return TX_OK;
+}
+int tx_graph_end(void* s, void** exec) {
+  cudaGraph_t g;
+  TX_CUDA(cudaStreamEndCapture((cudaStream_t)s, &g));
+  cudaGraphExec_t ge;
+  cudaError_t e = cudaGraphInstantiate(&ge, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
+  *exec = ge;
+  return TX_OK;
+}
+int tx_graph_launch(void* exec, void* s) {
+  TX_CUDA(cudaGraphLaunch((cudaGraphExec_t)exec, (cudaStream_t)s));
+  return TX_OK;
+}
+int tx_graph_destroy(void* exec) { TX_CUDA(cudaGraphExecDestroy((cudaGraphExec_t)exec)); return TX_OK; }
+
+int tx_copy(const tx_tensor* src, tx_tensor* dst, void* s) {
+  TX_CHECK(src && dst && src->dtype == dst->dtype, TX_E_ARG, "tx_copy: dtype mismatch");
+  TX_CHECK(src->ndim <= dst->ndim, TX_E_ARG, "tx_copy: source rank exceeds destination");
+  cudaStream_t st = (cudaStream_t)s;
+  switch (itemsize(dst->dtype)) {
+    case 1: return launch_copy<uint8_t>(src, dst, st);
+    case 4: return launch_copy<uint32_t>(src, dst, st);
+    case 8: return launch_copy<uint64_t>(src, dst, st);
+  }
+  return fail(TX_E_UNSUPPORTED, "tx_copy: dtype");
+}
+
+}  // extern "C"

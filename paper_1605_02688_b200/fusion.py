@@ -1,0 +1,159 @@
+"""Convex elementwise fusion (stage ``specialize``, name ``fuse_elemwise``).
+
+Replaces reference ``rewrites/fusion.py:47-144``, whose union-find joins every
+elementwise producer/consumer edge without a convexity check and therefore
+raises ``CycleDetected`` on any graph where a reduction or dot sits between
+two elementwise nodes of one group (SURVEY F2 — both training configs).
+
+Here groups grow greedily in topological order and a node joins its
+producer's group only if (a) its output has the group's iteration space
+(same rank and broadcast pattern, so one generated kernel covers every member)
+and (b) no path leaves the group and re-enters at the node (convexity),
+checked against per-node ancestor sets.  Each group of >= 2 nodes becomes one
+``Composite`` whose program is the NVRTC cache key; values consumed outside the
+group become extra kernel outputs; 0-d and single-element constants are
+inlined as literals.
+"""
+from __future__ import annotations
+
+from .elemwise import Composite, Elemwise, EwProgram
+from .graph import Constant, apply
+from .rewrite import register_rewrite
+
+
+def _fusable(node) -> bool:
+    return isinstance(node.op, (Elemwise, Composite)) and len(node.outputs) >= 1
+
+
+def _space(node):
+    t = node.outputs[0].type
+    if any(o.type.broadcastable != t.broadcastable for o in node.outputs):
+        return None
+    return t.broadcastable
+
+
+def _inline(x) -> bool:
+    return isinstance(x, Constant) and x.value.size == 1
+
+
+@register_rewrite("fuse_elemwise", "specialize", "global")
+def fuse_elemwise(fgraph, ctx, emit) -> int:
+    order = fgraph.toposort()
+    anc: dict[int, frozenset] = {}
+    for n in order:
+        s = set()
+        for x in n.inputs:
+            if x.owner is not None and x.owner.id in fgraph.nodes:
+                s.add(x.owner.id)
+                s |= anc[x.owner.id]
+        anc[n.id] = frozenset(s)
+
+    group_of: dict[int, int] = {}
+    members: dict[int, list] = {}
+    for n in order:
+        if not _fusable(n) or _space(n) is None:
+            continue
+        joined = None
+        for x in n.inputs:
+            p = x.owner
+            if p is None or p.id not in group_of:
+                continue
+            g = group_of[p.id]
+            if _space(members[g][0]) != _space(n):
+                continue
+            gset = {m.id for m in members[g]}
+            ok = True
+            for y in n.inputs:
+                q = y.owner
+                if q is None or q.id in gset:
+                    continue
+                if anc[q.id] & gset:  # a path leaves the group and comes back
+                    ok = False
+                    break
+            if ok:
+                joined = g
+                break
+        if joined is None:
+            group_of[n.id] = n.id
+            members[n.id] = [n]
+        else:
+            group_of[n.id] = joined
+            members[joined].append(n)
+
+    applied = 0
+    for root in sorted(members):
+        grp = members[root]
+        if len(grp) >= 2 and _fuse(fgraph, grp, emit):
+            applied += 1
+    return applied
+
+
+def _fuse(fgraph, grp, emit) -> bool:
+    ids = {n.id for n in grp}
+    produced = {o.id for n in grp for o in n.outputs}
+    leaves, leaf_pos = [], {}
+    consts, const_pos = [], {}
+    for n in grp:
+        for x in n.inputs:
+            if x.id in produced:
+                continue
+            if _inline(x):
+                key = (x.type.dtype, x.value.reshape(()).item())
+                if key not in const_pos:
+                    const_pos[key] = len(consts)
+                    consts.append(key)
+            elif x.id not in leaf_pos:
+                leaf_pos[x.id] = len(leaves)
+                leaves.append(x)
+    boundary = []
+    for n in grp:
+        for o in n.outputs:
+            if fgraph.is_output(o) or any(c.id not in ids for c in fgraph.node_clients(o)):
+                boundary.append(o)
+    if not boundary:
+        return False
+
+    refs: dict[int, tuple] = {}
+    prog_nodes = []
+
+    def ref_of(x):
+        if x.id in refs:
+            return refs[x.id]
+        if x.id in leaf_pos:
+            return ("in", leaf_pos[x.id])
+        return ("const", const_pos[(x.type.dtype, x.value.reshape(()).item())])
+
+    for n in grp:
+        if isinstance(n.op, Elemwise):
+            prog_nodes.append((n.op.kernel, [ref_of(x) for x in n.inputs], n.outputs[0].type.dtype))
+            refs[n.outputs[0].id] = ("node", len(prog_nodes) - 1)
+        else:  # splice an inner Composite's program
+            p = n.op.program
+            local = {}
+            outer_in = [ref_of(x) for x in n.inputs]
+            for j, (k, rr, dt) in enumerate(p.nodes):
+                mapped = []
+                for kind, i in rr:
+                    if kind == "in":
+                        mapped.append(outer_in[i])
+                    elif kind == "node":
+                        mapped.append(local[i])
+                    else:
+                        key = p.consts[i]
+                        if key not in const_pos:
+                            const_pos[key] = len(consts)
+                            consts.append(key)
+                        mapped.append(("const", const_pos[key]))
+                prog_nodes.append((k, mapped, dt))
+                local[j] = ("node", len(prog_nodes) - 1)
+            for o, r in zip(n.outputs, p.outputs):
+                refs[o.id] = local[r[1]] if r[0] == "node" else (
+                    outer_in[r[1]] if r[0] == "in" else r)
+
+    prog = EwProgram([x.type.dtype for x in leaves], consts, prog_nodes, [refs[b.id] for b in boundary])
+    outs = apply(Composite(prog), leaves)
+    if any(o.type != b.type for o, b in zip(outs, boundary)):
+        return False
+    fgraph.replace_all(list(zip(boundary, outs)), "fuse_elemwise")
+    emit(node=grp[-1], replaced=f"group[{len(grp)}]", replacement=outs[0].owner.op.display_name)
+    return True

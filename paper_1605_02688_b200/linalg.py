@@ -1,0 +1,91 @@
+"""Dot: rank-1/2 inner products (reference ``ops/linalg.py:13-123``).
+
+Lowered to ``tx_gemm``: operand transposes arrive as strides (DimShuffle
+views), and the native dispatcher chooses the tcgen05/TMEM TF32 tensor-core
+kernel for large fp32 problems, a memory-bound skinny kernel when one of
+M/N/K is tiny (the ``[B,10]`` softmax layers), and a SIMT kernel for float64.
+"""
+from __future__ import annotations
+
+from .dtypes import is_float, promote
+from .errors import ShapeMismatch, TypeMismatch
+from .graph import TensorType, Variable, apply
+from .op import DISCONNECTED, UNKNOWN_SHAPE, Op, register_op
+from .shaping import dimshuffle
+
+
+@register_op
+class Dot(Op):
+    name = "dot"
+
+    def infer_types(self, input_types):
+        a, b = input_types
+        if a.ndim not in (1, 2) or b.ndim not in (1, 2):
+            raise TypeMismatch(f"dot expects rank 1 or 2 operands, got {a.ndim} and {b.ndim}")
+        if a.ndim == 2 and b.ndim == 2:
+            bc = (a.broadcastable[0], b.broadcastable[1])
+        elif a.ndim == 2:
+            bc = (a.broadcastable[0],)
+        elif b.ndim == 2:
+            bc = (b.broadcastable[1],)
+        else:
+            bc = ()
+        return [TensorType(promote(a.dtype, b.dtype), bc)]
+
+    def check_runtime_shapes(self, node, shapes):
+        a, b = shapes
+        ka = a[-1]
+        kb = b[0] if len(b) >= 1 else 1
+        if ka != kb:
+            raise ShapeMismatch(f"dot: inner dimensions disagree ({tuple(a)} vs {tuple(b)})")
+
+    def infer_shape(self, node, input_shapes):
+        a, b = input_shapes
+        if a is UNKNOWN_SHAPE or b is UNKNOWN_SHAPE:
+            return [UNKNOWN_SHAPE]
+        an, bn = len(a), len(b)
+        if an == 2 and bn == 2:
+            return [(a[0], b[1])]
+        if an == 2:
+            return [(a[0],)]
+        if bn == 2:
+            return [(b[1],)]
+        return [()]
+
+    def grad(self, inputs, output_grads):
+        from .elemwise import sum_to_matching_shape
+        (a, b), (v,) = inputs, output_grads
+        an, bn = a.type.ndim, b.type.ndim
+        if an == 2 and bn == 2:
+            ga, gb = dot(v, dimshuffle(b, (1, 0))), dot(dimshuffle(a, (1, 0)), v)
+        elif an == 2:
+            ga = dimshuffle(v, (0, "x")) * dimshuffle(b, ("x", 0))
+            gb = dot(dimshuffle(a, (1, 0)), v)
+        elif bn == 2:
+            ga = dot(b, v)
+            gb = dimshuffle(a, (0, "x")) * dimshuffle(v, ("x", 0))
+        else:
+            ga, gb = v * b, v * a
+        return [DISCONNECTED if not is_float(x.type.dtype) else sum_to_matching_shape(g, x)
+                for x, g in ((a, ga), (b, gb))]
+
+    def rop(self, inputs, input_perturbations):
+        (a, b), (da, db) = inputs, input_perturbations
+        terms = ([dot(da, b)] if da is not None else []) + ([dot(a, db)] if db is not None else [])
+        if not terms:
+            return [None]
+        return [terms[0] if len(terms) == 1 else terms[0] + terms[1]]
+
+    def fold(self, values):
+        import numpy as np
+        a, b = values
+        if a.size * b.size > 1 << 16:
+            return None
+        return [np.asarray(np.dot(a, b))]
+
+    def lower(self, node, plan):
+        plan.emit_dot(node)
+
+
+def dot(a: Variable, b: Variable) -> Variable:
+    return apply(Dot(), [a, b])[0]

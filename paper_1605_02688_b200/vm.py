@@ -1,0 +1,957 @@
+"""The device VM: ``compile`` / ``CompiledFunction`` on B200.
+
+Replaces the reference linker/VM (``runtime.py:174-553``), which walks a
+Python thunk per node over NumPy arrays (~15 us of dispatch per node, SURVEY
+F7) and copies every input in and every output out.  Here a call is:
+
+  1. bind inputs (host arrays are copied H2D into plan-owned buffers; CUDA
+     tensors are bound by pointer) and device-resident shared storage;
+  2. look up / build a *step plan* for the (shapes, pointers, shared
+     versions) signature: concrete shape inference with the reference's
+     runtime checks, zero-copy views for DimShuffle, a liveness-planned arena
+     (exact-size block reuse plus in-place reuse for elementwise kernels), and
+     one launch closure per node calling the C ABI;
+  3. replay the plan as one CUDA graph (captured on first use);
+  4. copy the explicit outputs D2H.
+
+Updates are written on the device: when every other reader of a shared
+variable is scheduled before the update's producer (enforced with extra
+scheduling edges, like the reference's destroy-before-read edges at
+``runtime.py:305-317``) the producer writes straight into the shared storage;
+otherwise the new value is committed by a copy after all reads.  There is no
+host execution path.
+"""
+from __future__ import annotations
+
+import threading
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import codegen, native
+from .dtypes import ITEMSIZE, np_dtype
+from .elemwise import Composite, Elemwise, EwProgram
+from .errors import (NotSupported, ShapeMismatch, TexprError, TypeMismatch,
+                     UnderdeterminedOutputs)
+from .graph import Constant, FunctionGraph, Variable, clone_outputs
+from .op import UNKNOWN_SHAPE
+from .rewrite import RewriteContext, run_preset
+from .shared import SharedVariable, torch_dtype
+
+INF = 1 << 60
+ALIGN = 256
+
+
+def _torch():
+    import torch
+    return torch
+
+
+@dataclass(frozen=True)
+class UpdatePair:
+    shared: SharedVariable
+    new_value: Variable
+
+
+@dataclass
+class Profile:
+    call_count: int = 0
+    total_time: float = 0.0
+    node_calls: dict = field(default_factory=dict)
+    node_time: dict = field(default_factory=dict)
+    node_bytes: dict = field(default_factory=dict)
+    stage_times: dict = field(default_factory=dict)
+
+    def record_node(self, node_id, seconds, nbytes):
+        self.node_calls[node_id] = self.node_calls.get(node_id, 0) + 1
+        self.node_time[node_id] = self.node_time.get(node_id, 0.0) + seconds
+        self.node_bytes[node_id] = self.node_bytes.get(node_id, 0) + nbytes
+
+    def as_json(self, fn):
+        return {"call_count": self.call_count, "total_time": self.total_time,
+                "nodes": [{"id": n.id, "op": getattr(n.op, "display_name", n.op.name),
+                           "calls": self.node_calls.get(n.id, 0), "time": self.node_time.get(n.id, 0.0),
+                           "bytes": self.node_bytes.get(n.id, 0)} for n in fn.order],
+                "stages": [{"stage": s, "time": t} for s, t in sorted(self.stage_times.items())]}
+
+    def as_table(self, fn):
+        rows = [f"calls: {self.call_count}   total: {self.total_time:.6f}s",
+                f"{'op':<32}{'calls':>8}{'time (s)':>14}{'bytes':>14}"]
+        for e in sorted(self.as_json(fn)["nodes"], key=lambda e: -e["time"]):
+            rows.append(f"{e['op'][:31]:<32}{e['calls']:>8}{e['time']:>14.6f}{e['bytes']:>14}")
+        return "\n".join(rows)
+
+
+# ---------------------------------------------------------------------------
+# storage & layouts
+
+class Storage:
+    __slots__ = ("kind", "nbytes", "offset", "ptr", "last_use", "alias", "name")
+
+    def __init__(self, kind, nbytes=0, ptr=None, name=""):
+        self.kind = kind          # arena | input | shared | const
+        self.nbytes = nbytes
+        self.offset = None
+        self.ptr = ptr
+        self.last_use = -1
+        self.alias = None
+        self.name = name
+
+    def root(self):
+        s = self
+        while s.alias is not None:
+            s = s.alias
+        return s
+
+
+class Layout:
+    __slots__ = ("storage", "offset", "shape", "strides", "dtype")
+
+    def __init__(self, storage, offset, shape, strides, dtype):
+        self.storage, self.offset = storage, offset
+        self.shape, self.strides, self.dtype = tuple(shape), tuple(strides), dtype
+
+    @property
+    def numel(self):
+        n = 1
+        for s in self.shape:
+            n *= s
+        return n
+
+    def contiguous(self) -> bool:
+        exp = 1
+        for s, st in zip(reversed(self.shape), reversed(self.strides)):
+            if s != 1 and st != exp:
+                return False
+            exp *= s
+        return True
+
+
+def contiguous_strides(shape):
+    st, acc = [], 1
+    for s in reversed(shape):
+        st.append(acc)
+        acc *= s
+    return tuple(reversed(st))
+
+
+class ArenaAllocator:
+    """Offsets for step-lifetime buffers: exact-size reuse, else first-fit."""
+
+    def __init__(self):
+        self.top = 0
+        self.free: list[tuple[int, int]] = []
+
+    def alloc(self, nbytes):
+        n = max(ALIGN, (nbytes + ALIGN - 1) // ALIGN * ALIGN)
+        best = None
+        for i, (off, sz) in enumerate(self.free):
+            if sz == n:
+                best = i
+                break
+            if sz > n and (best is None or sz < self.free[best][1]):
+                best = i
+        if best is not None:
+            off, sz = self.free.pop(best)
+            if sz > n:
+                self.free.append((off + n, sz - n))
+            return off
+        off = self.top
+        self.top += n
+        return off
+
+    def release(self, off, nbytes):
+        n = max(ALIGN, (nbytes + ALIGN - 1) // ALIGN * ALIGN)
+        self.free.append((off, n))
+        self.free.sort()
+        merged = []
+        for o, s in self.free:
+            if merged and merged[-1][0] + merged[-1][1] == o:
+                merged[-1] = (merged[-1][0], merged[-1][1] + s)
+            else:
+                merged.append((o, s))
+        self.free = merged
+
+
+# ---------------------------------------------------------------------------
+# compile
+
+def compile(inputs, outputs, updates=(), preset="fast_run", allow_gc=True, nan_guard=None, include=(),
+            exclude=(), conv_impl="gemm", max_passes=8, *, cuda_graph=True, gemm_mode="auto",
+            data_parallel=None) -> "CompiledFunction":
+    """Build a callable computing ``outputs`` from ``inputs`` on the B200.
+
+    Signature and semantics follow reference ``runtime.py:174-259``; extra
+    keyword-only options: ``cuda_graph`` (capture/replay steps), ``gemm_mode``
+    ("auto" tcgen05 TF32 where eligible | "simt" exact fp32 products) and
+    ``data_parallel`` (a :class:`dp.DataParallel` group for synchronous
+    gradient allreduce).
+    """
+    if nan_guard is not None:
+        raise NotSupported("nan_guard is not implemented by the B200 VM")
+    single = isinstance(outputs, Variable)
+    outputs = [outputs] if single else list(outputs)
+    inputs = list(inputs)
+    ups = []
+    for u in updates:
+        pair = u if isinstance(u, UpdatePair) else UpdatePair(*u)
+        if not isinstance(pair.shared, SharedVariable):
+            raise TypeMismatch(f"update target {pair.shared!r} is not a shared variable")
+        if pair.shared.type != pair.new_value.type:
+            raise TypeMismatch(f"update for {pair.shared!r} has type {pair.new_value.type}, "
+                               f"expected {pair.shared.type}")
+        ups.append(pair)
+    uvals = [p.new_value for p in ups]
+    declared = {id(v) for v in inputs}
+    found, seen, stack = [], set(), list(outputs + uvals)
+    while stack:
+        v = stack.pop()
+        if v.id in seen or id(v) in declared:
+            continue
+        seen.add(v.id)
+        if v.owner is not None:
+            stack.extend(v.owner.inputs)
+        elif isinstance(v, SharedVariable):
+            found.append(v)
+        elif not isinstance(v, Constant):
+            raise UnderdeterminedOutputs(f"{v!r} is needed to compute the outputs but is neither an "
+                                         "input nor a shared variable")
+    found.sort(key=lambda v: v.id)
+    full = inputs + found
+    repl = {v: Variable(v.type, v.name) for v in full}
+    cloned, _ = clone_outputs(outputs + uvals, repl, copy_free=True)
+    fg = FunctionGraph([repl[v] for v in full], cloned)
+    fg.protected_inputs = {repl[v] for v in found}
+    ctx = RewriteContext(conv_impl=conv_impl, execution_bound=True, max_passes=max_passes)
+    _, log = run_preset(fg, preset, include=include, exclude=exclude, ctx=ctx)
+    return CompiledFunction(fg, len(outputs), [repl[v] for v in inputs], [(s, repl[s]) for s in found],
+                            [(p.shared, cloned[len(outputs) + i]) for i, p in enumerate(ups)],
+                            log, preset, single, allow_gc=allow_gc, cuda_graph=cuda_graph,
+                            gemm_mode=gemm_mode, data_parallel=data_parallel)
+
+
+function = compile
+
+
+class CompiledFunction:
+    def __init__(self, fgraph, n_outputs, input_vars, shared_bindings, updates, rewrite_log, preset,
+                 single_output=False, allow_gc=True, cuda_graph=True, gemm_mode="auto", data_parallel=None):
+        self.fgraph = fgraph
+        self.n_outputs = n_outputs
+        self.input_vars = list(input_vars)
+        self.shared_bindings = list(shared_bindings)
+        self.updates = list(updates)
+        self.rewrite_log = rewrite_log
+        self.preset = preset
+        self.single_output = single_output
+        self.allow_gc = allow_gc
+        self.cuda_graph = cuda_graph
+        self.gemm_mode = {"auto": native.GEMM_AUTO, "simt": native.GEMM_SIMT, "tc": native.GEMM_TC}[gemm_mode]
+        self.dp = data_parallel
+        self.profile = Profile(stage_times=dict(rewrite_log.stage_times))
+        self.nan_guard = None
+        self.has_lazy = False
+        self._lock = threading.Lock()
+        self._plans: dict = {}
+        self._consts: dict[int, object] = {}
+        self._stream = None
+        self.profile_nodes = False
+        self._direct, self.order = self._schedule()
+        self.thunks = {}
+
+    # -- scheduling --------------------------------------------------------
+    def _schedule(self):
+        """Toposort with update-in-place edges; returns (direct-write map, order)."""
+        g = self.fgraph
+        shared_var_of = {id(var): s for s, var in self.shared_bindings}
+        outputs_set = {v.id for v in g.outputs[: self.n_outputs]}
+        direct = {}
+        extra = {}
+        used_values = {}
+        for s, u in self.updates:
+            used_values[u.id] = used_values.get(u.id, 0) + 1
+        for s, u in self.updates:
+            var = next(v for sh, v in self.shared_bindings if sh is s)
+            p = u.owner
+            if p is None or used_values[u.id] > 1 or u.id in outputs_set:
+                continue
+            if getattr(p.op, "view_capable", False) or not hasattr(p.op, "lower"):
+                continue
+            # the shared value (or a view of it) must not be a returned output
+            # nor another update's value (those read the old value after the step)
+            if _aliases_output(g, var, self.n_outputs):
+                continue
+            if any(u2 is not u and (u2 is var or _is_view_of(u2, var)) for _, u2 in self.updates):
+                continue
+            readers = _readers_through_views(g, var)
+            reads_self = p in readers
+            if reads_self:
+                if not isinstance(p.op, (Elemwise, Composite)):
+                    continue
+                if any(x is not var and _is_view_of(x, var) for x in p.inputs):
+                    continue
+            others = [r for r in readers if r is not p]
+            trial = dict(extra)
+            trial[p] = set(trial.get(p, set())) | set(others)
+            try:
+                g.toposort(extra_deps=trial)
+            except TexprError:
+                continue
+            extra = trial
+            direct[u.id] = (s, var)
+        order = g.toposort(extra_deps=extra or None)
+        return direct, order
+
+    # -- calling -------------------------------------------------------------
+    def __call__(self, *values):
+        with self._lock:
+            return self._call(values, device_out=False)
+
+    def call_device(self, *values, sync: bool = False):
+        """Run with CUDA-tensor (or host) inputs; returns CUDA tensors that
+        alias internal buffers until the next call.  No host sync unless asked."""
+        with self._lock:
+            return self._call(values, device_out=True, sync=sync)
+
+    @property
+    def output_vars(self):
+        return self.fgraph.outputs[: self.n_outputs]
+
+    def thunk_count(self, node_id):
+        return self.profile.node_calls.get(node_id, 0)
+
+    def _lib(self):
+        lib = native.device_library()
+        if self._stream is None:
+            t = _torch()
+            self._tstream = t.cuda.Stream()
+            self._stream = self._tstream.cuda_stream
+        return lib
+
+    def _call(self, values, device_out, sync=True):
+        t0 = time.perf_counter()
+        if len(values) != len(self.input_vars):
+            raise TypeMismatch(f"function expects {len(self.input_vars)} inputs, got {len(values)}")
+        lib = self._lib()
+        t = _torch()
+        binds = []
+        for var, val in zip(self.input_vars, values):
+            binds.append(_bind_input(var, val))
+        shared_state = []
+        for s, var in self.shared_bindings:
+            dev = s.device_tensor()
+            why = var.type.shape_matches(np_dtype(var.type.dtype), tuple(dev.shape))
+            if why is not None:
+                raise TypeMismatch(f"shared {s!r} holds a nonconforming value: {why}")
+            shared_state.append((dev.data_ptr(), tuple(dev.shape), s.version))
+        key = (tuple((b.shape, b.dev_ptr) for b in binds), tuple(shared_state))
+        plan = self._plans.get(key)
+        if plan is None:
+            plan = StepPlan(self, lib, binds, key)
+            self._plans[key] = plan
+        stream = self._stream
+        if any(b.dev_ptr is not None for b in binds) or device_out:
+            self._tstream.wait_stream(t.cuda.current_stream())
+        plan.upload_inputs(binds, stream)
+        if self.profile_nodes:
+            plan.run_profiled(stream, self.profile)
+        else:
+            plan.run(stream)
+            for n in self.order:
+                self.profile.node_calls[n.id] = self.profile.node_calls.get(n.id, 0) + 1
+        if device_out:
+            outs = plan.device_outputs()
+            t.cuda.current_stream().wait_stream(self._tstream)
+            if sync:
+                lib.stream_sync(stream)
+        else:
+            outs = plan.download_outputs(stream)
+        plan.check_flags()
+        plan.finish_updates()
+        self.profile.call_count += 1
+        self.profile.total_time += time.perf_counter() - t0
+        return outs[0] if self.single_output else outs
+
+    # -- copying (reference runtime.py:512-553) ------------------------------
+    def copy(self, swap=None, carry_updates=True, share_intermediate_storage=False):
+        swap = dict(swap or {})
+        for old, new in swap.items():
+            if old.type != new.type:
+                raise TypeMismatch(f"swap for {old!r} has type {new.type}, expected {old.type}")
+        twin = CompiledFunction.__new__(CompiledFunction)
+        twin.__dict__.update(self.__dict__)
+        twin.shared_bindings = [(swap.get(s, s), v) for s, v in self.shared_bindings]
+        twin.updates = [(swap.get(s, s), v) for s, v in self.updates] if carry_updates else []
+        twin._direct = {k: (swap.get(s, s), v) for k, (s, v) in self._direct.items()} if carry_updates else {}
+        twin.profile = Profile(stage_times=dict(self.profile.stage_times))
+        twin._lock = threading.Lock()
+        twin._plans = {}
+        twin._stream = None
+        return twin
+
+
+def _is_view_of(x, base) -> bool:
+    while x.owner is not None and getattr(x.owner.op, "view_capable", False):
+        x = x.owner.inputs[0]
+        if x is base:
+            return True
+    return False
+
+
+def _readers_through_views(g, var):
+    out, stack = set(), [var]
+    while stack:
+        v = stack.pop()
+        for c in g.node_clients(v):
+            if getattr(c.op, "view_capable", False):
+                stack.extend(c.outputs)
+            else:
+                out.add(c)
+    return out
+
+
+def _aliases_output(g, var, n_outputs):
+    outs = g.outputs[:n_outputs]
+    return any(o is var or _is_view_of(o, var) for o in outs)
+
+
+# ---------------------------------------------------------------------------
+# input binding
+
+class _Bind:
+    __slots__ = ("shape", "dev_ptr", "host", "tensor", "dtype")
+
+
+def _bind_input(var, val) -> _Bind:
+    b = _Bind()
+    b.dtype = var.type.dtype
+    t = None
+    try:
+        import torch
+        if isinstance(val, torch.Tensor):
+            t = val
+    except ImportError:  # pragma: no cover
+        pass
+    if t is not None:
+        want = torch_dtype(var.type.dtype)
+        if t.dtype != want:
+            raise TypeMismatch(f"value for input {var!r} has dtype {t.dtype}, expected {var.type.dtype}")
+        why = var.type.shape_matches(np_dtype(var.type.dtype), tuple(t.shape))
+        if why is not None:
+            raise TypeMismatch(f"value for input {var!r} rejected: {why}")
+        b.shape = tuple(t.shape)
+        if t.is_cuda:
+            if not t.is_contiguous():
+                t = t.contiguous()
+            b.dev_ptr, b.host, b.tensor = t.data_ptr(), None, t
+        else:
+            b.dev_ptr, b.host, b.tensor = None, t.contiguous(), None
+        return b
+    try:
+        arr = np.array(val, dtype=np_dtype(var.type.dtype), copy=None)
+    except (ValueError, TypeError) as exc:
+        raise TypeMismatch(f"bad value for input {var!r}: {exc}") from exc
+    why = var.type.value_matches(arr)
+    if why is not None:
+        raise TypeMismatch(f"value for input {var!r} rejected: {why}")
+    if var.type.dtype == "bool":
+        arr = arr.astype(np.uint8)
+    b.shape, b.dev_ptr, b.tensor = arr.shape, None, None
+    b.host = np.ascontiguousarray(arr)
+    return b
+
+
+# ---------------------------------------------------------------------------
+# the step plan
+
+class StepPlan:
+    def __init__(self, fn: CompiledFunction, lib, binds, key):
+        self.fn, self.lib = fn, lib
+        t = _torch()
+        g = fn.fgraph
+        self.lay: dict[int, Layout] = {}
+        self.keep = []                       # torch tensors that must stay alive
+        self.in_storage = []                 # (Storage, nbytes) for host-bound inputs
+        self.ws: dict[int, tuple] = {}       # node id -> (Storage, nbytes)
+        self.flag = None
+        order = fn.order
+        pos = {n.id: i for i, n in enumerate(order)}
+        n_steps = len(order)
+
+        # ---- bound storages: inputs, shared, constants
+        for var, b in zip(fn.input_vars, binds):
+            nb = int(np.prod(b.shape, dtype=np.int64)) * ITEMSIZE[var.type.dtype]
+            if b.dev_ptr is not None:
+                st = Storage("input", nb, ptr=b.dev_ptr, name=var.name or "")
+            else:
+                st = Storage("input", nb, name=var.name or "")
+                buf = t.empty(max(nb, 1), dtype=t.uint8, device="cuda")
+                self.keep.append(buf)
+                st.ptr = buf.data_ptr()
+                self.in_storage.append((st, nb))
+            self.lay[var.id] = Layout(st, 0, b.shape, contiguous_strides(b.shape), var.type.dtype)
+        in_ids = {v.id for v in fn.input_vars}
+        self.host_inputs = [(st, nb) for st, nb in self.in_storage]
+        self.shared_storage = {}
+        for s, var in fn.shared_bindings:
+            if var.id in self.lay:  # also declared as an explicit input
+                continue
+            dev = s.device_tensor()
+            st = Storage("shared", dev.numel() * dev.element_size(), ptr=dev.data_ptr(), name=s.name or "")
+            self.shared_storage[id(s)] = st
+            self.lay[var.id] = Layout(st, 0, tuple(dev.shape), contiguous_strides(tuple(dev.shape)), var.type.dtype)
+        for n in order:
+            for x in n.inputs:
+                if isinstance(x, Constant) and x.id not in self.lay:
+                    self.lay[x.id] = self._const_layout(x)
+
+        # ---- shapes and layouts, node by node
+        direct = fn._direct
+        self.pending_outputs = {}
+        for n in order:
+            ins = [self.lay[x.id] for x in n.inputs]
+            shapes = [l.shape for l in ins]
+            n.op.check_runtime_shapes(n, shapes)
+            outs = n.op.infer_shape(n, shapes)
+            for o, s in zip(n.outputs, outs):
+                if s is UNKNOWN_SHAPE or any(d is None for d in s):
+                    raise NotSupported(f"cannot infer the runtime shape of {o!r} ({n.op.name})")
+            if getattr(n.op, "view_capable", False):
+                base = ins[0]
+                shape, strides, off = n.op.view_layout(n, [(base.shape, base.strides, base.offset)])
+                self.lay[n.outputs[0].id] = Layout(base.storage, off, shape, strides, n.outputs[0].type.dtype)
+                continue
+            for o, s in zip(n.outputs, outs):
+                s = tuple(int(d) for d in s)
+                d = direct.get(o.id)
+                if d is not None:
+                    sh, var = d
+                    slay = self.lay.get(var.id)
+                    if slay is not None and slay.shape == s and slay.storage.kind == "shared":
+                        self.lay[o.id] = Layout(slay.storage, 0, s, contiguous_strides(s), o.type.dtype)
+                        continue
+                nb = int(np.prod(s, dtype=np.int64)) * ITEMSIZE[o.type.dtype]
+                st = Storage("arena", nb, name=getattr(n.op, "display_name", n.op.name))
+                self.lay[o.id] = Layout(st, 0, s, contiguous_strides(s), o.type.dtype)
+            wsb = self._workspace_bytes(n)
+            if wsb:
+                self.ws[n.id] = (Storage("arena", wsb, name="ws"), wsb)
+
+        # ---- tail: output snapshots, contiguous copies, update commits
+        written = set()
+        self.commits = []      # (src Layout, dst Layout)
+        self.late_updates = [] # (shared, Layout) for shape-changing updates
+        for s, u in fn.updates:
+            var = next(v for sh, v in fn.shared_bindings if sh is s)
+            ul = self.lay[u.id] if u.id in self.lay else self._const_layout(u)
+            slay = self.lay.get(var.id)
+            if slay is not None and ul.storage is slay.storage and ul.offset == 0:
+                written.add(id(slay.storage))
+                continue  # written in place (or identity update)
+            if slay is not None and ul.shape == slay.shape:
+                self.commits.append((ul, slay))
+                written.add(id(slay.storage))
+            else:
+                self.late_updates.append((s, ul))
+        self.tail_copies = []  # (src, dst) executed before commits
+        self.out_lays = []
+        for v in g.outputs[: fn.n_outputs]:
+            if isinstance(v, Constant) and v.id not in self.lay:
+                self.out_lays.append(("const", v.value))
+                continue
+            lay = self.lay[v.id]
+            if not lay.contiguous() or id(lay.storage) in written or lay.offset != 0:
+                nb = lay.numel * ITEMSIZE[lay.dtype]
+                dst = Layout(Storage("arena", nb, name="out"), 0, lay.shape, contiguous_strides(lay.shape), lay.dtype)
+                self.tail_copies.append((lay, dst))
+                lay = dst
+            self.out_lays.append(("dev", lay))
+        # a commit must not read storage that this call overwrites: snapshot it
+        fixed = []
+        for src, dst in self.commits:
+            if id(src.storage) in written:
+                nb = src.numel * ITEMSIZE[src.dtype]
+                snap = Layout(Storage("arena", nb, name="snap"), 0, src.shape, contiguous_strides(src.shape), src.dtype)
+                self.tail_copies.append((src, snap))
+                src = snap
+            fixed.append((src, dst))
+        self.commits = fixed
+
+        # ---- liveness over storages
+        def touch(lay_, step):
+            r = lay_.storage
+            r.last_use = max(r.last_use, step)
+
+        for i, n in enumerate(order):
+            for x in n.inputs:
+                touch(self.lay[x.id], i)
+        end = n_steps
+        for src, dst in self.tail_copies:
+            touch(src, end)
+            touch(dst, INF)
+        for src, dst in self.commits:
+            touch(src, end + 1)
+        for _, ul in self.late_updates:
+            touch(ul, INF)
+        for kind, lay in self.out_lays:
+            if kind == "dev":
+                touch(lay, INF)
+        for v in g.outputs:
+            if v.id in self.lay:
+                touch(self.lay[v.id], INF)
+
+        # ---- arena allocation with in-place reuse for elementwise kernels
+        alloc = ArenaAllocator()
+        live_at: dict[int, list] = {}
+
+        def assign(st, step=INF):
+            if st.kind != "arena" or st.offset is not None or st.alias is not None:
+                return
+            st.offset = alloc.alloc(st.nbytes)
+            if st.last_use < INF and step < INF:
+                live_at.setdefault(max(st.last_use, step), []).append(st)
+
+        for i, n in enumerate(order):
+            if getattr(n.op, "view_capable", False):
+                continue
+            taken = set()
+            inplace_ok = isinstance(n.op, (Elemwise, Composite))
+            for o in n.outputs:
+                ol = self.lay[o.id]
+                st = ol.storage
+                if st.kind != "arena" or st.offset is not None:
+                    continue
+                if inplace_ok:
+                    for x in n.inputs:
+                        xl = self.lay[x.id]
+                        xs = xl.storage
+                        if (xs.kind == "arena" and xs.alias is None and xs.offset is not None
+                                and id(xs) not in taken and xs.last_use == i and xl.offset == 0
+                                and xl.shape == ol.shape and xl.dtype == ol.dtype and xl.contiguous()
+                                and xs.nbytes == st.nbytes):
+                            st.alias = xs
+                            taken.add(id(xs))
+                            xs.last_use = max(xs.last_use, st.last_use)
+                            lst = live_at.get(i)
+                            if lst and xs in lst:
+                                lst.remove(xs)
+                            if xs.last_use < INF:
+                                live_at.setdefault(xs.last_use, []).append(xs)
+                            break
+                if st.alias is None:
+                    assign(st, i)
+            w = self.ws.get(n.id)
+            if w is not None:
+                w[0].offset = alloc.alloc(w[1])
+                alloc.release(w[0].offset, w[1])
+            for st in live_at.pop(i, []):
+                alloc.release(st.offset, st.nbytes)
+        for src, dst in self.tail_copies:
+            assign(dst.storage)
+        # any arena storage not yet placed (e.g. unused outputs)
+        for lay in list(self.lay.values()):
+            assign(lay.storage.root())
+        if any(codegen.has_int_div(getattr(n.op, "program", None) or EwProgram.single(n.op.kernel, [x.type.dtype for x in n.inputs]))
+               for n in order if isinstance(n.op, (Elemwise, Composite))):
+            self.flag = Storage("arena", 4, name="flag")
+            self.flag.offset = alloc.alloc(4)
+        self.arena_bytes = alloc.top
+        self.arena = t.empty(max(alloc.top, ALIGN), dtype=t.uint8, device="cuda")
+        base = self.arena.data_ptr()
+        for lay in list(self.lay.values()) + [d for _, d in self.tail_copies]:
+            r = lay.storage.root()
+            if r.kind == "arena" and r.ptr is None:
+                r.ptr = base + r.offset
+        for st, _ in self.ws.values():
+            st.ptr = base + st.offset
+        if self.flag is not None:
+            self.flag.ptr = base + self.flag.offset
+
+        # ---- launch closures
+        self.launches = []  # (node or None, fn)
+        self._cur = None
+        for n in order:
+            if getattr(n.op, "view_capable", False):
+                continue
+            self._cur = n
+            n.op.lower(n, self)
+        self._cur = None
+        for src, dst in self.tail_copies:
+            self._emit_copy(src, dst)
+        for src, dst in self.commits:
+            self._emit_copy(src, dst)
+        self.graph = None
+        self.captured = False
+        self._pinned_out = None
+
+    # -- helpers used by op.lower -------------------------------------------
+    def _const_layout(self, c: Constant) -> Layout:
+        cache = self.fn._consts
+        ent = cache.get(c.id)
+        if ent is None:
+            t = _torch()
+            arr = np.ascontiguousarray(c.value)
+            if c.type.dtype == "bool":
+                arr = arr.astype(np.uint8)
+            dev = t.from_numpy(arr.copy()).to("cuda") if arr.size else t.empty(1, dtype=t.uint8, device="cuda")
+            ent = dev
+            cache[c.id] = ent
+        st = Storage("const", c.value.nbytes, ptr=ent.data_ptr())
+        return Layout(st, 0, c.value.shape, contiguous_strides(c.value.shape), c.type.dtype)
+
+    def layout(self, var) -> Layout:
+        return self.lay[var.id]
+
+    def tx(self, var_or_layout, shape=None, strides=None) -> native.TxTensor:
+        lay = var_or_layout if isinstance(var_or_layout, Layout) else self.lay[var_or_layout.id]
+        r = lay.storage.root()
+        ptr = r.ptr + lay.offset * ITEMSIZE[lay.dtype]
+        return native.make_tensor(ptr, lay.dtype, lay.shape if shape is None else shape,
+                                  lay.strides if strides is None else strides)
+
+    def workspace(self, node):
+        w = self.ws.get(node.id)
+        if w is None:
+            return None, 0
+        return w[0].ptr, w[1]
+
+    def add_launch(self, fn):
+        self.launches.append((self._cur, fn))
+
+    def _workspace_bytes(self, n) -> int:
+        from .linalg import Dot
+        from .reduce import _Reduce
+        if isinstance(n.op, _Reduce):
+            x = self._tx_noptr(self.lay[n.inputs[0].id])
+            mask = sum(1 << a for a in n.op.axes)
+            if not mask:
+                return 0
+            return self.lib.reduce_workspace(n.op.tx_code, x, mask)
+        if isinstance(n.op, Dot) or hasattr(n.op, "gemm_operands"):
+            a, b, c = self._dot_views(n, noptr=True)
+            return self.lib.gemm_workspace(a, b, c, self.fn.gemm_mode)
+        return 0
+
+    def _tx_noptr(self, lay, shape=None, strides=None):
+        return native.make_tensor(16, lay.dtype, lay.shape if shape is None else shape,
+                                  lay.strides if strides is None else strides)
+
+    # -- emitters ---------------------------------------------------------------
+    def emit_elementwise(self, node, program: EwProgram):
+        lib = self.lib
+        h = codegen.CACHE.get(lib, program)
+        ops = [self.tx(o) for o in node.outputs] + [self.tx(x) for x in node.inputs]
+        arr = (native.TxTensor * len(ops))(*ops)
+        n_out, n_in = len(node.outputs), len(node.inputs)
+        flag = self.flag.ptr if (self.flag is not None and codegen.has_int_div(program)) else None
+        f = lib.lib.tx_ew_launch
+
+        def launch(stream):
+            lib.check(f(h, n_out, n_in, arr, flag, stream))
+        self.add_launch(launch)
+
+    def emit_reduce(self, node, code, axes):
+        from .reduce import TX_ARGMAX_ONEHOT
+        lib = self.lib
+        x = self.tx(node.inputs[0])
+        y = self.tx(node.outputs[0])
+        mask = 0
+        for a in axes:
+            mask |= 1 << a
+        if code == TX_ARGMAX_ONEHOT and mask == 0:
+            self.emit_elementwise(node, EwProgram([node.inputs[0].type.dtype], [(node.outputs[0].type.dtype, 1)],
+                                                  [("second", [("in", 0), ("const", 0)], node.outputs[0].type.dtype)],
+                                                  [("node", 0)]))
+            return
+        ws, wsb = self.workspace(node)
+        f = lib.lib.tx_reduce
+
+        def launch(stream):
+            lib.check(f(code, x, mask, y, ws, wsb, stream))
+        self.add_launch(launch)
+
+    def _dot_views(self, node, noptr=False):
+        a, b = node.inputs
+        c = node.outputs[0]
+        la, lb, lc = self.lay[a.id], self.lay[b.id], self.lay[c.id]
+        mk = self._tx_noptr if noptr else self.tx
+        # promote rank-1 operands to matrices
+        if len(la.shape) == 2:
+            A = mk(la)
+        else:
+            A = mk(la, (1, la.shape[0]), (0, la.strides[0]))
+        if len(lb.shape) == 2:
+            B = mk(lb)
+        else:
+            B = mk(lb, (lb.shape[0], 1), (lb.strides[0], 0))
+        M = A.shape[0]
+        N = B.shape[1]
+        if len(lc.shape) == 2:
+            C = mk(lc)
+        elif len(lc.shape) == 1:
+            C = mk(lc, (M, N), (lc.strides[0], 0) if len(la.shape) == 2 else (0, lc.strides[0]))
+        else:
+            C = mk(lc, (1, 1), (1, 1))
+        return A, B, C
+
+    def emit_dot(self, node, epilogue=None):
+        lib = self.lib
+        A, B, C = self._dot_views(node)
+        ws, wsb = self.workspace(node)
+        mode = self.fn.gemm_mode
+        epi = epilogue if epilogue is not None else native.TxEpilogue()
+        f = lib.lib.tx_gemm
+
+        def launch(stream):
+            lib.check(f(A, B, C, epi, mode, ws, wsb, stream))
+        self.add_launch(launch)
+
+    def _emit_copy(self, src: Layout, dst: Layout):
+        lib = self.lib
+        s, d = self.tx(src), self.tx(dst)
+
+        def launch(stream):
+            lib.copy(s, d, stream)
+        self.launches.append((None, launch))
+
+    # -- execution --------------------------------------------------------------
+    def upload_inputs(self, binds, stream):
+        hosts = [b for b in binds if b.dev_ptr is None]
+        for (st, nb), b in zip(self.host_inputs, hosts):
+            if nb == 0:
+                continue
+            if isinstance(b.host, np.ndarray):
+                self.lib.memcpy(st.ptr, b.host.ctypes.data, nb, 0, stream)
+            else:  # torch CPU tensor (pinned or not)
+                self.lib.memcpy(st.ptr, b.host.data_ptr(), nb, 0, stream)
+        self._host_refs = hosts  # keep sources alive until the stream is synced
+
+    def _launch_all(self, stream):
+        if self.flag is not None:
+            self.lib.memset(self.flag.ptr, 0, 4, stream)
+        for _, fn in self.launches:
+            fn(stream)
+
+    def run(self, stream):
+        if not self.fn.cuda_graph:
+            self._launch_all(stream)
+            return
+        if self.graph is None:
+            # first call runs eagerly (surfaces errors with a clean stack), then capture
+            self._launch_all(stream)
+            self.lib.graph_begin(stream)
+            try:
+                self._launch_all(stream)
+            except BaseException:
+                try:
+                    self.lib.graph_end(stream)
+                except Exception:
+                    pass
+                raise
+            self.graph = self.lib.graph_end(stream)
+            return
+        self.lib.graph_launch(self.graph, stream)
+
+    def run_profiled(self, stream, profile):
+        lib = self.lib
+        if self.flag is not None:
+            lib.memset(self.flag.ptr, 0, 4, stream)
+        ev = [lib.event_create() for _ in range(2)]
+        for node, fn in self.launches:
+            lib.event_record(ev[0], stream)
+            fn(stream)
+            lib.event_record(ev[1], stream)
+            lib.stream_sync(stream)
+            if node is not None:
+                nb = sum(self.lay[o.id].numel * ITEMSIZE[o.type.dtype] for o in node.outputs)
+                profile.record_node(node.id, lib.elapsed_ms(ev[0], ev[1]) * 1e-3, nb)
+        for n in self.fn.order:
+            if getattr(n.op, "view_capable", False):
+                profile.record_node(n.id, 0.0, 0)
+
+    def download_outputs(self, stream):
+        t = _torch()
+        if self._pinned_out is None:
+            self._pinned_out = []
+            for kind, lay in self.out_lays:
+                if kind == "dev":
+                    nb = lay.numel * ITEMSIZE[lay.dtype]
+                    self._pinned_out.append(t.empty(max(nb, 1), dtype=t.uint8, pin_memory=True))
+                else:
+                    self._pinned_out.append(None)
+        for (kind, lay), pin in zip(self.out_lays, self._pinned_out):
+            if kind == "dev":
+                nb = lay.numel * ITEMSIZE[lay.dtype]
+                if nb:
+                    self.lib.memcpy(pin.data_ptr(), self.tx(lay).data, nb, 1, stream)
+        self.lib.stream_sync(stream)
+        self._host_refs = None
+        outs = []
+        for (kind, lay), pin in zip(self.out_lays, self._pinned_out):
+            if kind == "const":
+                outs.append(np.array(lay, copy=True))
+                continue
+            nb = lay.numel * ITEMSIZE[lay.dtype]
+            raw = pin.numpy()[:nb]
+            dt = np.uint8 if lay.dtype == "bool" else np_dtype(lay.dtype)
+            arr = raw.view(dt).reshape(lay.shape).copy()
+            if lay.dtype == "bool":
+                arr = arr.astype(np.bool_)
+            outs.append(arr)
+        return outs
+
+    def device_outputs(self):
+        t = _torch()
+        outs = []
+        for kind, lay in self.out_lays:
+            if kind == "const":
+                outs.append(t.from_numpy(np.array(lay)).to("cuda"))
+                continue
+            outs.append(_torch_view(lay, self.tx(lay).data))
+        return outs
+
+    def check_flags(self):
+        if self.flag is None:
+            return
+        t = _torch()
+        self.lib.stream_sync(self.fn._stream)
+        v = t.empty(1, dtype=t.int32, pin_memory=True)
+        self.lib.memcpy(v.data_ptr(), self.flag.ptr, 4, 1, self.fn._stream)
+        self.lib.stream_sync(self.fn._stream)
+        if int(v.item()):
+            raise ZeroDivisionError("integer division by zero")
+
+    def finish_updates(self):
+        if not self.late_updates:
+            return
+        t = _torch()
+        self.lib.stream_sync(self.fn._stream)
+        for s, ul in self.late_updates:
+            view = _torch_view(ul, self.tx(ul).data)
+            with s._lock:
+                s._dev = view.clone()
+                s.version += 1
+        self.fn._plans.clear()
+
+
+def _torch_view(lay: Layout, ptr: int):
+    """A torch tensor aliasing device memory at ``ptr`` with ``lay``'s geometry."""
+    t = _torch()
+    dt = torch_dtype(lay.dtype)
+    if lay.numel == 0:
+        return t.empty(lay.shape, dtype=dt, device="cuda")
+    span = 1 + sum((s - 1) * st for s, st in zip(lay.shape, lay.strides))
+    return _wrap_device_pointer(ptr, span, dt).as_strided(lay.shape, lay.strides)
+
+
+def _wrap_device_pointer(ptr, numel, dtype):
+    """Wrap raw device memory (owned by a plan's arena / shared storage) as a
+    torch tensor via __cuda_array_interface__ (no copy)."""
+    t = _torch()
+    typestr = {t.float32: "<f4", t.float64: "<f8", t.int32: "<i4", t.int64: "<i8", t.uint8: "|u1"}[dtype]
+
+    class _CAI:
+        __cuda_array_interface__ = {"shape": (int(numel),), "typestr": typestr, "data": (int(ptr), False),
+                                    "version": 3, "strides": None}
+    return t.as_tensor(_CAI(), device="cuda")

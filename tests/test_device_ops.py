@@ -1,0 +1,217 @@
+"""Per-op parity of the B200 kernels against the reference's golden vectors
+and the CPU oracle.  Tolerances:
+  - add/sub/mul/div/neg/sqr/sqrt/maximum/second/switch, comparisons, isnan,
+    max, argmax (both forms), integer ops: bit-exact;
+  - exp/log/log1p/tanh/sigmoid/pow: |d-o| <= 1e-6 + 1e-5|o| (f32), CUDA libm
+    vs NumPy SIMD differ by ulps;
+  - sum: |d-o| <= 2e-6 * sum|x|;
+  - TF32 GEMM: |C-C_o| <= 2^-9 (|A||B|)_ij + 1e-6 (operands rounded to TF32);
+    CUDA-core GEMM paths: |C-C_o| <= 1e-5 (|A||B|)_ij + 1e-6.
+"""
+import numpy as np
+import pytest
+
+import paper_1605_02688_b200 as T
+from oracle import texpr_numpy as O
+from paper_1605_02688_b200.elemwise import make
+from paper_1605_02688_b200.errors import ShapeMismatch
+
+pytestmark = pytest.mark.gpu
+
+EXACT = ("add", "sub", "mul", "div", "neg", "sqr", "sqrt", "maximum", "second", "lt", "gt", "le", "ge", "eq",
+         "neq", "isnan")
+TRANSC = ("exp", "log", "log1p", "tanh", "sigmoid", "pow")
+
+
+def close(got, want, rtol, atol):
+    got, want = np.asarray(got), np.asarray(want)
+    assert got.shape == want.shape
+    nan_g, nan_w = np.isnan(got), np.isnan(want)
+    assert np.array_equal(nan_g, nan_w)
+    ok = ~nan_w
+    inf = np.isinf(want) & ok
+    assert np.array_equal(got[inf], want[inf])
+    fin = ok & ~inf
+    np.testing.assert_allclose(got[fin], want[fin], rtol=rtol, atol=atol)
+
+
+def exact(got, want):
+    got, want = np.asarray(got), np.asarray(want)
+    assert got.shape == want.shape, (got.shape, want.shape)
+    if got.dtype.kind == "f":
+        assert np.array_equal(np.isnan(got), np.isnan(want))
+        m = ~np.isnan(want)
+        assert np.array_equal(got[m], want[m])
+    else:
+        assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("dt", ["float32", "float64"])
+def test_elementwise_kernels(golden, dt):
+    a, b, c = golden[f"ew_{dt}_a"], golden[f"ew_{dt}_b"], golden[f"ew_{dt}_c"]
+    va, vb, vc = T.vector("a", dtype=dt), T.vector("b", dtype=dt), T.vector("c", dtype="bool")
+    tol = (1e-5, 1e-6) if dt == "float32" else (1e-12, 1e-14)
+    for k in EXACT + ("pow",):
+        if k in ("neg", "sqr", "sqrt", "isnan"):
+            got = T.compile([va], make(k, [va]), preset="none")(a)
+        else:
+            got = T.compile([va, vb], make(k, [va, vb]), preset="none")(a, b)
+        want = golden[f"ew_{dt}_{k}"]
+        if k in EXACT:
+            exact(got, want)
+        else:
+            close(got, want, *tol)
+    for k in TRANSC:
+        if k == "pow":
+            continue
+        got = T.compile([va], make(k, [va]), preset="none")(a)
+        close(got, golden[f"ew_{dt}_{k}"], *tol)
+    exact(T.compile([vc, va, vb], make("switch", [vc, va, vb]), preset="none")(c, a, b), golden[f"ew_{dt}_switch"])
+
+
+def test_integer_kernels_and_zero_division(golden):
+    a, b = golden["ew_int64_a"], golden["ew_int64_b"]
+    va, vb = T.vector("a", dtype="int64"), T.vector("b", dtype="int64")
+    for k in ("add", "sub", "mul", "div", "maximum", "lt", "eq"):
+        exact(T.compile([va, vb], make(k, [va, vb]), preset="none")(a, b), golden[f"ew_int64_{k}"])
+    f = T.compile([va, vb], make("div", [va, vb]), preset="none")
+    with pytest.raises(ZeroDivisionError):
+        f(a, np.zeros_like(b))
+
+
+def test_broadcast_composite(golden):
+    vX = T.matrix("X", dtype="float32")
+    vr = T.vector("r", dtype="float32")
+    vcol = T.matrix("col", dtype="float32", broadcastable=(False, True))
+    f = T.compile([vX, vr, vcol], T.tanh(vX + vr) * vcol - vr)
+    close(f(golden["bc_X"], golden["bc_r"], golden["bc_col"]), golden["bc_out"], 1e-5, 1e-6)
+
+
+def test_config2_expression_fused(golden):
+    r7 = np.random.default_rng(7)
+    ins = [r7.standard_normal(40000, dtype=np.float32) for _ in range(4)]
+    a, b, c, d = (T.vector(s, dtype="float32") for s in "abcd")
+    f = T.compile([a, b, c, d], T.sigmoid(a * b + c) ** 2 - d)
+    assert sum(1 for n in f.order if n.op.name == "composite") == 1 and len(f.order) == 1
+    close(f(*ins), golden["cfg2_fused"], 1e-5, 1e-6)
+    # unaligned / odd length exercises the scalar tail and the non-vector path
+    g = f(*[x[1:40000 - 3] for x in ins])
+    close(g, golden["cfg2_fused"][1:40000 - 3], 1e-5, 1e-6)
+
+
+@pytest.mark.parametrize("ax", [(0,), (1,), (0, 1)])
+def test_reductions_golden(golden, ax):
+    X = golden["red_X"]
+    v = T.matrix("R", dtype="float32")
+    tag = "".join(map(str, ax))
+    f = T.compile([v], [T.sum(v, axis=ax), T.max(v, axis=ax), T.argmax_onehot(v, axis=ax)])
+    s, m, oh = f(X)
+    exact(m, golden[f"red_max_{tag}"])
+    exact(oh, golden[f"red_argmax_onehot_{tag}"])
+    want = golden[f"red_sum_{tag}"]
+    close(s, want, 0, 2e-6 * float(np.nansum(np.abs(X))))
+
+
+@pytest.mark.parametrize("ax", [(0, 2), (1,), (0, 1, 2), (2,), (0,)])
+def test_reductions_rank3_f64(golden, ax):
+    X = golden["red3_X"]
+    v = T.tensor3("R3", dtype="float64")
+    tag = "".join(map(str, ax))
+    s, m, oh = T.compile([v], [T.sum(v, axis=ax), T.max(v, axis=ax), T.argmax_onehot(v, axis=ax)])(X)
+    exact(m, golden[f"red3_max_{tag}"])
+    exact(oh, golden[f"red3_argmax_onehot_{tag}"])
+    close(s, golden[f"red3_sum_{tag}"], 1e-12, 1e-12)
+
+
+@pytest.mark.parametrize("shape", [(4099, 3001), (3, 70000), (70000, 3), (1, 1), (1, 200000), (33, 600)])
+def test_reduction_forms(shape, rng):
+    """ROW / split-ROW / warp-ROW / COL(+splits) / degenerate shapes."""
+    X = rng.standard_normal(shape).astype(np.float32)
+    X.flat[rng.integers(0, X.size, 3)] = X.max() + 1  # ties at the max
+    v = T.matrix("X", dtype="float32")
+    for ax in ((0,), (1,), (0, 1)):
+        f = T.compile([v], [T.sum(v, axis=ax), T.max(v, axis=ax), T.argmax(v, axis=ax)])
+        s, m, am = f(X)
+        exact(m, O.reduce_max(X, ax))
+        exact(am, O.argmax_index(X, ax))
+        close(s, O.reduce_sum(X, ax), 0, 2e-6 * float(np.abs(X).sum()) + 1e-6)
+
+
+def test_reduction_strided_views(rng):
+    X = rng.standard_normal((300, 500)).astype(np.float32)
+    v = T.matrix("X", dtype="float32")
+    vt = T.transpose(v)
+    f = T.compile([v], [T.sum(vt, axis=0), T.max(vt, axis=1), T.argmax(vt, axis=None)])
+    s, m, am = f(X)
+    close(s, X.T.sum(axis=0), 1e-5, 1e-5)
+    exact(m, O.reduce_max(X.T, (1,)))
+    exact(am, O.argmax_index(X.T, (0, 1)))
+
+
+def test_nan_propagation_max_and_argmax():
+    X = np.arange(24, dtype=np.float32).reshape(4, 6)
+    X[1, 2] = np.nan
+    X[2, 5] = np.nan
+    X[2, 1] = np.nan
+    v = T.matrix("X", dtype="float32")
+    m, am, oh = T.compile([v], [T.max(v, axis=1), T.argmax(v, axis=1), T.argmax_onehot(v, axis=0)])(X)
+    exact(m, O.reduce_max(X, (1,)))
+    exact(am, O.argmax_index(X, (1,)))
+    exact(oh, O.argmax_onehot(X, (0,)))
+
+
+def test_dot_golden(golden):
+    A, B, v = golden["dot_A"], golden["dot_B"], golden["dot_v"]
+    vA, vB, vv = T.matrix("A", dtype="float32"), T.matrix("B", dtype="float32"), T.vector("v", dtype="float32")
+    f = T.compile([vA, vB, vv], [T.dot(vA, vB), T.dot(vA, vv), T.dot(vv, vB), T.dot(vv, vv), T.dot(T.transpose(vA), vA)])
+    outs = f(A, B, v)
+    for got, key, (x, y) in zip(outs, ("dot_mm", "dot_mv", "dot_vm", "dot_vv", "dot_tn"),
+                                ((A, B), (A, v), (v, B), (v, v), (A.T, A))):
+        bound = np.abs(x).astype(np.float64) @ np.abs(y).astype(np.float64)
+        assert np.all(np.abs(got - golden[key]) <= 1e-5 * bound + 1e-6)
+
+
+def _gemm_case(M, N, K, ta, tb, mode, rng):
+    a = rng.standard_normal((K, M) if ta else (M, K)).astype(np.float32)
+    b = rng.standard_normal((N, K) if tb else (K, N)).astype(np.float32)
+    va, vb = T.matrix("a", dtype="float32"), T.matrix("b", dtype="float32")
+    ea = T.transpose(va) if ta else va
+    eb = T.transpose(vb) if tb else vb
+    f = T.compile([va, vb], T.dot(ea, eb), gemm_mode=mode)
+    got = f(a, b)
+    A = (a.T if ta else a).astype(np.float64)
+    B = (b.T if tb else b).astype(np.float64)
+    return got, A @ B, np.abs(A) @ np.abs(B)
+
+
+@pytest.mark.parametrize("M,N,K", [(256, 512, 256), (300, 520, 784), (784, 1024, 1000), (1024, 4096, 128),
+                                   (129, 65, 33)])
+@pytest.mark.parametrize("ta,tb", [(False, False), (False, True), (True, False), (True, True)])
+def test_gemm_tcgen05_layouts(M, N, K, ta, tb, rng):
+    got, want, bound = _gemm_case(M, N, K, ta, tb, "auto", rng)
+    err = np.abs(got - want)
+    assert np.all(err <= 2.0 ** -9 * bound + 1e-6), float((err / (bound + 1e-30)).max())
+
+
+@pytest.mark.parametrize("M,N,K", [(8192, 10, 4096), (600, 10, 784), (8192, 4096, 10), (784, 10, 600),
+                                   (4096, 10, 8192), (5, 300, 77), (7, 9, 11)])
+def test_gemm_skinny_and_simt_exactish(M, N, K, rng):
+    for ta in (False, True):
+        got, want, bound = _gemm_case(M, N, K, ta, False, "auto", rng)
+        assert np.all(np.abs(got - want) <= 1e-5 * bound + 1e-6)
+
+
+def test_gemm_simt_mode_and_f64(rng):
+    got, want, bound = _gemm_case(200, 300, 150, True, False, "simt", rng)
+    assert np.all(np.abs(got - want) <= 1e-5 * bound + 1e-6)
+    a = rng.standard_normal((70, 50))
+    b = rng.standard_normal((50, 90))
+    va, vb = T.matrix("a"), T.matrix("b")
+    np.testing.assert_allclose(T.compile([va, vb], T.dot(va, vb))(a, b), a @ b, rtol=1e-12, atol=1e-12)
+
+
+def test_dot_shape_mismatch_raises():
+    va, vb = T.matrix("a", dtype="float32"), T.matrix("b", dtype="float32")
+    f = T.compile([va, vb], T.dot(va, vb))
+    with pytest.raises(ShapeMismatch):
+        f(np.zeros((3, 4), np.float32), np.zeros((5, 6), np.float32))

@@ -1,0 +1,171 @@
+"""Runtime semantics of the device VM, mirroring the reference's
+tests/test_runtime.py (compile/call, shared state, updates, broadcast
+enforcement, copies) plus CUDA-graph replay and device-tensor calls."""
+import numpy as np
+import pytest
+
+import paper_1605_02688_b200 as T
+from paper_1605_02688_b200.errors import ShapeMismatch, TypeMismatch, UnderdeterminedOutputs
+
+pytestmark = pytest.mark.gpu
+
+
+def test_compile_and_call_basic():
+    x = T.vector("x")
+    f = T.compile([x], [x + 1.0], preset="none")
+    np.testing.assert_array_equal(f([1.0, 2.0])[0], [2.0, 3.0])
+
+
+def test_single_output_convenience():
+    x = T.scalar("x")
+    f = T.compile([x], x * 2.0, preset="none")
+    assert float(f(3.0)) == 6.0
+
+
+def test_compile_from_intermediate_skips_producers(rng):
+    x = T.vector("x")
+    h = T.exp(x)
+    y = T.sum(h * 2.0)
+    f = T.compile([h], y, preset="none")
+    assert all(getattr(n.op, "kernel", "") != "exp" for n in f.order)
+    hv = rng.standard_normal(4)
+    assert float(f(hv)) == pytest.approx(float(np.sum(hv * 2.0)))
+
+
+def test_underdetermined_outputs_rejected():
+    x, y = T.vector("x"), T.vector("y")
+    with pytest.raises(UnderdeterminedOutputs):
+        T.compile([x], [x + y], preset="none")
+
+
+def test_shared_updates_counter():
+    s = T.shared(np.array(0.0), name="s")
+    f = T.compile([], [s], updates=[(s, s + 1.0)], preset="none")
+    outs = [float(f()[0]) for _ in range(3)]
+    assert outs == [0.0, 1.0, 2.0]  # outputs see the value before the update
+    assert float(s.get_value()) == 3.0
+
+
+def test_update_in_place_when_safe():
+    W = T.shared(np.ones((64, 32), np.float32), name="W")
+    x = T.matrix("x", dtype="float32")
+    y = T.sum(T.dot(x, W))
+    f = T.compile([x], [y], updates=[(W, W - 0.5 * W)])
+    xv = np.ones((4, 64), np.float32)
+    assert float(f(xv)[0]) == 4 * 32 * 64
+    assert float(f(xv)[0]) == 4 * 32 * 64 * 0.5
+    np.testing.assert_array_equal(W.get_value(), np.full((64, 32), 0.25, np.float32))
+
+
+def test_swap_updates_read_old_values():
+    a = T.shared(np.array([1.0, 2.0]), name="a")
+    b = T.shared(np.array([3.0, 4.0]), name="b")
+    f = T.compile([], [], updates=[(a, b), (b, a)])
+    f()
+    np.testing.assert_array_equal(a.get_value(), [3.0, 4.0])
+    np.testing.assert_array_equal(b.get_value(), [1.0, 2.0])
+
+
+def test_updates_may_reference_outputs():
+    s = T.shared(np.zeros(3), name="s")
+    x = T.vector("x")
+    y = x * 2.0
+    f = T.compile([x], [y], updates=[(s, s + y)])
+    f([1.0, 2.0, 3.0])
+    out = f([1.0, 1.0, 1.0])
+    np.testing.assert_array_equal(out[0], [2.0, 2.0, 2.0])
+    np.testing.assert_array_equal(s.get_value(), [4.0, 6.0, 8.0])
+
+
+def test_two_functions_same_region_coexist(rng):
+    x = T.vector("x")
+    h = T.tanh(x)
+    f1 = T.compile([x], T.sum(h))
+    f2 = T.compile([x], T.sum(h * h))
+    p = rng.standard_normal(5)
+    assert float(f1(p)) == pytest.approx(float(np.sum(np.tanh(p))))
+    assert float(f2(p)) == pytest.approx(float(np.sum(np.tanh(p) ** 2)))
+
+
+def test_update_pair_type_checked():
+    s = T.shared(np.zeros(3), name="s")
+    bad = T.scalar("b")
+    with pytest.raises(TypeMismatch):
+        T.compile([bad], [bad], updates=[(s, bad)])
+
+
+def test_broadcastable_dims_enforced_at_call():
+    x = T.make_input(T.TensorType("float64", (True, False)), "x")
+    f = T.compile([x], [x * 2.0])
+    f(np.zeros((1, 4)))
+    with pytest.raises(TypeMismatch):
+        f(np.zeros((3, 4)))
+
+
+def test_runtime_broadcast_requires_declaration():
+    x, y = T.matrix("x"), T.matrix("y")
+    f = T.compile([x, y], x + y)
+    with pytest.raises(ShapeMismatch):
+        f(np.zeros((3, 4)), np.zeros((1, 4)))
+
+
+def test_wrong_dtype_rejected():
+    x = T.vector("x", dtype="float64")
+    f = T.compile([x], [x + 1.0])
+    with pytest.raises(TypeMismatch):
+        f(np.array(["a", "b"], dtype=object))
+
+
+def test_shared_set_value_and_shape_change():
+    s = T.shared(np.zeros(3, np.float32), name="s")
+    f = T.compile([], [s * 2.0])
+    np.testing.assert_array_equal(f()[0], [0, 0, 0])
+    s.set_value(np.ones(3, np.float32))
+    np.testing.assert_array_equal(f()[0], [2, 2, 2])
+    s.set_value(np.arange(5, dtype=np.float32))
+    np.testing.assert_array_equal(f()[0], 2 * np.arange(5, dtype=np.float32))
+    with pytest.raises(TypeMismatch):
+        s.set_value(np.zeros((2, 2)))
+
+
+def test_graph_replay_is_stable(rng):
+    x = T.matrix("x", dtype="float32")
+    f = T.compile([x], [T.sum(T.exp(x) * 2.0, axis=1), T.max(x)])
+    xv = rng.standard_normal((100, 37)).astype(np.float32)
+    first = f(xv)
+    for _ in range(5):
+        again = f(xv)
+        for a, b in zip(first, again):
+            np.testing.assert_array_equal(a, b)
+    assert f.profile.call_count == 6
+
+
+def test_call_device_with_torch_tensors(rng):
+    import torch
+    x = T.vector("x", dtype="float32")
+    f = T.compile([x], [T.sqr(x) + 1.0])
+    xv = torch.from_numpy(rng.standard_normal(1000).astype(np.float32)).cuda()
+    (y,) = f.call_device(xv, sync=True)
+    assert y.is_cuda
+    np.testing.assert_allclose(y.cpu().numpy(), xv.cpu().numpy() ** 2 + 1.0, rtol=1e-6)
+
+
+def test_copy_with_swap():
+    s = T.shared(np.array(1.0), name="s")
+    s2 = T.shared(np.array(10.0), name="s2")
+    f = T.compile([], [s], updates=[(s, s * 2.0)])
+    g = f.copy(swap={s: s2})
+    g()
+    assert float(s2.get_value()) == 20.0 and float(s.get_value()) == 1.0
+    h = f.copy(carry_updates=False)
+    h()
+    assert float(s.get_value()) == 1.0
+
+
+def test_profile_nodes_records_times(rng):
+    x = T.matrix("x", dtype="float32")
+    f = T.compile([x], [T.sum(T.tanh(x), axis=0)])
+    f.profile_nodes = True
+    f(rng.standard_normal((64, 64)).astype(np.float32))
+    assert all(f.profile.node_calls[n.id] == 1 for n in f.order)
+    assert sum(f.profile.node_time.values()) > 0
