@@ -144,7 +144,7 @@ def bench_ew(T, C, steps, warmup, lib_holder):
     stream = f._stream
     ms = time_device(lambda: f.call_device(*ins), lib, stream, steps)
     # correctness spot check against the oracle formula on a sample
-    out = f.call_device(*ins, sync=True)[0]
+    out = f.call_device(*ins, sync=True)
     idx = torch.randint(0, EW_N, (4096,), device="cuda", generator=gen)
     from oracle import texpr_numpy as O
     want = O.eval_composite_plain(f.order[0].op.program, [x[idx].cpu().numpy() for x in ins])[0]

@@ -78,14 +78,17 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
-// UMMA shared-memory descriptor, SWIZZLE_128B (sm100 "version 1" layout).
-__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+// UMMA shared-memory descriptor (sm100 "version 1").  layout: 2 = SWIZZLE_128B
+// (K-major operands: 8-row x 128 B atoms), 1 = SWIZZLE_128B_BASE32B (the only
+// MN-major layout for 32-bit types: 128 B rows swizzled in 32 B granules,
+// 4-row / 512 B atoms).
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFF);
   d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
   d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
   d |= (uint64_t)1 << 46;
-  d |= (uint64_t)2 << 61;
+  d |= (uint64_t)layout << 61;
   return d;
 }
 
@@ -201,8 +204,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)p.a_mn << 15) |
                            ((uint32_t)p.b_mn << 16) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
     // descriptor geometry per operand layout
-    const uint32_t a_lbo = p.a_mn ? 4096u : 16u, a_step = p.a_mn ? 1024u : 32u;
-    const uint32_t b_lbo = p.b_mn ? 4096u : 16u, b_step = p.b_mn ? 1024u : 32u;
+    // K-major: LBO unused (16 B), SBO = 1024 B between 8-row atoms, +32 B per k-step.
+    // MN-major: LBO = 4096 B between 32-element MN blocks (one TMA box each),
+    //           SBO = 512 B between 4-row K groups, +1024 B per k-step (8 rows).
+    const uint32_t a_lbo = p.a_mn ? 4096u : 16u, a_sbo = p.a_mn ? 512u : 1024u, a_step = p.a_mn ? 1024u : 32u;
+    const uint32_t b_lbo = p.b_mn ? 4096u : 16u, b_sbo = p.b_mn ? 512u : 1024u, b_step = p.b_mn ? 1024u : 32u;
+    const uint32_t a_lay = p.a_mn ? 1u : 2u, b_lay = p.b_mn ? 1u : 2u;
     int stage = 0;
     uint32_t phase = 0;
     int it = 0;
@@ -220,8 +227,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const uint32_t sb = sa + A_BYTES;
 #pragma unroll
           for (int kk = 0; kk < BK / 8; ++kk) {
-            const uint64_t da = sdesc(sa + kk * a_step, a_lbo, 1024);
-            const uint64_t db = sdesc(sb + kk * b_step, b_lbo, 1024);
+            const uint64_t da = sdesc(sa + kk * a_step, a_lbo, a_sbo, a_lay);
+            const uint64_t db = sdesc(sb + kk * b_step, b_lbo, b_sbo, b_lay);
             umma_tf32(tmem_d, da, db, idesc, (kb | kk) != 0);
           }
           umma_commit(empty + stage);
@@ -299,7 +306,7 @@ static EncodeFn encode_fn() {
 
 // inner-contiguous 2D map: dims {inner, outer}, outer stride in elements
 static int make_map(CUtensorMap* m, const void* base, int64_t inner, int64_t outer, int64_t ostride, int box_inner,
-                    int box_outer) {
+                    int box_outer, bool mn_major) {
   EncodeFn enc = encode_fn();
   TX_CHECK(enc, TX_E_NODEVICE, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
@@ -307,7 +314,9 @@ static int make_map(CUtensorMap* m, const void* base, int64_t inner, int64_t out
   cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer};
   cuuint32_t es[2] = {1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_TFLOAT32, 2, const_cast<void*>(base), dims, strides, box, es,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(TX_E_CUDA, "cuTensorMapEncodeTiled failed (code " + std::to_string((int)r) + ")");
   return TX_OK;
@@ -335,11 +344,11 @@ int gemm_tc(const G& g, cudaStream_t st) {
   const bool a_mn = !(g.sak == 1 && g.sam % 4 == 0 && g.sam >= g.K);
   const bool b_mn = (g.sbn == 1 && g.sbk % 4 == 0 && g.sbk >= g.N);
   CUtensorMap ma, mb;
-  if (a_mn) rc = make_map(&ma, g.A, g.M, g.K, g.sak, 32, 32);
-  else rc = make_map(&ma, g.A, g.K, g.M, g.sam, 32, BM);
+  if (a_mn) rc = make_map(&ma, g.A, g.M, g.K, g.sak, 32, 32, true);
+  else rc = make_map(&ma, g.A, g.K, g.M, g.sam, 32, BM, false);
   if (rc) return rc;
-  if (b_mn) rc = make_map(&mb, g.B, g.N, g.K, g.sbk, 32, 32);
-  else rc = make_map(&mb, g.B, g.K, g.N, g.sbn, 32, BN);
+  if (b_mn) rc = make_map(&mb, g.B, g.N, g.K, g.sbk, 32, 32, true);
+  else rc = make_map(&mb, g.B, g.K, g.N, g.sbn, 32, BN, false);
   if (rc) return rc;
   TcParams p;
   p.C = (float*)g.C;

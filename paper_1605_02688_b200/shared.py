@@ -64,7 +64,7 @@ class SharedVariable(Variable):
                 host = self._host
                 if self.type.dtype == "bool":
                     host = host.astype(np.uint8)
-                self._dev = t.from_numpy(np.ascontiguousarray(host)).to("cuda", non_blocking=False)
+                self._dev = t.from_numpy(np.array(host, order="C", copy=True)).to("cuda", non_blocking=False)
                 self._host = None
                 self.version += 1
             return self._dev

@@ -241,7 +241,9 @@ class CompiledFunction:
         self.n_outputs = n_outputs
         self.input_vars = list(input_vars)
         self.shared_bindings = list(shared_bindings)
-        self.updates = list(updates)
+        # update values are read from the rewritten graph's outputs (the
+        # variables captured at clone time may have been replaced)
+        self.updates = [(s, fgraph.outputs[n_outputs + i]) for i, (s, _) in enumerate(updates)]
         self.rewrite_log = rewrite_log
         self.preset = preset
         self.single_output = single_output
@@ -691,7 +693,7 @@ class StepPlan:
         ent = cache.get(c.id)
         if ent is None:
             t = _torch()
-            arr = np.ascontiguousarray(c.value)
+            arr = np.array(c.value, order="C", copy=True)
             if c.type.dtype == "bool":
                 arr = arr.astype(np.uint8)
             dev = t.from_numpy(arr.copy()).to("cuda") if arr.size else t.empty(1, dtype=t.uint8, device="cuda")
