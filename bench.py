@@ -197,6 +197,28 @@ def bench_mlp(T, C, B, steps, warmup, lib_holder, dp=None, n_global=None):
     return f, ms, cost
 
 
+def tf32_peak_cublas(n=8192, iters=20):
+    """cuBLAS TF32 GEMM throughput on this box (the TF32 roofline reference;
+    MEASURED_PEAKS.json only has bf16)."""
+    import torch
+    torch.backends.cuda.matmul.allow_tf32 = True
+    a = torch.randn(n, n, device="cuda")
+    b = torch.randn(n, n, device="cuda")
+    for _ in range(3):
+        a @ b
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    best = 1e30
+    for _ in range(iters):
+        s.record()
+        a @ b
+        e.record()
+        e.synchronize()
+        best = min(best, s.elapsed_time(e))
+    torch.backends.cuda.matmul.allow_tf32 = False
+    return 2 * n ** 3 / (best * 1e-3) / 1e12
+
+
 def bench_logreg(T, C, steps, warmup, lib_holder):
     import torch
     g = C.build_logreg(T)
@@ -334,6 +356,10 @@ def main():
     torch.cuda.empty_cache()
     if not args.skip_extra:
         extra = {}
+        try:
+            extra["tf32_cublas_tflops_8192cubed"] = round(tf32_peak_cublas(), 1)
+        except Exception as e:
+            extra["tf32_cublas_tflops_8192cubed"] = repr(e)[:200]
         try:
             fm, ms_m, cost = bench_mlp(T, C, 8192, max(5, args.steps // 2), 3, lib_holder)
             med = statistics.median(ms_m)

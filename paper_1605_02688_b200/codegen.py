@@ -130,6 +130,9 @@ def generate_source(p: EwProgram) -> str:
     vdecl = " ".join(f"V4<{C_TYPE[d]}> vout{k};" for k, d in enumerate(out_dt))
     vload = " ".join(f"const V4<{C_TYPE[d]}> vin{k} = tx_ld4(p{k} + (o_));" for k, d in enumerate(p.in_dtypes))
     vstore = " ".join(f"tx_st4(q{k} + (o_), vout{k});" for k in range(n_out))
+    vload2d = " ".join(f"const V4<{C_TYPE[d]}> vin{k} = tx_ld4b(p{k} + OFF({n_out + k}), a.strides[{n_out + k}][1]);"
+                       for k, d in enumerate(p.in_dtypes))
+    vstore2d = " ".join(f"tx_st4(q{k} + OFF({k}), vout{k});" for k in range(n_out))
     body = program_body(p)
     return "\n".join([
         "#define TX_KERNELS 1",
@@ -139,6 +142,8 @@ def generate_source(p: EwProgram) -> str:
         f"#define TX_VDECL {vdecl}",
         f"#define TX_VLOAD(o_) {vload}",
         f"#define TX_VSTORE(o_) {vstore}",
+        f"#define TX_VLOAD2D {vload2d}",
+        f"#define TX_VSTORE2D {vstore2d}",
         f"#define TX_BODY {body}",
         template_text(),
     ])

@@ -138,6 +138,39 @@ __device__ __forceinline__ void tx_st4(u8* p, const V4<u8>& x) {
   __stcs(reinterpret_cast<unsigned int*>(p), t);
 }
 
+
+// plain (cached) vector loads, for operands re-read across rows (bias rows)
+__device__ __forceinline__ V4<float> tx_ld4n(const float* p) {
+  float4 t = *reinterpret_cast<const float4*>(p);
+  return V4<float>{{t.x, t.y, t.z, t.w}};
+}
+__device__ __forceinline__ V4<int> tx_ld4n(const int* p) {
+  int4 t = *reinterpret_cast<const int4*>(p);
+  return V4<int>{{t.x, t.y, t.z, t.w}};
+}
+__device__ __forceinline__ V4<double> tx_ld4n(const double* p) {
+  double2 a = reinterpret_cast<const double2*>(p)[0], b = reinterpret_cast<const double2*>(p)[1];
+  return V4<double>{{a.x, a.y, b.x, b.y}};
+}
+__device__ __forceinline__ V4<i64> tx_ld4n(const i64* p) {
+  longlong2 a = reinterpret_cast<const longlong2*>(p)[0], b = reinterpret_cast<const longlong2*>(p)[1];
+  return V4<i64>{{a.x, a.y, b.x, b.y}};
+}
+__device__ __forceinline__ V4<u8> tx_ld4n(const u8* p) {
+  unsigned int t = *reinterpret_cast<const unsigned int*>(p);
+  return V4<u8>{{(u8)(t & 0xff), (u8)((t >> 8) & 0xff), (u8)((t >> 16) & 0xff), (u8)(t >> 24)}};
+}
+// 4 consecutive columns of one row: a vector load, or one value broadcast when
+// the operand is constant along the row (column-broadcast [B,1] operands)
+template <class T>
+__device__ __forceinline__ V4<T> tx_ld4b(const T* p, i64 s1) {
+  if (s1 == 0) {
+    const T v = *p;
+    return V4<T>{{v, v, v, v}};
+  }
+  return tx_ld4n(p);
+}
+
 // ------------------------------------------------------------ kernels
 // The generator defines, before including the kernels below:
 //   TX_PTRS            pointer declarations p<k> (inputs) and q<k> (outputs)
@@ -204,6 +237,35 @@ extern "C" __global__ void __launch_bounds__(256) tx_ew_2d(const TxEwArgs a) {
     TX_BODY
 #undef IN
 #undef OUT
+#undef OFF
+  }
+}
+
+
+// rank-2 with the contiguous dim vectorised: every operand has column stride
+// 0 or 1 and 16 B-aligned rows; 4 columns per thread, one row per grid.y step.
+extern "C" __global__ void __launch_bounds__(256) tx_ew_2dv(const TxEwArgs a) {
+  TX_PTRS
+  int* err = a.err;
+  (void)err;
+  const int rows = (int)a.shape[0];
+  const int cols4 = (int)(a.shape[1] >> 2);
+  const int c4 = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c4 >= cols4) return;
+  const i64 col = (i64)c4 << 2;
+  for (int row = blockIdx.y; row < rows; row += gridDim.y) {
+#define OFF(k) ((i64)row * a.strides[k][0] + col * a.strides[k][1])
+    TX_VDECL
+    TX_VLOAD2D
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+#define IN(k) vin##k.v[j]
+#define OUT(k, val) vout##k.v[j] = (val)
+      TX_BODY
+#undef IN
+#undef OUT
+    }
+    TX_VSTORE2D
 #undef OFF
   }
 }

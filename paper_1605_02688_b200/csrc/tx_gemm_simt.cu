@@ -67,48 +67,71 @@ __global__ void __launch_bounds__(256) simt_gemm(const T* __restrict__ A, const 
 }
 
 // ------------------------------------------------- N <= 16, A K-contiguous
-// C[m, n] = sum_k A[m, k] B[k, n].  Block = 8 warps x 4 rows; B[kc:kc+256, :N]
-// staged in shared memory and reused by all 32 rows of the block.
-template <int NN>
+// C[m, n] = sum_k A[m, k] B[k, n] (x.W3 / x.W in the softmax layers).  One
+// warp owns R rows; B[k0:k0+KC, :N] is staged TRANSPOSED in shared memory
+// (Bt[n][k]) so lanes read consecutive k (conflict-free 128-bit loads) and
+// every row of the CTA reuses it.  A is streamed with 128-bit loads.
+constexpr int RD_KC = 512;
+
+template <int NN, int R>
 __global__ void __launch_bounds__(256) rowdot_kernel(const float* __restrict__ A, const float* __restrict__ B,
                                                     float* __restrict__ C, int64_t M, int N, int64_t K, int64_t sam,
                                                     int64_t sbk, int64_t sbn, int64_t scm, int64_t scn, Epi<float> epi) {
-  constexpr int KC = 256;
-  __shared__ float Bs[KC][NN];
+  __shared__ __align__(16) float Bt[NN][RD_KC];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t row0 = (int64_t)blockIdx.x * 32 + warp * 4;
-  float acc[4][NN];
+  const int64_t row0 = ((int64_t)blockIdx.x * 8 + warp) * R;
+  const bool vec = (sam % 4 == 0) && (((uintptr_t)A & 15) == 0);
+  float acc[R][NN];
 #pragma unroll
-  for (int r = 0; r < 4; ++r)
+  for (int r = 0; r < R; ++r)
 #pragma unroll
     for (int n = 0; n < NN; ++n) acc[r][n] = 0.f;
-  for (int64_t k0 = 0; k0 < K; k0 += KC) {
+  for (int64_t k0 = 0; k0 < K; k0 += RD_KC) {
+    const int kc = (int)min((int64_t)RD_KC, K - k0);
     __syncthreads();
-    for (int e = threadIdx.x; e < KC * NN; e += 256) {
-      int kk = e / NN, n = e % NN;
-      int64_t gk = k0 + kk;
-      Bs[kk][n] = (gk < K && n < N) ? B[gk * sbk + n * sbn] : 0.f;
+    if (sbn == 1) {
+      for (int e = threadIdx.x; e < RD_KC * NN; e += 256) {
+        const int kk = e / NN, n = e % NN;
+        Bt[n][kk] = (kk < kc && n < N) ? B[(k0 + kk) * sbk + n] : 0.f;
+      }
+    } else {
+      for (int e = threadIdx.x; e < RD_KC * NN; e += 256) {
+        const int n = e / RD_KC, kk = e % RD_KC;
+        Bt[n][kk] = (kk < kc && n < N) ? B[(k0 + kk) * sbk + n * sbn] : 0.f;
+      }
     }
     __syncthreads();
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
+    for (int r = 0; r < R; ++r) {
       const int64_t m = row0 + r;
       if (m >= M) break;
       const float* a = A + m * sam + k0;
-#pragma unroll 4
-      for (int j = 0; j < KC / 32; ++j) {
-        const int kk = lane + 32 * j;
-        const float av = (k0 + kk < K) ? __ldg(a + kk) : 0.f;
+      if (vec && kc == RD_KC) {
 #pragma unroll
-        for (int n = 0; n < NN; ++n) acc[r][n] += av * Bs[kk][n];
+        for (int j = 0; j < RD_KC / 128; ++j) {
+          const int kk = j * 128 + lane * 4;
+          const float4 av = __ldg(reinterpret_cast<const float4*>(a + kk));
+#pragma unroll
+          for (int n = 0; n < NN; ++n) {
+            const float4 bv = *reinterpret_cast<const float4*>(&Bt[n][kk]);
+            acc[r][n] += av.x * bv.x + av.y * bv.y + av.z * bv.z + av.w * bv.w;
+          }
+        }
+      } else {
+        for (int kk = lane; kk < kc; kk += 32) {
+          const float av = __ldg(a + kk);
+#pragma unroll
+          for (int n = 0; n < NN; ++n) acc[r][n] += av * Bt[n][kk];
+        }
       }
     }
   }
 #pragma unroll
-  for (int r = 0; r < 4; ++r) {
+  for (int r = 0; r < R; ++r) {
 #pragma unroll
     for (int n = 0; n < NN; ++n) {
       float v = acc[r][n];
+#pragma unroll
       for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
       acc[r][n] = v;
     }
@@ -124,76 +147,111 @@ __global__ void __launch_bounds__(256) rowdot_kernel(const float* __restrict__ A
 }
 
 // ------------------------------------------------ K <= 16 (outer-product-like)
-// C[m, n] = sum_{k<K} A[m,k] B[k,n]; tile 32 rows x 256 cols; A and B tiles in smem.
+// C[m, n] = sum_{k<K} A[m,k] B[k,n] (dz.W3^T).  CTA tile 32 rows x 1024 cols,
+// 4 adjacent columns per thread held in registers, A tile broadcast from smem,
+// 128-bit stores; writing C is the whole cost.
 template <int KK>
 __global__ void __launch_bounds__(256) outer_kernel(const float* __restrict__ A, const float* __restrict__ B,
                                                    float* __restrict__ C, int64_t M, int64_t N, int K, int64_t sam,
                                                    int64_t sak, int64_t sbk, int64_t sbn, int64_t scm, int64_t scn,
                                                    Epi<float> epi) {
   __shared__ float As[32][KK];
-  __shared__ float Bs[KK][256];
-  const int64_t m0 = (int64_t)blockIdx.y * 32, n0 = (int64_t)blockIdx.x * 256;
+  const int64_t m0 = (int64_t)blockIdx.y * 32;
+  const int64_t n0 = ((int64_t)blockIdx.x * 256 + threadIdx.x) * 4;
   for (int e = threadIdx.x; e < 32 * KK; e += 256) {
-    int r = e / KK, k = e % KK;
+    const int r = e / KK, k = e % KK;
     As[r][k] = (m0 + r < M && k < K) ? A[(m0 + r) * sam + k * sak] : 0.f;
   }
-  for (int e = threadIdx.x; e < KK * 256; e += 256) {
-    int k, c;
-    if (sbn == 1) { k = e / 256; c = e % 256; } else { k = e % KK; c = e / KK; }
-    Bs[k][c] = (k < K && n0 + c < N) ? B[k * sbk + (n0 + c) * sbn] : 0.f;
-  }
   __syncthreads();
-  const int64_t n = n0 + threadIdx.x;
-  if (n >= N) return;
-  float b[KK];
+  if (n0 >= N) return;
+  float b[KK][4];
 #pragma unroll
-  for (int k = 0; k < KK; ++k) b[k] = Bs[k][threadIdx.x];
-  for (int r = 0; r < 32; ++r) {
+  for (int k = 0; k < KK; ++k)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) b[k][j] = (k < K && n0 + j < N) ? __ldg(B + k * sbk + (n0 + j) * sbn) : 0.f;
+  const bool vst = scn == 1 && (scm % 4 == 0) && (((uintptr_t)C & 15) == 0) && n0 + 4 <= N;
+  const int rows = (int)min((int64_t)32, M - m0);
+  for (int r = 0; r < rows; ++r) {
     const int64_t m = m0 + r;
-    if (m >= M) break;
-    float acc = 0.f;
+    float o[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-    for (int k = 0; k < KK; ++k) acc += As[r][k] * b[k];
-    C[m * scm + n * scn] = epi.apply(acc, m, n);
+    for (int k = 0; k < KK; ++k) {
+      const float av = As[r][k];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) o[j] += av * b[k][j];
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) o[j] = epi.apply(o[j], m, n0 + j);
+    if (vst) {
+      *reinterpret_cast<float4*>(C + m * scm + n0) = make_float4(o[0], o[1], o[2], o[3]);
+    } else {
+      for (int j = 0; j < 4 && n0 + j < N; ++j) C[m * scm + (n0 + j) * scn] = o[j];
+    }
   }
 }
 
 // ------------------------------------- N <= 16, A M-contiguous (x^T . dz form)
-// C[m, n] = sum_k A[k-th row][m] * B[k, n]: a column reduction over k.
-// grid.x covers m (one column per thread), grid.y splits k; partials [S][M][N]
-// are combined in order by kred_finalize (deterministic).
+// C[m, n] = sum_k A[k*sak + m] * B[k, n]: a column reduction over k.  Each
+// thread owns 4 adjacent m (128-bit loads along the contiguous M axis); B rows
+// are broadcast from smem; grid.y splits k and writes partials [S][M][N]
+// that kred_finalize sums in fixed order (deterministic, no atomics).
+constexpr int KR_KC = 64;
+
 template <int NN>
 __global__ void __launch_bounds__(256) kred_kernel(const float* __restrict__ A, const float* __restrict__ B,
                                                   float* __restrict__ P, int64_t M, int N, int64_t K, int64_t sak,
                                                   int64_t sbk, int64_t sbn, int splits) {
-  constexpr int KC = 64;
-  __shared__ float Bs[KC][NN];
-  const int64_t m = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  __shared__ float Bs[KR_KC][NN];
+  const int64_t m0 = ((int64_t)blockIdx.x * 256 + threadIdx.x) * 4;
   const int64_t chunk = (K + splits - 1) / splits;
   const int64_t klo = (int64_t)blockIdx.y * chunk, khi = min(K, klo + chunk);
-  float acc[NN];
+  const bool vec = (sak % 4 == 0) && (((uintptr_t)A & 15) == 0) && m0 + 4 <= M;
+  float acc[4][NN];
 #pragma unroll
-  for (int n = 0; n < NN; ++n) acc[n] = 0.f;
-  for (int64_t k0 = klo; k0 < khi; k0 += KC) {
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int n = 0; n < NN; ++n) acc[j][n] = 0.f;
+  for (int64_t k0 = klo; k0 < khi; k0 += KR_KC) {
     __syncthreads();
-    for (int e = threadIdx.x; e < KC * NN; e += 256) {
-      int kk = e / NN, n = e % NN;
+    for (int e = threadIdx.x; e < KR_KC * NN; e += 256) {
+      const int kk = e / NN, n = e % NN;
       Bs[kk][n] = (k0 + kk < khi && n < N) ? B[(k0 + kk) * sbk + n * sbn] : 0.f;
     }
     __syncthreads();
-    if (m < M) {
-      const int kend = (int)min((int64_t)KC, khi - k0);
-      for (int kk = 0; kk < kend; ++kk) {
-        const float av = __ldcs(A + (k0 + kk) * sak + m);
+    if (m0 < M) {
+      const int kend = (int)min((int64_t)KR_KC, khi - k0);
+      if (vec) {
+#pragma unroll 4
+        for (int kk = 0; kk < kend; ++kk) {
+          const float4 av = __ldcs(reinterpret_cast<const float4*>(A + (k0 + kk) * sak + m0));
 #pragma unroll
-        for (int n = 0; n < NN; ++n) acc[n] += av * Bs[kk][n];
+          for (int n = 0; n < NN; ++n) {
+            const float bv = Bs[kk][n];
+            acc[0][n] += av.x * bv;
+            acc[1][n] += av.y * bv;
+            acc[2][n] += av.z * bv;
+            acc[3][n] += av.w * bv;
+          }
+        }
+      } else {
+        for (int kk = 0; kk < kend; ++kk) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            if (m0 + j >= M) break;
+            const float av = A[(k0 + kk) * sak + m0 + j];
+#pragma unroll
+            for (int n = 0; n < NN; ++n) acc[j][n] += av * Bs[kk][n];
+          }
+        }
       }
     }
   }
-  if (m < M) {
+  for (int j = 0; j < 4; ++j) {
+    const int64_t m = m0 + j;
+    if (m >= M) break;
 #pragma unroll
     for (int n = 0; n < NN; ++n)
-      if (n < N) P[((int64_t)blockIdx.y * M + m) * N + n] = acc[n];
+      if (n < N) P[((int64_t)blockIdx.y * M + m) * N + n] = acc[j][n];
   }
 }
 
@@ -210,16 +268,22 @@ __global__ void kred_finalize(const float* __restrict__ P, float* __restrict__ C
 
 template <int NN>
 static int launch_rowdot(const G& g, cudaStream_t st) {
-  unsigned blocks = (unsigned)((g.M + 31) / 32);
-  rowdot_kernel<NN><<<blocks, 256, 0, st>>>((const float*)g.A, (const float*)g.B, (float*)g.C, g.M, (int)g.N, g.K,
-                                            g.sam, g.sbk, g.sbn, g.scm, g.scn, g.epi_f);
+  if (g.M >= 4096) {
+    unsigned blocks = (unsigned)((g.M + 31) / 32);
+    rowdot_kernel<NN, 4><<<blocks, 256, 0, st>>>((const float*)g.A, (const float*)g.B, (float*)g.C, g.M, (int)g.N,
+                                                 g.K, g.sam, g.sbk, g.sbn, g.scm, g.scn, g.epi_f);
+  } else {
+    unsigned blocks = (unsigned)((g.M + 7) / 8);
+    rowdot_kernel<NN, 1><<<blocks, 256, 0, st>>>((const float*)g.A, (const float*)g.B, (float*)g.C, g.M, (int)g.N,
+                                                 g.K, g.sam, g.sbk, g.sbn, g.scm, g.scn, g.epi_f);
+  }
   TX_CUDA(cudaGetLastError());
   return TX_OK;
 }
 
 template <int KK>
 static int launch_outer(const G& g, cudaStream_t st) {
-  dim3 grid((unsigned)((g.N + 255) / 256), (unsigned)((g.M + 31) / 32));
+  dim3 grid((unsigned)((g.N + 1023) / 1024), (unsigned)((g.M + 31) / 32));
   outer_kernel<KK><<<grid, 256, 0, st>>>((const float*)g.A, (const float*)g.B, (float*)g.C, g.M, g.N, (int)g.K, g.sam,
                                          g.sak, g.sbk, g.sbn, g.scm, g.scn, g.epi_f);
   TX_CUDA(cudaGetLastError());
@@ -230,7 +294,7 @@ template <int NN>
 static int launch_kred(const G& g, void* ws, size_t wsb, cudaStream_t st) {
   int splits = kred_splits(g.M, g.K);
   TX_CHECK((size_t)splits * g.M * g.N * 4 <= wsb, TX_E_ARG, "tx_gemm: skinny workspace too small");
-  dim3 grid((unsigned)((g.M + 255) / 256), (unsigned)splits);
+  dim3 grid((unsigned)((g.M + 1023) / 1024), (unsigned)splits);
   kred_kernel<NN><<<grid, 256, 0, st>>>((const float*)g.A, (const float*)g.B, (float*)ws, g.M, (int)g.N, g.K, g.sak,
                                         g.sbk, g.sbn, splits);
   int64_t tot = g.M * g.N;
@@ -243,10 +307,10 @@ static int launch_kred(const G& g, void* ws, size_t wsb, cudaStream_t st) {
 }  // namespace
 
 int kred_splits(int64_t M, int64_t K) {
-  int64_t mblocks = (M + 255) / 256;
-  int64_t want = (int64_t)sm_count() * 4;
+  int64_t mblocks = (M + 1023) / 1024;
+  int64_t want = (int64_t)sm_count() * 2;
   int64_t s = (want + mblocks - 1) / mblocks;
-  int64_t maxs = K / 64;
+  int64_t maxs = K / 16;
   if (s > maxs) s = maxs;
   if (s > 1024) s = 1024;
   if (s < 1) s = 1;
@@ -265,20 +329,29 @@ int gemm_simt(const G& g, cudaStream_t st) {
   return TX_OK;
 }
 
+#define TX_WIDTHS(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16)
+
 int gemm_skinny(const G& g, int kind, void* ws, size_t wsb, cudaStream_t st) {
   if (kind == SK_OUTER) {
-    if (g.K <= 4) return launch_outer<4>(g, st);
-    if (g.K <= 8) return launch_outer<8>(g, st);
-    return launch_outer<16>(g, st);
+    switch ((int)g.K) {
+#define CASE(w) case w: return launch_outer<w>(g, st);
+      TX_WIDTHS(CASE)
+#undef CASE
+    }
+  } else if (kind == SK_ROWDOT) {
+    switch ((int)g.N) {
+#define CASE(w) case w: return launch_rowdot<w>(g, st);
+      TX_WIDTHS(CASE)
+#undef CASE
+    }
+  } else {
+    switch ((int)g.N) {
+#define CASE(w) case w: return launch_kred<w>(g, ws, wsb, st);
+      TX_WIDTHS(CASE)
+#undef CASE
+    }
   }
-  if (kind == SK_ROWDOT) {
-    if (g.N <= 4) return launch_rowdot<4>(g, st);
-    if (g.N <= 8) return launch_rowdot<8>(g, st);
-    return launch_rowdot<16>(g, st);
-  }
-  if (g.N <= 4) return launch_kred<4>(g, ws, wsb, st);
-  if (g.N <= 8) return launch_kred<8>(g, ws, wsb, st);
-  return launch_kred<16>(g, ws, wsb, st);
+  return fail(TX_E_ARG, "tx_gemm: skinny width out of range");
 }
 
 }  // namespace tx

@@ -88,7 +88,7 @@ static int nvrtc_compile(const char* source, const char* name, std::vector<char>
 
 struct EwKernel {
   CUmodule mod = nullptr;
-  CUfunction flat = nullptr, k2d = nullptr, knd = nullptr;
+  CUfunction flat = nullptr, k2d = nullptr, k2dv = nullptr, knd = nullptr;
   int occ_flat = 4, occ_nd = 4;
 };
 
@@ -129,6 +129,7 @@ int tx_ew_compile(const char* source, const char* name, void** out) {
   if (r != CUDA_SUCCESS) { delete k; return drv_fail(r, "cuModuleLoadData"); }
   if ((r = d.moduleGetFunction(&k->flat, k->mod, "tx_ew_flat")) != CUDA_SUCCESS ||
       (r = d.moduleGetFunction(&k->k2d, k->mod, "tx_ew_2d")) != CUDA_SUCCESS ||
+      (r = d.moduleGetFunction(&k->k2dv, k->mod, "tx_ew_2dv")) != CUDA_SUCCESS ||
       (r = d.moduleGetFunction(&k->knd, k->mod, "tx_ew_nd")) != CUDA_SUCCESS) {
     d.moduleUnload(k->mod);
     delete k;
@@ -230,6 +231,27 @@ int tx_ew_launch(void* h, int n_out, int n_in, const tx_tensor* ops, int* err_fl
       a.shape[0] = a.shape[1] = 1;
     }
     int64_t rows = a.shape[0], cols = a.shape[1];
+    // vectorised variant: column strides in {0,1}, outputs contiguous along
+    // columns, rows 16 B aligned for every vector-loaded operand
+    bool v2 = (cols % 4 == 0);
+    for (int op = 0; op < nops && v2; ++op) {
+      const int64_t s1 = a.strides[op][1], s0 = a.strides[op][0];
+      const int isz = itemsize(ops[op].dtype);
+      const uintptr_t pa = (uintptr_t)ops[op].data;
+      if (op < n_out && s1 != 1) v2 = false;
+      if (s1 != 0 && s1 != 1) v2 = false;
+      if (s1 == 1) {
+        const int64_t need = isz == 1 ? 4 : 16;
+        if ((pa % need) || ((s0 * isz) % need)) v2 = false;
+      }
+    }
+    if (v2) {
+      unsigned gx = (unsigned)((cols / 4 + 255) / 256);
+      int64_t gy = rows < 65535 ? rows : 65535;
+      r = d.launchKernel(k->k2dv, gx, (unsigned)gy, 1, 256, 1, 1, 0, s, params, nullptr);
+      if (r != CUDA_SUCCESS) return drv_fail(r, "cuLaunchKernel(tx_ew_2dv)");
+      return TX_OK;
+    }
     unsigned gx = (unsigned)((cols + 255) / 256);
     int64_t gy = rows;
     int64_t want = ((int64_t)sms * 8 + gx - 1) / gx;  // enough CTAs to fill the chip

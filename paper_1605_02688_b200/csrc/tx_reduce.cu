@@ -20,6 +20,7 @@
 #include <cfloat>
 #include <climits>
 #include <cstring>
+#include <type_traits>
 
 #include "tx_common.h"
 
@@ -49,6 +50,8 @@ struct Acc {
     if (OP == TX_SUM) v = T(0); else v = lowest<T>();
     i = LLONG_MAX;
   }
+  // Elements pushed by one thread arrive in increasing index order, so for
+  // argmax a strict ">" keeps the first maximum and the first NaN sticks.
   __device__ __forceinline__ void push(T x, long long idx) {
     if (OP == TX_SUM) {
       v = v + x;
@@ -57,9 +60,8 @@ struct Acc {
       if (isnan_<T>(v)) return;
       if (isnan_<T>(x) || x > v) v = x;
     } else {
-      // first-max with NaN as maximal; callers push in increasing idx order
-      // within a thread, merges use merge() which compares indices.
-      merge_pair(x, idx);
+      const bool take = (i == LLONG_MAX) | (x > v) | (isnan_<T>(x) & !isnan_<T>(v));
+      if (take) { v = x; i = idx; }
     }
   }
   __device__ __forceinline__ void merge_pair(T x, long long idx) {
@@ -116,8 +118,9 @@ template <> struct Vec4<int> { using type = int4; };
 // splits == 1: write the final result; else write partials [rows][splits].
 template <class T, int OP>
 __global__ void __launch_bounds__(kThreads) row_kernel(const T* __restrict__ x, int64_t rows, int64_t R, int64_t rs,
-                                                      int splits, T* __restrict__ out, long long* __restrict__ out_idx,
-                                                      T* __restrict__ pv, long long* __restrict__ pi) {
+                                                      int64_t es, int splits, T* __restrict__ out,
+                                                      long long* __restrict__ out_idx, T* __restrict__ pv,
+                                                      long long* __restrict__ pi) {
   const int64_t row = blockIdx.y + (int64_t)blockIdx.z * gridDim.y;
   if (row >= rows) return;
   const int64_t chunk = (R + splits - 1) / splits;
@@ -126,7 +129,9 @@ __global__ void __launch_bounds__(kThreads) row_kernel(const T* __restrict__ x, 
   const T* p = x + row * rs;
   Acc<T, OP> a;
   a.init();
-  if constexpr (sizeof(T) == 4 && (OP == TX_SUM || OP == TX_MAX) && !std::is_same<T, unsigned char>::value) {
+  if (es != 1) {
+    for (int64_t k = lo + threadIdx.x; k < hi; k += blockDim.x) a.push(p[k * es], k);
+  } else if constexpr (sizeof(T) == 4 && (OP == TX_SUM || OP == TX_MAX) && !std::is_same<T, unsigned char>::value) {
     // 128-bit path when the slice start is 16 B aligned
     int64_t head = lo;
     const int64_t mis = ((uintptr_t)(p + lo) & 15) / sizeof(T);
@@ -160,16 +165,14 @@ __global__ void __launch_bounds__(kThreads) row_kernel(const T* __restrict__ x, 
       for (int64_t k = threadIdx.x; k < nv; k += blockDim.x) {
         V q = __ldcs(pv4 + k);
         int64_t b = lo + 4 * k;
-        a.merge_pair(q.x, b); a.merge_pair(q.y, b + 1); a.merge_pair(q.z, b + 2); a.merge_pair(q.w, b + 3);
+        a.push(q.x, b); a.push(q.y, b + 1); a.push(q.z, b + 2); a.push(q.w, b + 3);
       }
-      for (int64_t t = lo + nv * 4 + threadIdx.x; t < hi; t += blockDim.x) a.merge_pair(p[t], t);
+      for (int64_t t = lo + nv * 4 + threadIdx.x; t < hi; t += blockDim.x) a.push(p[t], t);
     } else {
-      for (int64_t k = lo + threadIdx.x; k < hi; k += blockDim.x) a.merge_pair(p[k], k);
+      for (int64_t k = lo + threadIdx.x; k < hi; k += blockDim.x) a.push(p[k * es], k);
     }
   } else {
-    for (int64_t k = lo + threadIdx.x; k < hi; k += blockDim.x) {
-      if (OP == TX_SUM || OP == TX_MAX) a.push(p[k], k); else a.merge_pair(p[k], k);
-    }
+    for (int64_t k = lo + threadIdx.x; k < hi; k += blockDim.x) a.push(p[k * es], k);
   }
   a = block_reduce<T, OP>(a);
   if (threadIdx.x == 0) {
@@ -192,9 +195,7 @@ __global__ void __launch_bounds__(kThreads) row_warp_kernel(const T* __restrict_
   const T* p = x + row * rs;
   Acc<T, OP> a;
   a.init();
-  for (int64_t k = lane; k < R; k += 32) {
-    if (OP == TX_SUM || OP == TX_MAX) a.push(p[k * es], k); else a.merge_pair(p[k * es], k);
-  }
+  for (int64_t k = lane; k < R; k += 32) a.push(p[k * es], k);
   for (int off = 16; off > 0; off >>= 1) a.merge(shfl_down(a, off));
   if (lane == 0) {
     if (OP == TX_SUM || OP == TX_MAX) out[row] = a.v; else out_idx[row] = a.i;
@@ -304,7 +305,7 @@ __global__ void gen_kernel(const T* __restrict__ x, int64_t K, int64_t R, GenMet
   for (int64_t r = 0; r < R; ++r) {
     int64_t off = 0, u = r;
     for (int d = m.nr - 1; d >= 0; --d) { off += (u % m.rshape[d]) * m.rstride[d]; u /= m.rshape[d]; }
-    if (OP == TX_SUM || OP == TX_MAX) a.push(x[base + off], r); else a.merge_pair(x[base + off], r);
+    a.push(x[base + off], r);
   }
   if (OP == TX_SUM || OP == TX_MAX) out[o] = a.v; else out_idx[o] = a.i;
 }
@@ -398,56 +399,44 @@ static void make_plan(int op, const tx_tensor& x, uint32_t mask, int itemsz, Pla
   int mr = merge_dims(nr, rsh, rst);
   const int sms = sm_count();
   if (mk <= 1 && mr <= 1) {
-    int64_t kstride = mk == 1 ? kst[0] : 0;
-    int64_t rstride = mr == 1 ? rst[0] : 1;
-    if (R == 1 || rstride == 1) {
-      if (R <= 512 && K >= 8) {
-        p->form = ROWWARP;
-        p->ks = kstride;
-        p->es = 1;
-      } else {
-        p->form = ROW;
-        p->ks = kstride;
-        // split long rows so that at least ~4 CTAs per SM exist
-        int64_t want = (int64_t)sms * 4;
-        int64_t splits = 1;
-        if (K < want) {
-          splits = (want + K - 1) / K;
-          int64_t maxs = R / 4096;
-          if (splits > maxs) splits = maxs;
-          if (splits < 1) splits = 1;
-        }
-        p->splits = (int)splits;
-      }
-    } else if (kstride == 1 || K == 1) {
-      if (K == 1) {
-        // strided full reduce: treat as warp rows with element stride
-        p->form = ROWWARP;
-        p->ks = 0;
-        p->es = rstride;
-      } else {
-        p->form = COL;
-        p->rs = rstride;
-        int64_t colblocks = (K + 4 * kThreads - 1) / (4 * kThreads);
-        int64_t want = (int64_t)sms * 8;
-        int64_t splits = (want + colblocks - 1) / colblocks;
-        int64_t maxs = R / 64;
-        if (splits > maxs) splits = maxs;
-        if (splits > 65535) splits = 65535;
-        if (splits < 1) splits = 1;
-        p->splits = (int)splits;
-      }
-    } else if (R <= 512) {
+    const int64_t kstride = mk == 1 ? kst[0] : 0;
+    const int64_t rstride = mr == 1 ? rst[0] : 1;
+    if (kstride == 1 && K >= 512 && rstride != 1) {
+      // COL: kept dim contiguous and wide enough for coalesced 128-bit rows
+      p->form = COL;
+      p->rs = rstride;
+      int64_t colblocks = (K + 4 * kThreads - 1) / (4 * kThreads);
+      int64_t want = (int64_t)sms * 4;
+      int64_t splits = (want + colblocks - 1) / colblocks;
+      int64_t maxs = R / 256;
+      if (splits > maxs) splits = maxs;
+      if (splits > 65535) splits = 65535;
+      if (splits < 1) splits = 1;
+      p->splits = (int)splits;
+    } else if (R <= 512 && K >= 8) {
+      // one warp per output (softmax-sized rows, any element stride)
       p->form = ROWWARP;
       p->ks = kstride;
       p->es = rstride;
     } else {
-      p->form = GEN;
+      // one CTA (or a split of CTAs) per output, any element stride
+      p->form = ROW;
+      p->ks = kstride;
+      p->es = rstride;
+      int64_t want = (int64_t)sms * 4;
+      int64_t splits = 1;
+      if (K < want) {
+        splits = (want + K - 1) / K;
+        int64_t maxs = R / 4096;
+        if (splits > maxs) splits = maxs;
+        if (splits < 1) splits = 1;
+      }
+      p->splits = (int)splits;
     }
   } else {
     p->form = GEN;
   }
-  if (p->splits > 1) p->ws_partial = (size_t)p->splits * (size_t)p->K * (itemsz + 8);
+  if (p->splits > 1) p->ws_partial = (size_t)p->splits * (size_t)p->K * 16 + 64;
   if (op == TX_ARGMAX_ONEHOT) p->ws_idx = (size_t)p->K * 8;
 }
 
@@ -486,7 +475,7 @@ static int run(const tx_tensor& x, uint32_t mask, tx_tensor& y, char* ws, size_t
       unsigned gy = (unsigned)(rows < 65535 ? rows : 65535);
       unsigned gz = (unsigned)((rows + gy - 1) / gy);
       dim3 grid((unsigned)p.splits, gy, gz);
-      row_kernel<T, OP><<<grid, kThreads, 0, st>>>(xp, rows, p.R, p.ks, p.splits, out, out_idx, pv, pi);
+      row_kernel<T, OP><<<grid, kThreads, 0, st>>>(xp, rows, p.R, p.ks, p.es, p.splits, out, out_idx, pv, pi);
       if (p.splits > 1)
         finalize_splits<T, OP><<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(rows, p.splits, pv, pi, out, out_idx);
       break;
