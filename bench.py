@@ -372,6 +372,22 @@ def main():
             extra["mlp_b8192_1gpu"] = {"error": repr(e)[:300]}
         torch.cuda.empty_cache()
         try:
+            from paper_1605_02688_b200.dp import DataParallel
+            G = 65536
+            dp = DataParallel(world_size=ws, rank=rank)
+            fd, ms_d, cost_d = bench_mlp(T, C, G // ws, max(5, args.steps // 2), 3, lib_holder, dp=dp, n_global=G)
+            med = barrier_max(statistics.median(ms_d), ws)
+            extra["mlp_dp_global65536"] = {
+                "samples_per_s": round(G / (med * 1e-3), 1), "ms_per_step": round(med, 3), "n_gpus": ws,
+                "per_gpu_batch": G // ws, "scaling": "strong (fixed global batch)",
+                "tflops_total": round(MLP_FLOP_PER_SAMPLE * G / (med * 1e-3) / 1e12, 1),
+                "allreduce_buckets": len(fd._plans[next(iter(fd._plans))].buckets) if fd._plans else None,
+                "allreduce_bytes_per_step": 20037642 * 4 + 4, "cost_after": cost_d}
+            del fd
+        except Exception as e:
+            extra["mlp_dp_global65536"] = {"error": repr(e)[:300]}
+        torch.cuda.empty_cache()
+        try:
             ms_l, e2e_l, nl = bench_logreg(T, C, 20, 5, lib_holder)
             med = statistics.median(ms_l)
             extra["logreg_n600"] = {"samples_per_s": round(600 / (med * 1e-3), 1), "us_per_step": round(med * 1e3, 2),

@@ -259,3 +259,18 @@ def evaluate(outputs, bindings):
         else:
             res.append(np.asarray(o.get_value()))
     return res
+
+
+def evaluate_order(order, outputs, bindings, after_node=None):
+    """Like ``evaluate`` but over a given node order, calling
+    ``after_node(node, values)`` after each node (the data-parallel test uses
+    it to allreduce partial sums exactly where the device step does)."""
+    env = {var.id: np.asarray(val, dtype=np.dtype(var.type.dtype)) for var, val in bindings.items()}
+    for node in order:
+        args = [env[x.id] if x.id in env else np.asarray(x.value) for x in node.inputs]
+        res = [np.asarray(r) for r in run_node(node, args)]
+        if after_node is not None:
+            res = after_node(node, res) or res
+        for o, r in zip(node.outputs, res):
+            env[o.id] = r
+    return [env[o.id] if o.id in env else np.asarray(o.value) for o in outputs]

@@ -258,9 +258,18 @@ class CompiledFunction:
         self._plans: dict = {}
         self._consts: dict[int, object] = {}
         self._stream = None
+        self._comm_stream = None
         self.profile_nodes = False
         self._direct, self.order = self._schedule()
         self.thunks = {}
+        self.shard = None
+        if self.dp is not None:
+            from . import dp as _dp
+            self.shard = _dp.propagate(self.order, self.dp.input_states(self.input_vars))
+            for s, u in self.updates:
+                if self.shard.state.get(u.id, _dp.REPLICATED) not in (_dp.REPLICATED, _dp.PARTIAL):
+                    raise NotSupported(f"update of {s!r} depends on per-shard values without a reduction "
+                                       "over the data-parallel axis")
 
     # -- scheduling --------------------------------------------------------
     def _schedule(self):
@@ -390,7 +399,13 @@ class CompiledFunction:
         twin._lock = threading.Lock()
         twin._plans = {}
         twin._stream = None
+        twin._comm_stream = None
         return twin
+
+
+def native_dtype_code(dtype):
+    from .dtypes import DTYPE_CODE
+    return DTYPE_CODE[dtype]
 
 
 def _is_view_of(x, base) -> bool:
@@ -510,7 +525,10 @@ class StepPlan:
 
         # ---- shapes and layouts, node by node
         direct = fn._direct
-        self.pending_outputs = {}
+        partial_ids = set()
+        partial_vars = []
+        if fn.shard is not None:
+            partial_ids = {o.id for n in fn.shard.partial_nodes for o in n.outputs}
         for n in order:
             ins = [self.lay[x.id] for x in n.inputs]
             shapes = [l.shape for l in ins]
@@ -526,6 +544,12 @@ class StepPlan:
                 continue
             for o, s in zip(n.outputs, outs):
                 s = tuple(int(d) for d in s)
+                if o.id in partial_ids:
+                    nb = int(np.prod(s, dtype=np.int64)) * ITEMSIZE[o.type.dtype]
+                    st = Storage("bucket", nb, name="grad")
+                    self.lay[o.id] = Layout(st, 0, s, contiguous_strides(s), o.type.dtype)
+                    partial_vars.append((o, nb))
+                    continue
                 d = direct.get(o.id)
                 if d is not None:
                     sh, var = d
@@ -658,6 +682,25 @@ class StepPlan:
                for n in order if isinstance(n.op, (Elemwise, Composite))):
             self.flag = Storage("arena", 4, name="flag")
             self.flag.offset = alloc.alloc(4)
+        self.buckets = []  # (dtype, ptr, count, member vars)
+        if partial_vars:
+            from . import dp as _dp
+            info = []
+            for v, nb in sorted(partial_vars, key=lambda vn: pos[vn[0].owner.id]):
+                uses = [pos[c.id] for c in g.node_clients(v)]
+                info.append((v, nb, pos[v.owner.id], min(uses) if uses else None))
+            for members in _dp.make_buckets(info, fn.dp.bucket_bytes):
+                off, offs = 0, []
+                for v in members:
+                    offs.append(off)
+                    off += self.lay[v.id].numel * ITEMSIZE[v.type.dtype]
+                buf = t.zeros(max(off, ALIGN), dtype=t.uint8, device="cuda")
+                self.keep.append(buf)
+                for v, o in zip(members, offs):
+                    st = self.lay[v.id].storage
+                    st.ptr = buf.data_ptr() + o
+                count = off // ITEMSIZE[members[0].type.dtype]
+                self.buckets.append((members[0].type.dtype, buf.data_ptr(), count, members))
         self.arena_bytes = alloc.top
         self.arena = t.empty(max(alloc.top, ALIGN), dtype=t.uint8, device="cuda")
         base = self.arena.data_ptr()
@@ -673,11 +716,28 @@ class StepPlan:
         # ---- launch closures
         self.launches = []  # (node or None, fn)
         self._cur = None
-        for n in order:
-            if getattr(n.op, "view_capable", False):
-                continue
-            self._cur = n
-            n.op.lower(n, self)
+        bucket_after, bucket_wait = {}, {}
+        if self.buckets:
+            comm = fn.dp.comm(lib)
+            if fn._comm_stream is None:
+                fn._comm_stream = lib.stream_create()
+            for bi, (dt, ptr, count, members) in enumerate(self.buckets):
+                last = max(pos[v.owner.id] for v in members)
+                bucket_after.setdefault(last, []).append(bi)
+                first_use = min((pos[c.id] for v in members for c in g.node_clients(v)), default=None)
+                if first_use is not None:
+                    bucket_wait.setdefault(first_use, []).append(bi)
+            self._bucket_events = [(lib.event_create(), lib.event_create()) for _ in self.buckets]
+        for i, n in enumerate(order):
+            for bi in bucket_wait.get(i, []):
+                self._emit_bucket_wait(bi)
+            if not getattr(n.op, "view_capable", False):
+                self._cur = n
+                n.op.lower(n, self)
+            for bi in bucket_after.get(i, []):
+                self._emit_allreduce(bi, comm)
+        for bi in range(len(self.buckets)):
+            self._emit_bucket_wait(bi)
         self._cur = None
         for src, dst in self.tail_copies:
             self._emit_copy(src, dst)
@@ -808,6 +868,33 @@ class StepPlan:
         def launch(stream):
             lib.check(f(A, B, C, epi, mode, ws, wsb, stream))
         self.add_launch(launch)
+
+    def _emit_allreduce(self, bi, comm):
+        lib, cs = self.lib, self.fn._comm_stream
+        dt, ptr, count, _ = self.buckets[bi]
+        ready, done = self._bucket_events[bi]
+        code = native_dtype_code(dt)
+        f = lib.lib.tx_nccl_allreduce_sum
+
+        def launch(stream):
+            lib.event_record(ready, stream)
+            lib.stream_wait_event(cs, ready)
+            lib.check(f(comm, ptr, count, code, cs))
+            lib.event_record(done, cs)
+        self.launches.append((None, launch))
+
+    def _emit_bucket_wait(self, bi):
+        if getattr(self, "_waited", None) is None:
+            self._waited = set()
+        if bi in self._waited:
+            return
+        self._waited.add(bi)
+        lib = self.lib
+        done = self._bucket_events[bi][1]
+
+        def launch(stream):
+            lib.stream_wait_event(stream, done)
+        self.launches.append((None, launch))
 
     def _emit_copy(self, src: Layout, dst: Layout):
         lib = self.lib

@@ -107,3 +107,22 @@ def test_reductions_full_size():
         ref = O.reduce_sum(X, ax)
         bound = 2e-6 * (np.abs(X).sum(axis=ax) if len(ax) == 1 else np.abs(X).sum())
         assert np.all(np.abs(s - ref) <= bound)
+
+
+def test_data_parallel_single_rank_matches_plain_step():
+    """The DP path (sharding propagation, gradient buckets, NCCL allreduce
+    captured in the step graph) on one rank equals the plain step bit-for-bit."""
+    from paper_1605_02688_b200.dp import DataParallel
+    B, H = 256, 512
+    x, y = C.inputs_mlp(B=B)
+    ga = C.build_mlp(T, B=B, H=H)
+    fa = T.compile(ga["inputs"], ga["outputs"], updates=ga["updates"])
+    gb = C.build_mlp(T, B=B, H=H)
+    dp = DataParallel(world_size=1, rank=0, bucket_bytes=1 << 20)
+    fb = T.compile(gb["inputs"], gb["outputs"], updates=gb["updates"], data_parallel=dp)
+    assert len(fb.shard.partial_nodes) == 7
+    for _ in range(3):
+        ca, cb = fa(x, y)[0], fb(x, y)[0]
+        assert ca == cb
+    for pa, pb in zip(ga["params"], gb["params"]):
+        assert np.array_equal(pa.get_value(), pb.get_value())
