@@ -960,31 +960,30 @@ class StepPlan:
                 profile.record_node(n.id, 0.0, 0)
 
     def download_outputs(self, stream):
+        """D2H of the explicit outputs into fresh pinned host blocks (torch's
+        caching host allocator), returned as NumPy views — each call returns
+        new arrays (reference runtime.py:412-414) without a host-side copy."""
         t = _torch()
-        if self._pinned_out is None:
-            self._pinned_out = []
-            for kind, lay in self.out_lays:
-                if kind == "dev":
-                    nb = lay.numel * ITEMSIZE[lay.dtype]
-                    self._pinned_out.append(t.empty(max(nb, 1), dtype=t.uint8, pin_memory=True))
-                else:
-                    self._pinned_out.append(None)
-        for (kind, lay), pin in zip(self.out_lays, self._pinned_out):
-            if kind == "dev":
-                nb = lay.numel * ITEMSIZE[lay.dtype]
-                if nb:
-                    self.lib.memcpy(pin.data_ptr(), self.tx(lay).data, nb, 1, stream)
+        pins = []
+        for kind, lay in self.out_lays:
+            if kind != "dev":
+                pins.append(None)
+                continue
+            nb = lay.numel * ITEMSIZE[lay.dtype]
+            pin = t.empty(max(nb, 1), dtype=t.uint8, pin_memory=True)
+            if nb:
+                self.lib.memcpy(pin.data_ptr(), self.tx(lay).data, nb, 1, stream)
+            pins.append(pin)
         self.lib.stream_sync(stream)
         self._host_refs = None
         outs = []
-        for (kind, lay), pin in zip(self.out_lays, self._pinned_out):
+        for (kind, lay), pin in zip(self.out_lays, pins):
             if kind == "const":
                 outs.append(np.array(lay, copy=True))
                 continue
             nb = lay.numel * ITEMSIZE[lay.dtype]
-            raw = pin.numpy()[:nb]
             dt = np.uint8 if lay.dtype == "bool" else np_dtype(lay.dtype)
-            arr = raw.view(dt).reshape(lay.shape).copy()
+            arr = pin.numpy()[:nb].view(dt).reshape(lay.shape)
             if lay.dtype == "bool":
                 arr = arr.astype(np.bool_)
             outs.append(arr)
