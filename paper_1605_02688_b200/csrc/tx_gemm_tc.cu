@@ -31,17 +31,25 @@
 namespace tx {
 namespace {
 
+// Per-CTA tile: BM rows (one TMEM lane each) x BN accumulator columns.  With
+// CG = 2 a CTA pair computes a 256 x BN tile with one cta_group::2 MMA
+// stream: each CTA stages its 128 rows of A and half of B's columns, the
+// leader issues, TMEM holds each CTA's own 128 rows.
 constexpr int BM = 128;
 constexpr int BN = 256;
 constexpr int BK = 32;  // 32 fp32 = 128 B = one swizzle span
-constexpr int STAGES = 4;
-constexpr int A_BYTES = BM * BK * 4;  // 16 KB
-constexpr int B_BYTES = BN * BK * 4;  // 32 KB
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int NUM_THREADS = 192;
 constexpr int TMEM_COLS = 512;
 constexpr int GROUP_M = 16;
-constexpr size_t SMEM_BYTES = 1024 /*align slack*/ + (size_t)STAGES * STAGE_BYTES + 256 /*barriers*/;
+
+template <int CG>
+struct Cfg {
+  static constexpr int A_BYTES = BM * BK * 4;              // 16 KB
+  static constexpr int B_BYTES = (BN / CG) * BK * 4;       // 32 KB (CG=1) / 16 KB (CG=2)
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = CG == 1 ? 4 : 6;
+  static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + 256;
+};
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -75,6 +83,30 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
+// 2-SM load: executed by both CTAs of the pair; the transaction bytes land on
+// the LEADER's barrier (peer bit of the shared::cluster address cleared).
+constexpr uint32_t kPeerMask = 0xFEFFFFFFu;
+__device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
+      "[%2];" ::"r"(su32(dst)),
+      "l"((uint64_t)map), "r"(su32(bar) & kPeerMask), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// arrive on the leader CTA's copy of a barrier
+__device__ __forceinline__ void mbar_arrive_leader(uint64_t* b) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(su32(b) & kPeerMask) : "memory");
+}
+
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -92,18 +124,40 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
   return d;
 }
 
+template <int CG>
 __device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(a), "l"(b), "r"(idesc), "r"(acc)
-      : "memory");
+  if constexpr (CG == 1) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+  }
 }
 
+// tcgen05.commit: arrive (once) on a barrier when all prior MMAs of this
+// thread complete; CG = 2 multicasts the arrive to both CTAs of the pair.
+template <int CG>
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))
-               : "memory");
+  if constexpr (CG == 1) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))
+                 : "memory");
+  } else {
+    const uint16_t mask = 0x3;
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            su32(bar)),
+        "h"(mask)
+        : "memory");
+  }
 }
 
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
@@ -137,12 +191,16 @@ __device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int& mb
   nb = r / gsz;
 }
 
+template <int CG>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                    const TcParams p) {
+  using K_ = Cfg<CG>;
+  constexpr int STAGES = K_::STAGES;
+  constexpr int BNL = BN / CG;  // B columns staged by this CTA
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint64_t* full = (uint64_t*)(smem + STAGES * STAGE_BYTES);
+  uint64_t* full = (uint64_t*)(smem + STAGES * K_::STAGE_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -150,20 +208,31 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const uint32_t rank = CG == 2 ? cluster_rank() : 0;
+  const bool leader = rank == 0;
+  const int cluster_id = blockIdx.x / CG;
+  const int num_clusters = gridDim.x / CG;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }
-    for (int b = 0; b < 2; ++b) { mbar_init(tfull + b, 1); mbar_init(tempty + b, 4); }
+    for (int b = 0; b < 2; ++b) { mbar_init(tfull + b, 1); mbar_init(tempty + b, 4 * CG); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
-                 "r"(TMEM_COLS)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if constexpr (CG == 1) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
+                   "r"(TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
+                   "r"(TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int num_kb = (p.K + BK - 1) / BK;
@@ -174,84 +243,92 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&mapB) : "memory");
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+      for (int t = cluster_id; t < p.num_tiles; t += num_clusters) {
         int mb, nb;
         tile_coords(t, p.num_m, p.num_n, mb, nb);
-        const int m0 = mb * BM, n0 = nb * BN;
+        const int m0 = mb * BM * CG + (int)rank * BM;   // this CTA's rows
+        const int n0 = nb * BN + (int)rank * BNL;       // this CTA's half of B
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(empty + stage, phase ^ 1);
-          uint8_t* sa = smem + stage * STAGE_BYTES;
-          uint8_t* sb = sa + A_BYTES;
-          mbar_expect_tx(full + stage, STAGE_BYTES);
+          uint8_t* sa = smem + stage * K_::STAGE_BYTES;
+          uint8_t* sb = sa + K_::A_BYTES;
+          if (leader) mbar_expect_tx(full + stage, K_::STAGE_BYTES * CG);
           const int k0 = kb * BK;
+          auto load = [&](void* dst, const CUtensorMap* map, int c0, int c1) {
+            if constexpr (CG == 1) tma_load_2d(dst, map, full + stage, c0, c1);
+            else tma_load_2d_2sm(dst, map, full + stage, c0, c1);
+          };
           if (p.a_mn) {
 #pragma unroll
-            for (int j = 0; j < BM / 32; ++j) tma_load_2d(sa + j * 4096, &mapA, full + stage, m0 + 32 * j, k0);
+            for (int j = 0; j < BM / 32; ++j) load(sa + j * 4096, &mapA, m0 + 32 * j, k0);
           } else {
-            tma_load_2d(sa, &mapA, full + stage, k0, m0);
+            load(sa, &mapA, k0, m0);
           }
           if (p.b_mn) {
 #pragma unroll
-            for (int j = 0; j < BN / 32; ++j) tma_load_2d(sb + j * 4096, &mapB, full + stage, n0 + 32 * j, k0);
+            for (int j = 0; j < BNL / 32; ++j) load(sb + j * 4096, &mapB, n0 + 32 * j, k0);
           } else {
-            tma_load_2d(sb, &mapB, full + stage, k0, n0);
+            load(sb, &mapB, k0, n0);
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)p.a_mn << 15) |
-                           ((uint32_t)p.b_mn << 16) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
-    // descriptor geometry per operand layout
-    // K-major: LBO unused (16 B), SBO = 1024 B between 8-row atoms, +32 B per k-step.
-    // MN-major: LBO = 4096 B between 32-element MN blocks (one TMA box each),
-    //           SBO = 512 B between 4-row K groups, +1024 B per k-step (8 rows).
-    const uint32_t a_lbo = p.a_mn ? 4096u : 16u, a_sbo = p.a_mn ? 512u : 1024u, a_step = p.a_mn ? 1024u : 32u;
-    const uint32_t b_lbo = p.b_mn ? 4096u : 16u, b_sbo = p.b_mn ? 512u : 1024u, b_step = p.b_mn ? 1024u : 32u;
-    const uint32_t a_lay = p.a_mn ? 1u : 2u, b_lay = p.b_mn ? 1u : 2u;
-    int stage = 0;
-    uint32_t phase = 0;
-    int it = 0;
-    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
-      const int buf = it & 1;
-      const uint32_t use = (uint32_t)(it >> 1);
-      mbar_wait(tempty + buf, (use & 1) ^ 1);
-      tc_fence_after();
-      const uint32_t tmem_d = tmem_base + (uint32_t)(buf * BN);
-      for (int kb = 0; kb < num_kb; ++kb) {
-        mbar_wait(full + stage, phase);
+    if (leader) {
+      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)p.a_mn << 15) |
+                             ((uint32_t)p.b_mn << 16) | ((uint32_t)(BN >> 3) << 17) |
+                             ((uint32_t)((BM * CG) >> 4) << 24);
+      // descriptor geometry per operand layout
+      // K-major: LBO unused (16 B), SBO = 1024 B between 8-row atoms, +32 B per k-step.
+      // MN-major: LBO = 4096 B between 32-element MN blocks (one TMA box each),
+      //           SBO = 512 B between 4-row K groups, +1024 B per k-step (8 rows).
+      const uint32_t a_lbo = p.a_mn ? 4096u : 16u, a_sbo = p.a_mn ? 512u : 1024u, a_step = p.a_mn ? 1024u : 32u;
+      const uint32_t b_lbo = p.b_mn ? 4096u : 16u, b_sbo = p.b_mn ? 512u : 1024u, b_step = p.b_mn ? 1024u : 32u;
+      const uint32_t a_lay = p.a_mn ? 1u : 2u, b_lay = p.b_mn ? 1u : 2u;
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = cluster_id; t < p.num_tiles; t += num_clusters, ++it) {
+        const int buf = it & 1;
+        const uint32_t use = (uint32_t)(it >> 1);
+        mbar_wait(tempty + buf, (use & 1) ^ 1);
         tc_fence_after();
-        if (lane == 0) {
-          const uint32_t sa = su32(smem + stage * STAGE_BYTES);
-          const uint32_t sb = sa + A_BYTES;
+        const uint32_t tmem_d = tmem_base + (uint32_t)(buf * BN);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(full + stage, phase);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t sa = su32(smem + stage * K_::STAGE_BYTES);
+            const uint32_t sb = sa + K_::A_BYTES;
 #pragma unroll
-          for (int kk = 0; kk < BK / 8; ++kk) {
-            const uint64_t da = sdesc(sa + kk * a_step, a_lbo, a_sbo, a_lay);
-            const uint64_t db = sdesc(sb + kk * b_step, b_lbo, b_sbo, b_lay);
-            umma_tf32(tmem_d, da, db, idesc, (kb | kk) != 0);
+            for (int kk = 0; kk < BK / 8; ++kk) {
+              const uint64_t da = sdesc(sa + kk * a_step, a_lbo, a_sbo, a_lay);
+              const uint64_t db = sdesc(sb + kk * b_step, b_lbo, b_sbo, b_lay);
+              umma_tf32<CG>(tmem_d, da, db, idesc, (kb | kk) != 0);
+            }
+            umma_commit<CG>(empty + stage);
           }
-          umma_commit(empty + stage);
+          __syncwarp();
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
+        if (lane == 0) umma_commit<CG>(tfull + buf);
         __syncwarp();
-        if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
-      if (lane == 0) umma_commit(tfull + buf);
-      __syncwarp();
     }
   } else {
     // epilogue warps 2..5 -> TMEM lane quarter (warp % 4)
     const int q = warp & 3;
     int it = 0;
     const bool vec_ok = (p.ldc % 4 == 0) && (((uintptr_t)p.C & 15) == 0);
-    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
+    for (int t = cluster_id; t < p.num_tiles; t += num_clusters, ++it) {
       int mb, nb;
       tile_coords(t, p.num_m, p.num_n, mb, nb);
       const int buf = it & 1;
       const uint32_t use = (uint32_t)(it >> 1);
       mbar_wait(tfull + buf, use & 1);
       tc_fence_after();
-      const int row = mb * BM + q * 32 + lane;
+      const int row = mb * BM * CG + (int)rank * BM + q * 32 + lane;
       const uint32_t taddr = tmem_base + (uint32_t)(buf * BN) + ((uint32_t)(q * 32) << 16);
       float* crow = p.C + (int64_t)row * p.ldc;
       for (int c = 0; c < BN; c += 16) {
@@ -268,20 +345,30 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             for (int i = 0; i < 16; i += 4)
               *reinterpret_cast<float4*>(crow + n + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
           } else {
-            for (int i = 0; i < 16 && n + i < p.N; ++i) crow[n + i] = v[i];
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              if (n + i < p.N) crow[n + i] = v[i];
           }
         }
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(tempty + buf);
+      if (lane == 0) {
+        if constexpr (CG == 1) mbar_arrive(tempty + buf);
+        else mbar_arrive_leader(tempty + buf);
+      }
     }
   }
-  __syncthreads();
+  tc_fence_before();
+  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS)
-                 : "memory");
+    if constexpr (CG == 1)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS)
+                   : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS)
+                   : "memory");
   }
 }
 
@@ -291,7 +378,7 @@ typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void
                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 static EncodeFn g_encode = nullptr;
 static std::once_flag g_once;
-static bool g_attr_set = false;
+static bool g_attr_set[3] = {false, false, false};
 
 static EncodeFn encode_fn() {
   std::call_once(g_once, [] {
@@ -343,12 +430,19 @@ int gemm_tc(const G& g, cudaStream_t st) {
   if (rc) return fail(rc, "tx_gemm: operand layout not eligible for the tcgen05 path");
   const bool a_mn = !(g.sak == 1 && g.sam % 4 == 0 && g.sam >= g.K);
   const bool b_mn = (g.sbn == 1 && g.sbk % 4 == 0 && g.sbk >= g.N);
+  // 2-CTA pairs (cta_group::2) unless TX_GEMM_CG=1 or the problem is too small
+  // to give every SM pair a tile
+  const char* cg_s = getenv("TX_GEMM_CG");
+  const int cg_env = cg_s ? atoi(cg_s) : 2;
+  int cg = cg_env == 1 ? 1 : 2;
+  if (cg == 2 && g.M <= BM) cg = 1;
+  const int bnl = BN / cg;
   CUtensorMap ma, mb;
   if (a_mn) rc = make_map(&ma, g.A, g.M, g.K, g.sak, 32, 32, true);
   else rc = make_map(&ma, g.A, g.K, g.M, g.sam, 32, BM, false);
   if (rc) return rc;
   if (b_mn) rc = make_map(&mb, g.B, g.N, g.K, g.sbk, 32, 32, true);
-  else rc = make_map(&mb, g.B, g.K, g.N, g.sbn, 32, BN, false);
+  else rc = make_map(&mb, g.B, g.K, g.N, g.sbn, 32, bnl, false);
   if (rc) return rc;
   TcParams p;
   p.C = (float*)g.C;
@@ -358,16 +452,37 @@ int gemm_tc(const G& g, cudaStream_t st) {
   p.K = (int)g.K;
   p.a_mn = a_mn;
   p.b_mn = b_mn;
-  p.num_m = (int)((g.M + BM - 1) / BM);
+  p.num_m = (int)((g.M + BM * cg - 1) / (BM * cg));
   p.num_n = (int)((g.N + BN - 1) / BN);
   p.num_tiles = p.num_m * p.num_n;
   p.epi = g.epi_f;
-  if (!g_attr_set) {
-    TX_CUDA(cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES));
-    g_attr_set = true;
+  const int units = sm_count() / cg;
+  const int nclusters = p.num_tiles < units ? p.num_tiles : units;
+  if (cg == 1) {
+    if (!g_attr_set[1]) {
+      TX_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<1>::SMEM));
+      g_attr_set[1] = true;
+    }
+    tc_gemm_kernel<1><<<nclusters, NUM_THREADS, Cfg<1>::SMEM, st>>>(ma, mb, p);
+  } else {
+    if (!g_attr_set[2]) {
+      TX_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<2>::SMEM));
+      g_attr_set[2] = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * nclusters, 1, 1);
+    cfg.blockDim = dim3(NUM_THREADS, 1, 1);
+    cfg.dynamicSmemBytes = Cfg<2>::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    TX_CUDA(cudaLaunchKernelEx(&cfg, tc_gemm_kernel<2>, ma, mb, p));
   }
-  int grid = p.num_tiles < sm_count() ? p.num_tiles : sm_count();
-  tc_gemm_kernel<<<grid, NUM_THREADS, SMEM_BYTES, st>>>(ma, mb, p);
   TX_CUDA(cudaGetLastError());
   return TX_OK;
 }

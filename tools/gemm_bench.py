@@ -1,0 +1,58 @@
+"""TF32 GEMM microbenchmark over the MLP shapes and layouts (CUDA events on
+the VM stream; correctness vs an fp64 product on a sample of rows).
+
+    TX_GEMM_CG=1|2 python tools/gemm_bench.py
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_1605_02688_b200 as T  # noqa: E402
+from paper_1605_02688_b200 import native  # noqa: E402
+
+SHAPES = [  # (name, M, N, K, a_transposed, b_transposed)
+    ("G1 x.W1", 8192, 4096, 784, False, False),
+    ("G2 h1.W2", 8192, 4096, 4096, False, False),
+    ("G6 dz2.W2T", 8192, 4096, 4096, False, True),
+    ("G7 h1T.dz2", 4096, 4096, 8192, True, False),
+    ("G8 xT.dz1", 784, 4096, 8192, True, False),
+    ("TT", 4096, 4096, 4096, True, True),
+    ("8192^3 NN", 8192, 8192, 8192, False, False),
+]
+
+
+def main():
+    torch.cuda.set_device(0)
+    lib = native.device_library(0)
+    cg = os.environ.get("TX_GEMM_CG", "2")
+    for name, M, N, K, ta, tb in SHAPES:
+        a = torch.randn(K, M, device="cuda") if ta else torch.randn(M, K, device="cuda")
+        b = torch.randn(N, K, device="cuda") if tb else torch.randn(K, N, device="cuda")
+        va, vb = T.matrix("a", dtype="float32"), T.matrix("b", dtype="float32")
+        f = T.compile([va, vb], T.dot(T.transpose(va) if ta else va, T.transpose(vb) if tb else vb))
+        out = f.call_device(a, b, sync=True)
+        for _ in range(3):
+            f.call_device(a, b)
+        ev = [(lib.event_create(), lib.event_create()) for _ in range(10)]
+        for e0, e1 in ev:
+            lib.event_record(e0, f._stream)
+            f.call_device(a, b)
+            lib.event_record(e1, f._stream)
+        lib.stream_sync(f._stream)
+        ms = sorted(lib.elapsed_ms(e0, e1) for e0, e1 in ev)[len(ev) // 2]
+        out = f.call_device(a, b, sync=True)
+        A = (a.T if ta else a)
+        B = (b.T if tb else b)
+        rows = torch.randint(0, M, (64,), device="cuda")
+        ref = (A[rows].double() @ B.double())
+        bound = (A[rows].abs().double() @ B.abs().double())
+        err = ((out[rows].double() - ref).abs() / (bound + 1e-30)).max().item()
+        tf = 2 * M * N * K / (ms * 1e-3) / 1e12
+        print(f"CG={cg} {name:12s} M={M} N={N} K={K}: {ms:.3f} ms {tf:7.1f} TFLOP/s  max err/bound {err:.2e}", flush=True)
+
+
+if __name__ == "__main__":
+    main()
