@@ -106,6 +106,14 @@ int tx_ew_check(const char* source, const char* name, size_t* cubin_bytes);
 int tx_ew_launch(void* kernel, int n_out, int n_in, const tx_tensor* ops, int* err_flag, void* stream);
 int tx_ew_destroy(void* kernel);
 
+/* Generated single-entry kernels (row-fused softmax / cross-entropy regions:
+ * the composed graph of SURVEY Appendix B run as one warp-per-row kernel).
+ * `entry` names the extern "C" kernel; it takes one by-value argument
+ * struct, passed here by pointer. */
+int tx_kernel_compile(const char* source, const char* name, const char* entry, void** kernel);
+int tx_kernel_launch(void* kernel, unsigned grid, unsigned block, void* args, void* stream);
+int tx_kernel_destroy(void* kernel);
+
 /* ------------------------------------------------------------ reductions
  * Replaces Sum/Max/ArgmaxOnehot.perform (reference ops/reductions.py:87-188)
  * and adds an index argmax.  axes_mask bit i = reduce dim i. */
@@ -125,10 +133,20 @@ enum {
   TX_GEMM_TC = 2       /* force tcgen05 (error if the layout is ineligible) */
 };
 /* Optional fused epilogue applied to the accumulator before the store. */
-enum { TX_EPI_NONE = 0, TX_EPI_BIAS = 1, TX_EPI_BIAS_TANH = 2, TX_EPI_MUL_1MSQR = 3 };
+/* Fused epilogues, applied per output element with IEEE round-to-nearest
+ * (no FMA contraction) so they round exactly like the elementwise nodes they
+ * replace (the compile-time rewrite fuse_gemm_epilogue matches them):
+ *   BIAS            C = b[n] + acc                          add(b, dot)
+ *   BIAS_TANH       C = tanh(b[n] + acc)
+ *   MUL_1MSQR       C = acc * (1 - h^2)
+ *   BIAS_TANH_DUAL  C = tanh(b[n] + acc), C2 = 1 - C^2       the MLP forward composite
+ *   MUL_AUX         C = acc * g[m,n]                        mul(dot, g) in the backward */
+enum { TX_EPI_NONE = 0, TX_EPI_BIAS = 1, TX_EPI_BIAS_TANH = 2, TX_EPI_MUL_1MSQR = 3, TX_EPI_BIAS_TANH_DUAL = 4,
+       TX_EPI_MUL_AUX = 5 };
 typedef struct tx_epilogue {
   int32_t kind;
-  tx_tensor aux; /* BIAS*: bias row [N]; MUL_1MSQR: h [M,N] (C = acc*(1-h^2)) */
+  tx_tensor aux;  /* BIAS*: bias row [N]; MUL_*: [M,N] operand */
+  tx_tensor out2; /* BIAS_TANH_DUAL: second output [M,N] */
 } tx_epilogue;
 int tx_gemm_workspace(const tx_tensor* A, const tx_tensor* B, const tx_tensor* C, int mode,
                       size_t* bytes);

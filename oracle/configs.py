@@ -116,7 +116,8 @@ class CpuFunction:
         repl = {v: Variable(v.type, v.name) for v in full}
         cloned, _ = clone_outputs(outs + uvals, repl)
         self.fg = FunctionGraph([repl[v] for v in full], cloned)
-        run_preset(self.fg, preset, exclude=exclude)
+        # the reference has no GEMM epilogues: keep its node list
+        run_preset(self.fg, preset, exclude=tuple(exclude) + ("fuse_gemm_epilogue",))
         self.in_vars = [repl[v] for v in inputs]
         self.sh_vars = [repl[v] for v in found]
         self.n_out = len(outs)

@@ -226,6 +226,14 @@ def run_node(node, args):
         return [argmax_index(args[0], op.axes)]
     if name == "dot":
         return [dot(*args)]
+    if name == "dot_epilogue":  # the device's fused form of dot + its consumer
+        z = dot(args[0], args[1])
+        if op.kind == 1:
+            return [elemwise("add", [args[2], z])]
+        if op.kind == 4:
+            h = elemwise("tanh", [elemwise("add", [args[2], z])])
+            return [h, elemwise("sub", [np.asarray(1, dtype=h.dtype), elemwise("sqr", [h])])]
+        return [elemwise("mul", [z, args[2]])]
     if name == "dimshuffle":
         return [dimshuffle(args[0], op.pattern)]
     raise NotImplementedError(f"oracle has no kernel for op {name!r}")

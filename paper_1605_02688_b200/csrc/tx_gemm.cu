@@ -32,16 +32,26 @@ int build(const tx_tensor* A, const tx_tensor* B, const tx_tensor* C, const tx_e
   g->scn = C->shape[1] == 1 ? 1 : C->strides[1];
   if (epi && epi->kind != TX_EPI_NONE) {
     TX_CHECK(epi->aux.dtype == A->dtype, TX_E_ARG, "tx_gemm: epilogue operand dtype");
+    TX_CHECK(epi->kind >= TX_EPI_BIAS && epi->kind <= TX_EPI_MUL_AUX, TX_E_ARG, "tx_gemm: unknown epilogue");
     int64_t s0 = 0, s1 = 0;
-    if (epi->kind == TX_EPI_MUL_1MSQR) {
+    if (epi->kind == TX_EPI_MUL_1MSQR || epi->kind == TX_EPI_MUL_AUX) {
       TX_CHECK(epi->aux.ndim == 2 && epi->aux.shape[0] == g->M && epi->aux.shape[1] == g->N, TX_E_ARG,
-               "tx_gemm: epilogue h must be [M,N]");
+               "tx_gemm: epilogue operand must be [M,N]");
       s0 = epi->aux.strides[0];
       s1 = epi->aux.strides[1];
     } else {
       const tx_tensor& b = epi->aux;
       TX_CHECK(b.ndim >= 1 && b.shape[b.ndim - 1] == g->N, TX_E_ARG, "tx_gemm: bias must end in N");
       s1 = b.shape[b.ndim - 1] == 1 ? 0 : b.strides[b.ndim - 1];
+    }
+    if (epi->kind == TX_EPI_BIAS_TANH_DUAL) {
+      const tx_tensor& o = epi->out2;
+      TX_CHECK(o.dtype == A->dtype && o.ndim == 2 && o.shape[0] == g->M && o.shape[1] == g->N, TX_E_ARG,
+               "tx_gemm: second epilogue output must be [M,N]");
+      g->epi_f.out2 = (float*)o.data;
+      g->epi_d.out2 = (double*)o.data;
+      g->epi_f.o0 = g->epi_d.o0 = o.strides[0];
+      g->epi_f.o1 = g->epi_d.o1 = o.strides[1];
     }
     g->epi_f.kind = g->epi_d.kind = epi->kind;
     g->epi_f.aux = (const float*)epi->aux.data;
@@ -74,6 +84,8 @@ G transposed(const G& g) {
   t.scm = g.scn; t.scn = g.scm;
   std::swap(t.epi_f.s0, t.epi_f.s1);
   std::swap(t.epi_d.s0, t.epi_d.s1);
+  std::swap(t.epi_f.o0, t.epi_f.o1);
+  std::swap(t.epi_d.o0, t.epi_d.o1);
   return t;
 }
 

@@ -9,11 +9,16 @@ namespace tx {
 // Fused epilogue, evaluated per output element with IEEE round-to-nearest
 // intrinsics (no FMA contraction) so that it rounds exactly like the unfused
 // elementwise nodes it replaces (add(b, dot) -> tanh, mul(dot, 1 - sqr(h))).
+// apply() returns the primary output value; the DUAL kind also stores its
+// second output as a side effect, so every GEMM path (tcgen05, skinny, SIMT)
+// supports every epilogue through the same call.
 template <class T>
 struct Epi {
   int kind = TX_EPI_NONE;
   const T* aux = nullptr;
   int64_t s0 = 0, s1 = 0;  // aux strides (bias: s1 only)
+  T* out2 = nullptr;
+  int64_t o0 = 0, o1 = 0;  // out2 strides
   __device__ __forceinline__ T apply(T acc, int64_t m, int64_t n) const;
 };
 
@@ -26,6 +31,12 @@ __device__ __forceinline__ float Epi<float>::apply(float acc, int64_t m, int64_t
       float h = aux[m * s0 + n * s1];
       return __fmul_rn(acc, __fsub_rn(1.0f, __fmul_rn(h, h)));
     }
+    case TX_EPI_BIAS_TANH_DUAL: {
+      const float h = tanhf(__fadd_rn(aux[n * s1], acc));
+      out2[m * o0 + n * o1] = __fsub_rn(1.0f, __fmul_rn(h, h));
+      return h;
+    }
+    case TX_EPI_MUL_AUX: return __fmul_rn(acc, aux[m * s0 + n * s1]);
   }
   return acc;
 }
@@ -39,6 +50,12 @@ __device__ __forceinline__ double Epi<double>::apply(double acc, int64_t m, int6
       double h = aux[m * s0 + n * s1];
       return __dmul_rn(acc, __dsub_rn(1.0, __dmul_rn(h, h)));
     }
+    case TX_EPI_BIAS_TANH_DUAL: {
+      const double h = tanh(__dadd_rn(aux[n * s1], acc));
+      out2[m * o0 + n * o1] = __dsub_rn(1.0, __dmul_rn(h, h));
+      return h;
+    }
+    case TX_EPI_MUL_AUX: return __dmul_rn(acc, aux[m * s0 + n * s1]);
   }
   return acc;
 }

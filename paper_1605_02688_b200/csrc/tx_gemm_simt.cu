@@ -101,23 +101,32 @@ __global__ void __launch_bounds__(256) rowdot_kernel(const float* __restrict__ A
       }
     }
     __syncthreads();
+    if (vec && kc == RD_KC) {
+      // each B vector (NN float4 from smem) is reused by the warp's R rows:
+      // R independent 128-bit A loads in flight, NN/R smem loads per A load
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int64_t m = row0 + r;
-      if (m >= M) break;
-      const float* a = A + m * sam + k0;
-      if (vec && kc == RD_KC) {
+      for (int j = 0; j < RD_KC / 128; ++j) {
+        const int kk = j * 128 + lane * 4;
+        float4 bv[NN];
 #pragma unroll
-        for (int j = 0; j < RD_KC / 128; ++j) {
-          const int kk = j * 128 + lane * 4;
-          const float4 av = __ldg(reinterpret_cast<const float4*>(a + kk));
+        for (int n = 0; n < NN; ++n) bv[n] = *reinterpret_cast<const float4*>(&Bt[n][kk]);
+        float4 av[R];
 #pragma unroll
-          for (int n = 0; n < NN; ++n) {
-            const float4 bv = *reinterpret_cast<const float4*>(&Bt[n][kk]);
-            acc[r][n] += av.x * bv.x + av.y * bv.y + av.z * bv.z + av.w * bv.w;
-          }
-        }
-      } else {
+        for (int r = 0; r < R; ++r)
+          av[r] = (row0 + r < M) ? __ldg(reinterpret_cast<const float4*>(A + (row0 + r) * sam + k0 + kk))
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+          for (int n = 0; n < NN; ++n)
+            acc[r][n] += av[r].x * bv[n].x + av[r].y * bv[n].y + av[r].z * bv[n].z + av[r].w * bv[n].w;
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int64_t m = row0 + r;
+        if (m >= M) break;
+        const float* a = A + m * sam + k0;
         for (int kk = lane; kk < kc; kk += 32) {
           const float av = __ldg(a + kk);
 #pragma unroll
@@ -181,7 +190,8 @@ __global__ void __launch_bounds__(256) outer_kernel(const float* __restrict__ A,
       for (int j = 0; j < 4; ++j) o[j] += av * b[k][j];
     }
 #pragma unroll
-    for (int j = 0; j < 4; ++j) o[j] = epi.apply(o[j], m, n0 + j);
+    for (int j = 0; j < 4; ++j)
+      if (n0 + j < N) o[j] = epi.apply(o[j], m, n0 + j);
     if (vst) {
       *reinterpret_cast<float4*>(C + m * scm + n0) = make_float4(o[0], o[1], o[2], o[3]);
     } else {

@@ -38,7 +38,8 @@ namespace {
 constexpr int BM = 128;
 constexpr int BN = 256;
 constexpr int BK = 32;  // 32 fp32 = 128 B = one swizzle span
-constexpr int NUM_THREADS = 192;
+constexpr int EPI_WARPS = 8;  // two warps per TMEM lane quarter, each owning half the columns
+constexpr int NUM_THREADS = 64 + 32 * EPI_WARPS;
 constexpr int TMEM_COLS = 512;
 constexpr int GROUP_M = 16;
 
@@ -172,6 +173,21 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
 struct TcParams {
   float* C;
   int64_t ldc;
@@ -215,7 +231,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }
-    for (int b = 0; b < 2; ++b) { mbar_init(tfull + b, 1); mbar_init(tempty + b, 4 * CG); }
+    for (int b = 0; b < 2; ++b) { mbar_init(tfull + b, 1); mbar_init(tempty + b, EPI_WARPS * CG); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -317,10 +333,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   } else {
-    // epilogue warps 2..5 -> TMEM lane quarter (warp % 4)
+    // epilogue warps 2..9: TMEM lane quarter (warp % 4), column half (warp - 2) / 4.
+    // 32 columns per TMEM load; every global access is 128-bit.
     const int q = warp & 3;
+    const int half = (warp - 2) >> 2;
     int it = 0;
-    const bool vec_ok = (p.ldc % 4 == 0) && (((uintptr_t)p.C & 15) == 0);
+    const Epi<float>& E = p.epi;
+    const bool vec_ok = (p.ldc % 4 == 0) && (((uintptr_t)p.C & 15) == 0) &&
+                        (E.kind != TX_EPI_MUL_AUX || (E.s1 == 1 && E.s0 % 4 == 0 && ((uintptr_t)E.aux & 15) == 0)) &&
+                        (E.kind != TX_EPI_BIAS_TANH_DUAL || (E.o1 == 1 && E.o0 % 4 == 0 && ((uintptr_t)E.out2 & 15) == 0)) &&
+                        (E.kind != TX_EPI_BIAS && E.kind != TX_EPI_BIAS_TANH && E.kind != TX_EPI_BIAS_TANH_DUAL ||
+                         (E.s1 == 1 && ((uintptr_t)E.aux & 15) == 0)) &&
+                        E.kind != TX_EPI_MUL_1MSQR;
     for (int t = cluster_id; t < p.num_tiles; t += num_clusters, ++it) {
       int mb, nb;
       tile_coords(t, p.num_m, p.num_n, mb, nb);
@@ -329,26 +353,51 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_wait(tfull + buf, use & 1);
       tc_fence_after();
       const int row = mb * BM * CG + (int)rank * BM + q * 32 + lane;
-      const uint32_t taddr = tmem_base + (uint32_t)(buf * BN) + ((uint32_t)(q * 32) << 16);
+      const uint32_t taddr = tmem_base + (uint32_t)(buf * BN + half * (BN / 2)) + ((uint32_t)(q * 32) << 16);
       float* crow = p.C + (int64_t)row * p.ldc;
-      for (int c = 0; c < BN; c += 16) {
-        float v[16];
-        tmem_ld16(taddr + c, v);
-        const int n = nb * BN + c;
-        if (row < p.M && n < p.N) {
-          if (p.epi.kind != TX_EPI_NONE) {
+      const bool row_ok = row < p.M;
+#pragma unroll 1
+      for (int c = 0; c < BN / 2; c += 32) {
+        float v[32];
+        tmem_ld32(taddr + c, v);
+        const int n = nb * BN + half * (BN / 2) + c;
+        if (!row_ok || n >= p.N) continue;
+        if (vec_ok && n + 32 <= p.N) {
+          if (E.kind == TX_EPI_BIAS || E.kind == TX_EPI_BIAS_TANH || E.kind == TX_EPI_BIAS_TANH_DUAL) {
 #pragma unroll
-            for (int i = 0; i < 16; ++i) v[i] = p.epi.apply(v[i], row, n + i);
+            for (int i = 0; i < 32; i += 4) {
+              const float4 b4 = __ldg(reinterpret_cast<const float4*>(E.aux + n + i));
+              v[i] = __fadd_rn(b4.x, v[i]); v[i + 1] = __fadd_rn(b4.y, v[i + 1]);
+              v[i + 2] = __fadd_rn(b4.z, v[i + 2]); v[i + 3] = __fadd_rn(b4.w, v[i + 3]);
+            }
+            if (E.kind != TX_EPI_BIAS) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] = tanhf(v[i]);
+            }
+            if (E.kind == TX_EPI_BIAS_TANH_DUAL) {
+              float* g = E.out2 + (int64_t)row * E.o0 + n;
+#pragma unroll
+              for (int i = 0; i < 32; i += 4)
+                *reinterpret_cast<float4*>(g + i) = make_float4(
+                    __fsub_rn(1.0f, __fmul_rn(v[i], v[i])), __fsub_rn(1.0f, __fmul_rn(v[i + 1], v[i + 1])),
+                    __fsub_rn(1.0f, __fmul_rn(v[i + 2], v[i + 2])), __fsub_rn(1.0f, __fmul_rn(v[i + 3], v[i + 3])));
+            }
+          } else if (E.kind == TX_EPI_MUL_AUX) {
+            const float* g = E.aux + (int64_t)row * E.s0 + n;
+#pragma unroll
+            for (int i = 0; i < 32; i += 4) {
+              const float4 g4 = __ldcs(reinterpret_cast<const float4*>(g + i));
+              v[i] = __fmul_rn(v[i], g4.x); v[i + 1] = __fmul_rn(v[i + 1], g4.y);
+              v[i + 2] = __fmul_rn(v[i + 2], g4.z); v[i + 3] = __fmul_rn(v[i + 3], g4.w);
+            }
           }
-          if (vec_ok && n + 16 <= p.N) {
 #pragma unroll
-            for (int i = 0; i < 16; i += 4)
-              *reinterpret_cast<float4*>(crow + n + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-          } else {
+          for (int i = 0; i < 32; i += 4)
+            *reinterpret_cast<float4*>(crow + n + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+        } else {
 #pragma unroll
-            for (int i = 0; i < 16; ++i)
-              if (n + i < p.N) crow[n + i] = v[i];
-          }
+          for (int i = 0; i < 32; ++i)
+            if (n + i < p.N) crow[n + i] = E.kind != TX_EPI_NONE ? E.apply(v[i], row, n + i) : v[i];
         }
       }
       tc_fence_before();

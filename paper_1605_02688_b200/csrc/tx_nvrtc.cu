@@ -142,6 +142,48 @@ int tx_ew_compile(const char* source, const char* name, void** out) {
   return TX_OK;
 }
 
+// Generic generated kernels (row-fused regions): one module, one named entry
+// taking a single by-value argument struct.
+struct GenKernel {
+  CUmodule mod = nullptr;
+  CUfunction fn = nullptr;
+};
+
+int tx_kernel_compile(const char* source, const char* name, const char* entry, void** out) {
+  const Drv& d = drv();
+  TX_CHECK(d.ok, TX_E_NODEVICE, "CUDA driver entry points unavailable");
+  std::vector<char> cubin;
+  int rc = nvrtc_compile(source, name, &cubin);
+  if (rc) return rc;
+  GenKernel* k = new GenKernel();
+  CUresult r = d.moduleLoadData(&k->mod, cubin.data());
+  if (r != CUDA_SUCCESS) { delete k; return drv_fail(r, "cuModuleLoadData"); }
+  if ((r = d.moduleGetFunction(&k->fn, k->mod, entry)) != CUDA_SUCCESS) {
+    d.moduleUnload(k->mod);
+    delete k;
+    return drv_fail(r, "cuModuleGetFunction");
+  }
+  *out = k;
+  return TX_OK;
+}
+
+int tx_kernel_launch(void* h, unsigned grid, unsigned block, void* args, void* stream) {
+  GenKernel* k = (GenKernel*)h;
+  TX_CHECK(k && drv().ok, TX_E_ARG, "tx_kernel_launch: invalid handle");
+  void* params[] = {args};
+  CUresult r = drv().launchKernel(k->fn, grid, 1, 1, block, 1, 1, 0, (cudaStream_t)stream, params, nullptr);
+  if (r != CUDA_SUCCESS) return drv_fail(r, "cuLaunchKernel(generated)");
+  return TX_OK;
+}
+
+int tx_kernel_destroy(void* h) {
+  GenKernel* k = (GenKernel*)h;
+  if (!k) return TX_OK;
+  if (k->mod && drv().moduleUnload) drv().moduleUnload(k->mod);
+  delete k;
+  return TX_OK;
+}
+
 int tx_ew_destroy(void* h) {
   EwKernel* k = (EwKernel*)h;
   if (!k) return TX_OK;

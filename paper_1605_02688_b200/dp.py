@@ -93,26 +93,32 @@ def propagate(order, inputs_state: dict) -> ShardPlan:
                 st[n.outputs[0].id] = sharded(k)
             else:
                 st[n.outputs[0].id] = sharded(k - sum(1 for a in op.axes if a < k))
-        elif isinstance(op, Dot):
-            a, b = n.inputs
+        elif isinstance(op, Dot) or getattr(op, "gemm_operands", False):
+            a, b = n.inputs[:2]
             ka, kb = shard_axis(ins[0]), shard_axis(ins[1])
-            an, bn = a.type.ndim, b.type.ndim
-            contract_a = an - 1 if ka is not None else None
-            contract_b = 0 if kb is not None else None
+            an = a.type.ndim
             if ka is not None and kb is not None:
-                if ka == an - 1 and kb == 0:
-                    st[n.outputs[0].id] = PARTIAL
-                    plan.partial_nodes.append(n)
-                else:
+                if not (ka == an - 1 and kb == 0):
                     raise NotSupported("dot: both operands sharded on non-contracted axes")
+                out_state = PARTIAL
             elif ka is not None:
-                if ka == contract_a:
+                if ka == an - 1:
                     raise NotSupported("dot: contraction over a sharded axis of one operand only")
-                st[n.outputs[0].id] = sharded(0)
+                out_state = sharded(0)
             else:
-                if kb == contract_b:
+                if kb == 0:
                     raise NotSupported("dot: contraction over a sharded axis of one operand only")
-                st[n.outputs[0].id] = sharded(n.outputs[0].type.ndim - 1)
+                out_state = sharded(n.outputs[0].type.ndim - 1)
+            if len(n.inputs) > 2:  # fused GEMM epilogue operand (bias row or [M,N] factor)
+                if out_state == PARTIAL:
+                    raise NotSupported("a fused epilogue cannot act on a partial sum")
+                se = ins[2]
+                if se != REPLICATED and se != out_state:
+                    raise NotSupported("dot epilogue operand sharded differently from the product")
+            for o in n.outputs:
+                st[o.id] = out_state
+            if out_state == PARTIAL:
+                plan.partial_nodes.append(n)
         else:
             raise NotSupported(f"op {op.name} has no data-parallel sharding rule")
         if n in plan.partial_nodes:

@@ -157,3 +157,67 @@ def _fuse(fgraph, grp, emit) -> bool:
     fgraph.replace_all(list(zip(boundary, outs)), "fuse_elemwise")
     emit(node=grp[-1], replaced=f"group[{len(grp)}]", replacement=outs[0].owner.op.display_name)
     return True
+
+
+# ---------------------------------------------------------------------------
+# GEMM epilogue fusion (stage abstract_select, after elementwise fusion)
+
+def _match_bias_tanh_dual(prog, z_idx):
+    """{t0 = add(b, z); t1 = tanh(t0); t2 = sqr(t1); t3 = sub(1, t2)} with
+    outputs (t1, t3) — the MLP layer's forward Composite (tanh and the
+    1 - h^2 factor its gradient needs)."""
+    nodes = prog.nodes
+    if len(nodes) != 4 or len(prog.in_dtypes) != 2 or prog.outputs != (("node", 1), ("node", 3)):
+        return False
+    (k0, r0, _), (k1, r1, _), (k2, r2, _), (k3, r3, _) = nodes
+    b_idx = 1 - z_idx
+    if k0 != "add" or set(r0) != {("in", z_idx), ("in", b_idx)}:
+        return False
+    if k1 != "tanh" or r1 != (("node", 0),) or k2 != "sqr" or r2 != (("node", 1),):
+        return False
+    if k3 != "sub" or r3[1] != ("node", 2) or r3[0][0] != "const":
+        return False
+    return float(prog.consts[r3[0][1]][1]) == 1.0
+
+
+@register_rewrite("fuse_gemm_epilogue", "abstract_select", "global")
+def fuse_gemm_epilogue(fgraph, ctx, emit) -> int:
+    from .linalg import EPI_BIAS, EPI_BIAS_TANH_DUAL, EPI_MUL_AUX, Dot, DotEpilogue
+    applied = 0
+    for d in list(fgraph.toposort()):
+        if d.id not in fgraph.nodes or not isinstance(d.op, Dot):
+            continue
+        z = d.outputs[0]
+        a, b = d.inputs
+        if a.type.ndim != 2 or b.type.ndim != 2 or z.type.dtype not in ("float32", "float64"):
+            continue
+        if fgraph.is_output(z):
+            continue
+        clients = fgraph.node_clients(z)
+        if len(clients) != 1 or len(fgraph.clients[z]) != 1:
+            continue
+        c = clients[0]
+        kind, aux = None, None
+        if isinstance(c.op, Composite) and len(c.inputs) == 2 and z in c.inputs:
+            zi = c.inputs.index(z)
+            other = c.inputs[1 - zi]
+            if other is not z and other.type.ndim == 1 and other.type.dtype == z.type.dtype \
+                    and _match_bias_tanh_dual(c.op.program, zi):
+                kind, aux = EPI_BIAS_TANH_DUAL, other
+        elif isinstance(c.op, Elemwise) and c.op.kernel in ("mul", "add") and len(c.inputs) == 2:
+            other = c.inputs[1] if c.inputs[0] is z else c.inputs[0]
+            if other is z or other.type.dtype != z.type.dtype:
+                pass
+            elif c.op.kernel == "mul" and other.type.broadcastable == z.type.broadcastable == (False, False):
+                kind, aux = EPI_MUL_AUX, other
+            elif c.op.kernel == "add" and other.type.ndim == 1 and not other.type.broadcastable[0]:
+                kind, aux = EPI_BIAS, other
+        if kind is None:
+            continue
+        outs = apply(DotEpilogue(kind), [a, b, aux])
+        if [o.type for o in outs] != [o.type for o in c.outputs]:
+            continue
+        fgraph.replace_all(list(zip(c.outputs, outs)), "fuse_gemm_epilogue")
+        emit(node=c, replaced=f"dot+{getattr(c.op, 'display_name', c.op.name)}", replacement=outs[0].owner.op.display_name)
+        applied += 1
+    return applied

@@ -89,3 +89,70 @@ class Dot(Op):
 
 def dot(a: Variable, b: Variable) -> Variable:
     return apply(Dot(), [a, b])[0]
+
+
+# epilogue kinds (include/texpr_b200.h TX_EPI_*)
+EPI_BIAS, EPI_BIAS_TANH_DUAL, EPI_MUL_AUX = 1, 4, 5
+_EPI_NAMES = {EPI_BIAS: "bias", EPI_BIAS_TANH_DUAL: "bias_tanh_dual", EPI_MUL_AUX: "mul_aux"}
+
+
+@register_op
+class DotEpilogue(Op):
+    """dot(a, b) with its elementwise consumer folded into the GEMM epilogue.
+
+    Produced only by the ``fuse_gemm_epilogue`` rewrite (``fusion.py``) after
+    differentiation; inputs are (a, b, aux) and the outputs are exactly the
+    replaced consumer's outputs, computed with the same scalar ops in the
+    same order (see ``Epi`` in ``csrc/tx_gemm.h``):
+      bias            out = aux[n] + a.b
+      bias_tanh_dual  out = tanh(aux[n] + a.b), out2 = 1 - out^2
+      mul_aux         out = (a.b) * aux
+    """
+
+    name = "dot_epilogue"
+    has_grad = False
+    gemm_operands = True
+
+    def __init__(self, kind: int):
+        self.kind = int(kind)
+
+    @property
+    def display_name(self):
+        return f"dot+{_EPI_NAMES.get(self.kind, self.kind)}"
+
+    def attrs_key(self):
+        return (self.kind,)
+
+    def infer_types(self, input_types):
+        a, b, aux = input_types
+        (t,) = Dot().infer_types([a, b])
+        if self.kind == EPI_BIAS_TANH_DUAL:
+            return [t, t]
+        return [t]
+
+    def check_runtime_shapes(self, node, shapes):
+        Dot().check_runtime_shapes(node, shapes[:2])
+
+    def infer_shape(self, node, input_shapes):
+        (s,) = Dot().infer_shape(node, input_shapes[:2])
+        return [s, s] if self.kind == EPI_BIAS_TANH_DUAL else [s]
+
+    def grad(self, inputs, output_grads):
+        from .errors import NotDifferentiable
+        raise NotDifferentiable("dot_epilogue is created after differentiation")
+
+    def lower(self, node, plan):
+        from . import native
+        epi = native.TxEpilogue()
+        epi.kind = self.kind
+        epi.aux = plan.tx(node.inputs[2])
+        if self.kind == EPI_BIAS_TANH_DUAL:
+            epi.out2 = plan.tx(node.outputs[1])
+        plan.emit_dot(node, epilogue=epi)
+
+    def attrs_payload(self, encode_graph=None):
+        return {"kind": self.kind}
+
+    @classmethod
+    def from_payload(cls, payload, decode_graph=None):
+        return cls(payload["kind"])

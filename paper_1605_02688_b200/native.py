@@ -22,6 +22,7 @@ EXPORTS = [
     "tx_event_elapsed_ms", "tx_memcpy_async", "tx_memset_async", "tx_host_register", "tx_host_unregister",
     "tx_graph_begin", "tx_graph_end", "tx_graph_launch", "tx_graph_destroy", "tx_copy",
     "tx_ew_compile", "tx_ew_check", "tx_ew_launch", "tx_ew_destroy",
+    "tx_kernel_compile", "tx_kernel_launch", "tx_kernel_destroy",
     "tx_reduce_workspace", "tx_reduce",
     "tx_gemm_workspace", "tx_gemm", "tx_gemm_path",
     "tx_nccl_unique_id", "tx_nccl_init", "tx_nccl_allreduce_sum", "tx_nccl_destroy",
@@ -34,10 +35,10 @@ class TxTensor(ctypes.Structure):
 
 
 class TxEpilogue(ctypes.Structure):
-    _fields_ = [("kind", ctypes.c_int32), ("aux", TxTensor)]
+    _fields_ = [("kind", ctypes.c_int32), ("aux", TxTensor), ("out2", TxTensor)]
 
 
-EPI_NONE, EPI_BIAS, EPI_BIAS_TANH, EPI_MUL_1MSQR = 0, 1, 2, 3
+EPI_NONE, EPI_BIAS, EPI_BIAS_TANH, EPI_MUL_1MSQR, EPI_BIAS_TANH_DUAL, EPI_MUL_AUX = 0, 1, 2, 3, 4, 5
 GEMM_AUTO, GEMM_SIMT, GEMM_TC = 0, 1, 2
 
 
@@ -77,6 +78,8 @@ class Library:
             "tx_ew_compile": [ctypes.c_char_p, ctypes.c_char_p, P(vp)],
             "tx_ew_check": [ctypes.c_char_p, ctypes.c_char_p, P(sz)],
             "tx_ew_launch": [vp, ctypes.c_int, ctypes.c_int, P(TxTensor), vp, vp], "tx_ew_destroy": [vp],
+            "tx_kernel_compile": [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, P(vp)],
+            "tx_kernel_launch": [vp, ctypes.c_uint, ctypes.c_uint, vp, vp], "tx_kernel_destroy": [vp],
             "tx_reduce_workspace": [ctypes.c_int, P(TxTensor), ctypes.c_uint32, P(sz)],
             "tx_reduce": [ctypes.c_int, P(TxTensor), ctypes.c_uint32, P(TxTensor), vp, sz, vp],
             "tx_gemm_workspace": [P(TxTensor), P(TxTensor), P(TxTensor), ctypes.c_int, P(sz)],
@@ -162,6 +165,11 @@ class Library:
     def ew_compile(self, source: str, name: str):
         h = ctypes.c_void_p()
         self.check(self.lib.tx_ew_compile(source.encode(), name.encode(), ctypes.byref(h)))
+        return h.value
+
+    def kernel_compile(self, source: str, name: str, entry: str):
+        h = ctypes.c_void_p()
+        self.check(self.lib.tx_kernel_compile(source.encode(), name.encode(), entry.encode(), ctypes.byref(h)))
         return h.value
 
     def ew_check(self, source: str, name: str = "check") -> int:

@@ -1,0 +1,571 @@
+"""Plan-time row fusion: softmax / cross-entropy regions as one kernel.
+
+The reference has no softmax or cross-entropy op; the configs compose them
+from max, exp, sum, div, log, mul and DimShuffle, and ``grad`` adds ~25 more
+nodes.  On [B, 10] tensors every one of those nodes is
+pure launch latency.  With concrete shapes known (step-plan time), this
+module finds maximal convex groups of nodes that live in one *row space*
+(N rows x K <= 256 columns) and emits ONE generated kernel per group:
+
+  * one warp per row; a row vector lives in registers (lane c holds columns
+    c, c+32, ...), row scalars are warp-uniform;
+  * elementwise nodes and inlined Composite programs run per element
+    (same scalar spellings and rounding as ``codegen``);
+  * ``sum``/``max``/``argmax``/``argmax_onehot`` over the row are warp-shuffle
+    trees (max/argmax NaN- and tie-exact);
+  * reductions over the batch (``sum[0]`` -> bias gradient, ``sum[0,1]`` ->
+    cost) are group sinks: per-CTA partials in fixed order, then the last CTA
+    (ticket counter) combines the partials in block order — deterministic, no
+    float atomics;
+  * only values consumed outside the group are stored.
+
+Value classes inside a group: V row vector [N,K], S row scalar [N]/[N,1],
+C column vector [K]/[1,K] (broadcast over rows), U scalar.
+"""
+from __future__ import annotations
+
+import ctypes
+import threading
+
+from . import codegen
+from .dtypes import C_TYPE, ITEMSIZE, is_float
+from .elemwise import Composite, Elemwise, kernel_compute_dtype
+from .reduce import Argmax, ArgmaxOnehot, Max, Sum
+
+MAX_K = 256
+MAX_OPS = 48
+V, S, C, U = "V", "S", "C", "U"
+
+
+def classify(shape, N, K):
+    shape = tuple(shape)
+    if shape == (N, K):
+        return V
+    if shape in ((N,), (N, 1)):
+        return S
+    if shape in ((K,), (1, K)):
+        return C
+    if shape in ((), (1,), (1, 1)):
+        return U
+    return None
+
+
+def _combine(classes):
+    cs = set(classes)
+    if V in cs or (S in cs and C in cs):
+        return V
+    if S in cs:
+        return S
+    if C in cs:
+        return C
+    return U
+
+
+class RowArgs(ctypes.Structure):
+    _fields_ = [("N", ctypes.c_int64), ("K", ctypes.c_int32), ("pad", ctypes.c_int32),
+                ("ptr", ctypes.c_void_p * MAX_OPS), ("rs", ctypes.c_int64 * MAX_OPS),
+                ("cs", ctypes.c_int64 * MAX_OPS), ("ws", ctypes.c_void_p), ("counter", ctypes.c_void_p)]
+
+
+class RowGroup:
+    def __init__(self, N, K):
+        self.N, self.K = N, K
+        self.members = []          # nodes (views included), schedule order
+        self.member_ids = set()
+        self.values = {}           # var id -> class, for every group-produced value
+        self.sink_vars = set()     # var ids produced by sinks (not usable inside)
+        self.last_pos = -1
+        self.deferred = []         # non-members moved after the launch
+
+    def launchable(self):
+        return [n for n in self.members if not getattr(n.op, "view_capable", False)]
+
+
+# ---------------------------------------------------------------- grouping
+
+def _is_sink(n, shapes):
+    if not isinstance(n.op, Sum):
+        return False
+    shp = shapes(n.inputs[0])
+    if len(shp) == 2 and n.op.axes in ((0,), (0, 1)):
+        return True
+    return len(shp) == 1 and n.op.axes == (0,)
+
+
+def _node_fits(n, grp, shapes, allowed_in):
+    """Can node n join group grp (given the values the group already has)?"""
+    op = n.op
+    N, K = grp.N, grp.K
+    ins = [classify(shapes(x), N, K) for x in n.inputs]
+    outs = [classify(shapes(o), N, K) for o in n.outputs]
+    if any(c is None for c in ins + outs):
+        return False
+    if any(x.id in grp.sink_vars for x in n.inputs):
+        return False
+    # (not necessarily connected: any row-space node whose inputs are ready
+    # can run inside the group — fewer launches)
+    if not all(allowed_in(x) for x in n.inputs):
+        return False
+    if getattr(op, "view_capable", False):
+        return outs[0] == ins[0] or {outs[0], ins[0]} <= {U}
+    if isinstance(op, (Elemwise, Composite)):
+        prog_has_int_div = codegen.has_int_div(op.program) if isinstance(op, Composite) else (
+            op.kernel == "div" and not is_float(kernel_compute_dtype("div", [x.type.dtype for x in n.inputs])))
+        return not prog_has_int_div
+    if isinstance(op, (Sum, Max, ArgmaxOnehot, Argmax)):
+        if op.axes == (1,) and ins[0] == V:
+            return is_float(n.inputs[0].type.dtype)
+        return isinstance(op, Sum) and _is_sink(n, shapes) and ins[0] in (V, S)
+    return False
+
+
+def _seed(n, shapes, exclude_ids):
+    """A node that can open a group: a row reduction over [N, K] or an
+    elementwise node producing [N, K] (the logits' bias add), 2 <= K <= 256."""
+    if n.id in exclude_ids:
+        return None
+    op = n.op
+    if isinstance(op, (Sum, Max, ArgmaxOnehot, Argmax)) and op.axes == (1,):
+        shp = shapes(n.inputs[0])
+        if not is_float(n.inputs[0].type.dtype):
+            return None
+    elif isinstance(op, (Elemwise, Composite)):
+        shp = shapes(n.outputs[0])
+        if any(tuple(shapes(o)) != tuple(shp) for o in n.outputs):
+            return None
+        if isinstance(op, Composite) and codegen.has_int_div(op.program):
+            return None
+    else:
+        return None
+    if len(shp) != 2:
+        return None
+    N, K = shp
+    if not (2 <= K <= MAX_K) or N < 2 or N == K or N >= (1 << 31):
+        return None
+    grp = RowGroup(N, K)
+    for x in n.inputs:
+        if classify(shapes(x), N, K) is None:
+            return None
+    return grp
+
+
+def find_groups(plan, order, fgraph, exclude_ids=()):
+    """Greedy convex grouping over the schedule.
+
+    The group launches at its last member.  A non-member that reads a group
+    value (e.g. the scalar cost composite reading the batch-sum sink) is
+    *deferred* to run right after the launch, together with everything that
+    depends on it; a would-be member that needs a deferred value closes the
+    group instead.  Nodes in ``exclude_ids`` (data-parallel partial sums,
+    whose allreduce is positioned by the schedule) are never deferred: reading
+    a group value closes the group.  Groups with fewer than two launching
+    members are dropped (their deferred nodes stay in place).
+    """
+    shapes = lambda v: plan.lay[v.id].shape if v.id in plan.lay else tuple(v.value.shape)  # noqa: E731
+    groups, cur = [], None
+    deferred_out = set()
+
+    def close():
+        nonlocal cur
+        if cur is not None and len(cur.launchable()) >= 2:
+            groups.append(cur)
+        cur = None
+        deferred_out.clear()
+
+    def add(grp, n, i):
+        grp.members.append(n)
+        grp.member_ids.add(n.id)
+        grp.last_pos = i
+        sink = _is_sink(n, shapes)
+        for o in n.outputs:
+            grp.values[o.id] = classify(shapes(o), grp.N, grp.K)
+            if sink:
+                grp.sink_vars.add(o.id)
+
+    for i, n in enumerate(order):
+        reads_group = cur is not None and any(x.id in cur.values for x in n.inputs)
+        reads_deferred = any(x.id in deferred_out for x in n.inputs)
+        if cur is not None and not reads_deferred and n.id not in exclude_ids \
+                and _node_fits(n, cur, shapes, lambda x: True):
+            add(cur, n, i)
+            continue
+        if (reads_group or reads_deferred) and n.id not in exclude_ids:
+            cur.deferred.append(n)
+            for o in n.outputs:
+                deferred_out.add(o.id)
+            continue
+        if reads_group or reads_deferred:
+            close()
+        g = _seed(n, shapes, exclude_ids)
+        if g is not None:
+            close()
+            cur = g
+            add(cur, n, i)
+    close()
+    for grp in groups:
+        # deferred nodes positioned after the last member run in place
+        grp.deferred = [n for n in grp.deferred if order.index(n) < grp.last_pos]
+    return groups
+
+
+# ---------------------------------------------------------------- codegen
+
+_PRELUDE = r"""
+typedef long long i64;
+typedef unsigned char u8;
+#define TX_R %(R)d
+struct TxRowArgs { i64 N; int K; int pad; void* ptr[%(MAXOPS)d]; i64 rs[%(MAXOPS)d]; i64 cs[%(MAXOPS)d];
+                   double* ws; unsigned int* counter; };
+__device__ __forceinline__ float tx_sigmoid(float x) { float z = expf(-fabsf(x)); return x >= 0.0f ? 1.0f / (1.0f + z) : z / (1.0f + z); }
+__device__ __forceinline__ double tx_sigmoid(double x) { double z = exp(-fabs(x)); return x >= 0.0 ? 1.0 / (1.0 + z) : z / (1.0 + z); }
+__device__ __forceinline__ float tx_exp(float x) { return expf(x); }
+__device__ __forceinline__ double tx_exp(double x) { return exp(x); }
+__device__ __forceinline__ float tx_log(float x) { return logf(x); }
+__device__ __forceinline__ double tx_log(double x) { return log(x); }
+__device__ __forceinline__ float tx_log1p(float x) { return log1pf(x); }
+__device__ __forceinline__ double tx_log1p(double x) { return log1p(x); }
+__device__ __forceinline__ float tx_sqrt(float x) { return sqrtf(x); }
+__device__ __forceinline__ double tx_sqrt(double x) { return sqrt(x); }
+__device__ __forceinline__ float tx_tanh(float x) { return tanhf(x); }
+__device__ __forceinline__ double tx_tanh(double x) { return tanh(x); }
+__device__ __forceinline__ float tx_pow(float a, float b) { return powf(a, b); }
+__device__ __forceinline__ double tx_pow(double a, double b) { return pow(a, b); }
+template <class T> __device__ __forceinline__ T tx_exp(T x) { return (T)exp((double)x); }
+template <class T> __device__ __forceinline__ T tx_log(T x) { return (T)log((double)x); }
+template <class T> __device__ __forceinline__ T tx_log1p(T x) { return (T)log1p((double)x); }
+template <class T> __device__ __forceinline__ T tx_sqrt(T x) { return (T)sqrt((double)x); }
+template <class T> __device__ __forceinline__ T tx_tanh(T x) { return (T)tanh((double)x); }
+template <class T> __device__ __forceinline__ T tx_sigmoid(T x) { return (T)tx_sigmoid((double)x); }
+template <class T> __device__ __forceinline__ T tx_pow(T a, T b) { if (b < 0) return (T)0; T r = 1; while (b) { if (b & 1) r *= a; a *= a; b >>= 1; } return r; }
+__device__ __forceinline__ float tx_maximum(float a, float b) { return (a != a) ? a : (b != b) ? b : (a >= b ? a : b); }
+__device__ __forceinline__ double tx_maximum(double a, double b) { return (a != a) ? a : (b != b) ? b : (a >= b ? a : b); }
+template <class T> __device__ __forceinline__ T tx_maximum(T a, T b) { return a >= b ? a : b; }
+__device__ __forceinline__ float tx_div(float a, float b, int*) { return a / b; }
+__device__ __forceinline__ double tx_div(double a, double b, int*) { return a / b; }
+__device__ __forceinline__ u8 tx_isnan(float a) { return a != a; }
+__device__ __forceinline__ u8 tx_isnan(double a) { return a != a; }
+template <class T> __device__ __forceinline__ T tx_wsum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+template <class T> __device__ __forceinline__ T tx_wmax(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) { T w = __shfl_xor_sync(0xffffffffu, v, o); v = (v != v) ? v : ((w != w) ? w : (w > v ? w : v)); }
+  return v;
+}
+// first maximal (NaN counts as maximal) with index tie-break across lanes
+template <class T> __device__ __forceinline__ void tx_wargmax(T& v, int& i) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    T w = __shfl_xor_sync(0xffffffffu, v, o);
+    int j = __shfl_xor_sync(0xffffffffu, i, o);
+    bool vn = v != v, wn = w != w;
+    bool take = (j >= 0) && ((i < 0) || (vn && wn ? j < i : vn ? false : wn ? true : (w > v || (w == v && j < i))));
+    if (take) { v = w; i = j; }
+  }
+}
+"""
+
+
+class _Gen:
+    def __init__(self, grp: RowGroup, plan, fgraph):
+        self.grp, self.plan, self.fg = grp, plan, fgraph
+        self.N, self.K = grp.N, grp.K
+        self.R = (grp.K + 31) // 32
+        self.lines = []
+        self.name = {}      # var id -> C identifier
+        self.cls = {}       # var id -> class
+        self.dt = {}        # var id -> dtype
+        self.ops = []       # (var, role) operand slots: role in {"in", "out", "sink"}
+        self.slot = {}
+        self.sinks = []     # (var, class_of_sink_output, acc identifier, dtype, length)
+
+    def shape(self, v):
+        return self.plan.lay[v.id].shape if v.id in self.plan.lay else tuple(v.value.shape)
+
+    def operand(self, v, role):
+        key = (v.id, role)
+        if key not in self.slot:
+            self.slot[key] = len(self.ops)
+            self.ops.append((v, role))
+        return self.slot[key]
+
+    def emit(self, s):
+        self.lines.append(s)
+
+    # value access: per-element expression for class V/C arrays or scalar name
+    def at(self, vid, j="j"):
+        c = self.cls[vid]
+        return f"{self.name[vid]}[{j}]" if c in (V, C) else self.name[vid]
+
+    def leaf(self, v):
+        if v.id in self.name:
+            return
+        cls = classify(self.shape(v), self.N, self.K)
+        ct = C_TYPE[v.type.dtype]
+        k = self.operand(v, "in")
+        nm = f"L{k}"
+        p = f"((const {ct}*)a.ptr[{k}])"
+        if cls == V:
+            self.emit(f"{ct} {nm}[TX_R];")
+            self.emit(f"#pragma unroll\nfor (int j = 0; j < TX_R; ++j) {{ const int c = lane + 32 * j; "
+                      f"{nm}[j] = (active && c < K) ? {p}[row * a.rs[{k}] + (i64)c * a.cs[{k}]] : ({ct})0; }}")
+        elif cls == C:
+            self.emit(f"{ct} {nm}[TX_R];")
+            self.emit(f"#pragma unroll\nfor (int j = 0; j < TX_R; ++j) {{ const int c = lane + 32 * j; "
+                      f"{nm}[j] = (c < K) ? {p}[(i64)c * a.cs[{k}]] : ({ct})0; }}")
+        elif cls == S:
+            self.emit(f"const {ct} {nm} = active ? {p}[row * a.rs[{k}]] : ({ct})0;")
+        else:
+            self.emit(f"const {ct} {nm} = {p}[0];")
+        self.name[v.id], self.cls[v.id], self.dt[v.id] = nm, cls, v.type.dtype
+
+    def elementwise(self, out_id, out_dt, kernel, arg_ids_or_lits):
+        """arg_ids_or_lits: list of ("var", id) or ("lit", c_expr, dtype)."""
+        classes = [self.cls[a[1]] if a[0] == "var" else U for a in arg_ids_or_lits]
+        oc = _combine(classes)
+        dts = [self.dt[a[1]] if a[0] == "var" else a[2] for a in arg_ids_or_lits]
+        ct = C_TYPE[out_dt]
+        nm = f"t{len(self.name)}"
+
+        def args(j):
+            return [(self.at(a[1], j) if a[0] == "var" else a[1]) for a in arg_ids_or_lits]
+
+        if oc in (V, C):
+            self.emit(f"{ct} {nm}[TX_R];")
+            self.emit(f"#pragma unroll\nfor (int j = 0; j < TX_R; ++j) {nm}[j] = "
+                      f"{codegen.scalar_expr(kernel, args('j'), dts, out_dt)};")
+        else:
+            self.emit(f"const {ct} {nm} = {codegen.scalar_expr(kernel, args('j'), dts, out_dt)};")
+        self.name[out_id], self.cls[out_id], self.dt[out_id] = nm, oc, out_dt
+
+    def node(self, n):
+        op = n.op
+        for x in n.inputs:
+            if x.id not in self.name:
+                self.leaf(x)
+        if getattr(op, "view_capable", False):
+            o, x = n.outputs[0], n.inputs[0]
+            self.name[o.id], self.cls[o.id], self.dt[o.id] = self.name[x.id], self.cls[x.id], self.dt[x.id]
+            return
+        if isinstance(op, Elemwise):
+            self.elementwise(n.outputs[0].id, n.outputs[0].type.dtype, op.kernel,
+                             [("var", x.id) for x in n.inputs])
+            return
+        if isinstance(op, Composite):
+            p = op.program
+            inner = []
+            for j, (k, refs, dt) in enumerate(p.nodes):
+                args = []
+                for kind, i in refs:
+                    if kind == "in":
+                        args.append(("var", n.inputs[i].id))
+                    elif kind == "node":
+                        args.append(("var", inner[i]))
+                    else:
+                        d, val = p.consts[i]
+                        args.append(("lit", codegen.literal(d, val), d))
+                vid = ("c", n.id, j)
+                self.elementwise(vid, dt, k, args)
+                inner.append(vid)
+            for o, (kind, i) in zip(n.outputs, p.outputs):
+                src = inner[i] if kind == "node" else n.inputs[i].id if kind == "in" else None
+                if src is None:
+                    d, val = p.consts[i]
+                    self.elementwise(o.id, o.type.dtype, "second", [("lit", "0", d), ("lit", codegen.literal(d, val), d)])
+                else:
+                    self.name[o.id], self.cls[o.id], self.dt[o.id] = self.name[src], self.cls[src], self.dt[src]
+            return
+        x, o = n.inputs[0], n.outputs[0]
+        ct = C_TYPE[x.type.dtype]
+        xn = self.name[x.id]
+        nm = f"t{len(self.name)}"
+        if isinstance(op, Sum) and op.axes == (1,):
+            self.emit(f"{ct} {nm} = 0;")
+            self.emit(f"#pragma unroll\nfor (int j = 0; j < TX_R; ++j) if (lane + 32 * j < K) {nm} += {xn}[j];")
+            self.emit(f"{nm} = tx_wsum({nm});")
+            self.name[o.id], self.cls[o.id], self.dt[o.id] = nm, S, o.type.dtype
+        elif isinstance(op, Max) and op.axes == (1,):
+            self.emit(f"{ct} {nm} = {xn}[0];")
+            self.emit(f"#pragma unroll\nfor (int j = 1; j < TX_R; ++j) if (lane + 32 * j < K) {{ {ct} w = {xn}[j]; "
+                      f"{nm} = ({nm} != {nm}) ? {nm} : ((w != w) ? w : (w > {nm} ? w : {nm})); }}")
+            self.emit(f"if (lane >= K) {nm} = -__int_as_float(0x7f800000);" if ct == "float" else f"if (lane >= K) {nm} = -__longlong_as_double(0x7ff0000000000000LL);")
+            self.emit(f"{nm} = tx_wmax({nm});")
+            self.name[o.id], self.cls[o.id], self.dt[o.id] = nm, S, o.type.dtype
+        elif isinstance(op, (Argmax, ArgmaxOnehot)) and op.axes == (1,):
+            iv, ii = f"{nm}_v", f"{nm}_i"
+            self.emit(f"{ct} {iv} = {xn}[0]; int {ii} = lane < K ? lane : -1;")
+            self.emit(f"#pragma unroll\nfor (int j = 1; j < TX_R; ++j) {{ const int c = lane + 32 * j; "
+                      f"if (c < K) {{ {ct} w = {xn}[j]; if ({ii} < 0 || w > {iv} || (w != w && {iv} == {iv})) "
+                      f"{{ {iv} = w; {ii} = c; }} }} }}")
+            self.emit(f"tx_wargmax({iv}, {ii});")
+            if isinstance(op, Argmax):
+                self.emit(f"const i64 {nm} = (i64){ii};")
+                self.name[o.id], self.cls[o.id], self.dt[o.id] = nm, S, o.type.dtype
+            else:
+                ot = C_TYPE[o.type.dtype]
+                self.emit(f"{ot} {nm}[TX_R];")
+                self.emit(f"#pragma unroll\nfor (int j = 0; j < TX_R; ++j) {nm}[j] = (lane + 32 * j == {ii}) ? "
+                          f"({ot})1 : ({ot})0;")
+                self.name[o.id], self.cls[o.id], self.dt[o.id] = nm, V, o.type.dtype
+        elif isinstance(op, Sum):  # sinks: reduce over the batch
+            cin = self.cls[x.id]
+            acc = f"SK{len(self.sinks)}"
+            if op.axes == (0,) and cin == V:
+                self.emit(f"{ct} {acc}[TX_R];")
+                self.emit(f"#pragma unroll\nfor (int j = 0; j < TX_R; ++j) {acc}[j] = "
+                          f"(active && lane + 32 * j < K) ? {xn}[j] : ({ct})0;")
+                self.sinks.append((o, C, acc, x.type.dtype, self.K))
+            else:
+                if cin == V:
+                    self.emit(f"double {acc} = 0;")
+                    self.emit(f"#pragma unroll\nfor (int j = 0; j < TX_R; ++j) if (lane + 32 * j < K) {acc} += (double){xn}[j];")
+                    self.emit(f"{acc} = tx_wsum({acc});")
+                    self.emit(f"{acc} = active ? {acc} : 0.0;")
+                else:
+                    self.emit(f"const double {acc} = active ? (double){xn} : 0.0;")
+                self.sinks.append((o, U, acc, x.type.dtype, 1))
+            self.operand(o, "sink")
+        else:  # pragma: no cover
+            raise NotImplementedError(op.name)
+
+    def stores(self, store_ids):
+        for vid in store_ids:
+            v = store_ids[vid]
+            k = self.operand(v, "out")
+            ct = C_TYPE[v.type.dtype]
+            p = f"(({ct}*)a.ptr[{k}])"
+            c = self.cls[vid]
+            src = self.name[vid]
+            if c == V:
+                self.emit(f"if (active) {{\n#pragma unroll\nfor (int j = 0; j < TX_R; ++j) {{ const int c = lane + 32 * j; "
+                          f"if (c < K) {p}[row * a.rs[{k}] + (i64)c * a.cs[{k}]] = ({ct}){src}[j]; }} }}")
+            elif c == S:
+                self.emit(f"if (active && lane == 0) {p}[row * a.rs[{k}]] = ({ct}){src};")
+            elif c == C:
+                self.emit(f"if (blockIdx.x == 0 && warp == 0) {{\n#pragma unroll\nfor (int j = 0; j < TX_R; ++j) "
+                          f"{{ const int c = lane + 32 * j; if (c < K) {p}[(i64)c * a.cs[{k}]] = ({ct}){src}[j]; }} }}")
+            else:
+                self.emit(f"if (blockIdx.x == 0 && threadIdx.x == 0) {p}[0] = ({ct}){src};")
+
+    def finish_sinks(self):
+        if not self.sinks:
+            return 0
+        total = sum(L for *_, L in self.sinks)
+        self.emit(f"__shared__ double sk_smem[8][{total}];")
+        off = 0
+        offs = []
+        for (o, c, acc, dt, L) in self.sinks:
+            offs.append(off)
+            if c == C:
+                self.emit(f"#pragma unroll\nfor (int j = 0; j < TX_R; ++j) {{ const int c = lane + 32 * j; "
+                          f"if (c < K) sk_smem[warp][{off} + c] = (double){acc}[j]; }}")
+            else:
+                self.emit(f"if (lane == 0) sk_smem[warp][{off}] = (double){acc};")
+            off += L
+        self.emit("__syncthreads();")
+        # CTA partial in fixed warp order, in the sink's own precision
+        self.emit(f"for (int e = threadIdx.x; e < {total}; e += blockDim.x) {{")
+        for (o, c, acc, dt, L), so in zip(self.sinks, offs):
+            self.emit(f"  if (e >= {so} && e < {so + L}) {{ double s = 0; for (int w = 0; w < 8; ++w) "
+                      f"s += sk_smem[w][e]; a.ws[(i64)blockIdx.x * {total} + e] = s; }}")
+        self.emit("}")
+        self.emit("__threadfence(); __syncthreads();")
+        self.emit("__shared__ unsigned int sk_ticket; if (threadIdx.x == 0) sk_ticket = atomicAdd(a.counter, 1u);")
+        self.emit("__syncthreads();")
+        self.emit("if (sk_ticket == gridDim.x - 1) {")
+        self.emit("  __threadfence();")
+        self.emit("  __shared__ double sk_red[256];")
+        # every sink element: all 256 threads sum a strided slice of the block
+        # partials, then a fixed-shape tree -> deterministic
+        self.emit(f"  for (int e = 0; e < {total}; ++e) {{")
+        self.emit("    double s = 0;")
+        self.emit(f"    for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) s += __ldcg(a.ws + (i64)b * {total} + e);")
+        self.emit("    sk_red[threadIdx.x] = s; __syncthreads();")
+        self.emit("    for (int w = 128; w > 0; w >>= 1) { if (threadIdx.x < w) sk_red[threadIdx.x] += sk_red[threadIdx.x + w]; __syncthreads(); }")
+        self.emit("    if (threadIdx.x == 0) {")
+        for (o, c, acc, dt, L), so in zip(self.sinks, offs):
+            ot = C_TYPE[o.type.dtype]
+            k = self.slot[(o.id, "sink")]
+            self.emit(f"      if (e >= {so} && e < {so + L}) (({ot}*)a.ptr[{k}])[(i64)(e - {so}) * a.cs[{k}]] = ({ot})sk_red[0];")
+        self.emit("    }")
+        self.emit("    __syncthreads();")
+        self.emit("  }")
+        self.emit("  if (threadIdx.x == 0) *a.counter = 0u;")
+        self.emit("}")
+        return total
+
+    def source(self, body, total):
+        head = _PRELUDE % {"R": self.R, "MAXOPS": MAX_OPS}
+        return "\n".join([head, 'extern "C" __global__ void __launch_bounds__(256) tx_row(const TxRowArgs a) {',
+                          "const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;",
+                          "const i64 row = (i64)blockIdx.x * 8 + warp;",
+                          "const bool active = row < a.N;", "const int K = a.K;", "(void)lane;",
+                          "int* err = nullptr; (void)err;"]
+                         + body + ["}"])
+
+
+_CACHE: dict = {}
+_LOCK = threading.Lock()
+
+
+def emit_group(plan, grp: RowGroup, fgraph):
+    """Generate, compile (cached by source) and register the group's launch."""
+    import torch
+    members = grp.member_ids
+    # values consumed outside the group (or returned) must be stored
+    store = {}
+    for n in grp.members:
+        for o in n.outputs:
+            if o.id in grp.sink_vars:
+                continue
+            outside = fgraph.is_output(o) or any(c.id not in members for c in fgraph.node_clients(o))
+            if outside:
+                base = o
+                while base.owner is not None and getattr(base.owner.op, "view_capable", False) \
+                        and base.owner.id in members:
+                    base = base.owner.inputs[0]
+                if base.owner is not None and base.owner.id in members:
+                    store[base.id] = base
+    gen = _Gen(grp, plan, fgraph)
+    for n in grp.members:
+        gen.node(n)
+    gen.stores(store)
+    total = gen.finish_sinks()
+    src = gen.source(gen.lines, total)
+    lib = plan.lib
+    with _LOCK:
+        h = _CACHE.get(src)
+        if h is None:
+            h = lib.kernel_compile(src, f"row{len(_CACHE)}", "tx_row")
+            _CACHE[src] = h
+    args = RowArgs()
+    args.N, args.K = grp.N, grp.K
+    for k, (v, role) in enumerate(gen.ops):
+        lay = plan.lay[v.id] if v.id in plan.lay else plan._const_layout(v)
+        t = plan.tx(lay)
+        args.ptr[k] = t.data
+        shp, st = lay.shape, lay.strides
+        cls = classify(shp, grp.N, grp.K)
+        if cls == V:
+            args.rs[k], args.cs[k] = st[0], st[1]
+        elif cls == S:
+            args.rs[k], args.cs[k] = st[0], 0
+        elif cls == C:
+            args.rs[k], args.cs[k] = 0, st[-1]
+        else:
+            args.rs[k], args.cs[k] = 0, 1
+    grid = (grp.N + 7) // 8
+    if total:
+        ws = torch.zeros(grid * total * 8 + 256, dtype=torch.uint8, device="cuda")
+        plan.keep.append(ws)
+        args.ws = ws.data_ptr()
+        args.counter = ws.data_ptr() + grid * total * 8
+    f = lib.lib.tx_kernel_launch
+    ap = ctypes.cast(ctypes.pointer(args), ctypes.c_void_p)
+    plan.keep.append(args)
+
+    def launch(stream):
+        lib.check(f(h, grid, 256, ap, stream))
+    return launch, src

@@ -179,7 +179,7 @@ class ArenaAllocator:
 
 def compile(inputs, outputs, updates=(), preset="fast_run", allow_gc=True, nan_guard=None, include=(),
             exclude=(), conv_impl="gemm", max_passes=8, *, cuda_graph=True, gemm_mode="auto",
-            data_parallel=None) -> "CompiledFunction":
+            data_parallel=None, row_fusion=True) -> "CompiledFunction":
     """Build a callable computing ``outputs`` from ``inputs`` on the B200.
 
     Signature and semantics follow reference ``runtime.py:174-259``; extra
@@ -228,7 +228,7 @@ def compile(inputs, outputs, updates=(), preset="fast_run", allow_gc=True, nan_g
     return CompiledFunction(fg, len(outputs), [repl[v] for v in inputs], [(s, repl[s]) for s in found],
                             [(p.shared, cloned[len(outputs) + i]) for i, p in enumerate(ups)],
                             log, preset, single, allow_gc=allow_gc, cuda_graph=cuda_graph,
-                            gemm_mode=gemm_mode, data_parallel=data_parallel)
+                            gemm_mode=gemm_mode, data_parallel=data_parallel, row_fusion=row_fusion)
 
 
 function = compile
@@ -236,7 +236,8 @@ function = compile
 
 class CompiledFunction:
     def __init__(self, fgraph, n_outputs, input_vars, shared_bindings, updates, rewrite_log, preset,
-                 single_output=False, allow_gc=True, cuda_graph=True, gemm_mode="auto", data_parallel=None):
+                 single_output=False, allow_gc=True, cuda_graph=True, gemm_mode="auto", data_parallel=None,
+                 row_fusion=True):
         self.fgraph = fgraph
         self.n_outputs = n_outputs
         self.input_vars = list(input_vars)
@@ -251,6 +252,7 @@ class CompiledFunction:
         self.cuda_graph = cuda_graph
         self.gemm_mode = {"auto": native.GEMM_AUTO, "simt": native.GEMM_SIMT, "tc": native.GEMM_TC}[gemm_mode]
         self.dp = data_parallel
+        self.row_fusion = row_fusion
         self.profile = Profile(stage_times=dict(rewrite_log.stage_times))
         self.nan_guard = None
         self.has_lazy = False
@@ -627,6 +629,19 @@ class StepPlan:
             if v.id in self.lay:
                 touch(self.lay[v.id], INF)
 
+        # ---- row fusion (softmax / cross-entropy regions), decided with shapes
+        self.row_groups = []
+        if fn.row_fusion:
+            from . import rowfuse
+            excl = {n.id for n in fn.shard.partial_nodes} if fn.shard is not None else set()
+            self.row_groups = rowfuse.find_groups(self, order, g, excl)
+            for grp in self.row_groups:
+                produced = {o.id for n in grp.members for o in n.outputs}
+                for n in grp.members + grp.deferred:
+                    for x in n.inputs:
+                        if x.id not in produced and x.id in self.lay:
+                            touch(self.lay[x.id], grp.last_pos)  # read at (or after) the launch point
+
         # ---- arena allocation with in-place reuse for elementwise kernels
         alloc = ArenaAllocator()
         live_at: dict[int, list] = {}
@@ -728,10 +743,25 @@ class StepPlan:
                 if first_use is not None:
                     bucket_wait.setdefault(first_use, []).append(bi)
             self._bucket_events = [(lib.event_create(), lib.event_create()) for _ in self.buckets]
+        grouped = {n.id for grp in self.row_groups for n in grp.members}
+        deferred = {n.id for grp in self.row_groups for n in grp.deferred}
+        group_at = {grp.last_pos: grp for grp in self.row_groups}
         for i, n in enumerate(order):
             for bi in bucket_wait.get(i, []):
                 self._emit_bucket_wait(bi)
-            if not getattr(n.op, "view_capable", False):
+            if n.id in grouped:
+                if i in group_at:
+                    from . import rowfuse
+                    self._cur = n
+                    launch, _src = rowfuse.emit_group(self, group_at[i], g)
+                    self.add_launch(launch)
+                    for d in group_at[i].deferred:
+                        if not getattr(d.op, "view_capable", False):
+                            self._cur = d
+                            d.op.lower(d, self)
+            elif n.id in deferred:
+                continue
+            elif not getattr(n.op, "view_capable", False):
                 self._cur = n
                 n.op.lower(n, self)
             for bi in bucket_after.get(i, []):
@@ -834,7 +864,7 @@ class StepPlan:
         self.add_launch(launch)
 
     def _dot_views(self, node, noptr=False):
-        a, b = node.inputs
+        a, b = node.inputs[:2]
         c = node.outputs[0]
         la, lb, lc = self.lay[a.id], self.lay[b.id], self.lay[c.id]
         mk = self._tx_noptr if noptr else self.tx

@@ -38,7 +38,7 @@ def test_logreg_unfused_preset_matches():
     x, y = C.inputs_logreg()
     g = C.build_logreg(T)
     step = T.compile(g["inputs"], g["outputs"], updates=g["updates"], preset="fast_run", exclude=("fuse_elemwise",))
-    assert len(step.order) == 45
+    assert len(step.order) == 44  # 45 reference nodes, the logits bias add folded into the GEMM
     g2 = C.build_logreg(T)
     fused = T.compile(g2["inputs"], g2["outputs"], updates=g2["updates"])
     for _ in range(3):
@@ -116,13 +116,77 @@ def test_data_parallel_single_rank_matches_plain_step():
     B, H = 256, 512
     x, y = C.inputs_mlp(B=B)
     ga = C.build_mlp(T, B=B, H=H)
-    fa = T.compile(ga["inputs"], ga["outputs"], updates=ga["updates"])
+    fa = T.compile(ga["inputs"], ga["outputs"], updates=ga["updates"], row_fusion=False)
     gb = C.build_mlp(T, B=B, H=H)
     dp = DataParallel(world_size=1, rank=0, bucket_bytes=1 << 20)
-    fb = T.compile(gb["inputs"], gb["outputs"], updates=gb["updates"], data_parallel=dp)
+    fb = T.compile(gb["inputs"], gb["outputs"], updates=gb["updates"], data_parallel=dp, row_fusion=False)
     assert len(fb.shard.partial_nodes) == 7
     for _ in range(3):
         ca, cb = fa(x, y)[0], fb(x, y)[0]
         assert ca == cb
+    for pa, pb in zip(ga["params"], gb["params"]):
+        assert np.array_equal(pa.get_value(), pb.get_value())
+    # with row fusion the DP step keeps its partial sums outside the fused
+    # blocks (their allreduce is scheduled); results agree to rounding
+    gc = C.build_mlp(T, B=B, H=H)
+    fc = T.compile(gc["inputs"], gc["outputs"], updates=gc["updates"],
+                   data_parallel=DataParallel(world_size=1, rank=0))
+    gd = C.build_mlp(T, B=B, H=H)
+    fd = T.compile(gd["inputs"], gd["outputs"], updates=gd["updates"])
+    for _ in range(3):
+        cc, cd = fc(x, y)[0], fd(x, y)[0]
+        assert abs(cc - cd) <= 1e-5 * abs(cd)
+
+
+def test_row_fusion_matches_unfused_and_cuts_launches():
+    x, y = C.inputs_logreg()
+    ga = C.build_logreg(T)
+    fa = T.compile(ga["inputs"], ga["outputs"], updates=ga["updates"], row_fusion=False)
+    gb = C.build_logreg(T)
+    fb = T.compile(gb["inputs"], gb["outputs"], updates=gb["updates"])
+    for _ in range(4):
+        ca, cb = fa(x, y)[0], fb(x, y)[0]
+        assert abs(ca - cb) <= 1e-6 * abs(ca)
+    for pa, pb in zip(ga["params"], gb["params"]):
+        assert rel(pb.get_value(), pa.get_value()) < 1e-5
+    plan = next(iter(fb._plans.values()))
+    assert len(plan.row_groups) == 1
+    assert len(plan.launches) <= 8 < len(next(iter(fa._plans.values())).launches)
+
+
+def test_row_fusion_nan_and_ties_in_softmax_block():
+    """max/argmax inside the fused block keep NumPy's NaN / first-index rules."""
+    v = T.matrix("z", dtype="float32")
+    m = T.max(v, axis=1)
+    oh = T.argmax_onehot(v, axis=1)
+    s = T.sum(T.exp(v - T.dimshuffle(m, (0, "x"))), axis=1)
+    f = T.compile([v], [m, oh, s, T.argmax(v, axis=1)])
+    z = np.random.default_rng(3).standard_normal((300, 37)).astype(np.float32)
+    z[4, :] = 1.0
+    z[7, 5] = np.nan
+    z[9, 36] = np.nan
+    z[9, 2] = np.nan
+    got = f(z)
+    assert len(next(iter(f._plans.values())).row_groups) == 1
+    np.testing.assert_array_equal(got[0], O.reduce_max(z, (1,)))
+    np.testing.assert_array_equal(got[1], O.argmax_onehot(z, (1,)))
+    np.testing.assert_array_equal(got[3], O.argmax_index(z, (1,)))
+    ref = O.reduce_sum(np.exp(z - O.reduce_max(z, (1,))[:, None]), (1,))
+    np.testing.assert_allclose(got[2], ref, rtol=1e-5, equal_nan=True)
+
+
+def test_gemm_epilogue_fusion_is_bit_exact():
+    """dot+bias+tanh (+1-h^2) and dot*(1-h^2) fused into the GEMM epilogues
+    round exactly like the separate elementwise kernels."""
+    B, H = 256, 512
+    x, y = C.inputs_mlp(B=B)
+    ga = C.build_mlp(T, B=B, H=H)
+    fa = T.compile(ga["inputs"], ga["outputs"], updates=ga["updates"], exclude=("fuse_gemm_epilogue",))
+    gb = C.build_mlp(T, B=B, H=H)
+    fb = T.compile(gb["inputs"], gb["outputs"], updates=gb["updates"])
+    kinds = [getattr(n.op, "display_name", n.op.name) for n in fb.order]
+    assert kinds.count("dot+bias_tanh_dual") == 2 and kinds.count("dot+mul_aux") == 2
+    for _ in range(2):
+        assert fa(x, y)[0] == fb(x, y)[0]
     for pa, pb in zip(ga["params"], gb["params"]):
         assert np.array_equal(pa.get_value(), pb.get_value())

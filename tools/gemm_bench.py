@@ -24,6 +24,42 @@ SHAPES = [  # (name, M, N, K, a_transposed, b_transposed)
 ]
 
 
+def bench_fn(lib, f, args, reps=10):
+    f.call_device(*args, sync=True)
+    for _ in range(3):
+        f.call_device(*args)
+    ev = [(lib.event_create(), lib.event_create()) for _ in range(reps)]
+    for e0, e1 in ev:
+        lib.event_record(e0, f._stream)
+        f.call_device(*args)
+        lib.event_record(e1, f._stream)
+    lib.stream_sync(f._stream)
+    return sorted(lib.elapsed_ms(e0, e1) for e0, e1 in ev)[reps // 2]
+
+
+def epilogues(lib):
+    """The MLP's fused forward (tanh(b + x.W), 1 - h^2) and backward (dH * g) GEMMs."""
+    M, N = 8192, 4096
+    for K in (784, 4096):
+        x = torch.randn(M, K, device="cuda")
+        w = torch.randn(K, N, device="cuda") / K ** 0.5
+        bias = torch.randn(N, device="cuda")
+        vx, vw, vb = T.matrix("x", dtype="float32"), T.matrix("w", dtype="float32"), T.vector("b", dtype="float32")
+        h = T.tanh(T.dot(vx, vw) + vb)
+        for fuse in (True, False):
+            f = T.compile([vx, vw, vb], [h, 1.0 - T.sqr(h)], exclude=() if fuse else ("fuse_gemm_epilogue",))
+            ms = bench_fn(lib, f, (x, w, bias))
+            print(f"fwd K={K} fused={fuse}: {ms:.3f} ms ({2 * M * N * K / ms / 1e9:.1f} TFLOP/s incl. epilogue)", flush=True)
+    dz = torch.randn(M, N, device="cuda")
+    w2 = torch.randn(N, N, device="cuda")
+    g = torch.randn(M, N, device="cuda")
+    vd, vw2, vg = T.matrix("dz", dtype="float32"), T.matrix("w2", dtype="float32"), T.matrix("g", dtype="float32")
+    for fuse in (True, False):
+        f = T.compile([vd, vw2, vg], T.dot(vd, T.transpose(vw2)) * vg, exclude=() if fuse else ("fuse_gemm_epilogue",))
+        ms = bench_fn(lib, f, (dz, w2, g))
+        print(f"bwd dH*g fused={fuse}: {ms:.3f} ms ({2 * M * N * N / ms / 1e9:.1f} TFLOP/s incl. epilogue)", flush=True)
+
+
 def main():
     torch.cuda.set_device(0)
     lib = native.device_library(0)
@@ -52,6 +88,7 @@ def main():
         err = ((out[rows].double() - ref).abs() / (bound + 1e-30)).max().item()
         tf = 2 * M * N * K / (ms * 1e-3) / 1e12
         print(f"CG={cg} {name:12s} M={M} N={N} K={K}: {ms:.3f} ms {tf:7.1f} TFLOP/s  max err/bound {err:.2e}", flush=True)
+    epilogues(lib)
 
 
 if __name__ == "__main__":
