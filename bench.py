@@ -152,16 +152,49 @@ def bench_ew(T, C, steps, warmup, lib_holder):
     return f, ins, ms
 
 
-def bench_ew_e2e(f, steps=3):
+def bench_ew_e2e(f, steps=5):
     import torch
     host = [torch.randn(EW_N, dtype=torch.float32).pin_memory() for _ in range(4)]
-    f(*host)  # warm plan for host-bound inputs
+    f(*host)  # warm: builds the chunk pipeline (slot plans, captured graphs)
+    f(*host)
     t0 = time.perf_counter()
     for _ in range(steps):
         out = f(*host)
     dt = (time.perf_counter() - t0) / steps
     assert out.shape == (EW_N,)
     return dt, 4 * EW_N * 4, EW_N * 4
+
+
+def link_bandwidth(nbytes=1 << 30, reps=3):
+    """Pinned host<->device copy rates on this box (the e2e path's link bound):
+    H2D alone, D2H alone, and both directions at once."""
+    import torch
+    h = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    h2 = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    d = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    d2 = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def timed(fn):
+        best = 1e30
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            fn()
+            torch.cuda.synchronize()
+            best = min(best, time.perf_counter() - t0)
+        return best
+
+    def both():
+        with torch.cuda.stream(s1):
+            d.copy_(h, non_blocking=True)
+        with torch.cuda.stream(s2):
+            h2.copy_(d2, non_blocking=True)
+    th = timed(lambda: d.copy_(h, non_blocking=True))
+    td = timed(lambda: h2.copy_(d2, non_blocking=True))
+    tb = timed(both)
+    return {"h2d_gbs": round(nbytes / th / 1e9, 1), "d2h_gbs": round(nbytes / td / 1e9, 1),
+            "duplex_gbs_each": round(nbytes / tb / 1e9, 1)}
 
 
 def cpu_ew_baseline(T, C, budget_s=12.0, n=1 << 24):
@@ -338,7 +371,8 @@ def main():
                    "parallelism": f"replicas x{ws}"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
                      "frac": round(achieved / pk["hbm_gbs"], 4), "traffic": traffic,
-                     "peak_source": f"{pk['src']} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
+                     "peak_source": ("of measured: MEASURED_PEAKS.json hbm_gbs (copy)" if pk["src"] == "measured"
+                                     else "of fallback: B200_PROFILING.md 6.65 TB/s (MEASURED_PEAKS.json absent)"),
                      "kernel": "tx_ew_flat (NVRTC composite[5])"},
         "gpu_launches": args.steps,
         "clocks": clk.summary(),
@@ -348,7 +382,16 @@ def main():
             dt, hb, db = bench_ew_e2e(f)
             line["e2e"] = {"value": round(bytes_step / dt / 1e9, 2), "unit": "GB/s", "h2d_bytes_per_step": hb,
                            "d2h_bytes_per_step": db, "ms_per_step": round(dt * 1e3, 2),
-                           "path": "CompiledFunction.__call__ with pinned host torch tensors -> numpy result"}
+                           "path": "CompiledFunction.__call__ with pinned host torch tensors -> numpy result "
+                                   "(chunk-pipelined H2D / kernel / D2H, stream.py)"}
+            try:
+                lk = link_bandwidth()
+                bound_s = max(hb / (lk["h2d_gbs"] * 1e9), db / (lk["d2h_gbs"] * 1e9))
+                lk["e2e_bound_gbs"] = round(bytes_step / bound_s / 1e9, 2)
+                lk["e2e_frac_of_link_bound"] = round((bytes_step / dt / 1e9) / lk["e2e_bound_gbs"], 3)
+                line["e2e"]["link"] = lk
+            except Exception as e:  # pragma: no cover
+                line["e2e"]["link"] = {"error": repr(e)[:200]}
         except Exception as e:  # pragma: no cover
             line["e2e"] = {"error": repr(e)}
         line["cpu_baseline"] = cpu_ew_baseline(T, C)

@@ -12,6 +12,11 @@
 namespace tx {
 namespace {
 
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)), "l"(gmem)
+               : "memory");
+}
+
 // --------------------------------------------------------------- SIMT tiles
 // 64x64 tile, 256 threads, 4x4 outputs per thread, BK = 16; arbitrary strides.
 template <class T>
@@ -155,6 +160,100 @@ __global__ void __launch_bounds__(256) rowdot_kernel(const float* __restrict__ A
   }
 }
 
+// Whole-K variant: B (K x NN fp32, its natural row-major layout) is staged
+// ONCE per CTA in shared memory with cp.async (every thread issues all of its
+// 16-byte copies back to back, so the staging is one latency, not one per
+// element), and the CTA then walks row groups grid-stride (persistent): no
+// per-chunk __syncthreads, each lane keeps R x 2 independent 128-bit A loads
+// in flight.  Lane l handles k = 4l + 128j: the NN float4 at Bs[k*NN ..] are
+// B rows k..k+3.  This is the HBM-bound form for h2.W3 ([8192,4096] x
+// [4096,10]: 128 MB of A per call) and the logreg x.W.
+constexpr int RDF_MAX_SMEM = 200 * 1024;
+
+
+template <int NN, int R>
+__global__ void __launch_bounds__(512) rowdot_full_kernel(const float* __restrict__ A, const float* __restrict__ B,
+                                                         float* __restrict__ C, int64_t M, int N, int64_t K,
+                                                         int64_t sam, int64_t sbk, int64_t sbn, int64_t scm,
+                                                         int64_t scn, Epi<float> epi) {
+  extern __shared__ __align__(16) float Bs[];  // [K][NN]
+  const int64_t total = K * NN;
+  if (sbn == 1 && sbk == NN && N == NN && (((uintptr_t)B & 15) == 0) && total % 4 == 0) {
+    for (int64_t e = threadIdx.x; e < total / 4; e += blockDim.x) cp_async16(Bs + 4 * e, B + 4 * e);
+    asm volatile("cp.async.wait_all;" ::: "memory");
+  } else {
+#pragma unroll 4
+    for (int64_t e = threadIdx.x; e < total; e += blockDim.x) {
+      const int64_t k = e / NN;
+      const int n = (int)(e - k * NN);
+      Bs[e] = n < N ? B[k * sbk + (int64_t)n * sbn] : 0.f;
+    }
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int warps = blockDim.x >> 5;
+  const bool vec = (sam % 4 == 0) && (K % 4 == 0) && (((uintptr_t)A & 15) == 0);
+  for (int64_t g = (int64_t)blockIdx.x * warps + (threadIdx.x >> 5); g * R < M; g += (int64_t)gridDim.x * warps) {
+    const int64_t row0 = g * R;
+    float acc[R][NN];
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int n = 0; n < NN; ++n) acc[r][n] = 0.f;
+    if (vec) {
+#pragma unroll 2
+      for (int64_t kk = lane * 4; kk < K; kk += 128) {
+        float4 av[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          av[r] = (row0 + r < M) ? __ldcs(reinterpret_cast<const float4*>(A + (row0 + r) * sam + kk))
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+        float b[4 * NN];
+#pragma unroll
+        for (int q = 0; q < NN; ++q) {
+          const float4 t = reinterpret_cast<const float4*>(Bs + kk * NN)[q];
+          b[4 * q] = t.x; b[4 * q + 1] = t.y; b[4 * q + 2] = t.z; b[4 * q + 3] = t.w;
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+          for (int n = 0; n < NN; ++n)
+            acc[r][n] += av[r].x * b[n] + av[r].y * b[NN + n] + av[r].z * b[2 * NN + n] + av[r].w * b[3 * NN + n];
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int64_t m = row0 + r;
+        if (m >= M) break;
+        const float* a = A + m * sam;
+        for (int64_t kk = lane; kk < K; kk += 32) {
+          const float av = __ldg(a + kk);
+#pragma unroll
+          for (int n = 0; n < NN; ++n) acc[r][n] += av * Bs[kk * NN + n];
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+#pragma unroll
+      for (int n = 0; n < NN; ++n) {
+        float v = acc[r][n];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+        acc[r][n] = v;
+      }
+      const int64_t m = row0 + r;
+      if (m < M && lane < N) {
+        float v = 0.f;
+#pragma unroll
+        for (int n = 0; n < NN; ++n)
+          if (n == lane) v = acc[r][n];
+        C[m * scm + (int64_t)lane * scn] = epi.apply(v, m, lane);
+      }
+    }
+  }
+}
+
 // ------------------------------------------------ K <= 16 (outer-product-like)
 // C[m, n] = sum_{k<K} A[m,k] B[k,n] (dz.W3^T).  CTA tile 32 rows x 1024 cols,
 // 4 adjacent columns per thread held in registers, A tile broadcast from smem,
@@ -180,6 +279,37 @@ __global__ void __launch_bounds__(256) outer_kernel(const float* __restrict__ A,
     for (int j = 0; j < 4; ++j) b[k][j] = (k < K && n0 + j < N) ? __ldg(B + k * sbk + (n0 + j) * sbn) : 0.f;
   const bool vst = scn == 1 && (scm % 4 == 0) && (((uintptr_t)C & 15) == 0) && n0 + 4 <= N;
   const int rows = (int)min((int64_t)32, M - m0);
+  // [M,N] epilogue operand read with 128-bit loads, 4 rows in flight (dH*g:
+  // reading the aux tensor is half of this kernel's traffic)
+  const bool vaux = vst && (epi.kind == TX_EPI_MUL_AUX || epi.kind == TX_EPI_MUL_1MSQR) && epi.s1 == 1 &&
+                    (epi.s0 % 4 == 0) && (((uintptr_t)epi.aux & 15) == 0);
+  if (vaux && rows == 32) {
+#pragma unroll 1
+    for (int r0 = 0; r0 < 32; r0 += 4) {
+      float4 x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) x[u] = __ldcs(reinterpret_cast<const float4*>(epi.aux + (m0 + r0 + u) * epi.s0 + n0));
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int r = r0 + u;
+        float o[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int k = 0; k < KK; ++k) {
+          const float av = As[r][k];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) o[j] += av * b[k][j];
+        }
+        float g[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float f = epi.kind == TX_EPI_MUL_AUX ? g[j] : __fsub_rn(1.0f, __fmul_rn(g[j], g[j]));
+          o[j] = __fmul_rn(o[j], f);
+        }
+        __stcs(reinterpret_cast<float4*>(C + (m0 + r) * scm + n0), make_float4(o[0], o[1], o[2], o[3]));
+      }
+    }
+    return;
+  }
   for (int r = 0; r < rows; ++r) {
     const int64_t m = m0 + r;
     float o[4] = {0.f, 0.f, 0.f, 0.f};
@@ -202,17 +332,21 @@ __global__ void __launch_bounds__(256) outer_kernel(const float* __restrict__ A,
 
 // ------------------------------------- N <= 16, A M-contiguous (x^T . dz form)
 // C[m, n] = sum_k A[k*sak + m] * B[k, n]: a column reduction over k.  Each
-// thread owns 4 adjacent m (128-bit loads along the contiguous M axis); B rows
-// are broadcast from smem; grid.y splits k and writes partials [S][M][N]
-// that kred_finalize sums in fixed order (deterministic, no atomics).
+// thread owns 4 adjacent m (128-bit loads along the contiguous M axis) and
+// keeps KR_U of them in flight; B rows are broadcast from smem; grid.y splits
+// k and writes partials [S][M][N] that kred_finalize sums in fixed order
+// (deterministic, no atomics).  128-thread CTAs (512 m per CTA) keep the
+// partial volume S*M*N small for a given CTA count.
 constexpr int KR_KC = 64;
+constexpr int KR_THREADS = 128;
+constexpr int KR_U = 8;
 
 template <int NN>
-__global__ void __launch_bounds__(256) kred_kernel(const float* __restrict__ A, const float* __restrict__ B,
-                                                  float* __restrict__ P, int64_t M, int N, int64_t K, int64_t sak,
-                                                  int64_t sbk, int64_t sbn, int splits) {
+__global__ void __launch_bounds__(KR_THREADS) kred_kernel(const float* __restrict__ A, const float* __restrict__ B,
+                                                         float* __restrict__ P, int64_t M, int N, int64_t K,
+                                                         int64_t sak, int64_t sbk, int64_t sbn, int splits) {
   __shared__ float Bs[KR_KC][NN];
-  const int64_t m0 = ((int64_t)blockIdx.x * 256 + threadIdx.x) * 4;
+  const int64_t m0 = ((int64_t)blockIdx.x * KR_THREADS + threadIdx.x) * 4;
   const int64_t chunk = (K + splits - 1) / splits;
   const int64_t klo = (int64_t)blockIdx.y * chunk, khi = min(K, klo + chunk);
   const bool vec = (sak % 4 == 0) && (((uintptr_t)A & 15) == 0) && m0 + 4 <= M;
@@ -223,7 +357,7 @@ __global__ void __launch_bounds__(256) kred_kernel(const float* __restrict__ A, 
     for (int n = 0; n < NN; ++n) acc[j][n] = 0.f;
   for (int64_t k0 = klo; k0 < khi; k0 += KR_KC) {
     __syncthreads();
-    for (int e = threadIdx.x; e < KR_KC * NN; e += 256) {
+    for (int e = threadIdx.x; e < KR_KC * NN; e += KR_THREADS) {
       const int kk = e / NN, n = e % NN;
       Bs[kk][n] = (k0 + kk < khi && n < N) ? B[(k0 + kk) * sbk + n * sbn] : 0.f;
     }
@@ -231,8 +365,23 @@ __global__ void __launch_bounds__(256) kred_kernel(const float* __restrict__ A, 
     if (m0 < M) {
       const int kend = (int)min((int64_t)KR_KC, khi - k0);
       if (vec) {
-#pragma unroll 4
-        for (int kk = 0; kk < kend; ++kk) {
+        int kk = 0;
+        for (; kk + KR_U <= kend; kk += KR_U) {
+          float4 av[KR_U];
+#pragma unroll
+          for (int u = 0; u < KR_U; ++u) av[u] = __ldcs(reinterpret_cast<const float4*>(A + (k0 + kk + u) * sak + m0));
+#pragma unroll
+          for (int u = 0; u < KR_U; ++u)
+#pragma unroll
+            for (int n = 0; n < NN; ++n) {
+              const float bv = Bs[kk + u][n];
+              acc[0][n] += av[u].x * bv;
+              acc[1][n] += av[u].y * bv;
+              acc[2][n] += av[u].z * bv;
+              acc[3][n] += av[u].w * bv;
+            }
+        }
+        for (; kk < kend; ++kk) {
           const float4 av = __ldcs(reinterpret_cast<const float4*>(A + (k0 + kk) * sak + m0));
 #pragma unroll
           for (int n = 0; n < NN; ++n) {
@@ -265,19 +414,130 @@ __global__ void __launch_bounds__(256) kred_kernel(const float* __restrict__ A, 
   }
 }
 
+// Ring variant (M % 4 == 0, aligned, M-contiguous A): every thread streams its
+// own 16-byte column slice of A rows through a KR_S-stage cp.async ring in
+// shared memory (KR_S x KR_RU rows in flight per thread, independent of the
+// register budget), and the CTA's slice of B (chunk x NN) is staged once.
+// Only the issuing thread reads its ring slots, so there is no CTA barrier in
+// the loop.
+constexpr int KR_S = 4, KR_RU = 4;
+
+template <int NN>
+__global__ void __launch_bounds__(KR_THREADS) kred_ring_kernel(const float* __restrict__ A, const float* __restrict__ B,
+                                                              float* __restrict__ P, int64_t M, int N, int64_t K,
+                                                              int64_t sak, int64_t sbk, int64_t sbn, int splits) {
+  extern __shared__ __align__(16) float4 kr_smem[];
+  float4* ring = kr_smem;                                                  // [KR_S*KR_RU][KR_THREADS]
+  float* Bs = reinterpret_cast<float*>(kr_smem + KR_S * KR_RU * KR_THREADS);  // [chunk][NN]
+  const int tid = threadIdx.x;
+  const int64_t m0 = ((int64_t)blockIdx.x * KR_THREADS + tid) * 4;
+  const int64_t chunk = (K + splits - 1) / splits;
+  const int64_t klo = (int64_t)blockIdx.y * chunk, khi = min(K, klo + chunk);
+  const int nrows = (int)max((int64_t)0, khi - klo);
+#pragma unroll 4
+  for (int e = tid; e < nrows * NN; e += KR_THREADS) {
+    const int k = e / NN, n = e - k * NN;
+    Bs[e] = n < N ? B[(klo + k) * sbk + (int64_t)n * sbn] : 0.f;
+  }
+  __syncthreads();
+  const bool active = m0 < M;
+  const float* a0 = A + klo * sak + m0;
+  auto issue = [&](int r0) {
+#pragma unroll
+    for (int u = 0; u < KR_RU; ++u) {
+      const int r = r0 + u;
+      if (active && r < nrows) cp_async16(&ring[(r % (KR_S * KR_RU)) * KR_THREADS + tid], a0 + (int64_t)r * sak);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+#pragma unroll
+  for (int st = 0; st < KR_S; ++st) issue(st * KR_RU);
+  float acc[4][NN];
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int n = 0; n < NN; ++n) acc[j][n] = 0.f;
+  for (int r0 = 0; r0 < nrows; r0 += KR_RU) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(KR_S - 1) : "memory");
+#pragma unroll
+    for (int u = 0; u < KR_RU; ++u) {
+      const int r = r0 + u;
+      if (r < nrows) {
+        const float4 av = ring[(r % (KR_S * KR_RU)) * KR_THREADS + tid];
+#pragma unroll
+        for (int n = 0; n < NN; ++n) {
+          const float bv = Bs[r * NN + n];
+          acc[0][n] += av.x * bv;
+          acc[1][n] += av.y * bv;
+          acc[2][n] += av.z * bv;
+          acc[3][n] += av.w * bv;
+        }
+      }
+    }
+    issue(r0 + KR_S * KR_RU);
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  if (!active) return;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int64_t m = m0 + j;
+#pragma unroll
+    for (int n = 0; n < NN; ++n)
+      if (n < N) P[((int64_t)blockIdx.y * M + m) * N + n] = acc[j][n];
+  }
+}
+
+// sums the S partials of each output in split order; 8 independent loads in
+// flight per thread (the adds stay in order, so the result is deterministic)
 __global__ void kred_finalize(const float* __restrict__ P, float* __restrict__ C, int64_t M, int N, int splits,
                               int64_t scm, int64_t scn, Epi<float> epi) {
   int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (e >= M * N) return;
+  const int64_t MN = M * N;
+  if (e >= MN) return;
   int64_t m = e / N;
   int n = (int)(e - m * N);
   float v = 0.f;
-  for (int s = 0; s < splits; ++s) v += P[((int64_t)s * M + m) * N + n];
+  int s = 0;
+  for (; s + 8 <= splits; s += 8) {
+    float q[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) q[u] = __ldcs(P + (int64_t)(s + u) * MN + e);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v += q[u];
+  }
+  for (; s < splits; ++s) v += P[(int64_t)s * MN + e];
   C[m * scm + n * scn] = epi.apply(v, m, n);
+}
+
+template <int NN, int R>
+static int launch_rowdot_full(const G& g, int threads, size_t smem, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    TX_CUDA(cudaFuncSetAttribute(rowdot_full_kernel<NN, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, RDF_MAX_SMEM));
+    attr = true;
+  }
+  const int warps = threads / 32;
+  int64_t groups = (g.M + R - 1) / R;
+  int64_t blocks = (groups + warps - 1) / warps;
+  const int per_sm = (int)(RDF_MAX_SMEM / (smem + 1024)) > 0 ? (int)(RDF_MAX_SMEM / (smem + 1024)) : 1;
+  const int64_t cap = (int64_t)sm_count() * (per_sm < 4 ? per_sm : 4);
+  if (blocks > cap) blocks = cap;
+  rowdot_full_kernel<NN, R><<<(unsigned)blocks, threads, smem, st>>>((const float*)g.A, (const float*)g.B, (float*)g.C,
+                                                                     g.M, (int)g.N, g.K, g.sam, g.sbk, g.sbn, g.scm,
+                                                                     g.scn, g.epi_f);
+  TX_CUDA(cudaGetLastError());
+  return TX_OK;
 }
 
 template <int NN>
 static int launch_rowdot(const G& g, cudaStream_t st) {
+  const size_t smem = (size_t)NN * (size_t)g.K * 4;
+  if (smem <= (size_t)RDF_MAX_SMEM) {
+    // many rows: 16 warps x 4 rows per CTA, one CTA per SM; few rows (logreg):
+    // 4-warp CTAs, one row per warp, to spread over the SMs
+    if (g.M >= 4096) return launch_rowdot_full<NN, (NN <= 10 ? 4 : 2)>(g, 512, smem, st);
+    return launch_rowdot_full<NN, 1>(g, 128, smem, st);
+  }
   if (g.M >= 4096) {
     unsigned blocks = (unsigned)((g.M + 31) / 32);
     rowdot_kernel<NN, 4><<<blocks, 256, 0, st>>>((const float*)g.A, (const float*)g.B, (float*)g.C, g.M, (int)g.N,
@@ -304,8 +564,14 @@ template <int NN>
 static int launch_kred(const G& g, void* ws, size_t wsb, cudaStream_t st) {
   int splits = kred_splits(g.M, g.K);
   TX_CHECK((size_t)splits * g.M * g.N * 4 <= wsb, TX_E_ARG, "tx_gemm: skinny workspace too small");
-  dim3 grid((unsigned)((g.M + 1023) / 1024), (unsigned)splits);
-  kred_kernel<NN><<<grid, 256, 0, st>>>((const float*)g.A, (const float*)g.B, (float*)ws, g.M, (int)g.N, g.K, g.sak,
+  dim3 grid((unsigned)((g.M + 4 * KR_THREADS - 1) / (4 * KR_THREADS)), (unsigned)splits);
+  const int64_t chunk = (g.K + splits - 1) / splits;
+  const size_t smem = (size_t)KR_S * KR_RU * KR_THREADS * 16 + (size_t)chunk * NN * 4;
+  if (g.M % 4 == 0 && g.sak % 4 == 0 && ((uintptr_t)g.A & 15) == 0 && smem <= 48 * 1024) {
+    kred_ring_kernel<NN><<<grid, KR_THREADS, smem, st>>>((const float*)g.A, (const float*)g.B, (float*)ws, g.M,
+                                                         (int)g.N, g.K, g.sak, g.sbk, g.sbn, splits);
+  } else
+  kred_kernel<NN><<<grid, KR_THREADS, 0, st>>>((const float*)g.A, (const float*)g.B, (float*)ws, g.M, (int)g.N, g.K, g.sak,
                                         g.sbk, g.sbn, splits);
   int64_t tot = g.M * g.N;
   kred_finalize<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>((const float*)ws, (float*)g.C, g.M, (int)g.N, splits,
@@ -317,8 +583,8 @@ static int launch_kred(const G& g, void* ws, size_t wsb, cudaStream_t st) {
 }  // namespace
 
 int kred_splits(int64_t M, int64_t K) {
-  int64_t mblocks = (M + 1023) / 1024;
-  int64_t want = (int64_t)sm_count() * 2;
+  int64_t mblocks = (M + 4 * KR_THREADS - 1) / (4 * KR_THREADS);
+  int64_t want = (int64_t)sm_count() * 4;
   int64_t s = (want + mblocks - 1) / mblocks;
   int64_t maxs = K / 16;
   if (s > maxs) s = maxs;

@@ -95,6 +95,25 @@ __device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* ma
       : "memory");
 }
 
+// 3-D box for an MN-major operand tile: {32 MN, BK, MN-blocks} lands in smem
+// as consecutive 4 KB [32 k][32 mn] blocks -- one TMA instruction per operand
+// per stage instead of one per 32-wide MN block.
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+          su32(dst)),
+      "l"((uint64_t)map), "r"(su32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_2sm(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                                int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
+      "%5}], [%2];" ::"r"(su32(dst)),
+      "l"((uint64_t)map), "r"(su32(bar) & kPeerMask), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -193,6 +212,7 @@ struct TcParams {
   int64_t ldc;
   int M, N, K;
   int a_mn, b_mn;  // 1 = operand is MN-major in memory
+  int a_3d, b_3d;  // MN-major operand loaded with one 3-D box per stage
   int num_m, num_n, num_tiles;
   Epi<float> epi;
 };
@@ -274,13 +294,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if constexpr (CG == 1) tma_load_2d(dst, map, full + stage, c0, c1);
             else tma_load_2d_2sm(dst, map, full + stage, c0, c1);
           };
-          if (p.a_mn) {
+          auto load3 = [&](void* dst, const CUtensorMap* map, int c1, int c2) {
+            if constexpr (CG == 1) tma_load_3d(dst, map, full + stage, 0, c1, c2);
+            else tma_load_3d_2sm(dst, map, full + stage, 0, c1, c2);
+          };
+          if (p.a_3d) {
+            load3(sa, &mapA, k0, m0 / 32);
+          } else if (p.a_mn) {
 #pragma unroll
             for (int j = 0; j < BM / 32; ++j) load(sa + j * 4096, &mapA, m0 + 32 * j, k0);
           } else {
             load(sa, &mapA, k0, m0);
           }
-          if (p.b_mn) {
+          if (p.b_3d) {
+            load3(sb, &mapB, k0, n0 / 32);
+          } else if (p.b_mn) {
 #pragma unroll
             for (int j = 0; j < BNL / 32; ++j) load(sb + j * 4096, &mapB, n0 + 32 * j, k0);
           } else {
@@ -340,11 +368,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     int it = 0;
     const Epi<float>& E = p.epi;
     const bool vec_ok = (p.ldc % 4 == 0) && (((uintptr_t)p.C & 15) == 0) &&
-                        (E.kind != TX_EPI_MUL_AUX || (E.s1 == 1 && E.s0 % 4 == 0 && ((uintptr_t)E.aux & 15) == 0)) &&
+                        ((E.kind != TX_EPI_MUL_AUX && E.kind != TX_EPI_MUL_1MSQR) ||
+                         (E.s1 == 1 && E.s0 % 4 == 0 && ((uintptr_t)E.aux & 15) == 0)) &&
                         (E.kind != TX_EPI_BIAS_TANH_DUAL || (E.o1 == 1 && E.o0 % 4 == 0 && ((uintptr_t)E.out2 & 15) == 0)) &&
                         (E.kind != TX_EPI_BIAS && E.kind != TX_EPI_BIAS_TANH && E.kind != TX_EPI_BIAS_TANH_DUAL ||
-                         (E.s1 == 1 && ((uintptr_t)E.aux & 15) == 0)) &&
-                        E.kind != TX_EPI_MUL_1MSQR;
+                         (E.s1 == 1 && ((uintptr_t)E.aux & 15) == 0));
     for (int t = cluster_id; t < p.num_tiles; t += num_clusters, ++it) {
       int mb, nb;
       tile_coords(t, p.num_m, p.num_n, mb, nb);
@@ -382,11 +410,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     __fsub_rn(1.0f, __fmul_rn(v[i], v[i])), __fsub_rn(1.0f, __fmul_rn(v[i + 1], v[i + 1])),
                     __fsub_rn(1.0f, __fmul_rn(v[i + 2], v[i + 2])), __fsub_rn(1.0f, __fmul_rn(v[i + 3], v[i + 3])));
             }
-          } else if (E.kind == TX_EPI_MUL_AUX) {
+          } else if (E.kind == TX_EPI_MUL_AUX || E.kind == TX_EPI_MUL_1MSQR) {
             const float* g = E.aux + (int64_t)row * E.s0 + n;
+            const bool sq = E.kind == TX_EPI_MUL_1MSQR;  // aux is h: factor 1 - h^2
 #pragma unroll
             for (int i = 0; i < 32; i += 4) {
-              const float4 g4 = __ldcs(reinterpret_cast<const float4*>(g + i));
+              float4 g4 = __ldcs(reinterpret_cast<const float4*>(g + i));
+              if (sq) {
+                g4.x = __fsub_rn(1.0f, __fmul_rn(g4.x, g4.x)); g4.y = __fsub_rn(1.0f, __fmul_rn(g4.y, g4.y));
+                g4.z = __fsub_rn(1.0f, __fmul_rn(g4.z, g4.z)); g4.w = __fsub_rn(1.0f, __fmul_rn(g4.w, g4.w));
+              }
               v[i] = __fmul_rn(v[i], g4.x); v[i + 1] = __fmul_rn(v[i + 1], g4.y);
               v[i + 2] = __fmul_rn(v[i + 2], g4.z); v[i + 3] = __fmul_rn(v[i + 3], g4.w);
             }
@@ -458,6 +491,23 @@ static int make_map(CUtensorMap* m, const void* base, int64_t inner, int64_t out
   return TX_OK;
 }
 
+// MN-major operand as 3-D {32 (MN inner), K, MN/32}: element (mn, k) at
+// k*ld + mn; box {32, BK, blocks}.  Needs MN % 32 == 0 (no read past the last
+// row of the allocation).
+static int make_map_mn3d(CUtensorMap* m, const void* base, int64_t MN, int64_t K, int64_t ld, int blocks) {
+  EncodeFn enc = encode_fn();
+  TX_CHECK(enc, TX_E_NODEVICE, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {32, (cuuint64_t)K, (cuuint64_t)(MN / 32)};
+  cuuint64_t strides[2] = {(cuuint64_t)(ld * 4), 128};
+  cuuint32_t box[3] = {32, (cuuint32_t)BK, (cuuint32_t)blocks};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_TFLOAT32, 3, const_cast<void*>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(TX_E_CUDA, "cuTensorMapEncodeTiled (3d) failed (code " + std::to_string((int)r) + ")");
+  return TX_OK;
+}
+
 }  // namespace
 
 int gemm_tc_eligible(const G& g) {
@@ -487,10 +537,15 @@ int gemm_tc(const G& g, cudaStream_t st) {
   if (cg == 2 && g.M <= BM) cg = 1;
   const int bnl = BN / cg;
   CUtensorMap ma, mb;
-  if (a_mn) rc = make_map(&ma, g.A, g.M, g.K, g.sak, 32, 32, true);
+  const bool no3d = getenv("TX_GEMM_NO3D") != nullptr;
+  const bool a_3d = a_mn && g.M % 32 == 0 && !no3d;
+  const bool b_3d = b_mn && g.N % 32 == 0 && !no3d;
+  if (a_3d) rc = make_map_mn3d(&ma, g.A, g.M, g.K, g.sak, BM / 32);
+  else if (a_mn) rc = make_map(&ma, g.A, g.M, g.K, g.sak, 32, 32, true);
   else rc = make_map(&ma, g.A, g.K, g.M, g.sam, 32, BM, false);
   if (rc) return rc;
-  if (b_mn) rc = make_map(&mb, g.B, g.N, g.K, g.sbk, 32, 32, true);
+  if (b_3d) rc = make_map_mn3d(&mb, g.B, g.N, g.K, g.sbk, bnl / 32);
+  else if (b_mn) rc = make_map(&mb, g.B, g.N, g.K, g.sbk, 32, 32, true);
   else rc = make_map(&mb, g.B, g.K, g.N, g.sbn, 32, bnl, false);
   if (rc) return rc;
   TcParams p;
@@ -501,6 +556,8 @@ int gemm_tc(const G& g, cudaStream_t st) {
   p.K = (int)g.K;
   p.a_mn = a_mn;
   p.b_mn = b_mn;
+  p.a_3d = a_3d;
+  p.b_3d = b_3d;
   p.num_m = (int)((g.M + BM * cg - 1) / (BM * cg));
   p.num_n = (int)((g.N + BN - 1) / BN);
   p.num_tiles = p.num_m * p.num_n;

@@ -123,7 +123,9 @@ __global__ void __launch_bounds__(kThreads) row_kernel(const T* __restrict__ x, 
                                                       long long* __restrict__ pi) {
   const int64_t row = blockIdx.y + (int64_t)blockIdx.z * gridDim.y;
   if (row >= rows) return;
-  const int64_t chunk = (R + splits - 1) / splits;
+  // split chunks are a multiple of 4 elements so every split of an aligned
+  // row starts 16-byte aligned (the 128-bit paths below)
+  const int64_t chunk = splits == 1 ? R : (((R + splits - 1) / splits + 3) & ~(int64_t)3);
   const int64_t lo = (int64_t)blockIdx.x * chunk;
   const int64_t hi = min(R, lo + chunk);
   const T* p = x + row * rs;
@@ -162,7 +164,19 @@ __global__ void __launch_bounds__(kThreads) row_kernel(const T* __restrict__ x, 
       using V = typename Vec4<T>::type;
       const int64_t nv = (hi - lo) / 4;
       const V* pv4 = reinterpret_cast<const V*>(p + lo);
-      for (int64_t k = threadIdx.x; k < nv; k += blockDim.x) {
+      int64_t k = threadIdx.x;
+      const int64_t bd = blockDim.x;
+      for (; k + 3 * bd < nv; k += 4 * bd) {
+        V q[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) q[u] = __ldcs(pv4 + k + u * bd);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t b = lo + 4 * (k + u * bd);
+          a.push(q[u].x, b); a.push(q[u].y, b + 1); a.push(q[u].z, b + 2); a.push(q[u].w, b + 3);
+        }
+      }
+      for (; k < nv; k += bd) {
         V q = __ldcs(pv4 + k);
         int64_t b = lo + 4 * k;
         a.push(q.x, b); a.push(q.y, b + 1); a.push(q.z, b + 2); a.push(q.w, b + 3);
@@ -202,20 +216,26 @@ __global__ void __launch_bounds__(kThreads) row_warp_kernel(const T* __restrict_
   }
 }
 
+// one CTA per output merges that output's split partials (strided over the
+// CTA, then the shuffle tree) — splits can be several hundred (the all-axes
+// reduction of a 16384^2 matrix uses 592), too many for one serial thread.
 template <class T, int OP>
-__global__ void finalize_splits(int64_t rows, int splits, const T* __restrict__ pv, const long long* __restrict__ pi,
-                                T* __restrict__ out, long long* __restrict__ out_idx) {
-  int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (row >= rows) return;
+__global__ void __launch_bounds__(kThreads) finalize_splits(int64_t rows, int splits, const T* __restrict__ pv,
+                                                           const long long* __restrict__ pi, T* __restrict__ out,
+                                                           long long* __restrict__ out_idx) {
+  const int64_t row = blockIdx.x;
   Acc<T, OP> a;
   a.init();
-  for (int s = 0; s < splits; ++s) {
+  for (int s = threadIdx.x; s < splits; s += blockDim.x) {
     Acc<T, OP> b;
     b.v = pv[row * splits + s];
     b.i = pi[row * splits + s];
     a.merge(b);
   }
-  if (OP == TX_SUM || OP == TX_MAX) out[row] = a.v; else out_idx[row] = a.i;
+  a = block_reduce<T, OP>(a);
+  if (threadIdx.x == 0) {
+    if (OP == TX_SUM || OP == TX_MAX) out[row] = a.v; else out_idx[row] = a.i;
+  }
 }
 
 // ------------------------------------------------------------------ COL
@@ -265,25 +285,43 @@ done:
       if (OP == TX_SUM || OP == TX_MAX) out[c] = a[j].v; else out_idx[c] = a[j].i;
     } else {
       pv[(int64_t)blockIdx.y * K + c] = a[j].v;
-      pi[(int64_t)blockIdx.y * K + c] = a[j].i;
+      if (OP == TX_ARGMAX_INDEX || OP == TX_ARGMAX_ONEHOT) pi[(int64_t)blockIdx.y * K + c] = a[j].i;
     }
   }
 }
 
+// partials [splits][K]: a 32-column x 8-lane CTA, each lane merging every
+// 8th split (coalesced across columns), then the 8 lanes merged in order.
 template <class T, int OP>
-__global__ void finalize_cols(int64_t K, int splits, const T* __restrict__ pv, const long long* __restrict__ pi,
-                              T* __restrict__ out, long long* __restrict__ out_idx) {
-  int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (c >= K) return;
+__global__ void __launch_bounds__(256) finalize_cols(int64_t K, int splits, const T* __restrict__ pv,
+                                                    const long long* __restrict__ pi, T* __restrict__ out,
+                                                    long long* __restrict__ out_idx) {
+  __shared__ T sv[8][32];
+  __shared__ long long si[8][32];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t c = (int64_t)blockIdx.x * 32 + tx;
   Acc<T, OP> a;
   a.init();
-  for (int s = 0; s < splits; ++s) {
-    Acc<T, OP> b;
-    b.v = pv[(int64_t)s * K + c];
-    b.i = pi[(int64_t)s * K + c];
-    a.merge(b);
+  if (c < K) {
+    for (int s = ty; s < splits; s += 8) {
+      Acc<T, OP> b;
+      b.v = pv[(int64_t)s * K + c];
+      b.i = (OP == TX_ARGMAX_INDEX || OP == TX_ARGMAX_ONEHOT) ? pi[(int64_t)s * K + c] : 0;
+      a.merge(b);
+    }
   }
-  if (OP == TX_SUM || OP == TX_MAX) out[c] = a.v; else out_idx[c] = a.i;
+  sv[ty][tx] = a.v;
+  si[ty][tx] = a.i;
+  __syncthreads();
+  if (ty == 0 && c < K) {
+    for (int j = 1; j < 8; ++j) {
+      Acc<T, OP> b;
+      b.v = sv[j][tx];
+      b.i = si[j][tx];
+      a.merge(b);
+    }
+    if (OP == TX_SUM || OP == TX_MAX) out[c] = a.v; else out_idx[c] = a.i;
+  }
 }
 
 // ------------------------------------------------------------------ GEN
@@ -408,7 +446,7 @@ static void make_plan(int op, const tx_tensor& x, uint32_t mask, int itemsz, Pla
       int64_t colblocks = (K + 4 * kThreads - 1) / (4 * kThreads);
       int64_t want = (int64_t)sms * 4;
       int64_t splits = (want + colblocks - 1) / colblocks;
-      int64_t maxs = R / 256;
+      int64_t maxs = R / 64;
       if (splits > maxs) splits = maxs;
       if (splits > 65535) splits = 65535;
       if (splits < 1) splits = 1;
@@ -477,7 +515,7 @@ static int run(const tx_tensor& x, uint32_t mask, tx_tensor& y, char* ws, size_t
       dim3 grid((unsigned)p.splits, gy, gz);
       row_kernel<T, OP><<<grid, kThreads, 0, st>>>(xp, rows, p.R, p.ks, p.es, p.splits, out, out_idx, pv, pi);
       if (p.splits > 1)
-        finalize_splits<T, OP><<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(rows, p.splits, pv, pi, out, out_idx);
+        finalize_splits<T, OP><<<(unsigned)rows, kThreads, 0, st>>>(rows, p.splits, pv, pi, out, out_idx);
       break;
     }
     case ROWWARP: {
@@ -492,7 +530,7 @@ static int run(const tx_tensor& x, uint32_t mask, tx_tensor& y, char* ws, size_t
       dim3 grid(gx, (unsigned)p.splits);
       col_kernel<T, OP><<<grid, kThreads, 0, st>>>(xp, p.R, p.K, p.rs, p.splits, vec, out, out_idx, pv, pi);
       if (p.splits > 1)
-        finalize_cols<T, OP><<<(unsigned)((p.K + 255) / 256), 256, 0, st>>>(p.K, p.splits, pv, pi, out, out_idx);
+        finalize_cols<T, OP><<<(unsigned)((p.K + 31) / 32), 256, 0, st>>>(p.K, p.splits, pv, pi, out, out_idx);
       break;
     }
     case GEN: {

@@ -180,10 +180,67 @@ def _match_bias_tanh_dual(prog, z_idx):
     return float(prog.consts[r3[0][1]][1]) == 1.0
 
 
+def _sole_dot_client(fgraph, z, Dot):
+    """z = dot(a, b) feeding exactly one consumer (and not a graph output)."""
+    if z.owner is None or not isinstance(z.owner.op, Dot) or fgraph.is_output(z):
+        return False
+    a, b = z.owner.inputs
+    return a.type.ndim == 2 and b.type.ndim == 2 and len(fgraph.node_clients(z)) == 1 \
+        and len(fgraph.clients[z]) == 1
+
+
+def _fuse_tanh_layers(fgraph, emit) -> int:
+    """Forward layer h = tanh(b + x.W) whose 1 - h^2 only feeds backward
+    products mul(dz.W^T, 1 - h^2): emit dot+bias_tanh for h and
+    dot+mul_1msqr(h) for each backward product, so 1 - h^2 is never
+    materialised (one [B,H] store and one [B,H] load fewer per layer than the
+    dual-output form).  Same scalar ops and rounding order as the unfused
+    nodes (sqr, sub(1, .), mul)."""
+    from .linalg import EPI_BIAS_TANH, EPI_MUL_1MSQR, Dot, DotEpilogue
+    applied = 0
+    for c in list(fgraph.toposort()):
+        if c.id not in fgraph.nodes or not isinstance(c.op, Composite) or len(c.inputs) != 2:
+            continue
+        zi = next((i for i, x in enumerate(c.inputs) if _sole_dot_client(fgraph, x, Dot)), None)
+        if zi is None:
+            continue
+        z, bias = c.inputs[zi], c.inputs[1 - zi]
+        if bias is z or bias.type.ndim != 1 or bias.type.dtype != z.type.dtype \
+                or not _match_bias_tanh_dual(c.op.program, zi):
+            continue
+        h, g = c.outputs
+        users = fgraph.node_clients(g)
+        if fgraph.is_output(g) or not users:
+            continue
+        back = []
+        for m in users:
+            if not (isinstance(m.op, Elemwise) and m.op.kernel == "mul" and len(m.inputs) == 2):
+                break
+            z2 = m.inputs[1] if m.inputs[0] is g else m.inputs[0]
+            if z2 is g or z2.type != g.type or not _sole_dot_client(fgraph, z2, Dot) \
+                    or m.outputs[0].type != z2.type:
+                break
+            back.append((m, z2))
+        else:
+            a, b = z.owner.inputs
+            (hn,) = apply(DotEpilogue(EPI_BIAS_TANH), [a, b, bias])
+            if hn.type != h.type:
+                continue
+            repl = [(h, hn)]
+            for m, z2 in back:
+                a2, b2 = z2.owner.inputs
+                (o,) = apply(DotEpilogue(EPI_MUL_1MSQR), [a2, b2, hn])
+                repl.append((m.outputs[0], o))
+            fgraph.replace_all(repl, "fuse_gemm_epilogue")
+            emit(node=c, replaced="dot+composite[tanh,1-h^2]", replacement=f"dot+bias_tanh + {len(back)} dot+mul_1msqr")
+            applied += 1 + len(back)
+    return applied
+
+
 @register_rewrite("fuse_gemm_epilogue", "abstract_select", "global")
 def fuse_gemm_epilogue(fgraph, ctx, emit) -> int:
     from .linalg import EPI_BIAS, EPI_BIAS_TANH_DUAL, EPI_MUL_AUX, Dot, DotEpilogue
-    applied = 0
+    applied = _fuse_tanh_layers(fgraph, emit)
     for d in list(fgraph.toposort()):
         if d.id not in fgraph.nodes or not isinstance(d.op, Dot):
             continue

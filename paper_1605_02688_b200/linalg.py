@@ -92,8 +92,9 @@ def dot(a: Variable, b: Variable) -> Variable:
 
 
 # epilogue kinds (include/texpr_b200.h TX_EPI_*)
-EPI_BIAS, EPI_BIAS_TANH_DUAL, EPI_MUL_AUX = 1, 4, 5
-_EPI_NAMES = {EPI_BIAS: "bias", EPI_BIAS_TANH_DUAL: "bias_tanh_dual", EPI_MUL_AUX: "mul_aux"}
+EPI_BIAS, EPI_BIAS_TANH, EPI_MUL_1MSQR, EPI_BIAS_TANH_DUAL, EPI_MUL_AUX = 1, 2, 3, 4, 5
+_EPI_NAMES = {EPI_BIAS: "bias", EPI_BIAS_TANH: "bias_tanh", EPI_MUL_1MSQR: "mul_1msqr",
+              EPI_BIAS_TANH_DUAL: "bias_tanh_dual", EPI_MUL_AUX: "mul_aux"}
 
 
 @register_op
@@ -105,6 +106,8 @@ class DotEpilogue(Op):
     replaced consumer's outputs, computed with the same scalar ops in the
     same order (see ``Epi`` in ``csrc/tx_gemm.h``):
       bias            out = aux[n] + a.b
+      bias_tanh       out = tanh(aux[n] + a.b)
+      mul_1msqr       out = (a.b) * (1 - aux^2)      (aux = the forward's h)
       bias_tanh_dual  out = tanh(aux[n] + a.b), out2 = 1 - out^2
       mul_aux         out = (a.b) * aux
     """

@@ -476,21 +476,19 @@ class _Gen:
         self.emit("__syncthreads();")
         self.emit("if (sk_ticket == gridDim.x - 1) {")
         self.emit("  __threadfence();")
-        self.emit("  __shared__ double sk_red[256];")
-        # every sink element: all 256 threads sum a strided slice of the block
-        # partials, then a fixed-shape tree -> deterministic
-        self.emit(f"  for (int e = 0; e < {total}; ++e) {{")
+        # one warp per sink element (elements strided over the 8 warps): lanes
+        # sum a fixed strided slice of the block partials, then a fixed xor
+        # tree -> deterministic, and no CTA-wide barriers in the loop
+        self.emit(f"  for (int e = warp; e < {total}; e += 8) {{")
         self.emit("    double s = 0;")
-        self.emit(f"    for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) s += __ldcg(a.ws + (i64)b * {total} + e);")
-        self.emit("    sk_red[threadIdx.x] = s; __syncthreads();")
-        self.emit("    for (int w = 128; w > 0; w >>= 1) { if (threadIdx.x < w) sk_red[threadIdx.x] += sk_red[threadIdx.x + w]; __syncthreads(); }")
-        self.emit("    if (threadIdx.x == 0) {")
+        self.emit(f"    for (unsigned b = lane; b < gridDim.x; b += 32) s += __ldcg(a.ws + (i64)b * {total} + e);")
+        self.emit("    s = tx_wsum(s);")
+        self.emit("    if (lane == 0) {")
         for (o, c, acc, dt, L), so in zip(self.sinks, offs):
             ot = C_TYPE[o.type.dtype]
             k = self.slot[(o.id, "sink")]
-            self.emit(f"      if (e >= {so} && e < {so + L}) (({ot}*)a.ptr[{k}])[(i64)(e - {so}) * a.cs[{k}]] = ({ot})sk_red[0];")
+            self.emit(f"      if (e >= {so} && e < {so + L}) (({ot}*)a.ptr[{k}])[(i64)(e - {so}) * a.cs[{k}]] = ({ot})s;")
         self.emit("    }")
-        self.emit("    __syncthreads();")
         self.emit("  }")
         self.emit("  if (threadIdx.x == 0) *a.counter = 0u;")
         self.emit("}")

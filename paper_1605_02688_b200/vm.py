@@ -261,6 +261,9 @@ class CompiledFunction:
         self._consts: dict[int, object] = {}
         self._stream = None
         self._comm_stream = None
+        self._xfer = None
+        self._pipes: dict = {}
+        self.pipelined = True
         self.profile_nodes = False
         self._direct, self.order = self._schedule()
         self.thunks = {}
@@ -342,6 +345,12 @@ class CompiledFunction:
             self._stream = self._tstream.cuda_stream
         return lib
 
+    def _xfer_streams(self, lib):
+        """(H2D, D2H) copy streams for chunk-pipelined host calls."""
+        if self._xfer is None:
+            self._xfer = (lib.stream_create(), lib.stream_create())
+        return self._xfer
+
     def _call(self, values, device_out, sync=True):
         t0 = time.perf_counter()
         if len(values) != len(self.input_vars):
@@ -359,6 +368,22 @@ class CompiledFunction:
                 raise TypeMismatch(f"shared {s!r} holds a nonconforming value: {why}")
             shared_state.append((dev.data_ptr(), tuple(dev.shape), s.version))
         key = (tuple((b.shape, b.dev_ptr) for b in binds), tuple(shared_state))
+        if self.pipelined and not device_out and key not in self._plans:
+            from . import stream as _stream
+            pipe = self._pipes.get(key)
+            if pipe is None and _stream.eligible(self, binds, device_out):
+                try:
+                    pipe = _stream.Pipeline(self, lib, binds)
+                except _stream._NotChunkable:
+                    pipe = False
+                self._pipes[key] = pipe
+            if pipe:
+                outs = pipe.run(binds)
+                for n in self.order:
+                    self.profile.node_calls[n.id] = self.profile.node_calls.get(n.id, 0) + 1
+                self.profile.call_count += 1
+                self.profile.total_time += time.perf_counter() - t0
+                return outs[0] if self.single_output else outs
         plan = self._plans.get(key)
         if plan is None:
             plan = StepPlan(self, lib, binds, key)
@@ -400,8 +425,10 @@ class CompiledFunction:
         twin.profile = Profile(stage_times=dict(self.profile.stage_times))
         twin._lock = threading.Lock()
         twin._plans = {}
+        twin._pipes = {}
         twin._stream = None
         twin._comm_stream = None
+        twin._xfer = None
         return twin
 
 
@@ -993,17 +1020,17 @@ class StepPlan:
         """D2H of the explicit outputs into fresh pinned host blocks (torch's
         caching host allocator), returned as NumPy views — each call returns
         new arrays (reference runtime.py:412-414) without a host-side copy."""
-        t = _torch()
+        from .stream import HOST_POOL
         pins = []
         for kind, lay in self.out_lays:
             if kind != "dev":
                 pins.append(None)
                 continue
             nb = lay.numel * ITEMSIZE[lay.dtype]
-            pin = t.empty(max(nb, 1), dtype=t.uint8, pin_memory=True)
+            ptr, base = HOST_POOL.take(nb)
             if nb:
-                self.lib.memcpy(pin.data_ptr(), self.tx(lay).data, nb, 1, stream)
-            pins.append(pin)
+                self.lib.memcpy(ptr, self.tx(lay).data, nb, 1, stream)
+            pins.append(base)
         self.lib.stream_sync(stream)
         self._host_refs = None
         outs = []
@@ -1013,7 +1040,7 @@ class StepPlan:
                 continue
             nb = lay.numel * ITEMSIZE[lay.dtype]
             dt = np.uint8 if lay.dtype == "bool" else np_dtype(lay.dtype)
-            arr = pin.numpy()[:nb].view(dt).reshape(lay.shape)
+            arr = pin[:nb].view(dt).reshape(lay.shape)
             if lay.dtype == "bool":
                 arr = arr.astype(np.bool_)
             outs.append(arr)

@@ -169,3 +169,56 @@ def test_profile_nodes_records_times(rng):
     f(rng.standard_normal((64, 64)).astype(np.float32))
     assert all(f.profile.node_calls[n.id] == 1 for n in f.order)
     assert sum(f.profile.node_time.values()) > 0
+
+
+# -- chunk-pipelined host calls (stream.py) ------------------------------------
+
+def _pipe_used(f):
+    return any(p for p in f._pipes.values())
+
+
+def test_pipelined_host_call_matches_device_call_ragged():
+    """Host inputs above stream.MIN_BYTES run as overlapped H2D/compute/D2H
+    chunks; results must be bit-identical to the single-plan device call,
+    including a ragged last chunk."""
+    import torch
+    from oracle import configs as C
+    from oracle import texpr_numpy as O
+    g = C.build_ew(T)
+    f = T.compile(g["inputs"], g["outputs"])
+    n = (1 << 24) + 77
+    ins = C.inputs_ew(n, seed=7)
+    got = f(*ins)
+    assert _pipe_used(f)
+    dev = f.call_device(*[torch.from_numpy(a).cuda() for a in ins], sync=True).cpu().numpy()
+    np.testing.assert_array_equal(got, dev)
+    idx = np.random.default_rng(0).integers(0, n, 4096)
+    want = O.eval_composite_plain(f.order[0].op.program, [a[idx] for a in ins])[0]
+    np.testing.assert_allclose(got[idx], want, rtol=1e-5, atol=1e-6)
+    # pinned torch inputs take the same path; a second call reuses the slots
+    pins = [torch.from_numpy(a).pin_memory() for a in ins]
+    np.testing.assert_array_equal(f(*pins), dev)
+
+
+def test_pipelined_multi_output_matrix_and_bool():
+    a, b = T.matrix("a", dtype="float32"), T.matrix("b", dtype="float32")
+    f = T.compile([a, b], [T.tanh(a) * b, T.gt(a, b), a - b])
+    rng = np.random.default_rng(3)
+    av = rng.standard_normal((4099, 4096), dtype=np.float32)
+    bv = rng.standard_normal((4099, 4096), dtype=np.float32)
+    o1, o2, o3 = f(av, bv)
+    assert _pipe_used(f)
+    assert o2.dtype == np.bool_ and o2.shape == av.shape
+    np.testing.assert_array_equal(o2, av > bv)
+    np.testing.assert_array_equal(o3, av - bv)
+    np.testing.assert_allclose(o1, np.tanh(av) * bv, rtol=1e-5, atol=1e-6)
+
+
+def test_pipelined_integer_division_by_zero_raises():
+    a, b = T.vector("a", dtype="int32"), T.vector("b", dtype="int32")
+    f = T.compile([a, b], a / b)  # integer div floors and raises on zero (ops/elemwise.py:49-55)
+    av = np.ones(1 << 25, np.int32)
+    bv = np.ones(1 << 25, np.int32)
+    bv[-5] = 0
+    with pytest.raises(ZeroDivisionError):
+        f(av, bv)

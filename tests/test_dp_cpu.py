@@ -130,6 +130,6 @@ def test_propagation_through_fused_gemm_epilogues():
     fg = FunctionGraph([repl[v] for v in ins], outs)
     run_preset(fg, "fast_run")
     names = [getattr(n.op, "display_name", n.op.name) for n in fg.toposort()]
-    assert names.count("dot+bias_tanh_dual") == 2 and names.count("dot+mul_aux") == 2
+    assert names.count("dot+bias_tanh") == 2 and names.count("dot+mul_1msqr") == 2
     plan = dp.propagate(fg.toposort(), {repl[v].id: dp.sharded(0) for v in g["inputs"]})
     assert len(plan.partial_nodes) == 7

@@ -60,11 +60,30 @@ def epilogues(lib):
         print(f"bwd dH*g fused={fuse}: {ms:.3f} ms ({2 * M * N * N / ms / 1e9:.1f} TFLOP/s incl. epilogue)", flush=True)
 
 
+def cublas_ms(A, B, reps=10):
+    torch.backends.cuda.matmul.allow_tf32 = True
+    for _ in range(3):
+        A @ B
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ts = []
+    for _ in range(reps):
+        s.record()
+        A @ B
+        e.record()
+        e.synchronize()
+        ts.append(s.elapsed_time(e))
+    torch.backends.cuda.matmul.allow_tf32 = False
+    return sorted(ts)[reps // 2]
+
+
 def main():
     torch.cuda.set_device(0)
     lib = native.device_library(0)
     cg = os.environ.get("TX_GEMM_CG", "2")
+    only = sys.argv[1:]
     for name, M, N, K, ta, tb in SHAPES:
+        if only and name.split()[0] not in only:
+            continue
         a = torch.randn(K, M, device="cuda") if ta else torch.randn(M, K, device="cuda")
         b = torch.randn(N, K, device="cuda") if tb else torch.randn(K, N, device="cuda")
         va, vb = T.matrix("a", dtype="float32"), T.matrix("b", dtype="float32")
@@ -87,8 +106,11 @@ def main():
         bound = (A[rows].abs().double() @ B.abs().double())
         err = ((out[rows].double() - ref).abs() / (bound + 1e-30)).max().item()
         tf = 2 * M * N * K / (ms * 1e-3) / 1e12
-        print(f"CG={cg} {name:12s} M={M} N={N} K={K}: {ms:.3f} ms {tf:7.1f} TFLOP/s  max err/bound {err:.2e}", flush=True)
-    epilogues(lib)
+        cb = cublas_ms(A, B) if not only else float("nan")
+        print(f"CG={cg} {name:12s} M={M} N={N} K={K}: {ms:.3f} ms {tf:7.1f} TFLOP/s  max err/bound {err:.2e}"
+              f"   | cuBLAS TF32 same layout {cb:.3f} ms {2 * M * N * K / (cb * 1e-3) / 1e12:7.1f} TFLOP/s", flush=True)
+    if not only:
+        epilogues(lib)
 
 
 if __name__ == "__main__":
