@@ -31,6 +31,7 @@ sys.path.insert(0, ROOT)
 EW_N = 1 << 28
 EW_BYTES_PER_ELEM = 20
 MLP_FLOP_PER_SAMPLE = 113.75e6  # 931.87 GFLOP / 8192 samples
+TF32_NOMINAL = 1130.0           # dense TF32 TFLOP/s, B200 nominal (B200_PROFILING.md); no measured TF32 peak exists
 
 
 def peaks():
@@ -116,6 +117,19 @@ def barrier(ws):
     if ws > 1:
         import torch.distributed as dist
         dist.barrier()
+
+
+def time_device_block(fn_launch, lib, stream, steps):
+    """Mean ms per step of `steps` back-to-back calls bracketed by one event
+    pair (a training loop: host enqueue overlaps the device work)."""
+    a, b = lib.event_create(), lib.event_create()
+    lib.stream_sync(stream)
+    lib.event_record(a, stream)
+    for _ in range(steps):
+        fn_launch()
+    lib.event_record(b, stream)
+    lib.stream_sync(stream)
+    return lib.elapsed_ms(a, b) / steps
 
 
 def time_device(fn_launch, lib, stream, steps):
@@ -230,6 +244,13 @@ def bench_mlp(T, C, B, steps, warmup, lib_holder, dp=None, n_global=None):
     return f, ms, cost
 
 
+def kernel_launches(f):
+    """Launch closures of the function's (single) step plan: one per kernel
+    or library call the captured graph replays."""
+    plan = next(iter(f._plans.values()))
+    return len(plan.launches)
+
+
 def tf32_peak_cublas(n=8192, iters=20):
     """cuBLAS TF32 GEMM throughput on this box (the TF32 roofline reference;
     MEASURED_PEAKS.json only has bf16)."""
@@ -261,12 +282,12 @@ def bench_logreg(T, C, steps, warmup, lib_holder):
     for _ in range(warmup):
         f.call_device(xd, yd)
     lib = lib_holder()
-    ms = time_device(lambda: f.call_device(xd, yd), lib, f._stream, steps * 10)
+    ms = [time_device_block(lambda: f.call_device(xd, yd), lib, f._stream, steps * 10) for _ in range(5)]
     t0 = time.perf_counter()
     for _ in range(steps):
         f(x, y)
     e2e = (time.perf_counter() - t0) / steps
-    return ms, e2e, sum(1 for n in f.order if not getattr(n.op, "view_capable", False))
+    return ms, e2e, kernel_launches(f)
 
 
 def bench_reduce(T, C, steps, lib_holder):
@@ -408,8 +429,10 @@ def main():
             med = statistics.median(ms_m)
             extra["mlp_b8192_1gpu"] = {"samples_per_s": round(8192 / (med * 1e-3), 1), "ms_per_step": round(med, 3),
                                        "tflops": round(MLP_FLOP_PER_SAMPLE * 8192 / (med * 1e-3) / 1e12, 1),
+                                       "frac_of_tf32_nominal_1130": round(MLP_FLOP_PER_SAMPLE * 8192 / (med * 1e-3) / 1e12 / TF32_NOMINAL, 3),
                                        "cost_after": cost,
-                                       "launches_per_step": len([1 for n in fm.order if not getattr(n.op, 'view_capable', False)])}
+                                       "graph_nodes": len([1 for n in fm.order if not getattr(n.op, 'view_capable', False)]),
+                                       "launches_per_step": kernel_launches(fm)}
             del fm
         except Exception as e:
             extra["mlp_b8192_1gpu"] = {"error": repr(e)[:300]}
@@ -439,6 +462,8 @@ def main():
             extra["logreg_n600"] = {"error": repr(e)[:300]}
         try:
             extra["careduce_16384sq_GBs"] = bench_reduce(T, C, 10, lib_holder)
+            extra["careduce_frac_of_hbm_peak"] = {k: round(v / pk["hbm_gbs"], 3)
+                                                  for k, v in extra["careduce_16384sq_GBs"].items()}
         except Exception as e:
             extra["careduce_16384sq_GBs"] = {"error": repr(e)[:300]}
         line["extra"] = extra

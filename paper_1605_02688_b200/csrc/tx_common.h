@@ -68,6 +68,9 @@ struct Space {
 void collapse(int ndim, const int64_t* shape, int nops, const int64_t (*strides)[TX_MAX_RANK], Space* out);
 
 int sm_count();
+// cuTensorMapEncodeTiled through the runtime's driver entry point (nullptr
+// when no driver is present); shared by the GEMM and reduction TMA paths
+void* tmap_encoder();
 int reduce_launch(int op, const tx_tensor& x, uint32_t mask, tx_tensor& y, void* ws, size_t ws_bytes,
                   cudaStream_t st);
 

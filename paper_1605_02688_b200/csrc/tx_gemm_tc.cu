@@ -458,20 +458,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-static EncodeFn g_encode = nullptr;
-static std::once_flag g_once;
 static bool g_attr_set[3] = {false, false, false};
 
-static EncodeFn encode_fn() {
-  std::call_once(g_once, [] {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      g_encode = (EncodeFn)p;
-  });
-  return g_encode;
-}
+static EncodeFn encode_fn() { return (EncodeFn)tmap_encoder(); }
 
 // inner-contiguous 2D map: dims {inner, outer}, outer stride in elements
 static int make_map(CUtensorMap* m, const void* base, int64_t inner, int64_t outer, int64_t ostride, int box_inner,
@@ -509,6 +498,19 @@ static int make_map_mn3d(CUtensorMap* m, const void* base, int64_t MN, int64_t K
 }
 
 }  // namespace
+
+void* tmap_encoder() {
+  static std::once_flag once;
+  static void* fn = nullptr;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = p;
+  });
+  return fn;
+}
 
 int gemm_tc_eligible(const G& g) {
   if (g.dtype != TX_F32) return TX_E_UNSUPPORTED;

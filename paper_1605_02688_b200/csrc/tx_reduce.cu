@@ -12,12 +12,20 @@
 //   COL    kept elements contiguous ("axis 0"): each thread owns 4 adjacent
 //          columns (one 128-bit load per row), rows split across grid.y into
 //          partials combined in fixed order by a finalize kernel.
+//   COLTMA the COL case for 4-byte types when TMA can address the matrix:
+//          [16 rows x 256 columns] tiles are streamed by one producer lane
+//          with cp.async.bulk.tensor into a 4-stage shared-memory ring
+//          (mbarrier transaction counts), 8 consumer warps reduce them
+//          column-per-thread; up to 192 KB in flight per SM regardless of
+//          the register budget.
 //   GEN    anything else: one thread per output, div/mod addressing.
 // max / argmax are bit-exact with NumPy: NaN propagates (and counts as the
 // maximum for argmax), and the first maximal element wins ties.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cfloat>
+#include <cstdlib>
 #include <climits>
 #include <cstring>
 #include <type_traits>
@@ -290,6 +298,87 @@ done:
   }
 }
 
+// ------------------------------------------------------------------ COLTMA
+constexpr int CT_COLS = 256, CT_ROWS = 16, CT_STAGES = 4;
+constexpr int CT_THREADS = CT_COLS + 32;  // 8 consumer warps + 1 producer warp
+constexpr size_t CT_SMEM = (size_t)CT_STAGES * CT_ROWS * CT_COLS * 4 + 2 * CT_STAGES * 8 + 128;
+
+__device__ __forceinline__ uint32_t sa32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+template <class T, int OP>
+__global__ void __launch_bounds__(CT_THREADS) col_tma_kernel(const __grid_constant__ CUtensorMap map, int64_t R,
+                                                            int64_t K, int splits, T* __restrict__ out,
+                                                            long long* __restrict__ out_idx, T* __restrict__ pv,
+                                                            long long* __restrict__ pi) {
+  extern __shared__ __align__(128) uint8_t ct_smem[];
+  T* tiles = reinterpret_cast<T*>(ct_smem);  // [STAGES][ROWS][COLS]
+  uint64_t* full = reinterpret_cast<uint64_t*>(ct_smem + (size_t)CT_STAGES * CT_ROWS * CT_COLS * sizeof(T));
+  uint64_t* empty = full + CT_STAGES;
+  const int64_t c0 = (int64_t)blockIdx.x * CT_COLS;
+  int64_t chunk = (R + splits - 1) / splits;
+  chunk = (chunk + CT_ROWS - 1) / CT_ROWS * CT_ROWS;
+  const int64_t lo = (int64_t)blockIdx.y * chunk, hi = min(R, lo + chunk);
+  const int ntiles = hi > lo ? (int)((hi - lo + CT_ROWS - 1) / CT_ROWS) : 0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < CT_STAGES; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa32(full + s)) : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sa32(empty + s)), "r"(CT_COLS / 32) : "memory");
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto wait = [](uint64_t* b, uint32_t parity) {
+    uint32_t done = 0;
+    do {
+      asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                   : "=r"(done) : "r"(sa32(b)), "r"(parity) : "memory");
+    } while (!done);
+  };
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == CT_COLS / 32) {  // producer
+    if (lane == 0) {
+      for (int i = 0; i < ntiles; ++i) {
+        const int s = i % CT_STAGES;
+        wait(empty + s, ((i / CT_STAGES) & 1) ^ 1);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa32(full + s)),
+                     "r"((uint32_t)(CT_ROWS * CT_COLS * sizeof(T))) : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+                sa32(tiles + (size_t)s * CT_ROWS * CT_COLS)),
+            "l"((uint64_t)&map), "r"(sa32(full + s)), "r"((int)c0), "r"((int)(lo + (int64_t)i * CT_ROWS))
+            : "memory");
+      }
+    }
+    return;
+  }
+  const int t = threadIdx.x;
+  Acc<T, OP> a;
+  a.init();
+  for (int i = 0; i < ntiles; ++i) {
+    const int s = i % CT_STAGES;
+    wait(full + s, (i / CT_STAGES) & 1);
+    const T* tile = tiles + (size_t)s * CT_ROWS * CT_COLS;
+    const int64_t r0 = lo + (int64_t)i * CT_ROWS;
+    const int nr = (int)min((int64_t)CT_ROWS, hi - r0);
+    if (nr == CT_ROWS) {
+#pragma unroll
+      for (int r = 0; r < CT_ROWS; ++r) a.push(tile[r * CT_COLS + t], r0 + r);
+    } else {
+      for (int r = 0; r < nr; ++r) a.push(tile[r * CT_COLS + t], r0 + r);
+    }
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sa32(empty + s)) : "memory");
+  }
+  const int64_t c = c0 + t;
+  if (c >= K) return;
+  if (splits == 1) {
+    if (OP == TX_SUM || OP == TX_MAX) out[c] = a.v; else out_idx[c] = a.i;
+  } else {
+    pv[(int64_t)blockIdx.y * K + c] = a.v;
+    if (OP == TX_ARGMAX_INDEX || OP == TX_ARGMAX_ONEHOT) pi[(int64_t)blockIdx.y * K + c] = a.i;
+  }
+}
+
 // partials [splits][K]: a 32-column x 8-lane CTA, each lane merging every
 // 8th split (coalesced across columns), then the 8 lanes merged in order.
 template <class T, int OP>
@@ -387,7 +476,7 @@ __global__ void onehot_cols(T* __restrict__ y, int64_t R, int64_t K, const long 
 }
 
 // ------------------------------------------------------------------ planning
-enum Form { ROW, ROWWARP, COL, GEN };
+enum Form { ROW, ROWWARP, COL, COLTMA, GEN };
 
 struct Plan {
   Form form;
@@ -436,6 +525,7 @@ static void make_plan(int op, const tx_tensor& x, uint32_t mask, int itemsz, Pla
   int mk = merge_dims(nk, ksh, kst);
   int mr = merge_dims(nr, rsh, rst);
   const int sms = sm_count();
+  int col_splits_max = 1;
   if (mk <= 1 && mr <= 1) {
     const int64_t kstride = mk == 1 ? kst[0] : 0;
     const int64_t rstride = mr == 1 ? rst[0] : 1;
@@ -451,6 +541,29 @@ static void make_plan(int op, const tx_tensor& x, uint32_t mask, int itemsz, Pla
       if (splits > 65535) splits = 65535;
       if (splits < 1) splits = 1;
       p->splits = (int)splits;
+      // the workspace must fit either form (the query may see another pointer)
+      col_splits_max = (int)splits;
+      if (itemsz == 4 && ((uintptr_t)x.data & 15) == 0 && (rstride * 4) % 16 == 0 && rstride >= K &&
+          R < (int64_t)INT32_MAX && K < (int64_t)INT32_MAX && tmap_encoder() && !getenv("TX_REDUCE_NO_TMA")) {
+        // one wave of 3 CTAs per SM (64 KB ring each)
+        p->form = COLTMA;
+        const int64_t strips = (K + CT_COLS - 1) / CT_COLS;
+        int64_t want = (int64_t)sms * 3;
+        int64_t sp = (want + strips - 1) / strips;
+        int64_t maxs = R / (4 * CT_ROWS);
+        if (sp > maxs) sp = maxs;
+        if (sp > 65535) sp = 65535;
+        if (sp < 1) sp = 1;
+        p->splits = (int)sp;
+      }
+      {
+        const int64_t strips = (K + CT_COLS - 1) / CT_COLS;
+        int64_t sp = ((int64_t)sms * 3 + strips - 1) / strips;
+        int64_t maxs = R / (4 * CT_ROWS);
+        if (sp > maxs) sp = maxs;
+        if (sp > 65535) sp = 65535;
+        if (sp > col_splits_max) col_splits_max = (int)sp;
+      }
     } else if (R <= 512 && K >= 8) {
       // one warp per output (softmax-sized rows, any element stride)
       p->form = ROWWARP;
@@ -474,7 +587,8 @@ static void make_plan(int op, const tx_tensor& x, uint32_t mask, int itemsz, Pla
   } else {
     p->form = GEN;
   }
-  if (p->splits > 1) p->ws_partial = (size_t)p->splits * (size_t)p->K * 16 + 64;
+  if (col_splits_max > p->splits) p->ws_partial = (size_t)col_splits_max * (size_t)p->K * 16 + 64;
+  else if (p->splits > 1) p->ws_partial = (size_t)p->splits * (size_t)p->K * 16 + 64;
   if (op == TX_ARGMAX_ONEHOT) p->ws_idx = (size_t)p->K * 8;
 }
 
@@ -529,6 +643,31 @@ static int run(const tx_tensor& x, uint32_t mask, tx_tensor& y, char* ws, size_t
       unsigned gx = (unsigned)((p.K + 4 * kThreads - 1) / (4 * kThreads));
       dim3 grid(gx, (unsigned)p.splits);
       col_kernel<T, OP><<<grid, kThreads, 0, st>>>(xp, p.R, p.K, p.rs, p.splits, vec, out, out_idx, pv, pi);
+      if (p.splits > 1)
+        finalize_cols<T, OP><<<(unsigned)((p.K + 31) / 32), 256, 0, st>>>(p.K, p.splits, pv, pi, out, out_idx);
+      break;
+    }
+    case COLTMA: {
+      typedef CUresult (*Enc)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+      Enc enc = (Enc)tmap_encoder();
+      CUtensorMap map;
+      cuuint64_t dims[2] = {(cuuint64_t)p.K, (cuuint64_t)p.R};
+      cuuint64_t gstr[1] = {(cuuint64_t)(p.rs * 4)};
+      cuuint32_t box[2] = {(cuuint32_t)CT_COLS, (cuuint32_t)CT_ROWS};
+      cuuint32_t es[2] = {1, 1};
+      CUtensorMapDataType dt = std::is_same<T, float>::value ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_INT32;
+      CUresult r = enc(&map, dt, 2, (void*)xp, dims, gstr, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                       CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      TX_CHECK(r == CUDA_SUCCESS, TX_E_CUDA, "tx_reduce: cuTensorMapEncodeTiled failed");
+      static bool attr = false;
+      if (!attr) {
+        TX_CUDA(cudaFuncSetAttribute(col_tma_kernel<T, OP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CT_SMEM));
+        attr = true;
+      }
+      dim3 grid((unsigned)((p.K + CT_COLS - 1) / CT_COLS), (unsigned)p.splits);
+      col_tma_kernel<T, OP><<<grid, CT_THREADS, CT_SMEM, st>>>(map, p.R, p.K, p.splits, out, out_idx, pv, pi);
       if (p.splits > 1)
         finalize_cols<T, OP><<<(unsigned)((p.K + 31) / 32), 256, 0, st>>>(p.K, p.splits, pv, pi, out, out_idx);
       break;

@@ -58,10 +58,22 @@ class UpdatePair:
 class Profile:
     call_count: int = 0
     total_time: float = 0.0
-    node_calls: dict = field(default_factory=dict)
+    _node_calls: dict = field(default_factory=dict)
     node_time: dict = field(default_factory=dict)
     node_bytes: dict = field(default_factory=dict)
     stage_times: dict = field(default_factory=dict)
+    # whole-graph replays not yet folded into the per-node counts (a replay
+    # runs every node once; folding lazily keeps the per-call cost O(1))
+    _pending: int = 0
+    _order: tuple = ()
+
+    @property
+    def node_calls(self):
+        if self._pending:
+            for nid in self._order:
+                self._node_calls[nid] = self._node_calls.get(nid, 0) + self._pending
+            self._pending = 0
+        return self._node_calls
 
     def record_node(self, node_id, seconds, nbytes):
         self.node_calls[node_id] = self.node_calls.get(node_id, 0) + 1
@@ -266,6 +278,8 @@ class CompiledFunction:
         self.pipelined = True
         self.profile_nodes = False
         self._direct, self.order = self._schedule()
+        self.profile._order = tuple(n.id for n in self.order)
+        self._events = None
         self.thunks = {}
         self.shard = None
         if self.dp is not None:
@@ -379,8 +393,7 @@ class CompiledFunction:
                 self._pipes[key] = pipe
             if pipe:
                 outs = pipe.run(binds)
-                for n in self.order:
-                    self.profile.node_calls[n.id] = self.profile.node_calls.get(n.id, 0) + 1
+                self.profile._pending += 1
                 self.profile.call_count += 1
                 self.profile.total_time += time.perf_counter() - t0
                 return outs[0] if self.single_output else outs
@@ -389,18 +402,24 @@ class CompiledFunction:
             plan = StepPlan(self, lib, binds, key)
             self._plans[key] = plan
         stream = self._stream
+        if self._events is None:
+            self._events = (lib.event_create(), lib.event_create())
+        cur = None
         if any(b.dev_ptr is not None for b in binds) or device_out:
-            self._tstream.wait_stream(t.cuda.current_stream())
+            # order after the caller's stream (inputs produced there)
+            cur = t.cuda.current_stream().cuda_stream
+            lib.event_record(self._events[0], cur)
+            lib.stream_wait_event(stream, self._events[0])
         plan.upload_inputs(binds, stream)
         if self.profile_nodes:
             plan.run_profiled(stream, self.profile)
         else:
             plan.run(stream)
-            for n in self.order:
-                self.profile.node_calls[n.id] = self.profile.node_calls.get(n.id, 0) + 1
+            self.profile._pending += 1
         if device_out:
             outs = plan.device_outputs()
-            t.cuda.current_stream().wait_stream(self._tstream)
+            lib.event_record(self._events[1], stream)
+            lib.stream_wait_event(cur, self._events[1])
             if sync:
                 lib.stream_sync(stream)
         else:
@@ -422,7 +441,8 @@ class CompiledFunction:
         twin.shared_bindings = [(swap.get(s, s), v) for s, v in self.shared_bindings]
         twin.updates = [(swap.get(s, s), v) for s, v in self.updates] if carry_updates else []
         twin._direct = {k: (swap.get(s, s), v) for k, (s, v) in self._direct.items()} if carry_updates else {}
-        twin.profile = Profile(stage_times=dict(self.profile.stage_times))
+        twin.profile = Profile(stage_times=dict(self.profile.stage_times), _order=self.profile._order)
+        twin._events = None
         twin._lock = threading.Lock()
         twin._plans = {}
         twin._pipes = {}
@@ -803,6 +823,7 @@ class StepPlan:
         self.graph = None
         self.captured = False
         self._pinned_out = None
+        self._dev_outs = None
 
     # -- helpers used by op.lower -------------------------------------------
     def _const_layout(self, c: Constant) -> Layout:
@@ -1047,6 +1068,8 @@ class StepPlan:
         return outs
 
     def device_outputs(self):
+        if self._dev_outs is not None:
+            return list(self._dev_outs)
         t = _torch()
         outs = []
         for kind, lay in self.out_lays:
@@ -1054,6 +1077,8 @@ class StepPlan:
                 outs.append(t.from_numpy(np.array(lay)).to("cuda"))
                 continue
             outs.append(_torch_view(lay, self.tx(lay).data))
+        # the views alias plan-owned buffers at fixed addresses: build once
+        self._dev_outs = tuple(outs)
         return outs
 
     def check_flags(self):

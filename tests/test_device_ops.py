@@ -123,7 +123,8 @@ def test_reductions_rank3_f64(golden, ax):
     close(s, golden[f"red3_sum_{tag}"], 1e-12, 1e-12)
 
 
-@pytest.mark.parametrize("shape", [(4099, 3001), (3, 70000), (70000, 3), (1, 1), (1, 200000), (33, 600)])
+@pytest.mark.parametrize("shape", [(4099, 3001), (3, 70000), (70000, 3), (1, 1), (1, 200000), (33, 600),
+                                   (4100, 3000), (1001, 1040)])
 def test_reduction_forms(shape, rng):
     """ROW / split-ROW / warp-ROW / COL(+splits) / degenerate shapes."""
     X = rng.standard_normal(shape).astype(np.float32)
@@ -135,6 +136,29 @@ def test_reduction_forms(shape, rng):
         exact(m, O.reduce_max(X, ax))
         exact(am, O.argmax_index(X, ax))
         close(s, O.reduce_sum(X, ax), 0, 2e-6 * float(np.abs(X).sum()) + 1e-6)
+
+
+def test_column_reduction_tma_nan_ties_int(rng):
+    """Axis-0 reductions on TMA-addressable matrices (16-byte row pitch): the
+    COLTMA form (cp.async.bulk.tensor ring) must stay bit-exact for max /
+    argmax with NaNs and ties, including a ragged last tile and strip."""
+    X = rng.standard_normal((2051, 1300)).astype(np.float32)
+    X[7, 3] = X[900, 3] = 50.0          # tie: first row wins
+    X[5, 1299] = np.nan                 # NaN propagates / wins argmax
+    X[2050, 1299] = np.nan
+    X[2050, 0] = 99.0                   # max in the ragged last row tile
+    v = T.matrix("X", dtype="float32")
+    s, m, am, oh = T.compile([v], [T.sum(v, axis=0), T.max(v, axis=0), T.argmax(v, axis=0),
+                                   T.argmax_onehot(v, axis=0)])(X)
+    exact(m, O.reduce_max(X, (0,)))
+    exact(am, O.argmax_index(X, (0,)))
+    exact(oh, O.argmax_onehot(X, (0,)))
+    close(s, O.reduce_sum(X, (0,)), 0, 2e-6 * float(np.nansum(np.abs(X))) + 1e-6)
+    Xi = rng.integers(-1000, 1000, (3000, 1024)).astype(np.int32)
+    vi = T.matrix("Xi", dtype="int32")
+    si, mi = T.compile([vi], [T.sum(vi, axis=0), T.max(vi, axis=0)])(Xi)
+    exact(mi, Xi.max(axis=0))
+    exact(si, Xi.sum(axis=0, dtype=np.int32))
 
 
 def test_reduction_strided_views(rng):
