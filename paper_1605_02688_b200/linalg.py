@@ -144,6 +144,26 @@ class DotEpilogue(Op):
         from .errors import NotDifferentiable
         raise NotDifferentiable("dot_epilogue is created after differentiation")
 
+    def expand(self, inputs):
+        """The reference-op form (``dot`` + ``elemwise``) of this node, with the
+        same scalar operations in the same order as the epilogue -- used to
+        save portable graphs (``serialize.portable_outputs``)."""
+        from .elemwise import make
+        a, b, aux = inputs
+        z = dot(a, b)
+        if self.kind == EPI_BIAS:
+            return [make("add", [aux, z])]
+        if self.kind == EPI_BIAS_TANH:
+            return [make("tanh", [make("add", [aux, z])])]
+        if self.kind == EPI_MUL_1MSQR:
+            return [make("mul", [z, make("sub", [1.0, make("sqr", [aux])])])]
+        if self.kind == EPI_BIAS_TANH_DUAL:
+            h = make("tanh", [make("add", [aux, z])])
+            return [h, make("sub", [1.0, make("sqr", [h])])]
+        if self.kind == EPI_MUL_AUX:
+            return [make("mul", [z, aux])]
+        raise NotImplementedError(f"epilogue kind {self.kind}")
+
     def lower(self, node, plan):
         from . import native
         epi = native.TxEpilogue()

@@ -430,6 +430,12 @@ class CompiledFunction:
         self.profile.total_time += time.perf_counter() - t0
         return outs[0] if self.single_output else outs
 
+    # -- serialization (reference runtime.py:555-569) -------------------------
+    def save(self) -> bytes:
+        from .serialize import encode_function
+        with self._lock:
+            return encode_function(self)
+
     # -- copying (reference runtime.py:512-553) ------------------------------
     def copy(self, swap=None, carry_updates=True, share_intermediate_storage=False):
         swap = dict(swap or {})
@@ -450,6 +456,18 @@ class CompiledFunction:
         twin._comm_stream = None
         twin._xfer = None
         return twin
+
+
+def save(fn: CompiledFunction) -> bytes:
+    """``TXFN`` container bytes (reference ``runtime.py:563-564``)."""
+    return fn.save()
+
+
+def load(data: bytes, force_reoptimize: bool = False, **compile_options) -> CompiledFunction:
+    """Rebuild a function from ``TXFN`` bytes (reference ``runtime.py:567-570``);
+    files written by the reference load too."""
+    from .serialize import decode_function
+    return decode_function(data, force_reoptimize=force_reoptimize, **compile_options)
 
 
 def native_dtype_code(dtype):
