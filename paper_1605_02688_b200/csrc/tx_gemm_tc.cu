@@ -48,8 +48,15 @@ struct Cfg {
   static constexpr int A_BYTES = BM * BK * 4;              // 16 KB
   static constexpr int B_BYTES = (BN / CG) * BK * 4;       // 32 KB (CG=1) / 16 KB (CG=2)
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = CG == 1 ? 4 : 6;
-  static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + 256;
+  static constexpr int STAGES = CG == 1 ? 4 : 5;
+  static constexpr size_t RING = (size_t)STAGES * STAGE_BYTES;
+  // epilogue staging: one [32 rows x 32 cols] fp32 tile (4 KB, 128B-swizzled)
+  // per epilogue warp, drained by TMA stores
+  static constexpr size_t STAGING = (size_t)EPI_WARPS * 4096;
+  // CG = 2 also stages the [M,N] epilogue operand (x(1-h^2), x aux) per warp
+  // with TMA loads (coalesced; the per-row register loads are 32 rows wide)
+  static constexpr size_t AUX_STAGING = CG == 2 ? (size_t)EPI_WARPS * 4096 : 0;
+  static constexpr size_t SMEM = 1024 + RING + STAGING + AUX_STAGING + 256;
 };
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -113,6 +120,19 @@ __device__ __forceinline__ void tma_load_3d_2sm(void* dst, const CUtensorMap* ma
       "l"((uint64_t)map), "r"(su32(bar) & kPeerMask), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
+
+// smem -> global tile store (bulk async group of the issuing thread)
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"((uint64_t)map),
+               "r"(su32(src)), "r"(c0), "r"(c1)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void tma_store_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void tma_store_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -213,6 +233,9 @@ struct TcParams {
   int M, N, K;
   int a_mn, b_mn;  // 1 = operand is MN-major in memory
   int a_3d, b_3d;  // MN-major operand loaded with one 3-D box per stage
+  int dbg_nostore;  // diagnostics only (TX_GEMM_DBG_NOSTORE): epilogue drains TMEM without storing
+  int tma_store;    // C written by TMA tile stores from swizzled smem staging
+  int tma_aux;      // [M,N] epilogue operand read by TMA tile loads (CG = 2)
   int num_m, num_n, num_tiles;
   Epi<float> epi;
 };
@@ -230,17 +253,19 @@ __device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int& mb
 template <int CG>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                   const __grid_constant__ CUtensorMap mapC, const __grid_constant__ CUtensorMap mapX,
                    const TcParams p) {
   using K_ = Cfg<CG>;
   constexpr int STAGES = K_::STAGES;
   constexpr int BNL = BN / CG;  // B columns staged by this CTA
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint64_t* full = (uint64_t*)(smem + STAGES * K_::STAGE_BYTES);
+  uint64_t* full = (uint64_t*)(smem + K_::RING + K_::STAGING + K_::AUX_STAGING);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+  uint64_t* auxbar = tempty + 2;                 // one per epilogue warp
+  uint32_t* tmem_slot = (uint32_t*)(auxbar + EPI_WARPS);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -252,6 +277,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }
     for (int b = 0; b < 2; ++b) { mbar_init(tfull + b, 1); mbar_init(tempty + b, EPI_WARPS * CG); }
+    for (int w = 0; w < EPI_WARPS; ++w) mbar_init(auxbar + w, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -366,6 +392,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int q = warp & 3;
     const int half = (warp - 2) >> 2;
     int it = 0;
+    uint32_t xphase = 0;
     const Epi<float>& E = p.epi;
     const bool vec_ok = (p.ldc % 4 == 0) && (((uintptr_t)p.C & 15) == 0) &&
                         ((E.kind != TX_EPI_MUL_AUX && E.kind != TX_EPI_MUL_1MSQR) ||
@@ -380,16 +407,112 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint32_t use = (uint32_t)(it >> 1);
       mbar_wait(tfull + buf, use & 1);
       tc_fence_after();
-      const int row = mb * BM * CG + (int)rank * BM + q * 32 + lane;
+      const int row0 = mb * BM * CG + (int)rank * BM + q * 32;
+      const int row = row0 + lane;
       const uint32_t taddr = tmem_base + (uint32_t)(buf * BN + half * (BN / 2)) + ((uint32_t)(q * 32) << 16);
       float* crow = p.C + (int64_t)row * p.ldc;
       const bool row_ok = row < p.M;
+      if (p.tma_store) {
+        // row `lane` of a [32 x 32] tile -> swizzled staging -> one TMA store
+        // per chunk (coalesced, asynchronous; TMA clips the M/N edges)
+        float* stg = reinterpret_cast<float*>(smem + K_::RING + (size_t)(warp - 2) * 4096);
+        const float* xstg = reinterpret_cast<const float*>(smem + K_::RING + K_::STAGING + (size_t)(warp - 2) * 4096);
+        uint64_t* xbar = auxbar + (warp - 2);
+#pragma unroll 1
+        for (int c = 0; c < BN / 2; c += 32) {
+          const int n = nb * BN + half * (BN / 2) + c;
+          const bool live = !(row0 >= p.M || n >= p.N || p.dbg_nostore);
+          if constexpr (CG == 2) {
+            if (p.tma_aux && live && lane == 0) {  // fetch this chunk's operand tile while TMEM drains
+              mbar_expect_tx(xbar, 4096);
+              tma_load_2d((void*)xstg, &mapX, xbar, n, row0);
+            }
+          }
+          float v[32];
+          tmem_ld32(taddr + c, v);
+          if (!live) continue;
+          if constexpr (CG == 2) {
+            if (p.tma_aux) {
+              mbar_wait(xbar, xphase);
+              xphase ^= 1;
+              const float4* xrow = reinterpret_cast<const float4*>(xstg + lane * 32);
+              const bool sq = E.kind == TX_EPI_MUL_1MSQR;
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                float4 g4 = xrow[j ^ (lane & 7)];
+                if (sq) {
+                  g4.x = __fsub_rn(1.0f, __fmul_rn(g4.x, g4.x)); g4.y = __fsub_rn(1.0f, __fmul_rn(g4.y, g4.y));
+                  g4.z = __fsub_rn(1.0f, __fmul_rn(g4.z, g4.z)); g4.w = __fsub_rn(1.0f, __fmul_rn(g4.w, g4.w));
+                }
+                v[4 * j] = __fmul_rn(v[4 * j], g4.x); v[4 * j + 1] = __fmul_rn(v[4 * j + 1], g4.y);
+                v[4 * j + 2] = __fmul_rn(v[4 * j + 2], g4.z); v[4 * j + 3] = __fmul_rn(v[4 * j + 3], g4.w);
+              }
+              __syncwarp();  // every lane has read the operand tile before the next TMA overwrites it
+            }
+          }
+          if (E.kind != TX_EPI_NONE) {
+            if (E.kind == TX_EPI_BIAS || E.kind == TX_EPI_BIAS_TANH) {
+              if (n + 32 <= p.N) {
+#pragma unroll
+                for (int i = 0; i < 32; i += 4) {
+                  const float4 b4 = __ldg(reinterpret_cast<const float4*>(E.aux + n + i));
+                  v[i] = __fadd_rn(b4.x, v[i]); v[i + 1] = __fadd_rn(b4.y, v[i + 1]);
+                  v[i + 2] = __fadd_rn(b4.z, v[i + 2]); v[i + 3] = __fadd_rn(b4.w, v[i + 3]);
+                }
+              } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                  if (n + i < p.N) v[i] = __fadd_rn(E.aux[n + i], v[i]);
+              }
+              if (E.kind == TX_EPI_BIAS_TANH) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] = tanhf(v[i]);
+              }
+            } else if (row_ok && !(CG == 2 && p.tma_aux)) {  // MUL_AUX / MUL_1MSQR: per-row [M,N] operand
+              const float* g = E.aux + (int64_t)row * E.s0 + n;
+              const bool sq = E.kind == TX_EPI_MUL_1MSQR;
+              if (n + 32 <= p.N) {
+#pragma unroll
+                for (int i = 0; i < 32; i += 4) {
+                  float4 g4 = __ldcs(reinterpret_cast<const float4*>(g + i));
+                  if (sq) {
+                    g4.x = __fsub_rn(1.0f, __fmul_rn(g4.x, g4.x)); g4.y = __fsub_rn(1.0f, __fmul_rn(g4.y, g4.y));
+                    g4.z = __fsub_rn(1.0f, __fmul_rn(g4.z, g4.z)); g4.w = __fsub_rn(1.0f, __fmul_rn(g4.w, g4.w));
+                  }
+                  v[i] = __fmul_rn(v[i], g4.x); v[i + 1] = __fmul_rn(v[i + 1], g4.y);
+                  v[i + 2] = __fmul_rn(v[i + 2], g4.z); v[i + 3] = __fmul_rn(v[i + 3], g4.w);
+                }
+              } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                  if (n + i < p.N) v[i] = E.apply(v[i], row, n + i);
+              }
+            }
+          }
+          if (lane == 0) tma_store_wait_read();  // previous chunk's store has read the staging tile
+          __syncwarp();
+          float4* srow = reinterpret_cast<float4*>(stg + lane * 32);
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            srow[j ^ (lane & 7)] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) tma_store_2d(&mapC, stg, n, row0);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (CG == 1) mbar_arrive(tempty + buf);
+          else mbar_arrive_leader(tempty + buf);
+        }
+        continue;
+      }
 #pragma unroll 1
       for (int c = 0; c < BN / 2; c += 32) {
         float v[32];
         tmem_ld32(taddr + c, v);
         const int n = nb * BN + half * (BN / 2) + c;
-        if (!row_ok || n >= p.N) continue;
+        if (!row_ok || n >= p.N || p.dbg_nostore) continue;
         if (vec_ok && n + 32 <= p.N) {
           if (E.kind == TX_EPI_BIAS || E.kind == TX_EPI_BIAS_TANH || E.kind == TX_EPI_BIAS_TANH_DUAL) {
 #pragma unroll
@@ -441,6 +564,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   }
+  if (warp >= 2 && lane == 0) tma_store_wait_all();
   tc_fence_before();
   if constexpr (CG == 2) cluster_sync(); else __syncthreads();
   if (warp == 1) {
@@ -564,6 +688,39 @@ int gemm_tc(const G& g, cudaStream_t st) {
   p.num_n = (int)((g.N + BN - 1) / BN);
   p.num_tiles = p.num_m * p.num_n;
   p.epi = g.epi_f;
+  p.dbg_nostore = getenv("TX_GEMM_DBG_NOSTORE") != nullptr;
+  // TMA tile stores need a 16-byte aligned C with a 16-byte row pitch; the
+  // dual-output epilogue (two stores per element) keeps the register path
+  CUtensorMap mc;
+  memset(&mc, 0, sizeof(mc));
+  p.tma_store = ((uintptr_t)g.C & 15) == 0 && (g.scm * 4) % 16 == 0 && g.scm >= g.N &&
+                g.epi_f.kind != TX_EPI_BIAS_TANH_DUAL && !getenv("TX_GEMM_NO_TMA_STORE");
+  if (p.tma_store) {
+    EncodeFn enc = encode_fn();
+    cuuint64_t dims[2] = {(cuuint64_t)g.N, (cuuint64_t)g.M};
+    cuuint64_t strides[1] = {(cuuint64_t)(g.scm * 4)};
+    cuuint32_t box[2] = {32, 32};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = enc(&mc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, g.C, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) p.tma_store = 0;
+  }
+  CUtensorMap mx;
+  memset(&mx, 0, sizeof(mx));
+  const Epi<float>& E = g.epi_f;
+  p.tma_aux = cg == 2 && p.tma_store && (E.kind == TX_EPI_MUL_AUX || E.kind == TX_EPI_MUL_1MSQR) && E.s1 == 1 &&
+              (E.s0 * 4) % 16 == 0 && E.s0 >= g.N && ((uintptr_t)E.aux & 15) == 0 && !getenv("TX_GEMM_NO_TMA_AUX");
+  if (p.tma_aux) {
+    EncodeFn enc = encode_fn();
+    cuuint64_t dims[2] = {(cuuint64_t)g.N, (cuuint64_t)g.M};
+    cuuint64_t strides[1] = {(cuuint64_t)(E.s0 * 4)};
+    cuuint32_t box[2] = {32, 32};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = enc(&mx, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(E.aux), dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) p.tma_aux = 0;
+  }
   const int units = sm_count() / cg;
   const int nclusters = p.num_tiles < units ? p.num_tiles : units;
   if (cg == 1) {
@@ -571,7 +728,7 @@ int gemm_tc(const G& g, cudaStream_t st) {
       TX_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<1>::SMEM));
       g_attr_set[1] = true;
     }
-    tc_gemm_kernel<1><<<nclusters, NUM_THREADS, Cfg<1>::SMEM, st>>>(ma, mb, p);
+    tc_gemm_kernel<1><<<nclusters, NUM_THREADS, Cfg<1>::SMEM, st>>>(ma, mb, mc, mx, p);
   } else {
     if (!g_attr_set[2]) {
       TX_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<2>::SMEM));
@@ -589,7 +746,7 @@ int gemm_tc(const G& g, cudaStream_t st) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    TX_CUDA(cudaLaunchKernelEx(&cfg, tc_gemm_kernel<2>, ma, mb, p));
+    TX_CUDA(cudaLaunchKernelEx(&cfg, tc_gemm_kernel<2>, ma, mb, mc, mx, p));
   }
   TX_CUDA(cudaGetLastError());
   return TX_OK;
