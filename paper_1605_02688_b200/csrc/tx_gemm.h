@@ -80,5 +80,6 @@ int kred_splits(int64_t M, int64_t K);
 // tcgen05 path: returns TX_E_UNSUPPORTED if the layout is ineligible
 int gemm_tc_eligible(const G& g);
 int gemm_tc(const G& g, cudaStream_t st);
+void choose_tile(const G& g, int* cg, int* bn);
 
 }  // namespace tx

@@ -233,6 +233,9 @@ struct TcParams {
   int M, N, K;
   int a_mn, b_mn;  // 1 = operand is MN-major in memory
   int a_3d, b_3d;  // MN-major operand loaded with one 3-D box per stage
+  int a_lim, b_lim;  // 3-D boxes cover MN < lim (whole 32-blocks); tiles reaching past it use the edge maps
+  int bn;           // N tile of this launch (<= BN, multiple of 32): chosen per shape against wave quantisation
+  int stage_tx;     // TMA bytes landing per stage on the leader's barrier
   int dbg_nostore;  // diagnostics only (TX_GEMM_DBG_NOSTORE): epilogue drains TMEM without storing
   int tma_store;    // C written by TMA tile stores from swizzled smem staging
   int tma_aux;      // [M,N] epilogue operand read by TMA tile loads (CG = 2)
@@ -254,10 +257,12 @@ template <int CG>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                    const __grid_constant__ CUtensorMap mapC, const __grid_constant__ CUtensorMap mapX,
+                   const __grid_constant__ CUtensorMap mapAe, const __grid_constant__ CUtensorMap mapBe,
                    const TcParams p) {
   using K_ = Cfg<CG>;
   constexpr int STAGES = K_::STAGES;
-  constexpr int BNL = BN / CG;  // B columns staged by this CTA
+  const int bn = p.bn;
+  const int BNL = bn / CG;  // B columns staged by this CTA
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* full = (uint64_t*)(smem + K_::RING + K_::STAGING + K_::AUX_STAGING);
@@ -309,12 +314,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         int mb, nb;
         tile_coords(t, p.num_m, p.num_n, mb, nb);
         const int m0 = mb * BM * CG + (int)rank * BM;   // this CTA's rows
-        const int n0 = nb * BN + (int)rank * BNL;       // this CTA's half of B
+        const int n0 = nb * bn + (int)rank * BNL;       // this CTA's half of B
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(empty + stage, phase ^ 1);
           uint8_t* sa = smem + stage * K_::STAGE_BYTES;
           uint8_t* sb = sa + K_::A_BYTES;
-          if (leader) mbar_expect_tx(full + stage, K_::STAGE_BYTES * CG);
+          if (leader) mbar_expect_tx(full + stage, (uint32_t)p.stage_tx);
           const int k0 = kb * BK;
           auto load = [&](void* dst, const CUtensorMap* map, int c0, int c1) {
             if constexpr (CG == 1) tma_load_2d(dst, map, full + stage, c0, c1);
@@ -324,19 +329,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if constexpr (CG == 1) tma_load_3d(dst, map, full + stage, 0, c1, c2);
             else tma_load_3d_2sm(dst, map, full + stage, 0, c1, c2);
           };
-          if (p.a_3d) {
+          if (p.a_3d && m0 + BM <= p.a_lim) {
             load3(sa, &mapA, k0, m0 / 32);
-          } else if (p.a_mn) {
+          } else if (p.a_mn) {  // 32-wide boxes: 2-D edge map (clipped at M)
+            const CUtensorMap* ma = p.a_3d ? &mapAe : &mapA;
 #pragma unroll
-            for (int j = 0; j < BM / 32; ++j) load(sa + j * 4096, &mapA, m0 + 32 * j, k0);
+            for (int j = 0; j < BM / 32; ++j) load(sa + j * 4096, ma, m0 + 32 * j, k0);
           } else {
             load(sa, &mapA, k0, m0);
           }
-          if (p.b_3d) {
+          if (p.b_3d && n0 + BNL <= p.b_lim) {
             load3(sb, &mapB, k0, n0 / 32);
           } else if (p.b_mn) {
-#pragma unroll
-            for (int j = 0; j < BNL / 32; ++j) load(sb + j * 4096, &mapB, n0 + 32 * j, k0);
+            const CUtensorMap* mb = p.b_3d ? &mapBe : &mapB;
+            for (int j = 0; j < BNL / 32; ++j) load(sb + j * 4096, mb, n0 + 32 * j, k0);
           } else {
             load(sb, &mapB, k0, n0);
           }
@@ -347,7 +353,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   } else if (warp == 1) {
     if (leader) {
       const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)p.a_mn << 15) |
-                             ((uint32_t)p.b_mn << 16) | ((uint32_t)(BN >> 3) << 17) |
+                             ((uint32_t)p.b_mn << 16) | ((uint32_t)(bn >> 3) << 17) |
                              ((uint32_t)((BM * CG) >> 4) << 24);
       // descriptor geometry per operand layout
       // K-major: LBO unused (16 B), SBO = 1024 B between 8-row atoms, +32 B per k-step.
@@ -364,7 +370,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const uint32_t use = (uint32_t)(it >> 1);
         mbar_wait(tempty + buf, (use & 1) ^ 1);
         tc_fence_after();
-        const uint32_t tmem_d = tmem_base + (uint32_t)(buf * BN);
+        const uint32_t tmem_d = tmem_base + (uint32_t)(buf * BN);  // buffers at 0 / 256 columns
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(full + stage, phase);
           tc_fence_after();
@@ -409,7 +415,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tc_fence_after();
       const int row0 = mb * BM * CG + (int)rank * BM + q * 32;
       const int row = row0 + lane;
-      const uint32_t taddr = tmem_base + (uint32_t)(buf * BN + half * (BN / 2)) + ((uint32_t)(q * 32) << 16);
+      // 32-column chunks of the bn-wide accumulator, alternating between the two warps of a lane quarter
+      const uint32_t taddr = tmem_base + (uint32_t)(buf * BN) + ((uint32_t)(q * 32) << 16);
+      const int nchunks = bn / 32;
       float* crow = p.C + (int64_t)row * p.ldc;
       const bool row_ok = row < p.M;
       if (p.tma_store) {
@@ -419,8 +427,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const float* xstg = reinterpret_cast<const float*>(smem + K_::RING + K_::STAGING + (size_t)(warp - 2) * 4096);
         uint64_t* xbar = auxbar + (warp - 2);
 #pragma unroll 1
-        for (int c = 0; c < BN / 2; c += 32) {
-          const int n = nb * BN + half * (BN / 2) + c;
+        for (int ci = half; ci < nchunks; ci += 2) {
+          const int c = ci * 32;
+          const int n = nb * bn + c;
           const bool live = !(row0 >= p.M || n >= p.N || p.dbg_nostore);
           if constexpr (CG == 2) {
             if (p.tma_aux && live && lane == 0) {  // fetch this chunk's operand tile while TMEM drains
@@ -508,10 +517,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         continue;
       }
 #pragma unroll 1
-      for (int c = 0; c < BN / 2; c += 32) {
+      for (int ci = half; ci < nchunks; ci += 2) {
+        const int c = ci * 32;
         float v[32];
         tmem_ld32(taddr + c, v);
-        const int n = nb * BN + half * (BN / 2) + c;
+        const int n = nb * bn + c;
         if (!row_ok || n >= p.N || p.dbg_nostore) continue;
         if (vec_ok && n + 32 <= p.N) {
           if (E.kind == TX_EPI_BIAS || E.kind == TX_EPI_BIAS_TANH || E.kind == TX_EPI_BIAS_TANH_DUAL) {
@@ -650,6 +660,30 @@ int gemm_tc_eligible(const G& g) {
   return TX_OK;
 }
 
+// Tile shape per launch: 256 x 256 CTA-pair tiles (cta_group::2), single-CTA
+// 128 x 256 when M <= 128.  Narrower N tiles (bn < 256) and single CTAs were
+// measured (r01, TX_GEMM_BN / TX_GEMM_CG) at 0.80-0.83 of the pair tile's
+// per-FLOP rate, which no wave-quantisation saving on the MLP shapes repays,
+// so they remain experiment switches only.
+void choose_tile(const G& g, int* cg_out, int* bn_out) {
+  const char* cg_s = getenv("TX_GEMM_CG");
+  const char* bn_s = getenv("TX_GEMM_BN");
+  int cg = 2;
+  // when both shapes fit in one wave (the M = 784 weight gradient: 112
+  // single-CTA tiles on 148 SMs vs 64 pair tiles on 74 pairs) the per-SM work
+  // is equal and uncoupled single CTAs measured ~5% faster (r01 A/B)
+  const int64_t sms = sm_count();
+  const int64_t t1 = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN);
+  const int64_t t2 = ((g.M + 2 * BM - 1) / (2 * BM)) * ((g.N + BN - 1) / BN);
+  if (t1 <= sms && t2 <= sms / 2) cg = 1;
+  if (cg_s) cg = atoi(cg_s) == 1 ? 1 : 2;
+  if (g.M <= BM) cg = 1;
+  int bn = bn_s ? atoi(bn_s) : BN;
+  if (bn < 32 || bn > BN || bn % (32 * cg) != 0) bn = BN;
+  *cg_out = cg;
+  *bn_out = bn;
+}
+
 int gemm_tc(const G& g, cudaStream_t st) {
   int rc = gemm_tc_eligible(g);
   if (rc) return fail(rc, "tx_gemm: operand layout not eligible for the tcgen05 path");
@@ -657,22 +691,36 @@ int gemm_tc(const G& g, cudaStream_t st) {
   const bool b_mn = (g.sbn == 1 && g.sbk % 4 == 0 && g.sbk >= g.N);
   // 2-CTA pairs (cta_group::2) unless TX_GEMM_CG=1 or the problem is too small
   // to give every SM pair a tile
-  const char* cg_s = getenv("TX_GEMM_CG");
-  const int cg_env = cg_s ? atoi(cg_s) : 2;
-  int cg = cg_env == 1 ? 1 : 2;
-  if (cg == 2 && g.M <= BM) cg = 1;
-  const int bnl = BN / cg;
+  int cg, bn;
+  choose_tile(g, &cg, &bn);
+  const int bnl = bn / cg;
   CUtensorMap ma, mb;
   const bool no3d = getenv("TX_GEMM_NO3D") != nullptr;
-  const bool a_3d = a_mn && g.M % 32 == 0 && !no3d;
-  const bool b_3d = b_mn && g.N % 32 == 0 && !no3d;
-  if (a_3d) rc = make_map_mn3d(&ma, g.A, g.M, g.K, g.sak, BM / 32);
-  else if (a_mn) rc = make_map(&ma, g.A, g.M, g.K, g.sak, 32, 32, true);
-  else rc = make_map(&ma, g.A, g.K, g.M, g.sam, 32, BM, false);
+  // MN-major operands: 3-D boxes over the whole 32-blocks (one TMA per stage);
+  // when MN % 32 != 0 the tile holding the ragged block uses 32-wide 2-D
+  // boxes from an edge map clipped at MN
+  const bool a_3d = a_mn && g.M >= 32 && !no3d;
+  const bool b_3d = b_mn && g.N >= 32 && !no3d;
+  CUtensorMap mae, mbe;
+  memset(&mae, 0, sizeof(mae));
+  memset(&mbe, 0, sizeof(mbe));
+  if (a_3d) {
+    rc = make_map_mn3d(&ma, g.A, g.M / 32 * 32, g.K, g.sak, BM / 32);
+    if (!rc && g.M % 32) rc = make_map(&mae, g.A, g.M, g.K, g.sak, 32, 32, true);
+  } else if (a_mn) {
+    rc = make_map(&ma, g.A, g.M, g.K, g.sak, 32, 32, true);
+  } else {
+    rc = make_map(&ma, g.A, g.K, g.M, g.sam, 32, BM, false);
+  }
   if (rc) return rc;
-  if (b_3d) rc = make_map_mn3d(&mb, g.B, g.N, g.K, g.sbk, bnl / 32);
-  else if (b_mn) rc = make_map(&mb, g.B, g.N, g.K, g.sbk, 32, 32, true);
-  else rc = make_map(&mb, g.B, g.K, g.N, g.sbn, 32, bnl, false);
+  if (b_3d) {
+    rc = make_map_mn3d(&mb, g.B, g.N / 32 * 32, g.K, g.sbk, bnl / 32);
+    if (!rc && g.N % 32) rc = make_map(&mbe, g.B, g.N, g.K, g.sbk, 32, 32, true);
+  } else if (b_mn) {
+    rc = make_map(&mb, g.B, g.N, g.K, g.sbk, 32, 32, true);
+  } else {
+    rc = make_map(&mb, g.B, g.K, g.N, g.sbn, 32, bnl, false);
+  }
   if (rc) return rc;
   TcParams p;
   p.C = (float*)g.C;
@@ -684,8 +732,12 @@ int gemm_tc(const G& g, cudaStream_t st) {
   p.b_mn = b_mn;
   p.a_3d = a_3d;
   p.b_3d = b_3d;
+  p.a_lim = (int)(g.M % 32 ? g.M / 32 * 32 : INT32_MAX);
+  p.b_lim = (int)(g.N % 32 ? g.N / 32 * 32 : INT32_MAX);
   p.num_m = (int)((g.M + BM * cg - 1) / (BM * cg));
-  p.num_n = (int)((g.N + BN - 1) / BN);
+  p.num_n = (int)((g.N + bn - 1) / bn);
+  p.bn = bn;
+  p.stage_tx = (Cfg<2>::A_BYTES + bnl * BK * 4) * cg;
   p.num_tiles = p.num_m * p.num_n;
   p.epi = g.epi_f;
   p.dbg_nostore = getenv("TX_GEMM_DBG_NOSTORE") != nullptr;
@@ -728,7 +780,7 @@ int gemm_tc(const G& g, cudaStream_t st) {
       TX_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<1>::SMEM));
       g_attr_set[1] = true;
     }
-    tc_gemm_kernel<1><<<nclusters, NUM_THREADS, Cfg<1>::SMEM, st>>>(ma, mb, mc, mx, p);
+    tc_gemm_kernel<1><<<nclusters, NUM_THREADS, Cfg<1>::SMEM, st>>>(ma, mb, mc, mx, mae, mbe, p);
   } else {
     if (!g_attr_set[2]) {
       TX_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<2>::SMEM));
@@ -746,7 +798,7 @@ int gemm_tc(const G& g, cudaStream_t st) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    TX_CUDA(cudaLaunchKernelEx(&cfg, tc_gemm_kernel<2>, ma, mb, mc, mx, p));
+    TX_CUDA(cudaLaunchKernelEx(&cfg, tc_gemm_kernel<2>, ma, mb, mc, mx, mae, mbe, p));
   }
   TX_CUDA(cudaGetLastError());
   return TX_OK;
