@@ -83,9 +83,41 @@ def fuse_elemwise(fgraph, ctx, emit) -> int:
     applied = 0
     for root in sorted(members):
         grp = members[root]
-        if len(grp) >= 2 and _fuse(fgraph, grp, emit):
-            applied += 1
+        if len(grp) >= 2:
+            applied += _fuse_capped(fgraph, grp, emit)
     return applied
+
+
+MAX_OPERANDS = 24  # generated kernel signature limit (codegen.generate_source)
+
+
+def _operands(fgraph, grp) -> int:
+    ids = {n.id for n in grp}
+    produced = {o.id for n in grp for o in n.outputs}
+    leaves = {x.id for n in grp for x in n.inputs if x.id not in produced and not _inline(x)}
+    boundary = sum(1 for n in grp for o in n.outputs
+                   if fgraph.is_output(o) or any(c.id not in ids for c in fgraph.node_clients(o)))
+    return len(leaves) + boundary
+
+
+def _fuse_capped(fgraph, grp, emit) -> int:
+    """Fuse a convex group; a group needing more kernel operands than the
+    generator supports is split at its topological midpoint (a prefix and the
+    matching suffix of a convex group are both convex and cannot form a
+    cycle with each other).  Groups are convex individually, but two groups
+    can still depend on each other through members of both (a1 -> b1 and
+    b2 -> a2); fusing the second would then close a cycle, so that group stays
+    unfused (``replace_all`` is transactional and reports it)."""
+    from .errors import CycleDetected
+    if len(grp) < 2:
+        return 0
+    if _operands(fgraph, grp) > MAX_OPERANDS:
+        half = len(grp) // 2
+        return _fuse_capped(fgraph, grp[:half], emit) + _fuse_capped(fgraph, grp[half:], emit)
+    try:
+        return 1 if _fuse(fgraph, grp, emit) else 0
+    except CycleDetected:
+        return 0
 
 
 def _fuse(fgraph, grp, emit) -> bool:

@@ -99,3 +99,319 @@ def transpose(x: Variable, axes=None) -> Variable:
     if axes is None:
         axes = tuple(reversed(range(x.type.ndim)))
     return dimshuffle(x, tuple(axes))
+
+
+# ---------------------------------------------------------------------------
+# Basic slicing, increment-into-slice and concatenation (reference
+# ``ops/shaping.py:107-479``).  On the device a slice is a view (offset plus
+# strides, negative for reversed steps), ``inc_subtensor`` is a copy followed
+# by an in-place add over the sliced view, and ``join`` copies each piece into
+# its slab of the output.  They exist for symbolic loops (``scan.py``): the
+# reversed-sequence streams of backpropagation through time.
+
+def _norm_item(item, what="index"):
+    if isinstance(item, (bool, np.bool_)):
+        raise TypeMismatch(f"unsupported {what} entry {item!r} (basic slicing only)")
+    if isinstance(item, (int, np.integer)):
+        return int(item)
+    if isinstance(item, (tuple, list)) and len(item) == 3:
+        return tuple(None if v is None else int(v) for v in item)
+    if isinstance(item, slice):
+        return tuple(None if v is None else int(v) for v in (item.start, item.stop, item.step))
+    raise TypeMismatch(f"unsupported {what} entry {item!r} (basic slicing only)")
+
+
+def _is_full_slice(entry):
+    return entry in ((None, None, None), (None, None, 1))
+
+
+def _slice_geometry(items, shape, strides, offset):
+    """(shape, strides, offset) of x[items] for a strided layout; raises
+    ShapeMismatch on an out-of-range integer index (NumPy's IndexError)."""
+    from .errors import ShapeMismatch
+    out_shape, out_strides = [], []
+    for i, item in enumerate(items):
+        n, st = shape[i], strides[i]
+        if isinstance(item, int):
+            j = item + n if item < 0 else item
+            if not 0 <= j < n:
+                raise ShapeMismatch(f"subtensor index {item} out of bounds for axis {i} with size {n}")
+            offset += j * st
+            continue
+        start, stop, step = slice(*item).indices(n)
+        length = len(range(start, stop, step))
+        if length > 0:
+            offset += start * st
+        out_shape.append(length)
+        out_strides.append(st * step)
+    out_shape.extend(shape[len(items):])
+    out_strides.extend(strides[len(items):])
+    return tuple(out_shape), tuple(out_strides), offset
+
+
+@register_op
+class Subtensor(Op):
+    """Basic slicing: per dim an integer index or a (start, stop, step)
+    triple (None = unspecified).  A zero-copy view on the device."""
+
+    name = "subtensor"
+    view_capable = True
+    view_map = {0: 0}
+
+    def __init__(self, items):
+        self.items = tuple(_norm_item(i) for i in items)
+
+    @property
+    def display_name(self):
+        return f"subtensor{self.items}"
+
+    def attrs_key(self):
+        return (self.items,)
+
+    def infer_types(self, input_types):
+        (t,) = input_types
+        if len(self.items) > t.ndim:
+            raise TypeMismatch(f"{len(self.items)} index entries for rank {t.ndim}")
+        out = []
+        for i, item in enumerate(self.items):
+            if isinstance(item, int):
+                continue
+            out.append(t.broadcastable[i] if _is_full_slice(item) else False)
+        out.extend(t.broadcastable[len(self.items):])
+        return [TensorType(t.dtype, tuple(out))]
+
+    def infer_shape(self, node, input_shapes):
+        (s,) = input_shapes
+        if s is UNKNOWN_SHAPE:
+            return [UNKNOWN_SHAPE]
+        out = []
+        for i, item in enumerate(self.items):
+            if isinstance(item, int):
+                continue
+            out.append(None if s[i] is None else len(range(*slice(*item).indices(s[i]))))
+        out.extend(s[len(self.items):])
+        return [tuple(out)]
+
+    def check_runtime_shapes(self, node, shapes):
+        _slice_geometry(self.items, shapes[0], (0,) * len(shapes[0]), 0)
+
+    def view_layout(self, node, in_layouts):
+        shape, strides, offset = in_layouts[0]
+        return _slice_geometry(self.items, shape, strides, offset)
+
+    def grad(self, inputs, output_grads):
+        from .elemwise import zeros_like
+        (x,), (v,) = inputs, output_grads
+        if not is_float(x.type.dtype):
+            return [DISCONNECTED]
+        return [inc_subtensor(zeros_like(x), v, self.items)]
+
+    def rop(self, inputs, input_perturbations):
+        (dx,) = input_perturbations
+        return [None if dx is None else apply(Subtensor(self.items), [dx])[0]]
+
+    def fold(self, values):
+        (x,) = values
+        return [np.ascontiguousarray(x[tuple(i if isinstance(i, int) else slice(*i) for i in self.items)])]
+
+    def attrs_payload(self, encode_graph=None):
+        return {"items": [i if isinstance(i, int) else list(i) for i in self.items]}
+
+    @classmethod
+    def from_payload(cls, payload, decode_graph=None):
+        return cls(tuple(i if isinstance(i, int) else tuple(i) for i in payload["items"]))
+
+
+def subtensor(x: Variable, key) -> Variable:
+    if not isinstance(key, tuple):
+        key = (key,)
+    return apply(Subtensor(key), [x])[0]
+
+
+def flip0(x: Variable) -> Variable:
+    """Reverse along the leading axis (a negative-stride view)."""
+    return subtensor(x, (slice(None, None, -1),))
+
+
+@register_op
+class IncSubtensor(Op):
+    """Copy of ``target`` with ``value`` added into the indexed region
+    (NumPy ``out[idx] += value``, value broadcast to the region)."""
+
+    name = "inc_subtensor"
+
+    def __init__(self, items):
+        self.items = tuple(_norm_item(i) for i in items)
+
+    @property
+    def display_name(self):
+        return f"inc_subtensor{self.items}"
+
+    def attrs_key(self):
+        return (self.items,)
+
+    def infer_types(self, input_types):
+        target, value = input_types
+        probe = Subtensor(self.items).infer_types([target])[0]
+        if probe.dtype != value.dtype or probe.ndim != value.ndim:
+            raise TypeMismatch(f"inc_subtensor value {value} does not match region type {probe}")
+        return [target]
+
+    def infer_shape(self, node, input_shapes):
+        return [input_shapes[0]]
+
+    def check_runtime_shapes(self, node, shapes):
+        from .errors import ShapeMismatch
+        region, _, _ = _slice_geometry(self.items, shapes[0], (0,) * len(shapes[0]), 0)
+        v = shapes[1]
+        for r, e in zip(reversed(region), reversed(v)):
+            if e != r and e != 1:
+                raise ShapeMismatch(f"inc_subtensor value of shape {tuple(v)} does not broadcast to region {region}")
+
+    def grad(self, inputs, output_grads):
+        (v,) = output_grads
+        out = []
+        for i, x in enumerate(inputs):
+            if not is_float(x.type.dtype):
+                out.append(DISCONNECTED)
+            elif i == 0:
+                out.append(v)
+            else:
+                out.append(apply(Subtensor(self.items), [v])[0])
+        return out
+
+    def rop(self, inputs, input_perturbations):
+        from .elemwise import zeros_like
+        dt, dv = input_perturbations
+        if dt is None and dv is None:
+            return [None]
+        dt = dt if dt is not None else zeros_like(inputs[0])
+        return [dt if dv is None else inc_subtensor(dt, dv, self.items)]
+
+    def lower(self, node, plan):
+        from .elemwise import EwProgram
+        out, target, value = node.outputs[0], node.inputs[0], node.inputs[1]
+        lo, lt, lv = plan.layout(out), plan.layout(target), plan.layout(value)
+        if lo.storage.root() is not lt.storage.root() or lo.offset != lt.offset or lo.strides != lt.strides:
+            plan.emit_copy_layouts(lt, lo)
+        shape, strides, off = _slice_geometry(self.items, lo.shape, lo.strides, lo.offset)
+        if 0 in shape:
+            return
+        region = plan.view_of(lo, shape, strides, off)
+        vs = [0] * len(shape)
+        for k in range(1, len(lv.shape) + 1):
+            vs[-k] = 0 if lv.shape[-k] == 1 else lv.strides[-k]
+        dt = out.type.dtype
+        prog = EwProgram.single("add", [dt, dt])
+        plan.emit_elementwise_tx(prog, [plan.tx(region)], [plan.tx(region), plan.tx(lv, shape, tuple(vs))])
+
+    def attrs_payload(self, encode_graph=None):
+        return {"items": [i if isinstance(i, int) else list(i) for i in self.items]}
+
+    @classmethod
+    def from_payload(cls, payload, decode_graph=None):
+        return cls(tuple(i if isinstance(i, int) else tuple(i) for i in payload["items"]))
+
+
+def inc_subtensor(target: Variable, value: Variable, items) -> Variable:
+    return apply(IncSubtensor(items), [target, value])[0]
+
+
+@register_op
+class Join(Op):
+    """Concatenate along one axis (reference ``ops/shaping.py:381-470``);
+    differentiable when every piece is guaranteed extent 1 on the axis."""
+
+    name = "join"
+
+    def __init__(self, axis: int):
+        self.axis = int(axis)
+
+    @property
+    def display_name(self):
+        return f"join[{self.axis}]"
+
+    def attrs_key(self):
+        return (self.axis,)
+
+    def infer_types(self, input_types):
+        if not input_types:
+            raise TypeMismatch("join of nothing")
+        ndim, dtype = input_types[0].ndim, input_types[0].dtype
+        for t in input_types:
+            if t.ndim != ndim or t.dtype != dtype:
+                raise TypeMismatch("join inputs must share rank and dtype")
+        if not 0 <= self.axis < ndim:
+            raise TypeMismatch(f"join axis {self.axis} out of range for rank {ndim}")
+        return [TensorType(dtype, tuple(all(t.broadcastable[i] for t in input_types) and i != self.axis
+                                        for i in range(ndim)))]
+
+    def infer_shape(self, node, input_shapes):
+        if any(s is UNKNOWN_SHAPE for s in input_shapes):
+            return [UNKNOWN_SHAPE]
+        out = []
+        for i in range(node.outputs[0].type.ndim):
+            dims = [s[i] for s in input_shapes]
+            if i == self.axis:
+                out.append(None if any(d is None for d in dims) else sum(dims))
+            else:
+                known = [d for d in dims if d is not None]
+                out.append(known[0] if known else None)
+        return [tuple(out)]
+
+    def check_runtime_shapes(self, node, shapes):
+        from .errors import ShapeMismatch
+        for i in range(len(shapes[0])):
+            if i != self.axis and len({s[i] for s in shapes}) > 1:
+                raise ShapeMismatch(f"join: pieces disagree on axis {i}: {[s[i] for s in shapes]}")
+
+    def grad(self, inputs, output_grads):
+        from .elemwise import sum_to_matching_shape
+        from .errors import NotDifferentiable
+        (v,) = output_grads
+        if any(not x.type.broadcastable[self.axis] for x in inputs):
+            raise NotDifferentiable("join gradient needs guaranteed extent-1 pieces along the axis "
+                                    "(general split boundaries are runtime values)")
+        grads = []
+        for i, x in enumerate(inputs):
+            if not is_float(x.type.dtype):
+                grads.append(DISCONNECTED)
+                continue
+            piece = apply(Subtensor(((None, None, None),) * self.axis + (i,)), [v])[0]
+            pattern = list(range(piece.type.ndim))
+            pattern.insert(self.axis, "x")
+            grads.append(sum_to_matching_shape(dimshuffle(piece, tuple(pattern)), x))
+        return grads
+
+    def rop(self, inputs, input_perturbations):
+        from .elemwise import zeros_like
+        if all(p is None for p in input_perturbations):
+            return [None]
+        return [apply(Join(self.axis), [p if p is not None else zeros_like(x)
+                                        for x, p in zip(inputs, input_perturbations)])[0]]
+
+    def lower(self, node, plan):
+        lo = plan.layout(node.outputs[0])
+        at = 0
+        for x in node.inputs:
+            lx = plan.layout(x)
+            n = lx.shape[self.axis]
+            if n:
+                shape = lo.shape[:self.axis] + (n,) + lo.shape[self.axis + 1:]
+                dst = plan.view_of(lo, shape, lo.strides, lo.offset + at * lo.strides[self.axis])
+                plan.emit_copy_layouts(lx, dst)
+            at += n
+
+    def fold(self, values):
+        return [np.concatenate(values, axis=self.axis)]
+
+    def attrs_payload(self, encode_graph=None):
+        return {"axis": self.axis}
+
+    @classmethod
+    def from_payload(cls, payload, decode_graph=None):
+        return cls(payload["axis"])
+
+
+def join(axis: int, *tensors: Variable) -> Variable:
+    return apply(Join(axis), list(tensors))[0]

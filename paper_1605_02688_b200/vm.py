@@ -281,6 +281,12 @@ class CompiledFunction:
         self.profile._order = tuple(n.id for n in self.order)
         self._events = None
         self.thunks = {}
+        # explicit scalar integer inputs that size a loop (scan n_steps): the
+        # trip count is baked into the step plan, so their VALUES join its key
+        from .scan import ScanOp
+        in_pos = {v.id: i for i, v in enumerate(self.input_vars)}
+        self._value_keyed = sorted({in_pos[n.inputs[0].id] for n in self.order
+                                    if isinstance(n.op, ScanOp) and n.op.has_nsteps and n.inputs[0].id in in_pos})
         self.shard = None
         if self.dp is not None:
             from . import dp as _dp
@@ -382,6 +388,14 @@ class CompiledFunction:
                 raise TypeMismatch(f"shared {s!r} holds a nonconforming value: {why}")
             shared_state.append((dev.data_ptr(), tuple(dev.shape), s.version))
         key = (tuple((b.shape, b.dev_ptr) for b in binds), tuple(shared_state))
+        if self._value_keyed:
+            vals = {}
+            for i in self._value_keyed:
+                b = binds[i]
+                src = b.tensor if b.tensor is not None else b.host
+                vals[self.input_vars[i].id] = int(np.asarray(src.cpu() if hasattr(src, "cpu") else src).reshape(()))
+            key = key + (tuple(sorted(vals.items())),)
+            self._bound_values = vals
         if self.pipelined and not device_out and key not in self._plans:
             from . import stream as _stream
             pipe = self._pipes.get(key)
@@ -550,8 +564,13 @@ def _bind_input(var, val) -> _Bind:
 # the step plan
 
 class StepPlan:
-    def __init__(self, fn: CompiledFunction, lib, binds, key):
+    def __init__(self, fn: CompiledFunction, lib, binds, key, shared_arena=None):
+        """``shared_arena``: a dict through which plans that never run
+        concurrently (the unrolled steps of a loop, ``scan.py``) share one
+        scratch arena allocation."""
         self.fn, self.lib = fn, lib
+        self.subplans = []                   # step plans of loops lowered into this plan
+        self.values = dict(getattr(fn, "_bound_values", None) or {})  # var id -> host value (loop trip counts)
         t = _torch()
         g = fn.fgraph
         self.lay: dict[int, Layout] = {}
@@ -599,8 +618,12 @@ class StepPlan:
         for n in order:
             ins = [self.lay[x.id] for x in n.inputs]
             shapes = [l.shape for l in ins]
-            n.op.check_runtime_shapes(n, shapes)
-            outs = n.op.infer_shape(n, shapes)
+            if getattr(n.op, "name", "") == "scan":
+                n.op.check_runtime_shapes(n, shapes, self.values)
+                outs = n.op.infer_shape(n, shapes, self.values)
+            else:
+                n.op.check_runtime_shapes(n, shapes)
+                outs = n.op.infer_shape(n, shapes)
             for o, s in zip(n.outputs, outs):
                 if s is UNKNOWN_SHAPE or any(d is None for d in s):
                     raise NotSupported(f"cannot infer the runtime shape of {o!r} ({n.op.name})")
@@ -782,7 +805,15 @@ class StepPlan:
                 count = off // ITEMSIZE[members[0].type.dtype]
                 self.buckets.append((members[0].type.dtype, buf.data_ptr(), count, members))
         self.arena_bytes = alloc.top
-        self.arena = t.empty(max(alloc.top, ALIGN), dtype=t.uint8, device="cuda")
+        need = max(alloc.top, ALIGN)
+        if shared_arena is not None:
+            cur = shared_arena.get("t")
+            if cur is None or cur.numel() < need:
+                cur = t.empty(need, dtype=t.uint8, device="cuda")
+                shared_arena["t"] = cur
+            self.arena = cur
+        else:
+            self.arena = t.empty(need, dtype=t.uint8, device="cuda")
         base = self.arena.data_ptr()
         for lay in list(self.lay.values()) + [d for _, d in self.tail_copies]:
             r = lay.storage.root()
@@ -861,6 +892,19 @@ class StepPlan:
     def layout(self, var) -> Layout:
         return self.lay[var.id]
 
+    def ptr_of(self, lay: Layout) -> int:
+        """Device address of a layout's first element."""
+        return lay.storage.root().ptr + lay.offset * ITEMSIZE[lay.dtype]
+
+    def scratch(self, shape, dtype) -> Layout:
+        """A contiguous step-lifetime device buffer outside the arena."""
+        t = _torch()
+        nb = int(np.prod(shape, dtype=np.int64)) * ITEMSIZE[dtype]
+        buf = t.empty(max(nb, ALIGN), dtype=t.uint8, device="cuda")
+        self.keep.append(buf)
+        st = Storage("scratch", nb, ptr=buf.data_ptr(), name="scratch")
+        return Layout(st, 0, tuple(shape), contiguous_strides(tuple(shape)), dtype)
+
     def tx(self, var_or_layout, shape=None, strides=None) -> native.TxTensor:
         lay = var_or_layout if isinstance(var_or_layout, Layout) else self.lay[var_or_layout.id]
         r = lay.storage.root()
@@ -895,7 +939,35 @@ class StepPlan:
         return native.make_tensor(16, lay.dtype, lay.shape if shape is None else shape,
                                   lay.strides if strides is None else strides)
 
+    def view_of(self, lay: Layout, shape, strides, offset) -> Layout:
+        """A layout over ``lay``'s storage (used by ops that write into or read
+        from sub-regions: inc_subtensor, join, scan histories)."""
+        return Layout(lay.storage, offset, shape, strides, lay.dtype)
+
     # -- emitters ---------------------------------------------------------------
+    def emit_copy_layouts(self, src: Layout, dst: Layout):
+        """Strided device copy src -> dst (same shape), attributed to the
+        node being lowered."""
+        lib = self.lib
+        s, d = self.tx(src), self.tx(dst)
+
+        def launch(stream):
+            lib.copy(s, d, stream)
+        self.add_launch(launch)
+
+    def emit_elementwise_tx(self, program: EwProgram, outs, ins):
+        """Launch ``program`` over explicit tensor descriptors (views)."""
+        lib = self.lib
+        h = codegen.CACHE.get(lib, program)
+        arr = (native.TxTensor * (len(outs) + len(ins)))(*outs, *ins)
+        n_out, n_in = len(outs), len(ins)
+        flag = self.flag.ptr if (self.flag is not None and codegen.has_int_div(program)) else None
+        f = lib.lib.tx_ew_launch
+
+        def launch(stream):
+            lib.check(f(h, n_out, n_in, arr, flag, stream))
+        self.add_launch(launch)
+
     def emit_elementwise(self, node, program: EwProgram):
         lib = self.lib
         h = codegen.CACHE.get(lib, program)
@@ -1099,14 +1171,17 @@ class StepPlan:
         self._dev_outs = tuple(outs)
         return outs
 
-    def check_flags(self):
+    def check_flags(self, stream=None):
+        stream = self.fn._stream if stream is None else stream
+        for sp in self.subplans:
+            sp.check_flags(stream)
         if self.flag is None:
             return
         t = _torch()
-        self.lib.stream_sync(self.fn._stream)
+        self.lib.stream_sync(stream)
         v = t.empty(1, dtype=t.int32, pin_memory=True)
-        self.lib.memcpy(v.data_ptr(), self.flag.ptr, 4, 1, self.fn._stream)
-        self.lib.stream_sync(self.fn._stream)
+        self.lib.memcpy(v.data_ptr(), self.flag.ptr, 4, 1, stream)
+        self.lib.stream_sync(stream)
         if int(v.item()):
             raise ZeroDivisionError("integer division by zero")
 

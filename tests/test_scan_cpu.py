@@ -1,0 +1,64 @@
+"""Loop construction on the host (no GPU): role/type checks, the BPTT and
+R-operator graphs, CSE of the re-applied forward loop, serialization of loop
+nodes (reference tests/test_scan.py construction cases)."""
+import numpy as np
+import pytest
+
+import paper_1605_02688_b200 as T
+from paper_1605_02688_b200.errors import LengthMismatch, MissingNonSequence, TypeMismatch
+from paper_1605_02688_b200.scan import ScanOp, scan
+
+
+def test_roles_types_and_errors():
+    xs, s0, w = T.matrix("xs"), T.vector("s0"), T.scalar("w")
+    (hist, ex), (final,) = scan(lambda x, s, w_: [s + x * w_, T.sum(x)], sequences=[xs], initial_states=[s0],
+                                non_sequences=[w])
+    op = hist.owner.op
+    assert isinstance(op, ScanOp) and (op.n_seqs, op.n_states, op.n_nonseqs, op.n_extras) == (1, 1, 1, 1)
+    assert hist.type.broadcastable == (False, False) and ex.type.ndim == 1 and final.type == s0.type
+    with pytest.raises(LengthMismatch):
+        scan(lambda s: s + 1.0, initial_states=[s0])
+    with pytest.raises(MissingNonSequence):
+        scan(lambda s: s * w, initial_states=[s0], n_steps=3, strict=True)
+    with pytest.raises(TypeMismatch):
+        scan(lambda x, s: s, sequences=[T.scalar("bad")], initial_states=[s0])
+
+
+def test_grad_and_rop_graphs_build_and_merge():
+    xs, h0, W = T.matrix("xs"), T.vector("h0"), T.matrix("W")
+    (hist,), (final,) = scan(lambda x, h, w: T.tanh(T.dot(w, h) + x), sequences=[xs], initial_states=[h0],
+                             non_sequences=[W])
+    gx, gh, gw = T.grad(T.sum(T.sqr(final)) + T.sum(hist), [xs, h0, W])
+    assert gx.type == xs.type and gh.type == h0.type and gw.type == W.type
+    f = T.compile([xs, h0, W], [final, gx, gh, gw])
+    loops = [n for n in f.order if isinstance(n.op, ScanOp)]
+    assert len(loops) == 2  # forward (re-applied inside the gradient, merged by CSE) + reversed
+    dirs = [T.matrix("dx"), T.vector("dh"), T.matrix("dW")]
+    r = T.rop([final], [xs, h0, W], dirs)[0]
+    assert r.type == final.type
+
+
+def test_structural_identity_and_document_round_trip():
+    def body(x, s):
+        return s * 2.0 + x
+    xs, s0 = T.vector("xs"), T.scalar("s0")
+    (a,), _ = scan(body, sequences=[xs], initial_states=[s0])
+    (b,), _ = scan(body, sequences=[xs], initial_states=[s0])
+    assert a.owner.op == b.owner.op and hash(a.owner.op) == hash(b.owner.op)
+    text = T.dump_graph([xs, s0], [a])
+    ins, outs, _, _ = T.load_graph(text)
+    assert isinstance(outs[0].owner.op, ScanOp) and outs[0].owner.op == a.owner.op
+    assert T.dump_graph(ins, outs) == text
+
+
+def test_subtensor_join_shapes():
+    x = T.matrix("x")
+    v = T.subtensor(x, (slice(1, None, 2), 3))
+    assert v.type.ndim == 1
+    assert v.owner.op.infer_shape(v.owner, [(7, 5)]) == [(3,)]
+    f0 = T.flip0(x)
+    assert f0.owner.op.view_layout(f0.owner, [((4, 5), (5, 1), 0)]) == ((4, 5), (-5, 1), 15)
+    j = T.join(0, x, x)
+    assert j.owner.op.infer_shape(j.owner, [(2, 5), (3, 5)]) == [(5, 5)]
+    with pytest.raises(TypeMismatch):
+        T.join(0, x, T.vector("v"))
