@@ -211,7 +211,7 @@ def select_rewrites(preset, include=(), exclude=()):
 
 
 def run_preset(fgraph: FunctionGraph, preset="fast_run", include=(), exclude=(), ctx=None):
-    from . import fusion  # noqa: F401  (registers the device passes)
+    from . import fusion, scan  # noqa: F401  (register the device and loop passes)
     ctx = ctx or RewriteContext()
     log = RewriteLog()
     chosen = select_rewrites(preset, include, exclude)

@@ -275,3 +275,47 @@ def test_scan_graph_document_round_trip(rng):
     b = run(ins, outs, pt)
     for x, y in zip(a, b):
         np.testing.assert_array_equal(x, y)
+
+
+# -- pinned to the REAL reference (tests/golden/make_scan_golden.py) ----------
+
+def _ref_gold():
+    import os
+    return np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "ref_scan_goldens.npz"))
+
+
+def test_rnn_matches_reference_goldens():
+    import sys, os
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden"))
+    from make_scan_golden import rnn_point
+    g = _ref_gold()
+    step, xs, h0, w, u = _rnn()
+    dirs = [T.matrix("dxs"), T.vector("dh0"), T.matrix("dw"), T.matrix("du")]
+    (hist,), (final,) = scan(step, sequences=[xs], initial_states=[h0], non_sequences=[w, u])
+    cost = T.sum(T.sqr(final)) + T.sum(hist * 0.5)
+    grads = T.grad(cost, [xs, h0, w, u])
+    jv = T.rop([final], [xs, h0, w, u], dirs)[0]
+    got = run([xs, h0, w, u] + dirs, [hist, final] + grads + [jv], rnn_point())
+    for v, k in zip(got, ["rnn_hist", "rnn_final", "rnn_gxs", "rnn_gh0", "rnn_gw", "rnn_gu", "rnn_rop"]):
+        assert rel_err(v, g[k]) <= 1e-11, k
+
+
+def test_nested_and_last_step_match_reference_goldens():
+    g = _ref_gold()
+    xv, a0 = T.vector("xv"), T.scalar("a0")
+
+    def outer_step(x_t, acc):
+        _, (inner_final,) = scan(lambda s, x: T.tanh(s + x), initial_states=[acc], non_sequences=[x_t], n_steps=3)
+        return acc * 0.5 + inner_final
+    (nh,), (nf,) = scan(outer_step, sequences=[xv], initial_states=[a0])
+    gn = T.grad(nf, [xv, a0])
+    r = np.random.default_rng(11)
+    got = run([xv, a0], [nh, nf] + gn, [r.standard_normal(6) * 0.5, np.array(0.2)])
+    for v, k in zip(got, ["nest_hist", "nest_final", "nest_gx", "nest_ga"]):
+        assert rel_err(v, g[k]) <= 1e-11, k
+    ys = T.vector("ys")
+    (lh,), _ = scan(lambda x, s: s * 0.9 + T.tanh(x), sequences=[ys], initial_states=[T.as_variable(0.0)])
+    f = T.compile([ys], [lh[-1] * 2.0])
+    assert any(n.op.name == "scan" and n.op.retention == ("last",) for n in f.order)
+    (v,) = f(np.random.default_rng(13).standard_normal(40))
+    assert rel_err(v, g["last_out"]) <= 1e-12

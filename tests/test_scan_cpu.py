@@ -62,3 +62,31 @@ def test_subtensor_join_shapes():
     assert j.owner.op.infer_shape(j.owner, [(2, 5), (3, 5)]) == [(5, 5)]
     with pytest.raises(TypeMismatch):
         T.join(0, x, T.vector("v"))
+
+
+def test_loop_rewrites_last_step_and_pushout():
+    from paper_1605_02688_b200.graph import FunctionGraph
+    from paper_1605_02688_b200.rewrite import run_preset
+    from paper_1605_02688_b200.scan import LAST
+    xs = T.vector("xs")
+    (hist,), _ = scan(lambda x, s: s + x, sequences=[xs], initial_states=[T.as_variable(0.0)])
+    fg = FunctionGraph([xs], [hist[-1] * 2.0])
+    _, log = run_preset(fg, "fast_run")
+    assert log.count(rewrite="loop_last_step_only") == 1
+    assert next(n for n in fg.toposort() if isinstance(n.op, ScanOp)).op.retention == (LAST,)
+    for out in (T.sum(hist), hist[-1] + T.sum(hist)):   # whole history consumed: keep it
+        fg = FunctionGraph([xs], [out])
+        run_preset(fg, "fast_run")
+        assert next(n for n in fg.toposort() if isinstance(n.op, ScanOp)).op.retention == ("full",)
+    w = T.scalar("w")
+    (h2,), _ = scan(lambda x, s, w_: s + x * T.exp(w_), sequences=[xs], initial_states=[T.as_variable(0.0)],
+                    non_sequences=[w])
+    fg = FunctionGraph([xs, w], [h2])
+    _, log = run_preset(fg, "fast_run")
+    assert log.count(rewrite="loop_pushout_invariants") == 1
+    loop = next(n for n in fg.toposort() if isinstance(n.op, ScanOp))
+    assert not any(getattr(n.op, "kernel", None) == "exp" for n in loop.op._order)
+    (h3,), _ = scan(lambda x, s: s * x, sequences=[xs], initial_states=[T.as_variable(1.0)])
+    fg = FunctionGraph([xs], [h3])
+    _, log = run_preset(fg, "fast_run")
+    assert log.count(rewrite="loop_pushout_invariants") == 0
