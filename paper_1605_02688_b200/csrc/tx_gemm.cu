@@ -121,6 +121,7 @@ int tx_gemm_workspace(const tx_tensor* A, const tx_tensor* B, const tx_tensor* C
     choose(g, mode, &path, &kind);
   }
   if (path == PATH_SKINNY && kind == SK_KRED) *bytes = (size_t)kred_splits(g.M, g.K) * g.M * g.N * 4 + 256;
+  if (path == PATH_TC) *bytes = gemm_tc_workspace(g);
   return TX_OK;
 }
 
@@ -146,7 +147,7 @@ int tx_gemm(const tx_tensor* A, const tx_tensor* B, tx_tensor* C, const tx_epilo
     if (p2 == PATH_SKINNY) return gemm_skinny(t, k2, ws, wsb, st);
   }
   switch (path) {
-    case PATH_TC: return gemm_tc(g, st);
+    case PATH_TC: return gemm_tc(g, ws, wsb, st);
     case PATH_SKINNY: return gemm_skinny(g, kind, ws, wsb, st);
     default: return gemm_simt(g, st);
   }

@@ -79,7 +79,10 @@ int gemm_skinny(const G& g, int kind, void* ws, size_t wsb, cudaStream_t st);
 int kred_splits(int64_t M, int64_t K);
 // tcgen05 path: returns TX_E_UNSUPPORTED if the layout is ineligible
 int gemm_tc_eligible(const G& g);
-int gemm_tc(const G& g, cudaStream_t st);
+int gemm_tc(const G& g, void* ws, size_t wsb, cudaStream_t st);
+size_t gemm_tc_workspace(const G& g);
 void choose_tile(const G& g, int* cg, int* bn);
+// C = epi(sum over splits of P[split][M][N]), fixed split order
+int splitk_finalize(const float* P, const G& g, int splits, cudaStream_t st);
 
 }  // namespace tx

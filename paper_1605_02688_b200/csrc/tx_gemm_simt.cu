@@ -593,6 +593,14 @@ int kred_splits(int64_t M, int64_t K) {
   return (int)s;
 }
 
+int splitk_finalize(const float* P, const G& g, int splits, cudaStream_t st) {
+  const int64_t tot = g.M * g.N;
+  kred_finalize<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(P, (float*)g.C, g.M, (int)g.N, splits, g.scm, g.scn,
+                                                              g.epi_f);
+  TX_CUDA(cudaGetLastError());
+  return TX_OK;
+}
+
 int gemm_simt(const G& g, cudaStream_t st) {
   dim3 grid((unsigned)((g.N + 63) / 64), (unsigned)((g.M + 63) / 64));
   if (g.dtype == TX_F32)

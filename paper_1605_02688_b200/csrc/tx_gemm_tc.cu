@@ -128,6 +128,12 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void*
                : "memory");
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"((uint64_t)map),
+               "r"(su32(src)), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
 __device__ __forceinline__ void tma_store_wait_read() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
@@ -234,6 +240,8 @@ struct TcParams {
   int a_mn, b_mn;  // 1 = operand is MN-major in memory
   int a_3d, b_3d;  // MN-major operand loaded with one 3-D box per stage
   int a_lim, b_lim;  // 3-D boxes cover MN < lim (whole 32-blocks); tiles reaching past it use the edge maps
+  int splits;       // split-K factor: work items are (tile, split); partial tiles go to a workspace
+  int kbs;          // k-blocks per split
   int bn;           // N tile of this launch (<= BN, multiple of 32): chosen per shape against wave quantisation
   int stage_tx;     // TMA bytes landing per stage on the leader's barrier
   int dbg_nostore;  // diagnostics only (TX_GEMM_DBG_NOSTORE): epilogue drains TMEM without storing
@@ -310,12 +318,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&mapB) : "memory");
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = cluster_id; t < p.num_tiles; t += num_clusters) {
+      for (int t = cluster_id; t < p.num_tiles * p.splits; t += num_clusters) {
         int mb, nb;
-        tile_coords(t, p.num_m, p.num_n, mb, nb);
+        tile_coords(t % p.num_tiles, p.num_m, p.num_n, mb, nb);
+        const int kb0 = (t / p.num_tiles) * p.kbs, kb1 = min(num_kb, kb0 + p.kbs);
         const int m0 = mb * BM * CG + (int)rank * BM;   // this CTA's rows
         const int n0 = nb * bn + (int)rank * BNL;       // this CTA's half of B
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(empty + stage, phase ^ 1);
           uint8_t* sa = smem + stage * K_::STAGE_BYTES;
           uint8_t* sb = sa + K_::A_BYTES;
@@ -365,13 +374,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int t = cluster_id; t < p.num_tiles; t += num_clusters, ++it) {
+      for (int t = cluster_id; t < p.num_tiles * p.splits; t += num_clusters, ++it) {
+        const int kb0 = (t / p.num_tiles) * p.kbs, kb1 = min(num_kb, kb0 + p.kbs);
         const int buf = it & 1;
         const uint32_t use = (uint32_t)(it >> 1);
         mbar_wait(tempty + buf, (use & 1) ^ 1);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + (uint32_t)(buf * BN);  // buffers at 0 / 256 columns
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(full + stage, phase);
           tc_fence_after();
           if (lane == 0) {
@@ -381,7 +391,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             for (int kk = 0; kk < BK / 8; ++kk) {
               const uint64_t da = sdesc(sa + kk * a_step, a_lbo, a_sbo, a_lay);
               const uint64_t db = sdesc(sb + kk * b_step, b_lbo, b_sbo, b_lay);
-              umma_tf32<CG>(tmem_d, da, db, idesc, (kb | kk) != 0);
+              umma_tf32<CG>(tmem_d, da, db, idesc, (kb != kb0) || (kk != 0));
             }
             umma_commit<CG>(empty + stage);
           }
@@ -406,9 +416,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         (E.kind != TX_EPI_BIAS_TANH_DUAL || (E.o1 == 1 && E.o0 % 4 == 0 && ((uintptr_t)E.out2 & 15) == 0)) &&
                         (E.kind != TX_EPI_BIAS && E.kind != TX_EPI_BIAS_TANH && E.kind != TX_EPI_BIAS_TANH_DUAL ||
                          (E.s1 == 1 && ((uintptr_t)E.aux & 15) == 0));
-    for (int t = cluster_id; t < p.num_tiles; t += num_clusters, ++it) {
+    for (int t = cluster_id; t < p.num_tiles * p.splits; t += num_clusters, ++it) {
       int mb, nb;
-      tile_coords(t, p.num_m, p.num_n, mb, nb);
+      tile_coords(t % p.num_tiles, p.num_m, p.num_n, mb, nb);
+      const int split = t / p.num_tiles;
       const int buf = it & 1;
       const uint32_t use = (uint32_t)(it >> 1);
       mbar_wait(tfull + buf, use & 1);
@@ -440,6 +451,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           float v[32];
           tmem_ld32(taddr + c, v);
           if (!live) continue;
+          if (p.splits > 1) {  // raw partial tile -> workspace [split][M][N]; the reduction applies the epilogue
+            if (lane == 0) tma_store_wait_read();
+            __syncwarp();
+            float4* prow = reinterpret_cast<float4*>(stg + lane * 32);
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              prow[j ^ (lane & 7)] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) tma_store_3d(&mapC, stg, n, row0, split);
+            continue;
+          }
           if constexpr (CG == 2) {
             if (p.tma_aux) {
               mbar_wait(xbar, xphase);
@@ -648,7 +671,12 @@ void* tmap_encoder() {
 
 int gemm_tc_eligible(const G& g) {
   if (g.dtype != TX_F32) return TX_E_UNSUPPORTED;
-  if (g.M < 64 || g.N < 64 || g.K < 16) return TX_E_UNSUPPORTED;
+  if (g.K < 16) return TX_E_UNSUPPORTED;
+  // a thin side (< 64 rows or columns) wastes most of a 128 x 256 tile, which
+  // still beats the CUDA-core tile kernel once the product is large (the
+  // [20 x 600] x [600 x 10000] per-step GEMMs of an LSTM language model);
+  // small thin products stay on the exact SIMT path
+  if ((g.M < 64 || g.N < 64) && (double)g.M * (double)g.N * (double)g.K < (double)(1 << 20)) return TX_E_UNSUPPORTED;
   if (g.M > INT32_MAX || g.N > INT32_MAX || g.K > INT32_MAX) return TX_E_UNSUPPORTED;
   if (g.scn != 1) return TX_E_UNSUPPORTED;
   if (((uintptr_t)g.A & 15) || ((uintptr_t)g.B & 15)) return TX_E_UNSUPPORTED;
@@ -684,7 +712,36 @@ void choose_tile(const G& g, int* cg_out, int* bn_out) {
   *bn_out = bn;
 }
 
-int gemm_tc(const G& g, cudaStream_t st) {
+// Split-K for launches that leave most SMs idle (few output tiles, long K:
+// the [20 x 10000] x [10000 x 600] gradient of an LSTM output layer is ONE
+// tile).  Work items become (tile, K-slice); raw partial tiles land in a
+// [splits][M][N] workspace through a 3-D TMA map and a second kernel sums
+// them in split order (deterministic) and applies the epilogue.
+void tc_splitk(const G& g, int* splits, int* kbs) {
+  int cg, bn;
+  choose_tile(g, &cg, &bn);
+  const int64_t tiles = ((g.M + BM * cg - 1) / (BM * cg)) * ((g.N + bn - 1) / bn);
+  const int64_t units = sm_count() / cg;
+  const int num_kb = (int)((g.K + BK - 1) / BK);
+  *splits = 1;
+  *kbs = num_kb;
+  if (getenv("TX_GEMM_NO_SPLITK") || tiles * 2 > units || num_kb < 8 || g.N % 4 != 0) return;
+  int64_t s = units / tiles;
+  if (s > num_kb / 4) s = num_kb / 4;
+  if (s > 64) s = 64;
+  if (s < 2) return;
+  const int k = (int)((num_kb + s - 1) / s);
+  *kbs = k;
+  *splits = (num_kb + k - 1) / k;
+}
+
+size_t gemm_tc_workspace(const G& g) {
+  int s, k;
+  tc_splitk(g, &s, &k);
+  return s > 1 ? (size_t)s * (size_t)g.M * (size_t)g.N * 4 + 256 : 0;
+}
+
+int gemm_tc(const G& g, void* ws, size_t wsb, cudaStream_t st) {
   int rc = gemm_tc_eligible(g);
   if (rc) return fail(rc, "tx_gemm: operand layout not eligible for the tcgen05 path");
   const bool a_mn = !(g.sak == 1 && g.sam % 4 == 0 && g.sam >= g.K);
@@ -739,6 +796,11 @@ int gemm_tc(const G& g, cudaStream_t st) {
   p.bn = bn;
   p.stage_tx = (Cfg<2>::A_BYTES + bnl * BK * 4) * cg;
   p.num_tiles = p.num_m * p.num_n;
+  tc_splitk(g, &p.splits, &p.kbs);
+  if (p.splits > 1 && (ws == nullptr || wsb < gemm_tc_workspace(g) || ((uintptr_t)ws & 15))) {
+    p.splits = 1;
+    p.kbs = (int)((g.K + BK - 1) / BK);
+  }
   p.epi = g.epi_f;
   p.dbg_nostore = getenv("TX_GEMM_DBG_NOSTORE") != nullptr;
   // TMA tile stores need a 16-byte aligned C with a 16-byte row pitch; the
@@ -757,10 +819,22 @@ int gemm_tc(const G& g, cudaStream_t st) {
                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) p.tma_store = 0;
   }
+  if (p.splits > 1) {
+    // partial tiles: 3-D map {N, M, splits} over the workspace (rows never spill into the next split)
+    EncodeFn enc = encode_fn();
+    cuuint64_t dims[3] = {(cuuint64_t)g.N, (cuuint64_t)g.M, (cuuint64_t)p.splits};
+    cuuint64_t strides[2] = {(cuuint64_t)(g.N * 4), (cuuint64_t)(g.M * g.N * 4)};
+    cuuint32_t box[3] = {32, 32, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = enc(&mc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, ws, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(TX_E_CUDA, "tx_gemm: split-K workspace map failed");
+    p.tma_store = 1;
+  }
   CUtensorMap mx;
   memset(&mx, 0, sizeof(mx));
   const Epi<float>& E = g.epi_f;
-  p.tma_aux = cg == 2 && p.tma_store && (E.kind == TX_EPI_MUL_AUX || E.kind == TX_EPI_MUL_1MSQR) && E.s1 == 1 &&
+  p.tma_aux = cg == 2 && p.tma_store && p.splits == 1 && (E.kind == TX_EPI_MUL_AUX || E.kind == TX_EPI_MUL_1MSQR) && E.s1 == 1 &&
               (E.s0 * 4) % 16 == 0 && E.s0 >= g.N && ((uintptr_t)E.aux & 15) == 0 && !getenv("TX_GEMM_NO_TMA_AUX");
   if (p.tma_aux) {
     EncodeFn enc = encode_fn();
@@ -774,7 +848,8 @@ int gemm_tc(const G& g, cudaStream_t st) {
     if (r != CUDA_SUCCESS) p.tma_aux = 0;
   }
   const int units = sm_count() / cg;
-  const int nclusters = p.num_tiles < units ? p.num_tiles : units;
+  const int work = p.num_tiles * p.splits;
+  const int nclusters = work < units ? work : units;
   if (cg == 1) {
     if (!g_attr_set[1]) {
       TX_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<1>::SMEM));
@@ -799,6 +874,10 @@ int gemm_tc(const G& g, cudaStream_t st) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     TX_CUDA(cudaLaunchKernelEx(&cfg, tc_gemm_kernel<2>, ma, mb, mc, mx, mae, mbe, p));
+  }
+  if (p.splits > 1) {
+    TX_CUDA(cudaGetLastError());
+    return splitk_finalize((const float*)ws, g, p.splits, st);
   }
   TX_CUDA(cudaGetLastError());
   return TX_OK;

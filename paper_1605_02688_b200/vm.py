@@ -564,10 +564,12 @@ def _bind_input(var, val) -> _Bind:
 # the step plan
 
 class StepPlan:
-    def __init__(self, fn: CompiledFunction, lib, binds, key, shared_arena=None):
+    def __init__(self, fn: CompiledFunction, lib, binds, key, shared_arena=None, out_binds=None):
         """``shared_arena``: a dict through which plans that never run
         concurrently (the unrolled steps of a loop, ``scan.py``) share one
-        scratch arena allocation."""
+        scratch arena allocation.  ``out_binds``: {var id: device pointer} --
+        node outputs written straight into caller-owned memory (a loop's
+        history slot) instead of the arena."""
         self.fn, self.lib = fn, lib
         self.subplans = []                   # step plans of loops lowered into this plan
         self.values = dict(getattr(fn, "_bound_values", None) or {})  # var id -> host value (loop trip counts)
@@ -639,6 +641,11 @@ class StepPlan:
                     st = Storage("bucket", nb, name="grad")
                     self.lay[o.id] = Layout(st, 0, s, contiguous_strides(s), o.type.dtype)
                     partial_vars.append((o, nb))
+                    continue
+                if out_binds and o.id in out_binds:
+                    nb = int(np.prod(s, dtype=np.int64)) * ITEMSIZE[o.type.dtype]
+                    st = Storage("bound", nb, ptr=out_binds[o.id], name="bound")
+                    self.lay[o.id] = Layout(st, 0, s, contiguous_strides(s), o.type.dtype)
                     continue
                 d = direct.get(o.id)
                 if d is not None:

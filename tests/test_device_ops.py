@@ -209,6 +209,7 @@ def _gemm_case(M, N, K, ta, tb, mode, rng):
 
 
 @pytest.mark.parametrize("M,N,K", [(256, 512, 256), (300, 520, 784), (784, 1024, 1000), (1024, 4096, 128), (352, 160, 96),
+                                   (20, 3000, 600), (700, 40, 1200), (20, 300, 8192), (64, 64, 20000),
                                    (129, 65, 33)])
 @pytest.mark.parametrize("ta,tb", [(False, False), (False, True), (True, False), (True, True)])
 def test_gemm_tcgen05_layouts(M, N, K, ta, tb, rng):
