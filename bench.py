@@ -290,6 +290,26 @@ def bench_logreg(T, C, steps, warmup, lib_holder):
     return ms, e2e, kernel_launches(f)
 
 
+def bench_lstm(T, lib_holder, steps=10):
+    """PTB-shaped LSTM language-model training steps through scan (PAPER.md
+    section 5.3 shapes: batch 20, small 200x20 steps, medium 600x40 steps,
+    vocabulary 10000, per-step softmax-xent, BPTT, SGD on every weight)."""
+    import torch
+    from tools.lstm_bench import CONFIGS, build
+    lib = lib_holder()
+    out = {}
+    for name, (H, L) in CONFIGS.items():
+        step, host = build(T, H, L)
+        dev = [torch.from_numpy(v).cuda() for v in host]
+        for _ in range(3):
+            step.call_device(*dev)
+        ms = time_device_block(lambda: step.call_device(*dev), lib, step._stream, steps)
+        out[name] = {"hidden": H, "steps": L, "batch": 20, "ms_per_batch": round(ms, 3),
+                     "words_per_s": round(20 * L / (ms * 1e-3), 1)}
+        del step, dev
+    return out
+
+
 def bench_reduce(T, C, steps, lib_holder):
     import torch
     n = 16384
@@ -460,6 +480,10 @@ def main():
                                     "e2e_us_per_step": round(e2e_l * 1e6, 1), "launches_per_step": nl}
         except Exception as e:
             extra["logreg_n600"] = {"error": repr(e)[:300]}
+        try:
+            extra["lstm_ptb_words_per_s"] = bench_lstm(T, lib_holder)
+        except Exception as e:
+            extra["lstm_ptb_words_per_s"] = {"error": repr(e)[:300]}
         try:
             extra["careduce_16384sq_GBs"] = bench_reduce(T, C, 10, lib_holder)
             extra["careduce_frac_of_hbm_peak"] = {k: round(v / pk["hbm_gbs"], 3)

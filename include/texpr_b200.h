@@ -118,6 +118,13 @@ int tx_kernel_destroy(void* kernel);
  * Replaces Sum/Max/ArgmaxOnehot.perform (reference ops/reductions.py:87-188)
  * and adds an index argmax.  axes_mask bit i = reduce dim i. */
 enum { TX_SUM = 0, TX_MAX = 1, TX_ARGMAX_ONEHOT = 2, TX_ARGMAX_INDEX = 3 };
+/* NaN guard (reference diagnostics.py:52-88 nan_guard_check, hooked per node
+ * at runtime.py:359-367): scan one float tensor and OR into flags[slot]
+ * bit 1 if it holds a NaN, bit 2 an infinity, bit 4 a finite value with
+ * |v| > big (checks enabled by `mode` bits 1/2/4).  Device-side only; the
+ * host reads the flag words once per step. */
+int tx_check_values(const tx_tensor* x, uint32_t* flags, int slot, int mode, double big, void* stream);
+
 int tx_reduce_workspace(int op, const tx_tensor* x, uint32_t axes_mask, size_t* bytes);
 int tx_reduce(int op, const tx_tensor* x, uint32_t axes_mask, tx_tensor* y,
               void* workspace, size_t workspace_bytes, void* stream);

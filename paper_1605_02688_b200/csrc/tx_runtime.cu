@@ -109,6 +109,28 @@ static int launch_copy(const tx_tensor* s, tx_tensor* d, cudaStream_t st) {
   return TX_OK;
 }
 
+// ---------------------------------------------------------------- NaN guard
+template <typename T>
+__global__ void check_values_kernel(const T* __restrict__ x, int64_t n, int nd, CopyMeta m, uint32_t* flags,
+                                    int slot, int mode, double big) {
+  uint32_t bits = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = i, off = 0;
+    for (int d = nd - 1; d >= 0; --d) {
+      const int64_t e = m.v[d];
+      off += (r % e) * m.v[nd + d];
+      r /= e;
+    }
+    const double v = (double)x[off];
+    if (v != v) bits |= 1u;
+    else if (v == INFINITY || v == -INFINITY) bits |= 2u;
+    else if (v > big || v < -big) bits |= 4u;
+  }
+  bits &= (uint32_t)mode;
+  bits = __reduce_or_sync(0xffffffffu, bits);
+  if ((threadIdx.x & 31) == 0 && bits) atomicOr(flags + slot, bits);
+}
+
 }  // namespace tx
 
 using namespace tx;
@@ -204,6 +226,34 @@ int tx_graph_launch(void* exec, void* s) {
   return TX_OK;
 }
 int tx_graph_destroy(void* exec) { TX_CUDA(cudaGraphExecDestroy((cudaGraphExec_t)exec)); return TX_OK; }
+
+int tx_check_values(const tx_tensor* x, uint32_t* flags, int slot, int mode, double big, void* s) {
+  TX_CHECK(x && flags, TX_E_ARG, "tx_check_values: null argument");
+  TX_CHECK(x->dtype == TX_F32 || x->dtype == TX_F64, TX_E_ARG, "tx_check_values: float tensors only");
+  const int64_t n = numel(*x);
+  if (n == 0) return TX_OK;
+  int64_t strides[1][TX_MAX_RANK];
+  for (int i = 0; i < x->ndim; ++i) strides[0][i] = x->strides[i];
+  Space sp;
+  collapse(x->ndim, x->shape, 1, strides, &sp);
+  CopyMeta m;
+  int nd = sp.ndim;
+  for (int i = 0; i < nd; ++i) {
+    m.v[i] = sp.shape[i];
+    m.v[nd + i] = sp.strides[0][i];
+  }
+  if (nd == 0) { m.v[0] = 1; m.v[1] = 0; nd = 1; }
+  int64_t blocks = (n + 255) / 256;
+  const int64_t cap = (int64_t)sm_count() * 8;
+  if (blocks > cap) blocks = cap;
+  cudaStream_t st = (cudaStream_t)s;
+  if (x->dtype == TX_F32)
+    check_values_kernel<float><<<(unsigned)blocks, 256, 0, st>>>((const float*)x->data, n, nd, m, flags, slot, mode, big);
+  else
+    check_values_kernel<double><<<(unsigned)blocks, 256, 0, st>>>((const double*)x->data, n, nd, m, flags, slot, mode, big);
+  TX_CUDA(cudaGetLastError());
+  return TX_OK;
+}
 
 int tx_copy(const tx_tensor* src, tx_tensor* dst, void* s) {
   TX_CHECK(src && dst && src->dtype == dst->dtype, TX_E_ARG, "tx_copy: dtype mismatch");

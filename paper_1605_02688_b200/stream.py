@@ -34,7 +34,8 @@ SLOTS = 3
 
 
 def eligible(fn, binds, device_out) -> bool:
-    if device_out or fn.updates or fn.shared_bindings or fn.dp is not None or fn.profile_nodes:
+    if (device_out or fn.updates or fn.shared_bindings or fn.dp is not None or fn.profile_nodes
+            or fn.nan_guard is not None):
         return False
     if not binds or any(b.dev_ptr is not None for b in binds):
         return False

@@ -200,8 +200,6 @@ def compile(inputs, outputs, updates=(), preset="fast_run", allow_gc=True, nan_g
     ``data_parallel`` (a :class:`dp.DataParallel` group for synchronous
     gradient allreduce).
     """
-    if nan_guard is not None:
-        raise NotSupported("nan_guard is not implemented by the B200 VM")
     single = isinstance(outputs, Variable)
     outputs = [outputs] if single else list(outputs)
     inputs = list(inputs)
@@ -240,7 +238,8 @@ def compile(inputs, outputs, updates=(), preset="fast_run", allow_gc=True, nan_g
     return CompiledFunction(fg, len(outputs), [repl[v] for v in inputs], [(s, repl[s]) for s in found],
                             [(p.shared, cloned[len(outputs) + i]) for i, p in enumerate(ups)],
                             log, preset, single, allow_gc=allow_gc, cuda_graph=cuda_graph,
-                            gemm_mode=gemm_mode, data_parallel=data_parallel, row_fusion=row_fusion)
+                            gemm_mode=gemm_mode, data_parallel=data_parallel, row_fusion=row_fusion,
+                            nan_guard=nan_guard)
 
 
 function = compile
@@ -249,7 +248,7 @@ function = compile
 class CompiledFunction:
     def __init__(self, fgraph, n_outputs, input_vars, shared_bindings, updates, rewrite_log, preset,
                  single_output=False, allow_gc=True, cuda_graph=True, gemm_mode="auto", data_parallel=None,
-                 row_fusion=True):
+                 row_fusion=True, nan_guard=None):
         self.fgraph = fgraph
         self.n_outputs = n_outputs
         self.input_vars = list(input_vars)
@@ -264,9 +263,9 @@ class CompiledFunction:
         self.cuda_graph = cuda_graph
         self.gemm_mode = {"auto": native.GEMM_AUTO, "simt": native.GEMM_SIMT, "tc": native.GEMM_TC}[gemm_mode]
         self.dp = data_parallel
-        self.row_fusion = row_fusion
+        self.nan_guard = nan_guard
+        self.row_fusion = row_fusion and nan_guard is None
         self.profile = Profile(stage_times=dict(rewrite_log.stage_times))
-        self.nan_guard = None
         self.has_lazy = False
         self._lock = threading.Lock()
         self._plans: dict = {}
@@ -278,6 +277,8 @@ class CompiledFunction:
         self.pipelined = True
         self.profile_nodes = False
         self._direct, self.order = self._schedule()
+        if self.nan_guard is not None:
+            self._direct = {}   # updates are committed only after the guard passed
         self.profile._order = tuple(n.id for n in self.order)
         self._events = None
         self.thunks = {}
@@ -430,6 +431,9 @@ class CompiledFunction:
         else:
             plan.run(stream)
             self.profile._pending += 1
+        if plan.guard_slots:
+            plan.check_guard(stream)      # raises NanDetected before any update is committed
+            plan.run_commits(stream)
         if device_out:
             outs = plan.device_outputs()
             lib.event_record(self._events[1], stream)
@@ -752,7 +756,7 @@ class StepPlan:
             if getattr(n.op, "view_capable", False):
                 continue
             taken = set()
-            inplace_ok = isinstance(n.op, (Elemwise, Composite))
+            inplace_ok = isinstance(n.op, (Elemwise, Composite)) and fn.nan_guard is None
             for o in n.outputs:
                 ol = self.lay[o.id]
                 st = ol.storage
@@ -782,7 +786,8 @@ class StepPlan:
                 w[0].offset = alloc.alloc(w[1])
                 alloc.release(w[0].offset, w[1])
             for st in live_at.pop(i, []):
-                alloc.release(st.offset, st.nbytes)
+                if fn.nan_guard is None:   # a guarded step keeps every value for its report
+                    alloc.release(st.offset, st.nbytes)
         for src, dst in self.tail_copies:
             assign(dst.storage)
         # any arena storage not yet placed (e.g. unused outputs)
@@ -849,6 +854,12 @@ class StepPlan:
         grouped = {n.id for grp in self.row_groups for n in grp.members}
         deferred = {n.id for grp in self.row_groups for n in grp.deferred}
         group_at = {grp.last_pos: grp for grp in self.row_groups}
+        self.guard_slots = []
+        self.commit_launches = []
+        if fn.nan_guard is not None:
+            n_slots = sum(len(n.inputs) + len(n.outputs) for n in order)
+            self._guard_buf = t.zeros(max(n_slots, 1), dtype=t.int32, device="cuda")
+            self.keep.append(self._guard_buf)
         for i, n in enumerate(order):
             for bi in bucket_wait.get(i, []):
                 self._emit_bucket_wait(bi)
@@ -867,6 +878,8 @@ class StepPlan:
             elif not getattr(n.op, "view_capable", False):
                 self._cur = n
                 n.op.lower(n, self)
+            if fn.nan_guard is not None:
+                self._emit_guard(n)
             for bi in bucket_after.get(i, []):
                 self._emit_allreduce(bi, comm)
         for bi in range(len(self.buckets)):
@@ -876,6 +889,11 @@ class StepPlan:
             self._emit_copy(src, dst)
         for src, dst in self.commits:
             self._emit_copy(src, dst)
+        if fn.nan_guard is not None and self.commits:
+            # updates land only after the guard passed (reference runtime.py:415-421)
+            n_commit = len(self.commits)
+            self.commit_launches = [fn_ for _, fn_ in self.launches[-n_commit:]]
+            del self.launches[-n_commit:]
         self.graph = None
         self.captured = False
         self._pinned_out = None
@@ -1044,6 +1062,52 @@ class StepPlan:
             lib.check(f(A, B, C, epi, mode, ws, wsb, stream))
         self.add_launch(launch)
 
+    def _emit_guard(self, node):
+        """Scan every float input and output of ``node`` (reference
+        diagnostics.py:52-88: inputs first, then outputs)."""
+        from .dtypes import is_float
+        cfg = self.fn.nan_guard
+        mode = cfg.mode()
+        big = float(cfg.big_threshold) if cfg.big_threshold is not None else 0.0
+        lib = self.lib
+        f = lib.lib.tx_check_values
+        base = self._guard_buf.data_ptr()
+        for label, vs in (("input", node.inputs), ("output", node.outputs)):
+            for k, v in enumerate(vs):
+                if not is_float(v.type.dtype):
+                    continue
+                lay = self.lay[v.id] if v.id in self.lay else self._const_layout(v)
+                if lay.numel == 0:
+                    continue
+                slot = len(self.guard_slots)
+                self.guard_slots.append((node, f"{label} {k}", lay))
+                tx = self.tx(lay)
+
+                def launch(stream, tx=tx, slot=slot):
+                    lib.check(f(tx, base, slot, mode, big, stream))
+                self.launches.append((None, launch))
+
+    def check_guard(self, stream):
+        """Read the guard words of the step just run; raise ``NanDetected``
+        for the first flagged tensor in execution order."""
+        from .diagnostics import NanReport, check_name, summarize
+        from .errors import NanDetected
+        self.lib.stream_sync(stream)
+        flags = self._guard_buf.cpu().numpy()
+        hit = np.flatnonzero(flags[: len(self.guard_slots)])
+        if hit.size == 0:
+            return
+        node, label, lay = self.guard_slots[int(hit[0])]
+        arr = _torch_view(lay, self.tx(lay).data).cpu().numpy()
+        trace = next((str(o.trace) for o in node.outputs if getattr(o, "trace", None) is not None), "")
+        raise NanDetected(NanReport(node_id=node.id, op=getattr(node.op, "display_name", node.op.name),
+                                    check=check_name(int(flags[hit[0]])), tensor=label, trace=trace,
+                                    value_summary=summarize(arr)))
+
+    def run_commits(self, stream):
+        for fn_ in self.commit_launches:
+            fn_(stream)
+
     def _emit_allreduce(self, bi, comm):
         lib, cs = self.lib, self.fn._comm_stream
         dt, ptr, count, _ = self.buckets[bi]
@@ -1094,6 +1158,8 @@ class StepPlan:
     def _launch_all(self, stream):
         if self.flag is not None:
             self.lib.memset(self.flag.ptr, 0, 4, stream)
+        if self.guard_slots:
+            self.lib.memset(self._guard_buf.data_ptr(), 0, 4 * len(self.guard_slots), stream)
         for _, fn in self.launches:
             fn(stream)
 
@@ -1121,6 +1187,8 @@ class StepPlan:
         lib = self.lib
         if self.flag is not None:
             lib.memset(self.flag.ptr, 0, 4, stream)
+        if self.guard_slots:
+            lib.memset(self._guard_buf.data_ptr(), 0, 4 * len(self.guard_slots), stream)
         ev = [lib.event_create() for _ in range(2)]
         for node, fn in self.launches:
             lib.event_record(ev[0], stream)

@@ -222,3 +222,39 @@ def test_pipelined_integer_division_by_zero_raises():
     bv[-5] = 0
     with pytest.raises(ZeroDivisionError):
         f(av, bv)
+
+
+# -- NaN guard (reference diagnostics.py:52-88; test_runtime.py:137-153) -------------
+
+def test_nan_guard_failed_call_leaves_shared_untouched():
+    s = T.shared(np.array(10.0), name="s")
+    x = T.vector("x")
+    f = T.compile([x], [T.sum(T.log(x))], updates=[(s, s + 1.0)], preset="none", nan_guard=T.NanGuardConfig())
+    f(np.array([1.0, 2.0]))
+    assert float(s.get_value()) == 11.0
+    from paper_1605_02688_b200.errors import NanDetected
+    with pytest.raises(NanDetected) as e:
+        f(np.array([-1.0, 2.0]))
+    assert float(s.get_value()) == 11.0   # unchanged by the failed call
+    r = e.value.report
+    assert r.check == "nan" and r.op == "log" and r.tensor == "output 0" and "shape (2,)" in r.value_summary
+    f(np.array([3.0, 2.0]))
+    assert float(s.get_value()) == 12.0
+
+
+def test_nan_guard_inf_big_and_inputs():
+    from paper_1605_02688_b200.errors import NanDetected
+    x = T.vector("x", dtype="float32")
+    f = T.compile([x], [T.exp(x) * 2.0], nan_guard=T.NanGuardConfig(big_threshold=1e6))
+    np.testing.assert_allclose(f(np.array([0.0, 1.0], np.float32))[0], [2.0, 2 * np.e], rtol=1e-6)
+    with pytest.raises(NanDetected) as e:
+        f(np.array([20.0, 0.0], np.float32))        # exp(20) = 4.9e8 > 1e6
+    assert e.value.report.check == "big"
+    with pytest.raises(NanDetected) as e:
+        f(np.array([100.0, 0.0], np.float32))       # exp overflows to inf
+    assert e.value.report.check == "inf"
+    with pytest.raises(NanDetected) as e:
+        f(np.array([np.nan, 0.0], np.float32))      # caught at the first node, on its input
+    assert e.value.report.check == "nan" and e.value.report.tensor == "input 0"
+    g = T.compile([x], [T.exp(x)], nan_guard=T.NanGuardConfig(check_inf=False, big_threshold=None))
+    assert np.isinf(g(np.array([100.0], np.float32))[0][0])
