@@ -277,8 +277,13 @@ class CompiledFunction:
         self.pipelined = True
         self.profile_nodes = False
         self._direct, self.order = self._schedule()
-        if self.nan_guard is not None:
-            self._direct = {}   # updates are committed only after the guard passed
+        self.has_lazy = any(getattr(n.op, "lazy", False) for n in self.order)
+        if self.nan_guard is not None or self.has_lazy:
+            self._direct = {}   # updates are committed only after the whole step (guard / lazy walk) finished
+        if self.has_lazy:
+            self.row_fusion = False
+            if self.dp is not None:
+                raise NotSupported("lazy ops (ifelse / breakpoint) in a data-parallel step")
         self.profile._order = tuple(n.id for n in self.order)
         self._events = None
         self.thunks = {}
@@ -426,13 +431,16 @@ class CompiledFunction:
             lib.event_record(self._events[0], cur)
             lib.stream_wait_event(stream, self._events[0])
         plan.upload_inputs(binds, stream)
-        if self.profile_nodes:
+        if self.has_lazy:
+            plan.run_lazy(stream, self.profile)
+        elif self.profile_nodes:
             plan.run_profiled(stream, self.profile)
         else:
             plan.run(stream)
             self.profile._pending += 1
         if plan.guard_slots:
             plan.check_guard(stream)      # raises NanDetected before any update is committed
+        if plan.commit_launches:
             plan.run_commits(stream)
         if device_out:
             outs = plan.device_outputs()
@@ -633,6 +641,11 @@ class StepPlan:
             for o, s in zip(n.outputs, outs):
                 if s is UNKNOWN_SHAPE or any(d is None for d in s):
                     raise NotSupported(f"cannot infer the runtime shape of {o!r} ({n.op.name})")
+            alias = getattr(n.op, "output_aliases", None)
+            if alias is not None:
+                for o, k in zip(n.outputs, alias()):
+                    self.lay[o.id] = ins[k]
+                continue
             if getattr(n.op, "view_capable", False):
                 base = ins[0]
                 shape, strides, off = n.op.view_layout(n, [(base.shape, base.strides, base.offset)])
@@ -756,7 +769,7 @@ class StepPlan:
             if getattr(n.op, "view_capable", False):
                 continue
             taken = set()
-            inplace_ok = isinstance(n.op, (Elemwise, Composite)) and fn.nan_guard is None
+            inplace_ok = isinstance(n.op, (Elemwise, Composite)) and fn.nan_guard is None and not fn.has_lazy
             for o in n.outputs:
                 ol = self.lay[o.id]
                 st = ol.storage
@@ -786,7 +799,9 @@ class StepPlan:
                 w[0].offset = alloc.alloc(w[1])
                 alloc.release(w[0].offset, w[1])
             for st in live_at.pop(i, []):
-                if fn.nan_guard is None:   # a guarded step keeps every value for its report
+                if fn.nan_guard is None and not fn.has_lazy:
+                    # a guarded step keeps every value for its report; a lazy
+                    # walk runs nodes out of schedule order
                     alloc.release(st.offset, st.nbytes)
         for src, dst in self.tail_copies:
             assign(dst.storage)
@@ -856,6 +871,7 @@ class StepPlan:
         group_at = {grp.last_pos: grp for grp in self.row_groups}
         self.guard_slots = []
         self.commit_launches = []
+        self.lazy_copies = {}
         if fn.nan_guard is not None:
             n_slots = sum(len(n.inputs) + len(n.outputs) for n in order)
             self._guard_buf = t.zeros(max(n_slots, 1), dtype=t.int32, device="cuda")
@@ -889,7 +905,7 @@ class StepPlan:
             self._emit_copy(src, dst)
         for src, dst in self.commits:
             self._emit_copy(src, dst)
-        if fn.nan_guard is not None and self.commits:
+        if (fn.nan_guard is not None or fn.has_lazy) and self.commits:
             # updates land only after the guard passed (reference runtime.py:415-421)
             n_commit = len(self.commits)
             self.commit_launches = [fn_ for _, fn_ in self.launches[-n_commit:]]
@@ -1086,6 +1102,78 @@ class StepPlan:
                 def launch(stream, tx=tx, slot=slot):
                     lib.check(f(tx, base, slot, mode, big, stream))
                 self.launches.append((None, launch))
+
+    def copy_launch(self, src: Layout, dst: Layout):
+        lib = self.lib
+        s, d = self.tx(src), self.tx(dst)
+
+        def launch(stream):
+            lib.copy(s, d, stream)
+        return launch
+
+    def host_copy(self, lay: Layout, stream) -> np.ndarray:
+        """Synchronous device->host copy of one value of the running step."""
+        self.lib.stream_sync(stream)
+        arr = _torch_view(lay, self.tx(lay).data).cpu().numpy()
+        return arr.astype(np.bool_) if lay.dtype == "bool" else arr
+
+    def run_lazy(self, stream, profile):
+        """Demand-driven walk (reference runtime.py:448-499): only the nodes
+        the outputs need through the taken branches run; conditions are read
+        on the host when an ifelse / breakpoint needs them."""
+        from .control import Breakpoint, IfElse, read_scalar
+        fn = self.fn
+        g = fn.fgraph
+        by_node = {}
+        tail = []
+        for node, launch in self.launches:
+            if node is None:
+                tail.append(launch)
+            else:
+                by_node.setdefault(node.id, []).append(launch)
+        if self.flag is not None:
+            self.lib.memset(self.flag.ptr, 0, 4, stream)
+        if self.guard_slots:
+            self.lib.memset(self._guard_buf.data_ptr(), 0, 4 * len(self.guard_slots), stream)
+        avail = {v.id for v in g.inputs}
+        for target in g.outputs:
+            stack = [target]
+            while stack:
+                v = stack[-1]
+                if v.id in avail or isinstance(v, Constant):
+                    stack.pop()
+                    continue
+                node = v.owner
+                if isinstance(node.op, IfElse):
+                    cond = node.inputs[0]
+                    if cond.id not in avail and not isinstance(cond, Constant):
+                        stack.append(cond)
+                        continue
+                    pick = 1 if bool(read_scalar(self, cond, stream)) else 2
+                    branch = node.inputs[pick]
+                    if branch.id not in avail and not isinstance(branch, Constant):
+                        stack.append(branch)
+                        continue
+                    self.lazy_copies[node.id][pick - 1](stream)
+                else:
+                    missing = [x for x in node.inputs if x.id not in avail and not isinstance(x, Constant)]
+                    if missing:
+                        stack.extend(missing)
+                        continue
+                    for launch in by_node.get(node.id, ()):
+                        launch(stream)
+                    if isinstance(node.op, Breakpoint):
+                        cv = read_scalar(self, node.inputs[0], stream)
+                        if bool(cv):
+                            mon = [self.host_copy(self.lay[x.id] if x.id in self.lay else self._const_layout(x),
+                                                  stream) for x in node.inputs[1:]]
+                            node.op.fire(cv, mon)
+                for o in node.outputs:
+                    avail.add(o.id)
+                profile.node_calls[node.id] = profile.node_calls.get(node.id, 0) + 1
+                stack.pop()
+        for launch in tail:
+            launch(stream)
 
     def check_guard(self, stream):
         """Read the guard words of the step just run; raise ``NanDetected``

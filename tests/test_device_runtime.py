@@ -258,3 +258,81 @@ def test_nan_guard_inf_big_and_inputs():
     assert e.value.report.check == "nan" and e.value.report.tensor == "input 0"
     g = T.compile([x], [T.exp(x)], nan_guard=T.NanGuardConfig(check_inf=False, big_threshold=None))
     assert np.isinf(g(np.array([100.0], np.float32))[0][0])
+
+
+# -- lazy conditional and breakpoint (reference test_runtime.py:84-131, test_ops.py:295-349) --
+
+def _lazy_fixture():
+    c, p = T.scalar("c"), T.vector("p")
+    expensive = T.exp(T.sqr(p)) * 3.0
+    cheap = p + 1.0
+    out = T.ifelse(c > 0.0, T.sum(expensive), T.sum(cheap))
+    f = T.compile([c, p], [out], preset="none")
+    roots = {True: next(n for n in f.order if getattr(n.op, "kernel", "") == "exp"),
+             False: next(n for n in f.order if getattr(n.op, "kernel", "") == "add")}
+    return f, roots
+
+
+def test_ifelse_untaken_branch_never_runs(rng):
+    f, roots = _lazy_fixture()
+    point = rng.standard_normal(4)
+    np.testing.assert_allclose(f(-1.0, point)[0], np.sum(point + 1.0), rtol=1e-12)
+    assert f.profile.node_calls.get(roots[True].id, 0) == 0
+    assert f.profile.node_calls.get(roots[False].id, 0) == 1
+    np.testing.assert_allclose(f(1.0, point)[0], np.sum(np.exp(point ** 2) * 3.0), rtol=1e-12)
+    assert f.profile.node_calls.get(roots[True].id, 0) == 1
+
+
+def test_ifelse_randomized_conditions_and_values(rng):
+    f, roots = _lazy_fixture()
+    taken = 0
+    for _ in range(30):
+        c = float(rng.standard_normal())
+        before = f.profile.node_calls.get(roots[True].id, 0)
+        f(c, rng.standard_normal(4))
+        assert f.profile.node_calls.get(roots[True].id, 0) - before == (1 if c > 0 else 0)
+        taken += c > 0
+    assert 0 < taken < 30
+    c, a, b = T.scalar("c"), T.vector("a"), T.vector("b")
+    g = T.compile([c, a, b], [T.ifelse(c > 0.0, a * 2.0, b * 3.0)], preset="none")
+    av, bv = rng.standard_normal(3), rng.standard_normal(3)
+    np.testing.assert_array_equal(g(1.0, av, bv)[0], av * 2.0)
+    np.testing.assert_array_equal(g(-1.0, av, bv)[0], bv * 3.0)
+
+
+def test_ifelse_gradient_and_updates(rng):
+    c, x = T.scalar("c"), T.vector("x")
+    w = T.shared(np.array([1.0, 2.0, 3.0]), name="w")
+    y = T.ifelse(c > 0.0, T.sum(w * x), T.sum(w * w))
+    gw = T.grad(y, w)
+    f = T.compile([c, x], [y, gw], updates=[(w, w - 0.1 * gw)])
+    xv = np.array([0.5, -1.0, 2.0])
+    yv, gv = f(1.0, xv)
+    assert float(yv) == pytest.approx(float(np.dot([1.0, 2.0, 3.0], xv)))
+    np.testing.assert_allclose(gv, xv)
+    np.testing.assert_allclose(w.get_value(), np.array([1.0, 2.0, 3.0]) - 0.1 * xv)
+
+
+def test_breakpoint_fires_passes_through_and_aborts():
+    from paper_1605_02688_b200.errors import BreakpointAbort
+    calls = []
+    T.register_breakpoint_handler("d1", lambda names, values: calls.append((names, [v.copy() for v in values])))
+    x = T.vector("x")
+    (mon,) = T.breakpoint_op(T.max(T.isnan(x)), [x], label="d1")
+    f = T.compile([x], [mon], preset="none")
+    np.testing.assert_array_equal(f(np.array([1.0, 2.0]))[0], [1.0, 2.0])
+    assert calls == []
+    v = np.array([1.0, np.nan, 3.0])
+    np.testing.assert_array_equal(f(v)[0], v)
+    assert len(calls) == 1 and np.array_equal(calls[0][1][0], v, equal_nan=True)
+    T.register_breakpoint_handler("d1", None)
+    s = T.shared(np.array(0.0), name="s")
+    T.register_breakpoint_handler("d3", lambda names, values: "abort")
+    y = T.scalar("y")
+    (m2,) = T.breakpoint_op(y > 0.0, [y], label="d3")
+    g = T.compile([y], [m2], updates=[(s, s + 1.0)], preset="none")
+    assert float(g(-1.0)[0]) == -1.0 and float(s.get_value()) == 1.0
+    with pytest.raises(BreakpointAbort):
+        g(1.0)
+    assert float(s.get_value()) == 1.0      # aborted call committed nothing
+    T.register_breakpoint_handler("d3", None)
