@@ -118,6 +118,14 @@ int tx_kernel_destroy(void* kernel);
  * Replaces Sum/Max/ArgmaxOnehot.perform (reference ops/reductions.py:87-188)
  * and adds an index argmax.  axes_mask bit i = reduce dim i. */
 enum { TX_SUM = 0, TX_MAX = 1, TX_ARGMAX_ONEHOT = 2, TX_ARGMAX_INDEX = 3 };
+/* 2-d convolution data movement (reference ops/conv.py:108-157); `win` =
+ * {kh, kw, stride_h, stride_w, pad_h, pad_w}.  tx_im2col: x[N,C,H,W] (any
+ * strides) -> cols[N*Ho*Wo, C*kh*kw] row-major, zero padding.  tx_col2im:
+ * dcols -> dx[N,C,H,W] contiguous, each element the sum of its taps in
+ * (u, v) order (deterministic).  The contractions are tx_gemm calls. */
+int tx_im2col(const tx_tensor* x, tx_tensor* cols, const int* win, void* stream);
+int tx_col2im(const tx_tensor* dcols, tx_tensor* dx, const int* win, int64_t Ho, int64_t Wo, void* stream);
+
 /* NaN guard (reference diagnostics.py:52-88 nan_guard_check, hooked per node
  * at runtime.py:359-367): scan one float tensor and OR into flags[slot]
  * bit 1 if it holds a NaN, bit 2 an infinity, bit 4 a finite value with

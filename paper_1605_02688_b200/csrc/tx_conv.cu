@@ -1,0 +1,132 @@
+// 2-d convolution data movement for the im2col -> tcgen05 GEMM lowering of
+// the reference's conv2d trio (pkg/src/texpr/ops/conv.py:108-157):
+//   tx_im2col  x[N,C,H,W] (any strides) -> cols[N*Ho*Wo, C*kh*kw] (row-major),
+//              zero outside the padded input (ops/conv.py:108-119)
+//   tx_col2im  dcols[N*Ho*Wo, C*kh*kw] -> dx[N,C,H,W]: the transpose, as a
+//              gather per input element summing its (u, v) taps in ascending
+//              order -- the same order as the reference's scatter loop
+//              (ops/conv.py:142-155), so no atomics and a deterministic sum.
+// The contractions themselves are tx_gemm calls (tensor cores for fp32).
+#include <cuda_runtime.h>
+
+#include "tx_common.h"
+
+namespace tx {
+namespace {
+
+struct ConvGeom {
+  int64_t N, C, H, W, Ho, Wo;
+  int kh, kw, sh, sw, ph, pw;
+  int64_t xs[4];  // input strides (elements)
+};
+
+template <class T>
+__global__ void im2col_kernel(const T* __restrict__ x, T* __restrict__ cols, ConvGeom g, int64_t total) {
+  const int64_t ckk = g.C * g.kh * g.kw;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = e / ckk, col = e - row * ckk;
+    const int64_t n = row / (g.Ho * g.Wo), p = row - n * (g.Ho * g.Wo);
+    const int64_t i = p / g.Wo, j = p - i * g.Wo;
+    const int64_t c = col / (g.kh * g.kw), r = col - c * (g.kh * g.kw);
+    const int u = (int)(r / g.kw), v = (int)(r - (int64_t)u * g.kw);
+    const int64_t h = i * g.sh - g.ph + u, w = j * g.sw - g.pw + v;
+    T val = T(0);
+    if (h >= 0 && h < g.H && w >= 0 && w < g.W) val = x[n * g.xs[0] + c * g.xs[1] + h * g.xs[2] + w * g.xs[3]];
+    cols[e] = val;
+  }
+}
+
+template <class T>
+__global__ void col2im_kernel(const T* __restrict__ dcols, T* __restrict__ dx, ConvGeom g, int64_t total) {
+  const int64_t ckk = g.C * g.kh * g.kw;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t t = e;
+    const int64_t w = t % g.W; t /= g.W;
+    const int64_t h = t % g.H; t /= g.H;
+    const int64_t c = t % g.C;
+    const int64_t n = t / g.C;
+    T acc = T(0);
+    for (int u = 0; u < g.kh; ++u) {
+      const int64_t hi = h + g.ph - u;
+      if (hi < 0 || hi % g.sh) continue;
+      const int64_t i = hi / g.sh;
+      if (i >= g.Ho) continue;
+      for (int v = 0; v < g.kw; ++v) {
+        const int64_t wi = w + g.pw - v;
+        if (wi < 0 || wi % g.sw) continue;
+        const int64_t j = wi / g.sw;
+        if (j >= g.Wo) continue;
+        acc += dcols[((n * g.Ho + i) * g.Wo + j) * ckk + (c * g.kh + u) * g.kw + v];
+      }
+    }
+    dx[e] = acc;
+  }
+}
+
+int geom(const tx_tensor* x4, const int* win, int64_t Ho, int64_t Wo, ConvGeom* g) {
+  TX_CHECK(x4->ndim == 4, TX_E_ARG, "conv: rank-4 tensors expected");
+  g->N = x4->shape[0]; g->C = x4->shape[1]; g->H = x4->shape[2]; g->W = x4->shape[3];
+  g->kh = win[0]; g->kw = win[1]; g->sh = win[2]; g->sw = win[3]; g->ph = win[4]; g->pw = win[5];
+  TX_CHECK(g->sh > 0 && g->sw > 0 && g->kh > 0 && g->kw > 0, TX_E_ARG, "conv: bad window");
+  g->Ho = Ho; g->Wo = Wo;
+  for (int i = 0; i < 4; ++i) g->xs[i] = x4->strides[i];
+  return TX_OK;
+}
+
+int64_t grid_for(int64_t n) {
+  int64_t b = (n + 255) / 256;
+  const int64_t cap = (int64_t)sm_count() * 16;
+  return b < cap ? (b < 1 ? 1 : b) : cap;
+}
+
+}  // namespace
+}  // namespace tx
+
+using namespace tx;
+
+extern "C" {
+
+int tx_im2col(const tx_tensor* x, tx_tensor* cols, const int* win, void* stream) {
+  TX_CHECK(x && cols && win && x->dtype == cols->dtype, TX_E_ARG, "tx_im2col: bad arguments");
+  TX_CHECK(cols->ndim == 2 && is_contiguous(*cols), TX_E_ARG, "tx_im2col: cols must be contiguous [rows, C*kh*kw]");
+  ConvGeom g;
+  const int64_t Ho = (x->shape[2] + 2 * win[4] - win[0]) / win[2] + 1;
+  const int64_t Wo = (x->shape[3] + 2 * win[5] - win[1]) / win[3] + 1;
+  int rc = geom(x, win, Ho, Wo, &g);
+  if (rc) return rc;
+  TX_CHECK(cols->shape[0] == g.N * Ho * Wo && cols->shape[1] == g.C * g.kh * g.kw, TX_E_ARG, "tx_im2col: cols shape");
+  const int64_t total = numel(*cols);
+  if (total == 0) return TX_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (x->dtype == TX_F32)
+    im2col_kernel<float><<<(unsigned)grid_for(total), 256, 0, st>>>((const float*)x->data, (float*)cols->data, g, total);
+  else if (x->dtype == TX_F64)
+    im2col_kernel<double><<<(unsigned)grid_for(total), 256, 0, st>>>((const double*)x->data, (double*)cols->data, g, total);
+  else
+    return fail(TX_E_UNSUPPORTED, "tx_im2col: float32/float64 only");
+  TX_CUDA(cudaGetLastError());
+  return TX_OK;
+}
+
+int tx_col2im(const tx_tensor* dcols, tx_tensor* dx, const int* win, int64_t Ho, int64_t Wo, void* stream) {
+  TX_CHECK(dcols && dx && win && dx->dtype == dcols->dtype, TX_E_ARG, "tx_col2im: bad arguments");
+  TX_CHECK(is_contiguous(*dx) && is_contiguous(*dcols), TX_E_ARG, "tx_col2im: contiguous operands expected");
+  ConvGeom g;
+  int rc = geom(dx, win, Ho, Wo, &g);
+  if (rc) return rc;
+  TX_CHECK(dcols->ndim == 2 && dcols->shape[0] == g.N * Ho * Wo && dcols->shape[1] == g.C * g.kh * g.kw, TX_E_ARG,
+           "tx_col2im: dcols shape");
+  const int64_t total = numel(*dx);
+  if (total == 0) return TX_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dx->dtype == TX_F32)
+    col2im_kernel<float><<<(unsigned)grid_for(total), 256, 0, st>>>((const float*)dcols->data, (float*)dx->data, g, total);
+  else if (dx->dtype == TX_F64)
+    col2im_kernel<double><<<(unsigned)grid_for(total), 256, 0, st>>>((const double*)dcols->data, (double*)dx->data, g, total);
+  else
+    return fail(TX_E_UNSUPPORTED, "tx_col2im: float32/float64 only");
+  TX_CUDA(cudaGetLastError());
+  return TX_OK;
+}
+
+}  // extern "C"

@@ -11,8 +11,9 @@ from .graph import Variable
 from .linalg import Dot, dot  # noqa: F401
 from .op import DISCONNECTED, OP_REGISTRY, UNKNOWN_SHAPE, Op, op_from_payload, register_op  # noqa: F401
 from .reduce import Argmax, ArgmaxOnehot, Max, Sum, argmax, argmax_onehot, max, sum  # noqa: F401
-from .shaping import (DimShuffle, IncSubtensor, Join, Subtensor, dimshuffle, flip0, inc_subtensor,  # noqa: F401
-                      join, subtensor, transpose)
+from .shaping import (DimShuffle, IncSubtensor, Join, Reshape, ShapeOf, Subtensor, dimshuffle, flip0,  # noqa: F401
+                      inc_subtensor, join, reshape, shape_of, subtensor, transpose)
+from .conv import Conv2d, conv2d  # noqa: F401
 
 
 def _binary(kernel):

@@ -211,7 +211,7 @@ def select_rewrites(preset, include=(), exclude=()):
 
 
 def run_preset(fgraph: FunctionGraph, preset="fast_run", include=(), exclude=(), ctx=None):
-    from . import fusion, scan  # noqa: F401  (register the device and loop passes)
+    from . import conv, fusion, scan  # noqa: F401  (register the device, loop and convolution passes)
     ctx = ctx or RewriteContext()
     log = RewriteLog()
     chosen = select_rewrites(preset, include, exclude)

@@ -415,3 +415,134 @@ class Join(Op):
 
 def join(axis: int, *tensors: Variable) -> Variable:
     return apply(Join(axis), list(tensors))[0]
+
+
+# ---------------------------------------------------------------------------
+# Runtime shape vectors and reshape (reference ``ops/shaping.py:281-378``).
+# Step plans know every shape before launching, so a ``shape_of`` value is a
+# plan-time constant (uploaded once per plan) and ops that take shape vectors
+# (reshape, the convolution gradients) read it at planning time.
+
+@register_op
+class ShapeOf(Op):
+    """Runtime shape of a tensor as an int64 vector of static length."""
+
+    name = "shape_of"
+    plan_value = True
+
+    def infer_types(self, input_types):
+        (t,) = input_types
+        return [TensorType("int64", (t.ndim == 1,))]
+
+    def infer_shape(self, node, input_shapes):
+        return [(node.inputs[0].type.ndim,)]
+
+    def value(self, node, input_shapes):
+        return np.asarray(input_shapes[0], dtype=np.int64)
+
+    def grad(self, inputs, output_grads):
+        return [DISCONNECTED]
+
+    def rop(self, inputs, input_perturbations):
+        return [None]
+
+    def lower(self, node, plan):
+        from .graph import Constant
+        c = Constant(plan.values[node.outputs[0].id], dtype="int64")
+        plan.emit_copy_layouts(plan._const_layout(c), plan.layout(node.outputs[0]))
+
+
+def shape_of(x: Variable) -> Variable:
+    return apply(ShapeOf(), [x])[0]
+
+
+def _shape_arg(node, k, values):
+    from .graph import Constant
+    v = node.inputs[k]
+    if isinstance(v, Constant):
+        return tuple(int(s) for s in v.value)
+    if values is not None and v.id in values:
+        return tuple(int(s) for s in values[v.id])
+    return None
+
+
+@register_op
+class Reshape(Op):
+    """Reshape against a shape vector; the output rank is static."""
+
+    name = "reshape"
+    uses_values = True
+
+    def __init__(self, ndim: int):
+        self.ndim = int(ndim)
+
+    @property
+    def display_name(self):
+        return f"reshape{{{self.ndim}}}"
+
+    def attrs_key(self):
+        return (self.ndim,)
+
+    def infer_types(self, input_types):
+        x, shp = input_types
+        if shp.ndim != 1 or shp.dtype not in ("int32", "int64"):
+            raise TypeMismatch("reshape expects a 1-d integer shape vector")
+        return [TensorType(x.dtype, (False,) * self.ndim)]
+
+    def infer_shape(self, node, input_shapes, values=None):
+        from .errors import ShapeMismatch
+        dims = _shape_arg(node, 1, values)
+        if dims is None:
+            return [(None,) * self.ndim]
+        xs = input_shapes[0]
+        if xs is UNKNOWN_SHAPE or any(d is None for d in xs):
+            return [dims if -1 not in dims else (None,) * self.ndim]
+        total = int(np.prod(xs, dtype=np.int64))
+        if dims.count(-1) == 1:
+            known = int(np.prod([d for d in dims if d != -1], dtype=np.int64))
+            if known == 0 or total % known:
+                raise ShapeMismatch(f"reshape: cannot reshape {tuple(xs)} to {dims}")
+            dims = tuple(total // known if d == -1 else d for d in dims)
+        if len(dims) != self.ndim or int(np.prod(dims, dtype=np.int64)) != total:
+            raise ShapeMismatch(f"reshape: cannot reshape {tuple(xs)} to {dims}")
+        return [dims]
+
+    def grad(self, inputs, output_grads):
+        x, _ = inputs
+        (v,) = output_grads
+        if not is_float(x.type.dtype):
+            return [DISCONNECTED, DISCONNECTED]
+        return [reshape(v, shape_of(x), ndim=x.type.ndim), DISCONNECTED]
+
+    def rop(self, inputs, input_perturbations):
+        dx, _ = input_perturbations
+        return [None if dx is None else reshape(dx, inputs[1], ndim=self.ndim)]
+
+    def lower(self, node, plan):
+        from .vm import contiguous_strides
+        lx, lo = plan.layout(node.inputs[0]), plan.layout(node.outputs[0])
+        if lo.numel == 0:
+            return
+        if not lx.contiguous():
+            tmp = plan.scratch(lx.shape, lx.dtype)
+            plan.emit_copy_layouts(lx, tmp)
+            lx = tmp
+        src = plan.view_of(lx, lo.shape, contiguous_strides(lo.shape), lx.offset)
+        plan.emit_copy_layouts(src, lo)
+
+    def attrs_payload(self, encode_graph=None):
+        return {"ndim": self.ndim}
+
+    @classmethod
+    def from_payload(cls, payload, decode_graph=None):
+        return cls(payload["ndim"])
+
+
+def reshape(x: Variable, shape, ndim: int | None = None) -> Variable:
+    from .graph import as_variable
+    if isinstance(shape, (tuple, list)):
+        ndim = len(shape)
+        shape = as_variable(np.asarray(shape, dtype=np.int64))
+    elif ndim is None:
+        raise TypeMismatch("reshape with a symbolic shape needs an explicit ndim")
+    return apply(Reshape(ndim), [x, shape])[0]

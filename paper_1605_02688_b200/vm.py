@@ -635,9 +635,14 @@ class StepPlan:
             if getattr(n.op, "name", "") == "scan":
                 n.op.check_runtime_shapes(n, shapes, self.values)
                 outs = n.op.infer_shape(n, shapes, self.values)
+            elif getattr(n.op, "uses_values", False):
+                n.op.check_runtime_shapes(n, shapes)
+                outs = n.op.infer_shape(n, shapes, self.values)
             else:
                 n.op.check_runtime_shapes(n, shapes)
                 outs = n.op.infer_shape(n, shapes)
+            if getattr(n.op, "plan_value", False):
+                self.values[n.outputs[0].id] = n.op.value(n, shapes)
             for o, s in zip(n.outputs, outs):
                 if s is UNKNOWN_SHAPE or any(d is None for d in s):
                     raise NotSupported(f"cannot infer the runtime shape of {o!r} ({n.op.name})")
@@ -994,6 +999,26 @@ class StepPlan:
 
         def launch(stream):
             lib.copy(s, d, stream)
+        self.add_launch(launch)
+
+    def emit_gemm(self, a: Layout, b: Layout, c: Layout, mode=None):
+        """C = A . B over explicit (possibly strided) layouts, with its own
+        step-lifetime workspace (convolution lowering)."""
+        lib = self.lib
+        A, B, C = self.tx(a), self.tx(b), self.tx(c)
+        mode = self.fn.gemm_mode if mode is None else mode
+        wsb = lib.gemm_workspace(A, B, C, mode)
+        ws = None
+        if wsb:
+            t = _torch()
+            buf = t.empty(wsb, dtype=t.uint8, device="cuda")
+            self.keep.append(buf)
+            ws = buf.data_ptr()
+        epi = native.TxEpilogue()
+        f = lib.lib.tx_gemm
+
+        def launch(stream):
+            lib.check(f(A, B, C, epi, mode, ws, wsb, stream))
         self.add_launch(launch)
 
     def emit_elementwise_tx(self, program: EwProgram, outs, ins):

@@ -1,0 +1,74 @@
+"""2-d convolution trio on the device (im2col -> tensor-core GEMM, col2im
+gather) against the REAL reference's outputs (tests/golden/make_conv_golden.py)
+and NumPy, plus reshape / shape_of and the implementation-selection rules
+(reference ops/conv.py, rewrites/convselect.py)."""
+import os
+import sys
+
+import numpy as np
+import pytest
+
+import paper_1605_02688_b200 as T
+from paper_1605_02688_b200.errors import AbstractOpRemaining, ShapeMismatch
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+sys.path.insert(0, GOLD)
+from make_conv_golden import CASES, case_inputs  # noqa: E402
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(np.asarray(a, np.float64) - b) / max(np.linalg.norm(np.asarray(b, np.float64)), 1e-30))
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
+@pytest.mark.parametrize("impl", ["gemm", "reference"])
+def test_conv_trio_matches_reference(case, impl):
+    g = np.load(os.path.join(GOLD, "ref_conv_goldens.npz"))
+    name, dt, xs, fs, st, pd, seed = case
+    x, f, _ = case_inputs(dt, xs, fs, seed)
+    vx, vf = T.tensor4("x", dtype=dt), T.tensor4("f", dtype=dt)
+    y = T.conv2d(vx, vf, stride=st, pad=pd)
+    w = T.as_variable(g[f"{name}_w"])
+    gx, gf = T.grad(T.sum(y * w), [vx, vf])
+    fn = T.compile([vx, vf], [y, gx, gf], conv_impl=impl)
+    assert all(n.op.algo == impl for n in fn.order if n.op.name == "conv2d")
+    # float64 and exact-fp32 ("reference") are tight; fp32 "gemm" runs TF32 tensor cores
+    tol = 1e-12 if dt == "float64" else (1e-6 if impl == "reference" else 3e-3)
+    for got, k in zip(fn(x, f), ("y", "gx", "gf")):
+        assert got.shape == g[f"{name}_{k}"].shape
+        assert _rel(got, g[f"{name}_{k}"]) <= tol, (k, _rel(got, g[f"{name}_{k}"]))
+
+
+def test_conv_forward_numpy_oracle_and_errors(rng):
+    x = rng.standard_normal((3, 4, 11, 9)).astype(np.float32)
+    f = rng.standard_normal((6, 4, 3, 3)).astype(np.float32)
+    vx, vf = T.tensor4("x", dtype="float32"), T.tensor4("f", dtype="float32")
+    (y,) = T.compile([vx, vf], [T.conv2d(vx, vf, stride=(2, 2), pad=(1, 1))], conv_impl="reference")(x, f)
+    xp = np.pad(x.astype(np.float64), ((0, 0), (0, 0), (1, 1), (1, 1)))
+    want = np.zeros((3, 6, 6, 5))
+    for i in range(6):
+        for j in range(5):
+            win = xp[:, :, 2 * i: 2 * i + 3, 2 * j: 2 * j + 3]
+            want[:, :, i, j] = np.einsum("nchw,kchw->nk", win, f.astype(np.float64))
+    assert _rel(y, want) <= 1e-6
+    with pytest.raises(AbstractOpRemaining):
+        T.compile([vx, vf], [T.conv2d(vx, vf)], conv_impl="none")(x, f)
+    with pytest.raises(ShapeMismatch):
+        T.compile([vx, vf], [T.conv2d(vx, vf)])(x, rng.standard_normal((6, 5, 3, 3)).astype(np.float32))
+
+
+def test_reshape_and_shape_of(rng):
+    x = T.tensor3("x", dtype="float32")
+    r = T.reshape(x, (4, -1))
+    s = T.shape_of(x)
+    g = T.grad(T.sum(r * r), x)
+    fn = T.compile([x], [r, s, g])
+    xv = rng.standard_normal((2, 4, 3)).astype(np.float32)
+    rv, sv, gv = fn(xv)
+    np.testing.assert_array_equal(rv, xv.reshape(4, 6))
+    np.testing.assert_array_equal(sv, [2, 4, 3])
+    np.testing.assert_array_equal(gv, 2 * xv)
+    xt = T.transpose(T.matrix("m", dtype="float32"))
+    (tv,) = T.compile([xt.owner.inputs[0]], [T.reshape(xt, (-1,))])(np.arange(6, dtype=np.float32).reshape(2, 3))
+    np.testing.assert_array_equal(tv, np.arange(6).reshape(2, 3).T.reshape(-1))
