@@ -155,13 +155,16 @@ enum {
  *   BIAS_TANH       C = tanh(b[n] + acc)
  *   MUL_1MSQR       C = acc * (1 - h^2)
  *   BIAS_TANH_DUAL  C = tanh(b[n] + acc), C2 = 1 - C^2       the MLP forward composite
- *   MUL_AUX         C = acc * g[m,n]                        mul(dot, g) in the backward */
+ *   MUL_AUX         C = acc * g[m,n]                        mul(dot, g) in the backward
+ *   SGD             C = w[m,n] - alpha * acc                sub(w, mul(lr, dot)): the SGD update of a
+ *                                                           weight from its gradient GEMM (C may alias w) */
 enum { TX_EPI_NONE = 0, TX_EPI_BIAS = 1, TX_EPI_BIAS_TANH = 2, TX_EPI_MUL_1MSQR = 3, TX_EPI_BIAS_TANH_DUAL = 4,
-       TX_EPI_MUL_AUX = 5 };
+       TX_EPI_MUL_AUX = 5, TX_EPI_SGD = 6 };
 typedef struct tx_epilogue {
   int32_t kind;
-  tx_tensor aux;  /* BIAS*: bias row [N]; MUL_*: [M,N] operand */
+  tx_tensor aux;  /* BIAS*: bias row [N]; MUL_* / SGD: [M,N] operand */
   tx_tensor out2; /* BIAS_TANH_DUAL: second output [M,N] */
+  double alpha;   /* SGD: the learning rate */
 } tx_epilogue;
 int tx_gemm_workspace(const tx_tensor* A, const tx_tensor* B, const tx_tensor* C, int mode,
                       size_t* bytes);

@@ -32,9 +32,9 @@ int build(const tx_tensor* A, const tx_tensor* B, const tx_tensor* C, const tx_e
   g->scn = C->shape[1] == 1 ? 1 : C->strides[1];
   if (epi && epi->kind != TX_EPI_NONE) {
     TX_CHECK(epi->aux.dtype == A->dtype, TX_E_ARG, "tx_gemm: epilogue operand dtype");
-    TX_CHECK(epi->kind >= TX_EPI_BIAS && epi->kind <= TX_EPI_MUL_AUX, TX_E_ARG, "tx_gemm: unknown epilogue");
+    TX_CHECK(epi->kind >= TX_EPI_BIAS && epi->kind <= TX_EPI_SGD, TX_E_ARG, "tx_gemm: unknown epilogue");
     int64_t s0 = 0, s1 = 0;
-    if (epi->kind == TX_EPI_MUL_1MSQR || epi->kind == TX_EPI_MUL_AUX) {
+    if (epi->kind == TX_EPI_MUL_1MSQR || epi->kind == TX_EPI_MUL_AUX || epi->kind == TX_EPI_SGD) {
       TX_CHECK(epi->aux.ndim == 2 && epi->aux.shape[0] == g->M && epi->aux.shape[1] == g->N, TX_E_ARG,
                "tx_gemm: epilogue operand must be [M,N]");
       s0 = epi->aux.strides[0];
@@ -54,6 +54,8 @@ int build(const tx_tensor* A, const tx_tensor* B, const tx_tensor* C, const tx_e
       g->epi_f.o1 = g->epi_d.o1 = o.strides[1];
     }
     g->epi_f.kind = g->epi_d.kind = epi->kind;
+    g->epi_f.alpha = (float)epi->alpha;
+    g->epi_d.alpha = epi->alpha;
     g->epi_f.aux = (const float*)epi->aux.data;
     g->epi_d.aux = (const double*)epi->aux.data;
     g->epi_f.s0 = g->epi_d.s0 = s0;

@@ -19,6 +19,7 @@ struct Epi {
   int64_t s0 = 0, s1 = 0;  // aux strides (bias: s1 only)
   T* out2 = nullptr;
   int64_t o0 = 0, o1 = 0;  // out2 strides
+  T alpha = T(0);          // SGD learning rate
   __device__ __forceinline__ T apply(T acc, int64_t m, int64_t n) const;
 };
 
@@ -37,6 +38,7 @@ __device__ __forceinline__ float Epi<float>::apply(float acc, int64_t m, int64_t
       return h;
     }
     case TX_EPI_MUL_AUX: return __fmul_rn(acc, aux[m * s0 + n * s1]);
+    case TX_EPI_SGD: return __fsub_rn(aux[m * s0 + n * s1], __fmul_rn(alpha, acc));
   }
   return acc;
 }
@@ -56,6 +58,7 @@ __device__ __forceinline__ double Epi<double>::apply(double acc, int64_t m, int6
       return h;
     }
     case TX_EPI_MUL_AUX: return __dmul_rn(acc, aux[m * s0 + n * s1]);
+    case TX_EPI_SGD: return __dsub_rn(aux[m * s0 + n * s1], __dmul_rn(alpha, acc));
   }
   return acc;
 }

@@ -411,7 +411,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     uint32_t xphase = 0;
     const Epi<float>& E = p.epi;
     const bool vec_ok = (p.ldc % 4 == 0) && (((uintptr_t)p.C & 15) == 0) &&
-                        ((E.kind != TX_EPI_MUL_AUX && E.kind != TX_EPI_MUL_1MSQR) ||
+                        ((E.kind != TX_EPI_MUL_AUX && E.kind != TX_EPI_MUL_1MSQR && E.kind != TX_EPI_SGD) ||
                          (E.s1 == 1 && E.s0 % 4 == 0 && ((uintptr_t)E.aux & 15) == 0)) &&
                         (E.kind != TX_EPI_BIAS_TANH_DUAL || (E.o1 == 1 && E.o0 % 4 == 0 && ((uintptr_t)E.out2 & 15) == 0)) &&
                         (E.kind != TX_EPI_BIAS && E.kind != TX_EPI_BIAS_TANH && E.kind != TX_EPI_BIAS_TANH_DUAL ||
@@ -469,6 +469,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               xphase ^= 1;
               const float4* xrow = reinterpret_cast<const float4*>(xstg + lane * 32);
               const bool sq = E.kind == TX_EPI_MUL_1MSQR;
+              if (E.kind == TX_EPI_SGD) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                  const float4 w4 = xrow[j ^ (lane & 7)];
+                  v[4 * j] = __fsub_rn(w4.x, __fmul_rn(E.alpha, v[4 * j]));
+                  v[4 * j + 1] = __fsub_rn(w4.y, __fmul_rn(E.alpha, v[4 * j + 1]));
+                  v[4 * j + 2] = __fsub_rn(w4.z, __fmul_rn(E.alpha, v[4 * j + 2]));
+                  v[4 * j + 3] = __fsub_rn(w4.w, __fmul_rn(E.alpha, v[4 * j + 3]));
+                }
+              } else
 #pragma unroll
               for (int j = 0; j < 8; ++j) {
                 float4 g4 = xrow[j ^ (lane & 7)];
@@ -499,6 +509,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               if (E.kind == TX_EPI_BIAS_TANH) {
 #pragma unroll
                 for (int i = 0; i < 32; ++i) v[i] = tanhf(v[i]);
+              }
+            } else if (row_ok && !(CG == 2 && p.tma_aux) && E.kind == TX_EPI_SGD) {
+              if (n + 32 <= p.N && E.s1 == 1 && (E.s0 % 4) == 0 && ((uintptr_t)E.aux & 15) == 0) {
+                const float* g = E.aux + (int64_t)row * E.s0 + n;
+#pragma unroll
+                for (int i = 0; i < 32; i += 4) {
+                  const float4 w4 = *reinterpret_cast<const float4*>(g + i);
+                  v[i] = __fsub_rn(w4.x, __fmul_rn(E.alpha, v[i])); v[i + 1] = __fsub_rn(w4.y, __fmul_rn(E.alpha, v[i + 1]));
+                  v[i + 2] = __fsub_rn(w4.z, __fmul_rn(E.alpha, v[i + 2]));
+                  v[i + 3] = __fsub_rn(w4.w, __fmul_rn(E.alpha, v[i + 3]));
+                }
+              } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                  if (n + i < p.N) v[i] = E.apply(v[i], row, n + i);
               }
             } else if (row_ok && !(CG == 2 && p.tma_aux)) {  // MUL_AUX / MUL_1MSQR: per-row [M,N] operand
               const float* g = E.aux + (int64_t)row * E.s0 + n;
@@ -565,6 +590,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 *reinterpret_cast<float4*>(g + i) = make_float4(
                     __fsub_rn(1.0f, __fmul_rn(v[i], v[i])), __fsub_rn(1.0f, __fmul_rn(v[i + 1], v[i + 1])),
                     __fsub_rn(1.0f, __fmul_rn(v[i + 2], v[i + 2])), __fsub_rn(1.0f, __fmul_rn(v[i + 3], v[i + 3])));
+            }
+          } else if (E.kind == TX_EPI_SGD) {
+            const float* g = E.aux + (int64_t)row * E.s0 + n;
+#pragma unroll
+            for (int i = 0; i < 32; i += 4) {
+              const float4 w4 = *reinterpret_cast<const float4*>(g + i);
+              v[i] = __fsub_rn(w4.x, __fmul_rn(E.alpha, v[i])); v[i + 1] = __fsub_rn(w4.y, __fmul_rn(E.alpha, v[i + 1]));
+              v[i + 2] = __fsub_rn(w4.z, __fmul_rn(E.alpha, v[i + 2])); v[i + 3] = __fsub_rn(w4.w, __fmul_rn(E.alpha, v[i + 3]));
             }
           } else if (E.kind == TX_EPI_MUL_AUX || E.kind == TX_EPI_MUL_1MSQR) {
             const float* g = E.aux + (int64_t)row * E.s0 + n;
@@ -834,7 +867,8 @@ int gemm_tc(const G& g, void* ws, size_t wsb, cudaStream_t st) {
   CUtensorMap mx;
   memset(&mx, 0, sizeof(mx));
   const Epi<float>& E = g.epi_f;
-  p.tma_aux = cg == 2 && p.tma_store && p.splits == 1 && (E.kind == TX_EPI_MUL_AUX || E.kind == TX_EPI_MUL_1MSQR) && E.s1 == 1 &&
+  p.tma_aux = cg == 2 && p.tma_store && p.splits == 1 &&
+              (E.kind == TX_EPI_MUL_AUX || E.kind == TX_EPI_MUL_1MSQR || E.kind == TX_EPI_SGD) && E.s1 == 1 &&
               (E.s0 * 4) % 16 == 0 && E.s0 >= g.N && ((uintptr_t)E.aux & 15) == 0 && !getenv("TX_GEMM_NO_TMA_AUX");
   if (p.tma_aux) {
     EncodeFn enc = encode_fn();

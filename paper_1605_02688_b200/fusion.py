@@ -269,10 +269,55 @@ def _fuse_tanh_layers(fgraph, emit) -> int:
     return applied
 
 
+def _match_sgd(prog, z_idx):
+    """{t0 = mul(lr, z); t1 = sub(w, t0)} with output t1 (either operand
+    order of the mul): the SGD update w - lr * grad.  Returns lr or None."""
+    if len(prog.nodes) != 2 or len(prog.in_dtypes) != 2 or prog.outputs != (("node", 1),):
+        return None
+    (k0, r0, _), (k1, r1, _) = prog.nodes
+    if k0 != "mul" or k1 != "sub" or r1 != (("in", 1 - z_idx), ("node", 0)):
+        return None
+    others = [r for r in r0 if r != ("in", z_idx)]
+    if len(r0) != 2 or len(others) != 1 or others[0][0] != "const":
+        return None
+    dt, val = prog.consts[others[0][1]]
+    return float(val), dt
+
+
+def _fuse_sgd_updates(fgraph, ctx, emit) -> int:
+    """w - lr * dot(a, b) (a weight's SGD step from its gradient GEMM) becomes
+    one GEMM whose epilogue reads w and writes the new w -- in place when the
+    update can be written directly (the dW matrix is never stored).  Skipped
+    for data-parallel steps, where the gradient is a partial sum that must be
+    all-reduced before the update."""
+    from .linalg import EPI_SGD, Dot, DotEpilogue
+    if getattr(ctx, "data_parallel", False):
+        return 0
+    applied = 0
+    for c in list(fgraph.toposort()):
+        if c.id not in fgraph.nodes or not isinstance(c.op, Composite) or len(c.inputs) != 2:
+            continue
+        zi = next((i for i, x in enumerate(c.inputs) if _sole_dot_client(fgraph, x, Dot)), None)
+        if zi is None:
+            continue
+        z, w = c.inputs[zi], c.inputs[1 - zi]
+        if w is z or w.type != z.type or c.outputs[0].type != z.type:
+            continue
+        m = _match_sgd(c.op.program, zi)
+        if m is None:
+            continue
+        a, b = z.owner.inputs
+        (o,) = apply(DotEpilogue(EPI_SGD, m[0], m[1]), [a, b, w])
+        fgraph.replace_all([(c.outputs[0], o)], "fuse_gemm_epilogue")
+        emit(node=c, replaced="dot+composite[sgd]", replacement="dot+sgd")
+        applied += 1
+    return applied
+
+
 @register_rewrite("fuse_gemm_epilogue", "abstract_select", "global")
 def fuse_gemm_epilogue(fgraph, ctx, emit) -> int:
     from .linalg import EPI_BIAS, EPI_BIAS_TANH_DUAL, EPI_MUL_AUX, Dot, DotEpilogue
-    applied = _fuse_tanh_layers(fgraph, emit)
+    applied = _fuse_tanh_layers(fgraph, emit) + _fuse_sgd_updates(fgraph, ctx, emit)
     for d in list(fgraph.toposort()):
         if d.id not in fgraph.nodes or not isinstance(d.op, Dot):
             continue

@@ -92,9 +92,9 @@ def dot(a: Variable, b: Variable) -> Variable:
 
 
 # epilogue kinds (include/texpr_b200.h TX_EPI_*)
-EPI_BIAS, EPI_BIAS_TANH, EPI_MUL_1MSQR, EPI_BIAS_TANH_DUAL, EPI_MUL_AUX = 1, 2, 3, 4, 5
+EPI_BIAS, EPI_BIAS_TANH, EPI_MUL_1MSQR, EPI_BIAS_TANH_DUAL, EPI_MUL_AUX, EPI_SGD = 1, 2, 3, 4, 5, 6
 _EPI_NAMES = {EPI_BIAS: "bias", EPI_BIAS_TANH: "bias_tanh", EPI_MUL_1MSQR: "mul_1msqr",
-              EPI_BIAS_TANH_DUAL: "bias_tanh_dual", EPI_MUL_AUX: "mul_aux"}
+              EPI_BIAS_TANH_DUAL: "bias_tanh_dual", EPI_MUL_AUX: "mul_aux", EPI_SGD: "sgd"}
 
 
 @register_op
@@ -110,21 +110,29 @@ class DotEpilogue(Op):
       mul_1msqr       out = (a.b) * (1 - aux^2)      (aux = the forward's h)
       bias_tanh_dual  out = tanh(aux[n] + a.b), out2 = 1 - out^2
       mul_aux         out = (a.b) * aux
+      sgd             out = aux - alpha * (a.b)      (a weight's SGD update from its gradient GEMM;
+                                                      the output may be written in place over aux)
     """
 
     name = "dot_epilogue"
     has_grad = False
     gemm_operands = True
 
-    def __init__(self, kind: int):
+    @property
+    def elementwise_in_place(self):
+        return self.kind == EPI_SGD
+
+    def __init__(self, kind: int, alpha: float = 0.0, alpha_dtype: str = "float32"):
         self.kind = int(kind)
+        self.alpha = float(alpha)
+        self.alpha_dtype = alpha_dtype
 
     @property
     def display_name(self):
         return f"dot+{_EPI_NAMES.get(self.kind, self.kind)}"
 
     def attrs_key(self):
-        return (self.kind,)
+        return (self.kind, self.alpha, self.alpha_dtype)
 
     def infer_types(self, input_types):
         a, b, aux = input_types
@@ -162,6 +170,9 @@ class DotEpilogue(Op):
             return [h, make("sub", [1.0, make("sqr", [h])])]
         if self.kind == EPI_MUL_AUX:
             return [make("mul", [z, aux])]
+        if self.kind == EPI_SGD:
+            from .graph import Constant
+            return [make("sub", [aux, make("mul", [Constant(self.alpha, dtype=self.alpha_dtype), z])])]
         raise NotImplementedError(f"epilogue kind {self.kind}")
 
     def lower(self, node, plan):
@@ -169,13 +180,14 @@ class DotEpilogue(Op):
         epi = native.TxEpilogue()
         epi.kind = self.kind
         epi.aux = plan.tx(node.inputs[2])
+        epi.alpha = self.alpha
         if self.kind == EPI_BIAS_TANH_DUAL:
             epi.out2 = plan.tx(node.outputs[1])
         plan.emit_dot(node, epilogue=epi)
 
     def attrs_payload(self, encode_graph=None):
-        return {"kind": self.kind}
+        return {"kind": self.kind, "alpha": self.alpha, "alpha_dtype": self.alpha_dtype}
 
     @classmethod
     def from_payload(cls, payload, decode_graph=None):
-        return cls(payload["kind"])
+        return cls(payload["kind"], payload.get("alpha", 0.0), payload.get("alpha_dtype", "float32"))

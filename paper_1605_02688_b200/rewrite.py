@@ -32,6 +32,7 @@ class RewriteContext:
     conv_impl: str = "gemm"
     execution_bound: bool = False
     max_passes: int = DEFAULT_MAX_PASSES
+    data_parallel: bool = False   # gradients are partial sums: no update fusion into their GEMMs
 
 
 @dataclass

@@ -233,7 +233,8 @@ def compile(inputs, outputs, updates=(), preset="fast_run", allow_gc=True, nan_g
     cloned, _ = clone_outputs(outputs + uvals, repl, copy_free=True)
     fg = FunctionGraph([repl[v] for v in full], cloned)
     fg.protected_inputs = {repl[v] for v in found}
-    ctx = RewriteContext(conv_impl=conv_impl, execution_bound=True, max_passes=max_passes)
+    ctx = RewriteContext(conv_impl=conv_impl, execution_bound=True, max_passes=max_passes,
+                         data_parallel=data_parallel is not None)
     _, log = run_preset(fg, preset, include=include, exclude=exclude, ctx=ctx)
     return CompiledFunction(fg, len(outputs), [repl[v] for v in inputs], [(s, repl[s]) for s in found],
                             [(p.shared, cloned[len(outputs) + i]) for i, p in enumerate(ups)],
@@ -329,7 +330,9 @@ class CompiledFunction:
             readers = _readers_through_views(g, var)
             reads_self = p in readers
             if reads_self:
-                if not isinstance(p.op, (Elemwise, Composite)):
+                # in place over the value it reads: fine for elementwise kernels and
+                # for the SGD GEMM epilogue (each element read, then written, once)
+                if not (isinstance(p.op, (Elemwise, Composite)) or getattr(p.op, "elementwise_in_place", False)):
                     continue
                 if any(x is not var and _is_view_of(x, var) for x in p.inputs):
                     continue
@@ -875,6 +878,7 @@ class StepPlan:
         deferred = {n.id for grp in self.row_groups for n in grp.deferred}
         group_at = {grp.last_pos: grp for grp in self.row_groups}
         self.guard_slots = []
+        self.row_sources = []        # generated row-fusion kernels (diagnostics)
         self.commit_launches = []
         self.lazy_copies = {}
         if fn.nan_guard is not None:
@@ -889,6 +893,7 @@ class StepPlan:
                     from . import rowfuse
                     self._cur = n
                     launch, _src = rowfuse.emit_group(self, group_at[i], g)
+                    self.row_sources.append(_src)
                     self.add_launch(launch)
                     for d in group_at[i].deferred:
                         if not getattr(d.op, "view_capable", False):

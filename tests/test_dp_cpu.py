@@ -122,14 +122,16 @@ def test_gloo_two_ranks_match_full_batch():
 def test_propagation_through_fused_gemm_epilogues():
     """With the device rewrites (GEMM epilogues), the same 7 partials."""
     from paper_1605_02688_b200.graph import FunctionGraph, Variable, clone_outputs
-    from paper_1605_02688_b200.rewrite import run_preset
+    from paper_1605_02688_b200.rewrite import RewriteContext, run_preset
     g = C.build_mlp(T, B=B, H=H)
     ins = g["inputs"] + g["params"]
     repl = {v: Variable(v.type, v.name) for v in ins}
     outs, _ = clone_outputs(g["outputs"] + [u for _, u in g["updates"]], repl)
     fg = FunctionGraph([repl[v] for v in ins], outs)
-    run_preset(fg, "fast_run")
+    # as compile(data_parallel=...) runs it: no SGD update fused into a partial-sum GEMM
+    run_preset(fg, "fast_run", ctx=RewriteContext(execution_bound=True, data_parallel=True))
     names = [getattr(n.op, "display_name", n.op.name) for n in fg.toposort()]
+    assert "dot+sgd" not in names
     assert names.count("dot+bias_tanh") == 2 and names.count("dot+mul_1msqr") == 2
     plan = dp.propagate(fg.toposort(), {repl[v].id: dp.sharded(0) for v in g["inputs"]})
     assert len(plan.partial_nodes) == 7
