@@ -5,6 +5,7 @@
 // Replaces np.dot for those shapes (reference ops/linalg.py:42-62); the
 // tensor-core path for large fp32 problems is tx_gemm_tc.cu.
 #include <cuda_runtime.h>
+#include <cstdlib>
 
 #include "tx_common.h"
 #include "tx_gemm.h"
@@ -171,14 +172,26 @@ __global__ void __launch_bounds__(256) rowdot_kernel(const float* __restrict__ A
 constexpr int RDF_MAX_SMEM = 200 * 1024;
 
 
-template <int NN, int R>
-__global__ void __launch_bounds__(512) rowdot_full_kernel(const float* __restrict__ A, const float* __restrict__ B,
+// TRANS: B is staged transposed, Bt[n][k] with the row pitch Kp = K rounded
+// up to 32 plus 4 floats, so the per-lane 128-bit reads of 4 consecutive k of
+// one column are bank-conflict free (the natural [k][n] layout puts lanes 160 B
+// apart: two-way conflicts on every read); the staging reads B coalesced.
+template <int NN, int R, bool TRANS = false>
+__global__ void __launch_bounds__(R >= 8 ? 256 : 512) rowdot_full_kernel(const float* __restrict__ A, const float* __restrict__ B,
                                                          float* __restrict__ C, int64_t M, int N, int64_t K,
                                                          int64_t sam, int64_t sbk, int64_t sbn, int64_t scm,
                                                          int64_t scn, Epi<float> epi) {
-  extern __shared__ __align__(16) float Bs[];  // [K][NN]
+  extern __shared__ __align__(16) float Bs[];  // [K][NN], or Bt [NN][Kp] when TRANS
   const int64_t total = K * NN;
-  if (sbn == 1 && sbk == NN && N == NN && (((uintptr_t)B & 15) == 0) && total % 4 == 0) {
+  const int64_t Kp = ((K + 31) & ~(int64_t)31) + 4;
+  if (TRANS) {
+#pragma unroll 8
+    for (int64_t e = threadIdx.x; e < total; e += blockDim.x) {
+      const int64_t k = e / NN;
+      const int n = (int)(e - k * NN);
+      Bs[n * Kp + k] = n < N ? B[k * sbk + (int64_t)n * sbn] : 0.f;
+    }
+  } else if (sbn == 1 && sbk == NN && N == NN && (((uintptr_t)B & 15) == 0) && total % 4 == 0) {
     for (int64_t e = threadIdx.x; e < total / 4; e += blockDim.x) cp_async16(Bs + 4 * e, B + 4 * e);
     asm volatile("cp.async.wait_all;" ::: "memory");
   } else {
@@ -208,17 +221,36 @@ __global__ void __launch_bounds__(512) rowdot_full_kernel(const float* __restric
         for (int r = 0; r < R; ++r)
           av[r] = (row0 + r < M) ? __ldcs(reinterpret_cast<const float4*>(A + (row0 + r) * sam + kk))
                                  : make_float4(0.f, 0.f, 0.f, 0.f);
-        float b[4 * NN];
+        if (TRANS) {
 #pragma unroll
-        for (int q = 0; q < NN; ++q) {
-          const float4 t = reinterpret_cast<const float4*>(Bs + kk * NN)[q];
-          b[4 * q] = t.x; b[4 * q + 1] = t.y; b[4 * q + 2] = t.z; b[4 * q + 3] = t.w;
+          for (int n = 0; n < NN; ++n) {
+            const float4 bv = *reinterpret_cast<const float4*>(Bs + n * Kp + kk);
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+              acc[r][n] += av[r].x * bv.x + av[r].y * bv.y + av[r].z * bv.z + av[r].w * bv.w;
+          }
+        } else {
+          // rows kk..kk+3 of B are NN float4 at a 16-byte aligned float4 index
+          const float4* B4 = reinterpret_cast<const float4*>(Bs) + (kk >> 2) * NN;
+          float b[4 * NN];
+#pragma unroll
+          for (int q = 0; q < NN; ++q) {
+            const float4 t = B4[q];
+            b[4 * q] = t.x; b[4 * q + 1] = t.y; b[4 * q + 2] = t.z; b[4 * q + 3] = t.w;
+          }
+          // four dependent FMAs straight into each accumulator (no separate
+          // multiply + add per term): the loop is issue-bound, not memory-bound
+#pragma unroll
+          for (int r = 0; r < R; ++r)
+#pragma unroll
+            for (int n = 0; n < NN; ++n) {
+              float a_ = acc[r][n];
+              a_ = fmaf(av[r].x, b[n], a_);
+              a_ = fmaf(av[r].y, b[NN + n], a_);
+              a_ = fmaf(av[r].z, b[2 * NN + n], a_);
+              acc[r][n] = fmaf(av[r].w, b[3 * NN + n], a_);
+            }
         }
-#pragma unroll
-        for (int r = 0; r < R; ++r)
-#pragma unroll
-          for (int n = 0; n < NN; ++n)
-            acc[r][n] += av[r].x * b[n] + av[r].y * b[NN + n] + av[r].z * b[2 * NN + n] + av[r].w * b[3 * NN + n];
       }
     } else {
 #pragma unroll
@@ -229,7 +261,7 @@ __global__ void __launch_bounds__(512) rowdot_full_kernel(const float* __restric
         for (int64_t kk = lane; kk < K; kk += 32) {
           const float av = __ldg(a + kk);
 #pragma unroll
-          for (int n = 0; n < NN; ++n) acc[r][n] += av * Bs[kk * NN + n];
+          for (int n = 0; n < NN; ++n) acc[r][n] += av * (TRANS ? Bs[n * Kp + kk] : Bs[kk * NN + n]);
         }
       }
     }
@@ -509,20 +541,22 @@ __global__ void kred_finalize(const float* __restrict__ P, float* __restrict__ C
   C[m * scm + n * scn] = epi.apply(v, m, n);
 }
 
-template <int NN, int R>
+template <int NN, int R, bool TRANS = false>
 static int launch_rowdot_full(const G& g, int threads, size_t smem, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    TX_CUDA(cudaFuncSetAttribute(rowdot_full_kernel<NN, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, RDF_MAX_SMEM));
+    TX_CUDA(cudaFuncSetAttribute(rowdot_full_kernel<NN, R, TRANS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 RDF_MAX_SMEM));
     attr = true;
   }
+  if (TRANS) smem = (size_t)NN * (size_t)(((g.K + 31) & ~(int64_t)31) + 4) * 4;
   const int warps = threads / 32;
   int64_t groups = (g.M + R - 1) / R;
   int64_t blocks = (groups + warps - 1) / warps;
   const int per_sm = (int)(RDF_MAX_SMEM / (smem + 1024)) > 0 ? (int)(RDF_MAX_SMEM / (smem + 1024)) : 1;
   const int64_t cap = (int64_t)sm_count() * (per_sm < 4 ? per_sm : 4);
   if (blocks > cap) blocks = cap;
-  rowdot_full_kernel<NN, R><<<(unsigned)blocks, threads, smem, st>>>((const float*)g.A, (const float*)g.B, (float*)g.C,
+  rowdot_full_kernel<NN, R, TRANS><<<(unsigned)blocks, threads, smem, st>>>((const float*)g.A, (const float*)g.B, (float*)g.C,
                                                                      g.M, (int)g.N, g.K, g.sam, g.sbk, g.sbn, g.scm,
                                                                      g.scn, g.epi_f);
   TX_CUDA(cudaGetLastError());
@@ -535,7 +569,17 @@ static int launch_rowdot(const G& g, cudaStream_t st) {
   if (smem <= (size_t)RDF_MAX_SMEM) {
     // many rows: 16 warps x 4 rows per CTA, one CTA per SM; few rows (logreg):
     // 4-warp CTAs, one row per warp, to spread over the SMs
-    if (g.M >= 4096) return launch_rowdot_full<NN, (NN <= 10 ? 4 : 2)>(g, 512, smem, st);
+    if (g.M >= 4096) {
+      const char* v = getenv("TX_RD_VARIANT");
+      const int var = v ? atoi(v) : 0;
+      if constexpr (NN <= 10) {
+        if (var == 1) return launch_rowdot_full<NN, 8>(g, 256, smem, st);
+        if (var == 2) return launch_rowdot_full<NN, 2>(g, 512, smem, st);
+        if (var == 3) return launch_rowdot_full<NN, 4, true>(g, 512, smem, st);
+        if (var == 4) return launch_rowdot_full<NN, 2, true>(g, 512, smem, st);
+      }
+      return launch_rowdot_full<NN, (NN <= 10 ? 4 : 2)>(g, 512, smem, st);
+    }
     return launch_rowdot_full<NN, 1>(g, 128, smem, st);
   }
   if (g.M >= 4096) {
