@@ -740,6 +740,10 @@ void choose_tile(const G& g, int* cg_out, int* bn_out) {
   if (cg_s) cg = atoi(cg_s) == 1 ? 1 : 2;
   if (g.M <= BM) cg = 1;
   int bn = bn_s ? atoi(bn_s) : BN;
+  // narrow products (the N <= 16 skinny GEMMs routed here): a 256-wide MMA
+  // would spend 16x the tensor time on padding -- use 32 / 64-wide tiles
+  if (!bn_s && g.N <= 32) { bn = 32; cg = 1; }
+  else if (!bn_s && g.N <= 64) bn = 64;
   if (bn < 32 || bn > BN || bn % (32 * cg) != 0) bn = BN;
   *cg_out = cg;
   *bn_out = bn;
