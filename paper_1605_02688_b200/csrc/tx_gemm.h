@@ -87,5 +87,9 @@ size_t gemm_tc_workspace(const G& g);
 void choose_tile(const G& g, int* cg, int* bn);
 // C = epi(sum over splits of P[split][M][N]), fixed split order
 int splitk_finalize(const float* P, const G& g, int splits, cudaStream_t st);
+// stream-K fix-up: tiles whose k-range was split across clusters get
+// C = epi(sum of their pieces in k order); whole tiles were stored directly
+int streamk_fixup(const float* P, const G& g, int num_m, int num_n, int bm, int bn, int num_kb, int nclusters,
+                  int group_m, cudaStream_t st = 0);
 
 }  // namespace tx

@@ -637,6 +637,64 @@ int kred_splits(int64_t M, int64_t K) {
   return (int)s;
 }
 
+namespace {
+__device__ __forceinline__ int sk_owner_h(int64_t u, int64_t U, int NC) {
+  int c = (int)((u * NC) / U);
+  while (c + 1 < NC && ((int64_t)(c + 1) * U) / NC <= u) ++c;
+  while (c > 0 && ((int64_t)c * U) / NC > u) --c;
+  return c;
+}
+
+// grid (remainder tile, 16-row slab): owners computed once per CTA, then each
+// thread sums 4 adjacent columns x 4 rows over the tile's pieces in k order
+// and applies the epilogue (32-bit index math, coalesced accesses)
+__global__ void __launch_bounds__(256) streamk_fixup_kernel(const float* __restrict__ P, float* __restrict__ C,
+                                                           int64_t M, int64_t N, int64_t scm, int64_t scn,
+                                                           Epi<float> epi, int num_m, int num_n, int bm, int bn,
+                                                           int num_kb, int NC, int group_m, int base) {
+  const int num_tiles = num_m * num_n;
+  const int64_t U2 = (int64_t)(num_tiles - base) * num_kb;
+  const int rt = blockIdx.x;
+  const int c0 = sk_owner_h((int64_t)rt * num_kb, U2, NC), c1 = sk_owner_h((int64_t)rt * num_kb + num_kb - 1, U2, NC);
+  if (c0 == c1) return;  // whole tile stored by its single owner
+  const int t = base + rt;
+  const int per_group = group_m * num_n;
+  const int g = t / per_group, first = g * group_m;
+  const int gsz = min(num_m - first, group_m);
+  const int r = t - g * per_group;
+  const int mb = first + r % gsz, nb = r / gsz;
+  const int64_t n0 = (int64_t)nb * bn + (threadIdx.x & 63) * 4;
+  const int64_t MN = M * N;
+  const int npieces = c1 - c0 + 1;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t m = (int64_t)mb * bm + (int64_t)blockIdx.y * 16 + (threadIdx.x >> 6) + 4 * i;
+    if (m >= M || (int64_t)blockIdx.y * 16 >= bm) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t n = n0 + j;
+      if (n >= N || n >= (int64_t)nb * bn + bn) continue;
+      float v = 0.f;
+      for (int q = 0; q < npieces; ++q) v += P[q * MN + m * N + n];
+      C[m * scm + n * scn] = epi.apply(v, m, n);
+    }
+  }
+}
+}  // namespace
+
+int streamk_fixup(const float* P, const G& g, int num_m, int num_n, int bm, int bn, int num_kb, int nclusters,
+                  int group_m, cudaStream_t st) {
+  const int num_tiles = num_m * num_n;
+  const int base = (num_tiles / nclusters) * nclusters;
+  if (num_tiles == base) return TX_OK;
+  TX_CHECK(bn <= 256, TX_E_ARG, "streamk_fixup: tile too wide");
+  dim3 grid((unsigned)(num_tiles - base), (unsigned)((bm + 15) / 16));
+  streamk_fixup_kernel<<<grid, 256, 0, st>>>(P, (float*)g.C, g.M, g.N, g.scm, g.scn, g.epi_f, num_m, num_n, bm, bn,
+                                             num_kb, nclusters, group_m, base);
+  TX_CUDA(cudaGetLastError());
+  return TX_OK;
+}
+
 int splitk_finalize(const float* P, const G& g, int splits, cudaStream_t st) {
   const int64_t tot = g.M * g.N;
   kred_finalize<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(P, (float*)g.C, g.M, (int)g.N, splits, g.scm, g.scn,

@@ -242,6 +242,9 @@ struct TcParams {
   int a_lim, b_lim;  // 3-D boxes cover MN < lim (whole 32-blocks); tiles reaching past it use the edge maps
   int splits;       // split-K factor: work items are (tile, split); partial tiles go to a workspace
   int kbs;          // k-blocks per split
+  int streamk;      // stream-K: cluster c owns the flat (tile, k-block) units [c*U/NC, (c+1)*U/NC)
+  int num_kb;       // k-blocks per tile
+  int nclusters;    // clusters of the launch (stream-K partition)
   int bn;           // N tile of this launch (<= BN, multiple of 32): chosen per shape against wave quantisation
   int stage_tx;     // TMA bytes landing per stage on the leader's barrier
   int dbg_nostore;  // diagnostics only (TX_GEMM_DBG_NOSTORE): epilogue drains TMEM without storing
@@ -261,12 +264,79 @@ __device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int& mb
   nb = r / gsz;
 }
 
+// One unit of work of a CTA (pair): k-blocks [kb0, kb1) of one output tile.
+// `full` = the segment covers the whole K of the tile (store C with the
+// epilogue); otherwise the raw partial goes to workspace slot `piece`.
+struct Seg {
+  int t, kb0, kb1, piece, full;
+};
+
+// Stream-K is hybrid: the floor(tiles / clusters) full waves go round robin
+// (whole tiles, so concurrently running tiles stay adjacent in the grouped
+// raster and share operand panels in L2); only the R remainder tiles are cut
+// into the flat (tile, k-block) sequence, cluster c taking units
+// [c*U2/NC, (c+1)*U2/NC) of U2 = R * num_kb.
+// owner cluster of remainder unit u under that partition
+__device__ __forceinline__ int sk_owner(int64_t u, int64_t U, int NC) {
+  int c = (int)((u * NC) / U);
+  while (c + 1 < NC && ((int64_t)(c + 1) * U) / NC <= u) ++c;
+  while (c > 0 && ((int64_t)c * U) / NC > u) --c;
+  return c;
+}
+
+__device__ __forceinline__ int64_t seg_begin(const TcParams& p, int c) {
+  if (!p.streamk) return c;
+  const int W = p.num_tiles / p.nclusters;
+  if (W > 0) return 0;
+  const int64_t U2 = (int64_t)(p.num_tiles - W * p.nclusters) * p.num_kb;
+  return W + ((int64_t)c * U2) / p.nclusters;
+}
+
+// every role of the CTA walks the same sequence of segments
+__device__ __forceinline__ bool seg_next(const TcParams& p, int c, int64_t& cur, Seg& s) {
+  if (!p.streamk) {  // round robin over (tile, split) items
+    if (cur >= (int64_t)p.num_tiles * p.splits) return false;
+    s.t = (int)(cur % p.num_tiles);
+    const int split = (int)(cur / p.num_tiles);
+    s.kb0 = split * p.kbs;
+    s.kb1 = min(p.num_kb, s.kb0 + p.kbs);
+    s.piece = split;
+    s.full = p.splits == 1;
+    cur += p.nclusters;
+    return true;
+  }
+  const int NC = p.nclusters;
+  const int W = p.num_tiles / NC;
+  const int base = W * NC;
+  const int64_t U2 = (int64_t)(p.num_tiles - base) * p.num_kb;
+  if (cur < W) {  // full-wave tile
+    s.t = c + (int)cur * NC;
+    s.kb0 = 0;
+    s.kb1 = p.num_kb;
+    s.piece = 0;
+    s.full = 1;
+    ++cur;
+    if (cur == W) cur = W + ((int64_t)c * U2) / NC;
+    return true;
+  }
+  const int64_t u = cur - W, u1 = ((int64_t)(c + 1) * U2) / NC;
+  if (u >= u1) return false;
+  const int rt = (int)(u / p.num_kb);
+  s.t = base + rt;
+  s.kb0 = (int)(u - (int64_t)rt * p.num_kb);
+  s.kb1 = (int)min((int64_t)p.num_kb, s.kb0 + (u1 - u));
+  s.piece = c - sk_owner((int64_t)rt * p.num_kb, U2, NC);
+  s.full = s.kb0 == 0 && s.kb1 == p.num_kb;
+  cur += s.kb1 - s.kb0;
+  return true;
+}
+
 template <int CG>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                    const __grid_constant__ CUtensorMap mapC, const __grid_constant__ CUtensorMap mapX,
                    const __grid_constant__ CUtensorMap mapAe, const __grid_constant__ CUtensorMap mapBe,
-                   const TcParams p) {
+                   const __grid_constant__ CUtensorMap mapP, const TcParams p) {
   using K_ = Cfg<CG>;
   constexpr int STAGES = K_::STAGES;
   const int bn = p.bn;
@@ -318,10 +388,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&mapB) : "memory");
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = cluster_id; t < p.num_tiles * p.splits; t += num_clusters) {
+      int64_t cur = seg_begin(p, cluster_id);
+      Seg sg;
+      while (seg_next(p, cluster_id, cur, sg)) {
         int mb, nb;
-        tile_coords(t % p.num_tiles, p.num_m, p.num_n, mb, nb);
-        const int kb0 = (t / p.num_tiles) * p.kbs, kb1 = min(num_kb, kb0 + p.kbs);
+        tile_coords(sg.t, p.num_m, p.num_n, mb, nb);
+        const int kb0 = sg.kb0, kb1 = sg.kb1;
         const int m0 = mb * BM * CG + (int)rank * BM;   // this CTA's rows
         const int n0 = nb * bn + (int)rank * BNL;       // this CTA's half of B
         for (int kb = kb0; kb < kb1; ++kb) {
@@ -374,8 +446,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int t = cluster_id; t < p.num_tiles * p.splits; t += num_clusters, ++it) {
-        const int kb0 = (t / p.num_tiles) * p.kbs, kb1 = min(num_kb, kb0 + p.kbs);
+      int64_t cur = seg_begin(p, cluster_id);
+      Seg sg;
+      for (; seg_next(p, cluster_id, cur, sg); ++it) {
+        const int kb0 = sg.kb0, kb1 = sg.kb1;
         const int buf = it & 1;
         const uint32_t use = (uint32_t)(it >> 1);
         mbar_wait(tempty + buf, (use & 1) ^ 1);
@@ -416,10 +490,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         (E.kind != TX_EPI_BIAS_TANH_DUAL || (E.o1 == 1 && E.o0 % 4 == 0 && ((uintptr_t)E.out2 & 15) == 0)) &&
                         (E.kind != TX_EPI_BIAS && E.kind != TX_EPI_BIAS_TANH && E.kind != TX_EPI_BIAS_TANH_DUAL ||
                          (E.s1 == 1 && ((uintptr_t)E.aux & 15) == 0));
-    for (int t = cluster_id; t < p.num_tiles * p.splits; t += num_clusters, ++it) {
+    int64_t cur = seg_begin(p, cluster_id);
+    Seg sg;
+    for (; seg_next(p, cluster_id, cur, sg); ++it) {
       int mb, nb;
-      tile_coords(t % p.num_tiles, p.num_m, p.num_n, mb, nb);
-      const int split = t / p.num_tiles;
+      tile_coords(sg.t, p.num_m, p.num_n, mb, nb);
+      const int split = sg.piece;
+      const bool partial = !sg.full;
       const int buf = it & 1;
       const uint32_t use = (uint32_t)(it >> 1);
       mbar_wait(tfull + buf, use & 1);
@@ -431,7 +508,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int nchunks = bn / 32;
       float* crow = p.C + (int64_t)row * p.ldc;
       const bool row_ok = row < p.M;
-      if (p.tma_store) {
+      if (p.tma_store || p.splits > 1) {  // (split-K: every segment is a partial tile -> workspace)
         // row `lane` of a [32 x 32] tile -> swizzled staging -> one TMA store
         // per chunk (coalesced, asynchronous; TMA clips the M/N edges)
         float* stg = reinterpret_cast<float*>(smem + K_::RING + (size_t)(warp - 2) * 4096);
@@ -443,7 +520,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const int n = nb * bn + c;
           const bool live = !(row0 >= p.M || n >= p.N || p.dbg_nostore);
           if constexpr (CG == 2) {
-            if (p.tma_aux && live && lane == 0) {  // fetch this chunk's operand tile while TMEM drains
+            if (p.tma_aux && live && !partial && lane == 0) {  // fetch this chunk's operand tile while TMEM drains
               mbar_expect_tx(xbar, 4096);
               tma_load_2d((void*)xstg, &mapX, xbar, n, row0);
             }
@@ -451,7 +528,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           float v[32];
           tmem_ld32(taddr + c, v);
           if (!live) continue;
-          if (p.splits > 1) {  // raw partial tile -> workspace [split][M][N]; the reduction applies the epilogue
+          if (partial) {  // raw partial tile -> workspace [piece][M][N]; the reduction applies the epilogue
             if (lane == 0) tma_store_wait_read();
             __syncwarp();
             float4* prow = reinterpret_cast<float4*>(stg + lane * 32);
@@ -460,7 +537,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               prow[j ^ (lane & 7)] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
             fence_async_smem();
             __syncwarp();
-            if (lane == 0) tma_store_3d(&mapC, stg, n, row0, split);
+            if (lane == 0) tma_store_3d(&mapP, stg, n, row0, split);
             continue;
           }
           if constexpr (CG == 2) {
@@ -754,6 +831,40 @@ void choose_tile(const G& g, int* cg_out, int* bn_out) {
 // tile).  Work items become (tile, K-slice); raw partial tiles land in a
 // [splits][M][N] workspace through a 3-D TMA map and a second kernel sums
 // them in split order (deterministic) and applies the epilogue.
+// Stream-K (the MLP's dW2 GEMM: 256 pair tiles on 74 pairs = 3.46 waves):
+// when the last wave would leave more than a tenth of the machine idle, the
+// remainder tiles are cut into an equal run of the flat (tile, k-block)
+// sequence per cluster (r01: 405 -> 381 us on that GEMM).  Segments that
+// cover a whole tile store C with the epilogue; the pieces of split tiles go
+// to a [pieces][M][N] workspace and a fix-up pass sums them in k order and
+// applies the epilogue (deterministic).
+void tc_streamk(const G& g, int splits, int* streamk, int* pieces, int* nclusters) {
+  int cg, bn;
+  choose_tile(g, &cg, &bn);
+  const int64_t tiles = ((g.M + BM * cg - 1) / (BM * cg)) * ((g.N + bn - 1) / bn);
+  const int64_t units = sm_count() / cg;
+  const int num_kb = (int)((g.K + BK - 1) / BK);
+  *streamk = 0;
+  *pieces = 1;
+  *nclusters = (int)(tiles < units ? tiles : units);
+  const char* e = getenv("TX_GEMM_STREAMK");
+  const int force = e ? atoi(e) : -1;
+  if (splits > 1 || force == 0 || g.N % 4 != 0 || num_kb < 4) return;
+  const int64_t waves = (tiles + units - 1) / units;
+  const double fill = (double)tiles / (double)(waves * units);
+  const int64_t rem = tiles % units;
+  // only with at least one full wave: when every tile would be split (fewer
+  // tiles than clusters) the extra partial traffic costs more than the
+  // balance gains (r01 A/B: the M = 784 weight gradient 115 -> 145 us)
+  if (rem == 0 || (force != 1 && !(fill < 0.9 && waves <= 8 && tiles >= units))) return;
+  const int64_t U2 = rem * num_kb;
+  const int64_t per = U2 / units;
+  if (per < 2) return;
+  *streamk = 1;
+  *nclusters = (int)units;
+  *pieces = (int)((num_kb + per - 1) / per + 1);
+}
+
 void tc_splitk(const G& g, int* splits, int* kbs) {
   int cg, bn;
   choose_tile(g, &cg, &bn);
@@ -773,9 +884,11 @@ void tc_splitk(const G& g, int* splits, int* kbs) {
 }
 
 size_t gemm_tc_workspace(const G& g) {
-  int s, k;
+  int s, k, sk, pieces, nc;
   tc_splitk(g, &s, &k);
-  return s > 1 ? (size_t)s * (size_t)g.M * (size_t)g.N * 4 + 256 : 0;
+  if (s > 1) return (size_t)s * (size_t)g.M * (size_t)g.N * 4 + 256;
+  tc_streamk(g, s, &sk, &pieces, &nc);
+  return sk ? (size_t)pieces * (size_t)g.M * (size_t)g.N * 4 + 256 : 0;
 }
 
 int gemm_tc(const G& g, void* ws, size_t wsb, cudaStream_t st) {
@@ -838,6 +951,10 @@ int gemm_tc(const G& g, void* ws, size_t wsb, cudaStream_t st) {
     p.splits = 1;
     p.kbs = (int)((g.K + BK - 1) / BK);
   }
+  p.num_kb = (int)((g.K + BK - 1) / BK);
+  int sk_pieces = 1, sk_nc = 1;
+  tc_streamk(g, p.splits, &p.streamk, &sk_pieces, &sk_nc);
+  if (p.streamk && (ws == nullptr || wsb < gemm_tc_workspace(g) || ((uintptr_t)ws & 15))) p.streamk = 0;
   p.epi = g.epi_f;
   p.dbg_nostore = getenv("TX_GEMM_DBG_NOSTORE") != nullptr;
   // TMA tile stores need a 16-byte aligned C with a 16-byte row pitch; the
@@ -856,17 +973,19 @@ int gemm_tc(const G& g, void* ws, size_t wsb, cudaStream_t st) {
                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) p.tma_store = 0;
   }
-  if (p.splits > 1) {
-    // partial tiles: 3-D map {N, M, splits} over the workspace (rows never spill into the next split)
+  if (p.streamk && !p.tma_store) p.streamk = 0;  // partial pieces need the TMA store path
+  CUtensorMap mp;
+  memset(&mp, 0, sizeof(mp));
+  if (p.splits > 1 || p.streamk) {
+    // partial tiles: 3-D map {N, M, splits | pieces} over the workspace (rows never spill into the next slot)
     EncodeFn enc = encode_fn();
-    cuuint64_t dims[3] = {(cuuint64_t)g.N, (cuuint64_t)g.M, (cuuint64_t)p.splits};
+    cuuint64_t dims[3] = {(cuuint64_t)g.N, (cuuint64_t)g.M, (cuuint64_t)(p.streamk ? sk_pieces : p.splits)};
     cuuint64_t strides[2] = {(cuuint64_t)(g.N * 4), (cuuint64_t)(g.M * g.N * 4)};
     cuuint32_t box[3] = {32, 32, 1};
     cuuint32_t es[3] = {1, 1, 1};
-    CUresult r = enc(&mc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, ws, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+    CUresult r = enc(&mp, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, ws, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(TX_E_CUDA, "tx_gemm: split-K workspace map failed");
-    p.tma_store = 1;
   }
   CUtensorMap mx;
   memset(&mx, 0, sizeof(mx));
@@ -887,13 +1006,14 @@ int gemm_tc(const G& g, void* ws, size_t wsb, cudaStream_t st) {
   }
   const int units = sm_count() / cg;
   const int work = p.num_tiles * p.splits;
-  const int nclusters = work < units ? work : units;
+  const int nclusters = p.streamk ? units : (work < units ? work : units);
+  p.nclusters = nclusters;
   if (cg == 1) {
     if (!g_attr_set[1]) {
       TX_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<1>::SMEM));
       g_attr_set[1] = true;
     }
-    tc_gemm_kernel<1><<<nclusters, NUM_THREADS, Cfg<1>::SMEM, st>>>(ma, mb, mc, mx, mae, mbe, p);
+    tc_gemm_kernel<1><<<nclusters, NUM_THREADS, Cfg<1>::SMEM, st>>>(ma, mb, mc, mx, mae, mbe, mp, p);
   } else {
     if (!g_attr_set[2]) {
       TX_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<2>::SMEM));
@@ -911,11 +1031,15 @@ int gemm_tc(const G& g, void* ws, size_t wsb, cudaStream_t st) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    TX_CUDA(cudaLaunchKernelEx(&cfg, tc_gemm_kernel<2>, ma, mb, mc, mx, mae, mbe, p));
+    TX_CUDA(cudaLaunchKernelEx(&cfg, tc_gemm_kernel<2>, ma, mb, mc, mx, mae, mbe, mp, p));
   }
   if (p.splits > 1) {
     TX_CUDA(cudaGetLastError());
     return splitk_finalize((const float*)ws, g, p.splits, st);
+  }
+  if (p.streamk) {
+    TX_CUDA(cudaGetLastError());
+    return streamk_fixup((const float*)ws, g, p.num_m, p.num_n, BM * cg, bn, p.num_kb, nclusters, GROUP_M, st);
   }
   TX_CUDA(cudaGetLastError());
   return TX_OK;
