@@ -173,6 +173,25 @@ int tx_gemm(const tx_tensor* A, const tx_tensor* B, tx_tensor* C, const tx_epilo
 /* Which path tx_gemm would take (0 simt, 1 skinny, 2 tcgen05). */
 int tx_gemm_path(const tx_tensor* A, const tx_tensor* B, const tx_tensor* C, int mode, int* path);
 
+/* ------------------------------------------------------ fused layer grad
+ * The backward of a tanh layer h feeding a narrow dense layer z = h.W + b
+ * (k = z's width <= 16; the MLP's 10-class output), one pass over h.
+ * Replaces, from the differentiated graph, Dot.grad's two products
+ * (reference ops/linalg.py:68-70), the tanh-grad composite
+ * (ops/elemwise.py:126-157) and the bias gradient Sum[0]
+ * (ops/reductions.py:87-112 via ops/elemwise.py:411-442):
+ *   dh = dot(dz, wt) * (1 - h^2)   dz [B,k], wt = W^T [k,H] (strides), h, dh [B,H]
+ *   gW = epi(dot(h^T, dz))         [H,k]; epi NONE or SGD (aux = W, C may alias it)
+ *   db = sum(dh, axis 0)           [H]; skipped when db is NULL or db->data is NULL
+ * gW and db are summed in a fixed order (deterministic).  Layouts the fused
+ * kernel does not take (float64, k > 16, unaligned rows) run the three ops
+ * through tx_gemm / tx_reduce with the same workspace. */
+int tx_narrow_grad_workspace(const tx_tensor* dz, const tx_tensor* wt, const tx_tensor* h, const tx_tensor* dh,
+                             const tx_tensor* gw, const tx_tensor* db, int mode, size_t* bytes);
+int tx_narrow_grad(const tx_tensor* dz, const tx_tensor* wt, const tx_tensor* h, tx_tensor* dh, tx_tensor* gw,
+                   const tx_epilogue* gw_epi, tx_tensor* db, int mode, void* workspace, size_t workspace_bytes,
+                   void* stream);
+
 /* ------------------------------------------------------------------ NCCL
  * Gradient sync for data-parallel updates (new; Platoon-style synchronous
  * DP).  libnccl.so.2 is dlopen'ed (the one torch loaded). */

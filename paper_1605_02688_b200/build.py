@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libtexpr_b200.so")
 SOURCES = ["tx_runtime.cu", "tx_nvrtc.cu", "tx_reduce.cu", "tx_gemm.cu", "tx_gemm_simt.cu",
-           "tx_gemm_tc.cu", "tx_nccl.cu", "tx_conv.cu"]
+           "tx_gemm_tc.cu", "tx_nccl.cu", "tx_conv.cu", "tx_narrow.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", 

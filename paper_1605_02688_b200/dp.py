@@ -67,6 +67,20 @@ def propagate(order, inputs_state: dict) -> ShardPlan:
             for o in n.outputs:
                 st[o.id] = REPLICATED
             continue
+        rule = getattr(op, "shard_rule", None)
+        if rule is not None:
+            outs = rule(ins, sharded, PARTIAL, REPLICATED)
+            if outs is None:
+                raise NotSupported(f"{op.name}: no data-parallel rule for operand states {ins}")
+            for o, s in zip(n.outputs, outs):
+                if s == PARTIAL:
+                    st[o.id] = REPLICATED  # reduced across ranks as soon as it is produced
+                    plan.partial_vars.add(o.id)
+                else:
+                    st[o.id] = s
+            if any(s == PARTIAL for s in outs):
+                plan.partial_nodes.append(n)
+            continue
         if isinstance(op, (Elemwise, Composite)):
             out_nd = n.outputs[0].type.ndim
             axes = set()

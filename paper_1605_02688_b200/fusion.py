@@ -17,6 +17,7 @@ inlined as literals.
 from __future__ import annotations
 
 from .elemwise import Composite, Elemwise, EwProgram
+from .errors import CycleDetected
 from .graph import Constant, apply
 from .rewrite import register_rewrite
 
@@ -314,6 +315,53 @@ def _fuse_sgd_updates(fgraph, ctx, emit) -> int:
     return applied
 
 
+def _fuse_narrow_grads(fgraph, emit) -> int:
+    """Backward of a tanh layer h feeding a narrow layer: the three nodes
+    that each stream a [B,H] tensor --
+        dh = dot+mul_1msqr(dz, wt, h)          (dz [B,k], k small)
+        gW = dot(h^T, dz)  or  dot+sgd(h^T, dz, w)
+        db = sum[0](dh)                         (optional)
+    -- become one narrow_grad node (one read of h, one write of dh)."""
+    from .linalg import EPI_MUL_1MSQR, EPI_SGD, Dot, DotEpilogue, NarrowLayerGrad
+    from .reduce import Sum
+    from .shaping import DimShuffle
+    applied = 0
+    for o in list(fgraph.toposort()):
+        if o.id not in fgraph.nodes or not (isinstance(o.op, DotEpilogue) and o.op.kind == EPI_MUL_1MSQR):
+            continue
+        dz, wt, h = o.inputs
+        if dz.type.ndim != 2 or wt.type.ndim != 2 or dz.type.dtype != h.type.dtype:
+            continue
+        k = None
+        for c in fgraph.node_clients(dz):
+            if c is o or len(c.inputs) < 2 or c.inputs[1] is not dz or not c.inputs[0].owner:
+                continue
+            t = c.inputs[0].owner
+            if not (isinstance(t.op, DimShuffle) and t.op.pattern == (1, 0) and t.inputs[0] is h):
+                continue
+            if type(c.op) is Dot or (isinstance(c.op, DotEpilogue) and c.op.kind == EPI_SGD):
+                k = c
+                break
+        if k is None:
+            continue
+        dh = o.outputs[0]
+        s = next((c for c in fgraph.node_clients(dh) if isinstance(c.op, Sum) and tuple(c.op.axes) == (0,)), None)
+        sgd = isinstance(k.op, DotEpilogue)
+        op = NarrowLayerGrad(sgd, k.op.alpha if sgd else 0.0, k.op.alpha_dtype if sgd else "float32", s is not None)
+        outs = apply(op, [dz, wt, h] + ([k.inputs[2]] if sgd else []))
+        old = [dh, k.outputs[0]] + ([s.outputs[0]] if s is not None else [])
+        if [v.type for v in outs] != [v.type for v in old]:
+            continue
+        try:
+            fgraph.replace_all(list(zip(old, outs)), "fuse_gemm_epilogue")
+        except CycleDetected:
+            continue
+        emit(node=o, replaced="dot+mul_1msqr, " + getattr(k.op, "display_name", k.op.name)
+             + (", sum[0]" if s is not None else ""), replacement=op.display_name)
+        applied += 1
+    return applied
+
+
 @register_rewrite("fuse_gemm_epilogue", "abstract_select", "global")
 def fuse_gemm_epilogue(fgraph, ctx, emit) -> int:
     from .linalg import EPI_BIAS, EPI_BIAS_TANH_DUAL, EPI_MUL_AUX, Dot, DotEpilogue
@@ -355,3 +403,11 @@ def fuse_gemm_epilogue(fgraph, ctx, emit) -> int:
         emit(node=c, replaced=f"dot+{getattr(c.op, 'display_name', c.op.name)}", replacement=outs[0].owner.op.display_name)
         applied += 1
     return applied
+
+
+@register_rewrite("fuse_narrow_grad", "abstract_select", "global")
+def fuse_narrow_grad(fgraph, ctx, emit) -> int:
+    """Runs after fuse_gemm_epilogue (registration order); separate so it can
+    be excluded on its own (its gW / db sums run in a different order than
+    the unfused kernels: equal within fp32 tolerance, not bitwise)."""
+    return _fuse_narrow_grads(fgraph, emit)

@@ -191,3 +191,131 @@ class DotEpilogue(Op):
     @classmethod
     def from_payload(cls, payload, decode_graph=None):
         return cls(payload["kind"], payload.get("alpha", 0.0), payload.get("alpha_dtype", "float32"))
+
+
+@register_op
+class NarrowLayerGrad(Op):
+    """The backward of a tanh layer ``h`` feeding a narrow dense layer
+    (``z = h.W + b``, z of width k <= 16), fused into one pass over h.
+
+    Produced only by the ``fuse_gemm_epilogue`` rewrite (``fusion.py``) from
+    nodes the differentiated graph already holds (reference Dot.grad
+    ``ops/linalg.py:68-70``, the tanh-grad composite, the bias gradient's
+    ``Sum[0]`` from ``sum_to_matching_shape`` ``ops/elemwise.py:411-442``).
+    Inputs (dz, wt, h[, w]); outputs, with the replaced nodes' rounding:
+      dh = dot(dz, wt) * (1 - h^2)        the dot+mul_1msqr node
+      gW = dot(h^T, dz)                   or, with ``sgd``, w - alpha * dot(h^T, dz)
+      db = sum(dh, axis=0)                only with ``with_db``
+    Lowered to ``tx_narrow_grad`` (``csrc/tx_narrow.cu``).
+    """
+
+    name = "narrow_grad"
+    has_grad = False
+    # the SGD output is written element by element in a second kernel after
+    # every read of w (and of its transposed view wt): in-place safe
+    elementwise_in_place = True
+    reads_before_writes = True
+
+    def __init__(self, sgd: bool = False, alpha: float = 0.0, alpha_dtype: str = "float32", with_db: bool = False):
+        self.sgd = bool(sgd)
+        self.alpha = float(alpha)
+        self.alpha_dtype = alpha_dtype
+        self.with_db = bool(with_db)
+
+    @property
+    def display_name(self):
+        return "narrow_grad" + ("+sgd" if self.sgd else "") + ("+db" if self.with_db else "")
+
+    def attrs_key(self):
+        return (self.sgd, self.alpha, self.alpha_dtype, self.with_db)
+
+    def infer_types(self, input_types):
+        dz, wt, h = input_types[:3]
+        (t_dh,) = Dot().infer_types([dz, wt])
+        t_gw = TensorType(t_dh.dtype, (h.broadcastable[1], dz.broadcastable[1]))
+        out = [t_dh, t_gw]
+        if self.with_db:
+            out.append(TensorType(t_dh.dtype, (t_dh.broadcastable[1],)))
+        return out
+
+    def check_runtime_shapes(self, node, shapes):
+        dz, wt, h = shapes[:3]
+        Dot().check_runtime_shapes(node, [dz, wt])
+        if tuple(h) != (dz[0], wt[1]):
+            raise ShapeMismatch(f"narrow_grad: h {tuple(h)} does not match dot(dz, wt) {(dz[0], wt[1])}")
+        if self.sgd and tuple(shapes[3]) != (h[1], dz[1]):
+            raise ShapeMismatch("narrow_grad: updated weight shape differs from the gradient's")
+
+    def infer_shape(self, node, input_shapes):
+        dz, wt, h = input_shapes[:3]
+        if UNKNOWN_SHAPE in (dz, wt, h):
+            return [UNKNOWN_SHAPE] * len(node.outputs)
+        out = [(dz[0], wt[1]), (h[1], dz[1])]
+        if self.with_db:
+            out.append((wt[1],))
+        return out
+
+    def grad(self, inputs, output_grads):
+        from .errors import NotDifferentiable
+        raise NotDifferentiable("narrow_grad is created after differentiation")
+
+    def shard_rule(self, states, sharded, partial, replicated):
+        """Data-parallel states: batch rows sharded, weights replicated ->
+        dh row-sharded, gW and db partial sums."""
+        dz, wt, h = states[:3]
+        if dz != sharded(0) or h != sharded(0) or wt != replicated or (self.sgd and states[3] != replicated):
+            return None
+        if self.sgd:
+            return None  # an update from a partial sum needs the allreduce first
+        return [sharded(0), partial] + ([partial] if self.with_db else [])
+
+    def expand(self, inputs):
+        """Reference-op form (dot, elemwise, sum) with the same scalar ops."""
+        from .elemwise import make
+        from .reduce import Sum
+        dz, wt, h = inputs[:3]
+        dh = make("mul", [dot(dz, wt), make("sub", [1.0, make("sqr", [h])])])
+        gw = dot(dimshuffle(h, (1, 0)), dz)
+        if self.sgd:
+            from .graph import Constant
+            gw = make("sub", [inputs[3], make("mul", [Constant(self.alpha, dtype=self.alpha_dtype), gw])])
+        out = [dh, gw]
+        if self.with_db:
+            out.append(apply(Sum((0,)), [dh])[0])
+        return out
+
+    def workspace_bytes(self, plan, node):
+        return plan.lib.narrow_grad_workspace(*self._tensors(plan, node, noptr=True), plan.fn.gemm_mode)
+
+    def _tensors(self, plan, node, noptr=False):
+        from . import native
+        mk = plan._tx_noptr if noptr else plan.tx
+        lay = plan.layout
+        dz, wt, h = (mk(lay(v)) for v in node.inputs[:3])
+        dh, gw = mk(lay(node.outputs[0])), mk(lay(node.outputs[1]))
+        db = mk(lay(node.outputs[2])) if self.with_db else native.TxTensor()
+        return dz, wt, h, dh, gw, db
+
+    def lower(self, node, plan):
+        from . import native
+        dz, wt, h, dh, gw, db = self._tensors(plan, node)
+        epi = native.TxEpilogue()
+        if self.sgd:
+            epi.kind = native.EPI_SGD
+            epi.aux = plan.tx(node.inputs[3])
+            epi.alpha = self.alpha
+        ws, wsb = plan.workspace(node)
+        mode = plan.fn.gemm_mode
+        lib = plan.lib
+        f = lib.lib.tx_narrow_grad
+
+        def launch(stream):
+            lib.check(f(dz, wt, h, dh, gw, epi, db, mode, ws, wsb, stream))
+        plan.add_launch(launch)
+
+    def attrs_payload(self, encode_graph=None):
+        return {"sgd": self.sgd, "alpha": self.alpha, "alpha_dtype": self.alpha_dtype, "with_db": self.with_db}
+
+    @classmethod
+    def from_payload(cls, payload, decode_graph=None):
+        return cls(payload["sgd"], payload["alpha"], payload["alpha_dtype"], payload["with_db"])

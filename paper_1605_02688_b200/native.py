@@ -24,7 +24,7 @@ EXPORTS = [
     "tx_ew_compile", "tx_ew_check", "tx_ew_launch", "tx_ew_destroy",
     "tx_kernel_compile", "tx_kernel_launch", "tx_kernel_destroy",
     "tx_reduce_workspace", "tx_reduce", "tx_check_values", "tx_im2col", "tx_col2im",
-    "tx_gemm_workspace", "tx_gemm", "tx_gemm_path",
+    "tx_gemm_workspace", "tx_gemm", "tx_gemm_path", "tx_narrow_grad_workspace", "tx_narrow_grad",
     "tx_nccl_unique_id", "tx_nccl_init", "tx_nccl_allreduce_sum", "tx_nccl_destroy",
 ]
 
@@ -88,6 +88,8 @@ class Library:
             "tx_gemm_workspace": [P(TxTensor), P(TxTensor), P(TxTensor), ctypes.c_int, P(sz)],
             "tx_gemm": [P(TxTensor), P(TxTensor), P(TxTensor), P(TxEpilogue), ctypes.c_int, vp, sz, vp],
             "tx_gemm_path": [P(TxTensor), P(TxTensor), P(TxTensor), ctypes.c_int, P(ctypes.c_int)],
+            "tx_narrow_grad_workspace": [P(TxTensor)] * 6 + [ctypes.c_int, P(sz)],
+            "tx_narrow_grad": [P(TxTensor)] * 5 + [P(TxEpilogue), P(TxTensor), ctypes.c_int, vp, sz, vp],
             "tx_nccl_unique_id": [ctypes.c_char_p], "tx_nccl_init": [ctypes.c_int, ctypes.c_int, ctypes.c_char_p, P(vp)],
             "tx_nccl_allreduce_sum": [vp, vp, sz, ctypes.c_int, vp], "tx_nccl_destroy": [vp],
         }
@@ -189,6 +191,11 @@ class Library:
         n = ctypes.c_size_t()
         self.check(self.lib.tx_gemm_workspace(ctypes.byref(a), ctypes.byref(b), ctypes.byref(c), mode,
                                               ctypes.byref(n)))
+        return n.value
+
+    def narrow_grad_workspace(self, dz, wt, h, dh, gw, db, mode=GEMM_AUTO) -> int:
+        n = ctypes.c_size_t()
+        self.check(self.lib.tx_narrow_grad_workspace(dz, wt, h, dh, gw, db, mode, ctypes.byref(n)))
         return n.value
 
     def gemm_path(self, a, b, c, mode=GEMM_AUTO) -> int:

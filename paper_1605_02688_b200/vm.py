@@ -334,7 +334,8 @@ class CompiledFunction:
                 # for the SGD GEMM epilogue (each element read, then written, once)
                 if not (isinstance(p.op, (Elemwise, Composite)) or getattr(p.op, "elementwise_in_place", False)):
                     continue
-                if any(x is not var and _is_view_of(x, var) for x in p.inputs):
+                if not getattr(p.op, "reads_before_writes", False) and \
+                        any(x is not var and _is_view_of(x, var) for x in p.inputs):
                     continue
             others = [r for r in readers if r is not p]
             trial = dict(extra)
@@ -631,7 +632,7 @@ class StepPlan:
         partial_ids = set()
         partial_vars = []
         if fn.shard is not None:
-            partial_ids = {o.id for n in fn.shard.partial_nodes for o in n.outputs}
+            partial_ids = set(fn.shard.partial_vars)
         for n in order:
             ins = [self.lay[x.id] for x in n.inputs]
             shapes = [l.shape for l in ins]
@@ -981,6 +982,8 @@ class StepPlan:
             if not mask:
                 return 0
             return self.lib.reduce_workspace(n.op.tx_code, x, mask)
+        if hasattr(n.op, "workspace_bytes"):
+            return n.op.workspace_bytes(self, n)
         if isinstance(n.op, Dot) or hasattr(n.op, "gemm_operands"):
             a, b, c = self._dot_views(n, noptr=True)
             return self.lib.gemm_workspace(a, b, c, self.fn.gemm_mode)

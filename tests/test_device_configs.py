@@ -120,7 +120,8 @@ def test_data_parallel_single_rank_matches_plain_step():
     gb = C.build_mlp(T, B=B, H=H)
     dp = DataParallel(world_size=1, rank=0, bucket_bytes=1 << 20)
     fb = T.compile(gb["inputs"], gb["outputs"], updates=gb["updates"], data_parallel=dp, row_fusion=False)
-    assert len(fb.shard.partial_nodes) == 7
+    # dW1..3, db1..3 and the cost's batch sum (the tanh layers' backward nodes carry two each)
+    assert len(fb.shard.partial_vars) == 7
     for _ in range(3):
         ca, cb = fa(x, y)[0], fb(x, y)[0]
         assert ca == cb
@@ -183,10 +184,32 @@ def test_gemm_epilogue_fusion_is_bit_exact():
     ga = C.build_mlp(T, B=B, H=H)
     fa = T.compile(ga["inputs"], ga["outputs"], updates=ga["updates"], exclude=("fuse_gemm_epilogue",))
     gb = C.build_mlp(T, B=B, H=H)
-    fb = T.compile(gb["inputs"], gb["outputs"], updates=gb["updates"])
+    fb = T.compile(gb["inputs"], gb["outputs"], updates=gb["updates"], exclude=("fuse_narrow_grad",))
     kinds = [getattr(n.op, "display_name", n.op.name) for n in fb.order]
     assert kinds.count("dot+bias_tanh") == 2 and kinds.count("dot+mul_1msqr") == 2
     for _ in range(2):
         assert fa(x, y)[0] == fb(x, y)[0]
     for pa, pb in zip(ga["params"], gb["params"]):
         assert np.array_equal(pa.get_value(), pb.get_value())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("B,H,K", [(256, 512, 10), (1000, 1028, 7), (8192, 4096, 10), (96, 64, 16), (40, 36, 1)])
+def test_narrow_grad_fusion_matches_unfused(B, H, K):
+    """The fused narrow-layer backward (dh, dW of the narrow layer, db in one
+    pass over h) equals the unfused dot+mul_1msqr / dot+sgd / sum[0] nodes
+    within fp32 reassociation, and the hidden layer's wide case (fallback
+    inside tx_narrow_grad) runs the same kernels as before."""
+    x, y = C.inputs_mlp(B=B, D=64, K=K)
+    ga = C.build_mlp(T, B=B, D=64, H=H, K=K)
+    fa = T.compile(ga["inputs"], ga["outputs"], updates=ga["updates"], exclude=("fuse_narrow_grad",))
+    gb = C.build_mlp(T, B=B, D=64, H=H, K=K)
+    fb = T.compile(gb["inputs"], gb["outputs"], updates=gb["updates"])
+    kinds = [getattr(n.op, "display_name", n.op.name) for n in fb.order]
+    assert kinds.count("narrow_grad+sgd+db") == 2 and "dot+mul_1msqr" not in kinds
+    for _ in range(3):
+        ca, cb = fa(x, y)[0], fb(x, y)[0]
+        assert abs(ca - cb) <= 1e-5 * abs(ca)
+    for pa, pb in zip(ga["params"], gb["params"]):
+        a, b = pa.get_value(), pb.get_value()
+        assert np.linalg.norm(a - b) <= 1e-5 * max(np.linalg.norm(a), 1e-30), pa.name

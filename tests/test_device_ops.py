@@ -240,3 +240,71 @@ def test_dot_shape_mismatch_raises():
     f = T.compile([va, vb], T.dot(va, vb))
     with pytest.raises(ShapeMismatch):
         f(np.zeros((3, 4), np.float32), np.zeros((5, 6), np.float32))
+
+
+def _narrow_case(B, H, k, rng, sgd=False, pad_h=0, dtype=np.float32, mode=0):
+    """tx_narrow_grad through the C ABI vs the oracle's three separate ops."""
+    import ctypes
+
+    import torch
+
+    from paper_1605_02688_b200 import native
+    lib = native.device_library(0)
+    dz = (rng.standard_normal((B, k)) * 1e-2).astype(dtype)
+    W = (rng.standard_normal((H, k)) * 0.05).astype(dtype)
+    h = np.tanh(rng.standard_normal((B, H))).astype(dtype)
+    want_dh = O.dot(dz, W.T) * (1 - h * h)
+    want_gw = O.dot(h.T, dz)
+    want_db = want_dh.astype(np.float64).sum(0)
+    tdev = {}
+    # h (and dh) optionally as row-padded views: ragged row pitch -> fallback path
+    hp = np.zeros((B, H + pad_h), dtype)
+    hp[:, :H] = h
+    tdev["dz"], tdev["W"], tdev["h"] = (torch.from_numpy(np.ascontiguousarray(v)).cuda() for v in (dz, W, hp))
+    tdev["dh"] = torch.zeros((B, H + pad_h), dtype=getattr(torch, np.dtype(dtype).name), device="cuda")
+    tdev["gw"] = tdev["W"] if sgd else torch.zeros((H, k), dtype=tdev["W"].dtype, device="cuda")
+    tdev["db"] = torch.zeros(H, dtype=tdev["W"].dtype, device="cuda")
+    dt = np.dtype(dtype).name
+    mk = native.make_tensor
+    tdz = mk(tdev["dz"].data_ptr(), dt, (B, k), (k, 1))
+    twt = mk(tdev["W"].data_ptr(), dt, (k, H), (1, k))
+    th = mk(tdev["h"].data_ptr(), dt, (B, H), (H + pad_h, 1))
+    tdh = mk(tdev["dh"].data_ptr(), dt, (B, H), (H + pad_h, 1))
+    tgw = mk(tdev["gw"].data_ptr(), dt, (H, k), (k, 1))
+    tdb = mk(tdev["db"].data_ptr(), dt, (H,), (1,))
+    epi = native.TxEpilogue()
+    lr = 0.25
+    if sgd:
+        epi.kind = native.EPI_SGD
+        epi.aux = mk(tdev["W"].data_ptr(), dt, (H, k), (k, 1))
+        epi.alpha = lr
+    wsb = lib.narrow_grad_workspace(tdz, twt, th, tdh, tgw, tdb, mode)
+    ws = torch.empty(max(wsb, 256), dtype=torch.uint8, device="cuda")
+    lib.check(lib.lib.tx_narrow_grad(tdz, twt, th, tdh, tgw, ctypes.byref(epi), tdb, mode,
+                                     ctypes.c_void_p(ws.data_ptr()), wsb, None))
+    torch.cuda.synchronize()
+    dh = tdev["dh"].cpu().numpy()[:, :H]
+    scale = O.dot(np.abs(dz), np.abs(W.T)) + 1e-30
+    # products are exact-fp32 FMAs (CUDA cores): reassociation-level error only
+    assert np.all(np.abs(dh - want_dh) <= 1e-5 * scale + 1e-7)
+    gw = tdev["gw"].cpu().numpy()
+    gscale = O.dot(np.abs(h.T), np.abs(dz)) + 1e-30
+    if sgd:
+        want_w = W - np.float32(lr) * want_gw
+        assert np.all(np.abs(gw - want_w) <= lr * (1e-5 * gscale) + 1e-6 * np.abs(W) + 1e-7)
+    else:
+        assert np.all(np.abs(gw - want_gw) <= 1e-5 * gscale + 1e-7)
+    db = tdev["db"].cpu().numpy()
+    assert np.all(np.abs(db - want_db) <= 2e-6 * np.abs(want_dh).sum(0) + 1e-7)
+
+
+@pytest.mark.parametrize("B,H,k", [(8192, 4096, 10), (1, 4, 1), (37, 1028, 16), (4100, 2052, 3), (40, 36, 7)])
+def test_narrow_grad_fused(B, H, k, rng):
+    _narrow_case(B, H, k, rng)
+
+
+def test_narrow_grad_sgd_in_place_and_fallbacks(rng):
+    _narrow_case(2048, 512, 10, rng, sgd=True)                  # fused, SGD epilogue writing over W
+    _narrow_case(300, 130, 10, rng, pad_h=2)                    # unaligned rows -> tx_gemm x2 + tx_reduce
+    _narrow_case(300, 128, 17, rng, mode=1)                      # k > 16 -> fallback (exact-fp32 GEMM mode)
+    _narrow_case(96, 64, 5, rng, sgd=True, dtype=np.float64)   # float64 -> fallback

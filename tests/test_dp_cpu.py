@@ -132,6 +132,12 @@ def test_propagation_through_fused_gemm_epilogues():
     run_preset(fg, "fast_run", ctx=RewriteContext(execution_bound=True, data_parallel=True))
     names = [getattr(n.op, "display_name", n.op.name) for n in fg.toposort()]
     assert "dot+sgd" not in names
-    assert names.count("dot+bias_tanh") == 2 and names.count("dot+mul_1msqr") == 2
+    assert names.count("dot+bias_tanh") == 2 and names.count("dot+mul_1msqr") == 0
+    # each tanh layer's backward (dh, dW of the next layer, db) is one fused
+    # node with two partial outputs
+    assert names.count("narrow_grad+db") == 2
     plan = dp.propagate(fg.toposort(), {repl[v].id: dp.sharded(0) for v in g["inputs"]})
-    assert len(plan.partial_nodes) == 7
+    assert len(plan.partial_nodes) == 5 and len(plan.partial_vars) == 7
+    ng = next(n for n in fg.toposort() if n.op.name == "narrow_grad")
+    assert plan.state[ng.outputs[0].id] == dp.sharded(0)
+    assert {o.id for o in ng.outputs[1:]} <= plan.partial_vars

@@ -73,22 +73,39 @@ def traffic(key, rep):
 
 
 def launches(path):
+    """Per-launch duration (and DRAM bytes when the capture had
+    dram__bytes_read/write.sum), then per-kernel totals."""
     rows = list(csv.reader(open(path)))
     hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     h = rows[hi]
     ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
-    print(f"{'#':>4} {'ns':>12}  kernel")
-    agg = collections.OrderedDict()
+    mi = h.index("Metric Name") if "Metric Name" in h else None
+    idi = h.index("ID") if "ID" in h else None
+    launches_ = collections.OrderedDict()  # launch id -> [name, ns, bytes]
     for n, r in enumerate(rows[hi + 1:]):
         if len(r) <= vi:
             continue
-        v = float(r[vi].replace(",", "")) * {"nsecond": 1, "usecond": 1e3, "msecond": 1e6}.get(r[ui], 1)
-        name = r[ki]
-        print(f"{n:>4} {v:>12.0f}  {name[:110]}")
-        agg.setdefault(name[:80], []).append(v)
-    print("\nper kernel (count, mean us, total us):")
-    for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
-        print(f"{len(v):>5} {sum(v) / len(v) / 1e3:>10.2f} {sum(v) / 1e3:>10.1f}  {k}")
+        key = r[idi] if idi is not None else n
+        metric = r[mi] if mi is not None else "gpu__time_duration.sum"
+        ent = launches_.setdefault(key, [r[ki], 0.0, None])
+        if metric.startswith("gpu__time_duration"):
+            ent[1] = float(r[vi].replace(",", "")) * {"nsecond": 1, "usecond": 1e3, "msecond": 1e6}.get(r[ui], 1)
+        elif metric.startswith("dram__bytes"):
+            ent[2] = (ent[2] or 0.0) + _bytes(r[vi], r[ui])
+    has_bytes = any(e[2] is not None for e in launches_.values())
+    print(f"{'#':>4} {'ns':>12} " + (f"{'DRAM MB':>9} {'GB/s':>7} " if has_bytes else "") + " kernel")
+    agg = collections.OrderedDict()
+    for n, (name, ns, nb) in enumerate(launches_.values()):
+        extra = f"{nb / 1e6:>9.1f} {nb / ns if ns else 0:>7.0f} " if has_bytes else ""
+        print(f"{n:>4} {ns:>12.0f} {extra} {name[:100]}")
+        a = agg.setdefault(name[:80], [0, 0.0, 0.0])
+        a[0] += 1
+        a[1] += ns
+        a[2] += nb or 0.0
+    print("\nper kernel (count, mean us, total us" + (", DRAM MB per launch, GB/s" if has_bytes else "") + "):")
+    for k, (c, ns, nb) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+        extra = f" {nb / c / 1e6:>9.1f} {nb / ns if ns else 0:>7.0f}" if has_bytes else ""
+        print(f"{c:>5} {ns / c / 1e3:>10.2f} {ns / 1e3:>10.1f}{extra}  {k}")
 
 
 if __name__ == "__main__":
