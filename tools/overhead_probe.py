@@ -54,5 +54,31 @@ def main():
     pstats.Stats(pr).sort_stats("tottime").print_stats(14)
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and len(sys.argv) == 1:
     main()
+
+
+def host_calls():
+    """f(x, y) with NumPy arrays (the public call): where its time goes."""
+    torch.cuda.set_device(0)
+    g = C.build_logreg(T)
+    f = T.compile(g["inputs"], g["outputs"], updates=g["updates"])
+    x, y = C.inputs_logreg()
+    for _ in range(5):
+        f(x, y)
+    n = 300
+    t0 = time.perf_counter()
+    for _ in range(n):
+        f(x, y)
+    t1 = time.perf_counter()
+    print(f"f(x, y) host arrays: {1e6 * (t1 - t0) / n:.1f} us/call")
+    pr = cProfile.Profile()
+    pr.enable()
+    for _ in range(200):
+        f(x, y)
+    pr.disable()
+    pstats.Stats(pr).sort_stats("tottime").print_stats(18)
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "host":
+    host_calls()
