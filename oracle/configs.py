@@ -117,7 +117,7 @@ class CpuFunction:
         cloned, _ = clone_outputs(outs + uvals, repl)
         self.fg = FunctionGraph([repl[v] for v in full], cloned)
         # the reference has no GEMM epilogues: keep its node list
-        run_preset(self.fg, preset, exclude=tuple(exclude) + ("fuse_gemm_epilogue",))
+        run_preset(self.fg, preset, exclude=tuple(exclude) + ("fuse_gemm_epilogue", "fuse_narrow_grad"))
         self.in_vars = [repl[v] for v in inputs]
         self.sh_vars = [repl[v] for v in found]
         self.n_out = len(outs)

@@ -786,7 +786,12 @@ int gemm_tc_eligible(const G& g) {
   // still beats the CUDA-core tile kernel once the product is large (the
   // [20 x 600] x [600 x 10000] per-step GEMMs of an LSTM language model);
   // small thin products stay on the exact SIMT path
-  if ((g.M < 64 || g.N < 64) && (double)g.M * (double)g.N * (double)g.K < (double)(1 << 20)) return TX_E_UNSUPPORTED;
+  if (g.M < 64 || g.N < 64) {
+    static const int thin_log2 = getenv("TX_GEMM_THIN_MIN") ? atoi(getenv("TX_GEMM_THIN_MIN")) : 20;
+    static const int64_t thin_kmin = getenv("TX_GEMM_THIN_KMIN") ? atoll(getenv("TX_GEMM_THIN_KMIN")) : 0;
+    if ((double)g.M * (double)g.N * (double)g.K < (double)(1ll << thin_log2) || g.K < thin_kmin)
+      return TX_E_UNSUPPORTED;
+  }
   if (g.M > INT32_MAX || g.N > INT32_MAX || g.K > INT32_MAX) return TX_E_UNSUPPORTED;
   if (g.scn != 1) return TX_E_UNSUPPORTED;
   if (((uintptr_t)g.A & 15) || ((uintptr_t)g.B & 15)) return TX_E_UNSUPPORTED;

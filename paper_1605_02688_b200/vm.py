@@ -279,8 +279,13 @@ class CompiledFunction:
         self.profile_nodes = False
         self._direct, self.order = self._schedule()
         self.has_lazy = any(getattr(n.op, "lazy", False) for n in self.order)
-        if self.nan_guard is not None or self.has_lazy:
-            self._direct = {}   # updates are committed only after the whole step (guard / lazy walk) finished
+        # integer division raises ZeroDivisionError from a device flag read after
+        # the step: like the NaN guard, that must happen before any update lands
+        self.has_int_div = any(codegen.has_int_div(getattr(n.op, "program", None)
+                                                   or EwProgram.single(n.op.kernel, [x.type.dtype for x in n.inputs]))
+                               for n in self.order if isinstance(n.op, (Elemwise, Composite)))
+        if self.nan_guard is not None or self.has_lazy or self.has_int_div:
+            self._direct = {}   # updates are committed only after the whole step (guard / lazy walk / flags) finished
         if self.has_lazy:
             self.row_fusion = False
             if self.dp is not None:
@@ -445,6 +450,8 @@ class CompiledFunction:
         if plan.guard_slots:
             plan.check_guard(stream)      # raises NanDetected before any update is committed
         if plan.commit_launches:
+            if plan.flag is not None:
+                plan.check_flags(stream)  # raises ZeroDivisionError before any update is committed
             plan.run_commits(stream)
         if device_out:
             outs = plan.device_outputs()
@@ -757,11 +764,14 @@ class StepPlan:
             excl = {n.id for n in fn.shard.partial_nodes} if fn.shard is not None else set()
             self.row_groups = rowfuse.find_groups(self, order, g, excl)
             for grp in self.row_groups:
-                produced = {o.id for n in grp.members for o in n.outputs}
+                # the group's kernel runs at its last member and the deferred
+                # nodes right after it: everything they read or write (member
+                # outputs included, even those only other members read) must
+                # stay allocated until then
                 for n in grp.members + grp.deferred:
-                    for x in n.inputs:
-                        if x.id not in produced and x.id in self.lay:
-                            touch(self.lay[x.id], grp.last_pos)  # read at (or after) the launch point
+                    for x in list(n.inputs) + list(n.outputs):
+                        if x.id in self.lay:
+                            touch(self.lay[x.id], grp.last_pos)
 
         # ---- arena allocation with in-place reuse for elementwise kernels
         alloc = ArenaAllocator()
@@ -916,7 +926,7 @@ class StepPlan:
             self._emit_copy(src, dst)
         for src, dst in self.commits:
             self._emit_copy(src, dst)
-        if (fn.nan_guard is not None or fn.has_lazy) and self.commits:
+        if (fn.nan_guard is not None or fn.has_lazy or fn.has_int_div) and self.commits:
             # updates land only after the guard passed (reference runtime.py:415-421)
             n_commit = len(self.commits)
             self.commit_launches = [fn_ for _, fn_ in self.launches[-n_commit:]]

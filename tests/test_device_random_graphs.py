@@ -1,0 +1,124 @@
+"""Semantic preservation on random graphs (the reference's property test
+``test_rewrites.py:306-319`` runs 40 random graphs through its rewrites at
+rel 1e-10): here 80 (f64) + 40 (f32) seeded random expression graphs — elementwise ops with
+row/column broadcasting, sum/max/argmax over either axis, dot, dimshuffle,
+softmax / log-softmax / cross-entropy-shaped row regions —
+are compiled for the device (fast_run: fusion, GEMM epilogues, row fusion)
+and compared with the reference algorithm on the oracle kernels
+(``oracle.configs.CpuFunction``: same preset minus the device-only GEMM
+rewrites, NumPy per node).
+
+Tolerances: float64 |d - o| <= 1e-9 * max|o| (CUDA libm vs NumPy differ by
+an ulp, amplified by at most a few cancellations), float32 4e-5 * max|o|;
+NaN / inf positions must agree exactly and argmax indices bit-exactly.
+"""
+import numpy as np
+import pytest
+
+import paper_1605_02688_b200 as T
+from oracle import configs as C
+from paper_1605_02688_b200.elemwise import make
+
+pytestmark = pytest.mark.gpu
+
+R, Cc = 37, 53
+UNARY = ("neg", "tanh", "sigmoid", "sqr", "exp")
+BINARY = ("add", "sub", "mul", "maximum")
+
+
+def _random_graph(seed, dt):
+    rng = np.random.default_rng(seed)
+    x = T.matrix("x", dtype=dt)
+    y = T.matrix("y", dtype=dt)
+    w = T.matrix("w", dtype=dt)         # [C, C] for dot
+    v = T.vector("v", dtype=dt)         # [C] row-broadcast operand
+    inputs = [x, y, w, v]
+    mats, vecs_c, vecs_r = [x, y], [v], []
+
+    def pick(pool):
+        return pool[int(rng.integers(len(pool)))]
+    for _ in range(int(rng.integers(6, 14))):
+        r = rng.random()
+        if r < 0.22:
+            k = UNARY[int(rng.integers(len(UNARY)))]
+            a = pick(mats)
+            if k == "exp":
+                a = T.tanh(a)            # keep exp's argument bounded
+            mats.append(make(k, [a]))
+        elif r < 0.55:
+            k = BINARY[int(rng.integers(len(BINARY)))]
+            a = pick(mats)
+            s = rng.random()
+            if s < 0.5:
+                b = pick(mats)
+            elif s < 0.75 and vecs_c:
+                b = pick(vecs_c)                          # [C] broadcast over rows
+            elif vecs_r:
+                b = T.dimshuffle(pick(vecs_r), (0, "x"))  # [R,1] broadcast over columns
+            else:
+                b = pick(mats)
+            mats.append(make(k, [a, b] if rng.random() < 0.5 else [b, a]))
+        elif r < 0.75:
+            a = pick(mats)
+            ax = int(rng.integers(2))
+            red = T.sum if rng.random() < 0.6 else T.max
+            (vecs_c if ax == 0 else vecs_r).append(red(a, axis=ax))
+        elif r < 0.82:
+            mats.append(T.dot(pick(mats), w))
+        elif r < 0.9:
+            # softmax-shaped row regions (what row fusion groups): max, exp,
+            # row sums, division, log, one-hot of the row argmax
+            a = pick(mats)
+            m = T.max(a, axis=1)
+            e = T.exp(a - T.dimshuffle(m, (0, "x")))
+            p = e / T.dimshuffle(T.sum(e, axis=1), (0, "x"))
+            k = int(rng.integers(3))
+            if k == 0:
+                mats.append(p)
+            elif k == 1:
+                vecs_r.append(-T.sum(T.tanh(pick(mats)) * T.log(p), axis=1))
+            else:
+                mats.append(T.argmax_onehot(a, axis=1) * p + T.log(p))
+        else:
+            if vecs_r:
+                mats.append(pick(mats) * T.dimshuffle(T.tanh(pick(vecs_r)), (0, "x")))
+            else:
+                mats.append(T.tanh(pick(mats)) + pick(mats))
+    outs = [mats[-1]]
+    if vecs_c:
+        outs.append(vecs_c[-1])
+    if vecs_r:
+        outs.append(vecs_r[-1])
+    if rng.random() < 0.5:
+        outs.append(T.argmax(mats[-1], axis=int(rng.integers(2))))
+    outs.append(T.sum(mats[int(rng.integers(len(mats)))]))
+    vals = [rng.standard_normal((R, Cc)), rng.standard_normal((R, Cc)),
+            rng.standard_normal((Cc, Cc)) / np.sqrt(Cc), rng.standard_normal(Cc)]
+    return inputs, outs, [a.astype(dt) for a in vals]
+
+
+def _check(got, want, rel):
+    got, want = np.asarray(got), np.asarray(want)
+    assert got.shape == want.shape and got.dtype == want.dtype
+    if want.dtype.kind in "iu":
+        np.testing.assert_array_equal(got, want)
+        return
+    assert np.array_equal(np.isnan(got), np.isnan(want))
+    inf = np.isinf(want)
+    assert np.array_equal(got[inf], want[inf])
+    fin = np.isfinite(want)
+    if fin.any():
+        scale = np.abs(want[fin]).max()
+        assert np.abs(got[fin] - want[fin]).max() <= rel * max(scale, 1e-300)
+
+
+@pytest.mark.parametrize("dt,rel", [("float64", 1e-9), ("float32", 4e-5)])
+def test_random_graphs_match_reference_algorithm(dt, rel):
+    for seed in range(80 if dt == "float64" else 40):
+        inputs, outs, vals = _random_graph(1000 + seed, dt)
+        dev = T.compile(inputs, outs)
+        ref = C.CpuFunction(T, inputs, outs)
+        got = dev(*vals)
+        want = ref(*vals)
+        for g, w in zip(got, want):
+            _check(g, w, rel)

@@ -336,3 +336,51 @@ def test_breakpoint_fires_passes_through_and_aborts():
         g(1.0)
     assert float(s.get_value()) == 1.0      # aborted call committed nothing
     T.register_breakpoint_handler("d3", None)
+
+
+def test_allow_gc_is_bit_exact(rng):
+    """reference test_runtime.py:177-186: keeping intermediates changes memory
+    use, never values (the device arena is planned once either way)."""
+    x = T.matrix("x", dtype="float32")
+    e = T.tanh(T.dot(x, x.T) * 0.5) - T.dimshuffle(T.sum(x, axis=1), (0, "x"))
+    v = rng.standard_normal((64, 48)).astype(np.float32)
+    a = T.compile([x], e, allow_gc=True)(v)
+    b = T.compile([x], e, allow_gc=False)(v)
+    assert np.array_equal(a, b)
+
+
+def test_no_device_allocations_after_the_second_call(rng):
+    """reference test_runtime.py:189-203 (zero node-output allocations on the
+    2nd call): after planning and graph capture a training step allocates
+    nothing on the device."""
+    import torch
+    from oracle import configs as C
+    g = C.build_mlp(T, B=256, H=128)
+    f = T.compile(g["inputs"], g["outputs"], updates=g["updates"])
+    x, y = C.inputs_mlp(B=256)
+    xd, yd = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+    for _ in range(3):
+        f.call_device(xd, yd, sync=True)
+    before = torch.cuda.memory_allocated()
+    for _ in range(5):
+        f.call_device(xd, yd, sync=True)
+    assert torch.cuda.memory_allocated() == before
+
+
+def test_device_fault_leaves_updates_uncommitted():
+    """reference test_runtime.py:137-171 (a failing node leaves shared state
+    untouched): an integer division by zero detected on the device fails the
+    call before the update is written back."""
+    s = T.shared(np.arange(6, dtype=np.int64), name="s")
+    a = T.vector("a", dtype="int64")
+    b = T.vector("b", dtype="int64")
+    from paper_1605_02688_b200.elemwise import make
+    q = make("div", [a, b])  # integer div floors, and flags a zero divisor on the device
+    f = T.compile([a, b], [q], updates=[(s, s + q)])
+    f(np.full(6, 7, np.int64), np.full(6, 2, np.int64))
+    assert np.array_equal(s.get_value(), np.arange(6) + 3)
+    with pytest.raises(ZeroDivisionError):
+        f(np.full(6, 7, np.int64), np.array([1, 2, 0, 4, 5, 6], np.int64))
+    assert np.array_equal(s.get_value(), np.arange(6) + 3)
+    f(np.full(6, 7, np.int64), np.full(6, 7, np.int64))
+    assert np.array_equal(s.get_value(), np.arange(6) + 4)
