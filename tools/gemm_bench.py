@@ -26,6 +26,13 @@ SHAPES = [  # (name, M, N, K, a_transposed, b_transposed)
     ("K1568 NN", 8192, 4096, 1568, False, False),
     ("K3136 NN", 8192, 4096, 3136, False, False),
     ("K800kk", 8192, 4096, 800, False, True),
+    # LSTM PTB medium per-step products (batch 20, hidden 600, vocabulary 10000)
+    ("L1 x.Wx", 20, 2400, 600, False, False),
+    ("L2 h.Wo", 20, 10000, 600, False, False),
+    ("L3 dy.WoT", 20, 600, 10000, False, True),
+    ("L4 hT.dy", 600, 10000, 20, True, False),
+    ("L5 dz.WxT", 20, 600, 2400, False, True),
+    ("L6 xT.dz", 600, 2400, 20, True, False),
 ]
 
 
