@@ -184,6 +184,32 @@ def test_nan_propagation_max_and_argmax():
     exact(oh, O.argmax_onehot(X, (0,)))
 
 
+@pytest.mark.parametrize("shape", [(64, 40000), (3, 1 << 20), (257, 4099)])
+def test_row_argmax_ties_nan_inf(shape, rng):
+    """Row argmax (axis 1 and all axes) over long rows -- many float4 chunks
+    per thread, rows split across CTAs -- with repeated maxima in different
+    chunks, all -inf rows, NaNs late in a row: first occurrence, NaN wins
+    (bit-exact with NumPy)."""
+    R, K = shape
+    X = rng.integers(-3, 4, size=shape).astype(np.float32)   # heavy ties
+    X[0, :] = -np.inf
+    X[1, K // 2] = np.nan
+    X[1, K - 1] = np.nan
+    if R > 2:
+        X[2, K - 2] = 7.0
+        X[2, 5] = 7.0
+    X = X[:, :]
+    v = T.matrix("X", dtype="float32")
+    f = T.compile([v], [T.argmax(v, axis=1), T.argmax(v), T.max(v, axis=1)])
+    am, aall, m = f(X)
+    exact(am, O.argmax_index(X, (1,)))
+    exact(aall, O.argmax_index(X, (0, 1)))
+    exact(m, O.reduce_max(X, (1,)))
+    Y = X[:, 1:]  # rows start misaligned: the scalar path
+    am2 = T.compile([v], T.argmax(v, axis=1))(np.ascontiguousarray(Y))
+    exact(am2, O.argmax_index(Y, (1,)))
+
+
 def test_dot_golden(golden):
     A, B, v = golden["dot_A"], golden["dot_B"], golden["dot_v"]
     vA, vB, vv = T.matrix("A", dtype="float32"), T.matrix("B", dtype="float32"), T.vector("v", dtype="float32")
