@@ -5,14 +5,16 @@ from max, exp, sum, div, log, mul and DimShuffle, and ``grad`` adds ~25 more
 nodes.  On [B, 10] tensors every one of those nodes is
 pure launch latency.  With concrete shapes known (step-plan time), this
 module finds maximal convex groups of nodes that live in one *row space*
-(N rows x K <= 256 columns) and emits ONE generated kernel per group:
+(N rows x K <= 10240 columns) and emits ONE generated kernel per group:
 
-  * one warp per row; a row vector lives in registers (lane c holds columns
-    c, c+32, ...), row scalars are warp-uniform;
+  * one warp per row (K <= 256) or one 1024-thread CTA per row (wider rows:
+    a vocabulary-sized softmax); a row vector lives in registers (thread c of
+    the row holds columns c, c+T, ...), row scalars are uniform over the row;
   * elementwise nodes and inlined Composite programs run per element
     (same scalar spellings and rounding as ``codegen``);
   * ``sum``/``max``/``argmax``/``argmax_onehot`` over the row are warp-shuffle
-    trees (max/argmax NaN- and tie-exact);
+    trees, then a fixed-order combine of the warp partials for wide rows
+    (max/argmax NaN- and tie-exact);
   * reductions over the batch (``sum[0]`` -> bias gradient, ``sum[0,1]`` ->
     cost) are group sinks: per-CTA partials in fixed order, then the last CTA
     (ticket counter) combines the partials in block order — deterministic, no
@@ -32,7 +34,9 @@ from .dtypes import C_TYPE, ITEMSIZE, is_float
 from .elemwise import Composite, Elemwise, kernel_compute_dtype
 from .reduce import Argmax, ArgmaxOnehot, Max, Sum
 
-MAX_K = 256
+MAX_K = 256          # warp-per-row form
+MAX_WIDE = 10240     # block-per-row form (1024 threads, <= 10 columns per thread)
+WIDE_T = 1024
 MAX_OPS = 48
 V, S, C, U = "V", "S", "C", "U"
 
@@ -115,7 +119,11 @@ def _node_fits(n, grp, shapes, allowed_in):
     if isinstance(op, (Sum, Max, ArgmaxOnehot, Argmax)):
         if op.axes == (1,) and ins[0] == V:
             return is_float(n.inputs[0].type.dtype)
-        return isinstance(op, Sum) and _is_sink(n, shapes) and ins[0] in (V, S)
+        if isinstance(op, Sum) and _is_sink(n, shapes) and ins[0] in (V, S):
+            # a wide row's column sums ([N, K] -> [K]) would be combined by a
+            # single CTA; they stay a separate (parallel) column reduction
+            return not (grp.K > MAX_K and ins[0] == V and op.axes == (0,))
+        return False
     return False
 
 
@@ -140,7 +148,7 @@ def _seed(n, shapes, exclude_ids):
     if len(shp) != 2:
         return None
     N, K = shp
-    if not (2 <= K <= MAX_K) or N < 2 or N == K or N >= (1 << 31):
+    if not (2 <= K <= MAX_WIDE) or N < 2 or N == K or N >= (1 << 31):
         return None
     grp = RowGroup(N, K)
     for x in n.inputs:
@@ -167,7 +175,11 @@ def find_groups(plan, order, fgraph, exclude_ids=()):
 
     def close():
         nonlocal cur
-        if cur is not None and len(cur.launchable()) >= 2:
+        # a wide-row (block-per-row) group pays only where it fuses row
+        # reductions; pure elementwise work on wide rows stays on the
+        # 128-bit elementwise kernels
+        if cur is not None and len(cur.launchable()) >= 2 and (cur.K <= MAX_K or any(
+                isinstance(n.op, (Sum, Max, ArgmaxOnehot, Argmax)) and n.op.axes == (1,) for n in cur.members)):
             groups.append(cur)
         cur = None
         deferred_out.clear()
@@ -189,6 +201,11 @@ def find_groups(plan, order, fgraph, exclude_ids=()):
                 and _node_fits(n, cur, shapes, lambda x: True):
             add(cur, n, i)
             continue
+        if (reads_group or reads_deferred) and cur is not None and len(cur.launchable()) < 2:
+            # a one-kernel group would only drag everything downstream into
+            # its deferred list (blocking later groups): drop it here
+            close()
+            reads_group = reads_deferred = False
         if (reads_group or reads_deferred) and n.id not in exclude_ids:
             cur.deferred.append(n)
             for o in n.outputs:
@@ -214,6 +231,7 @@ _PRELUDE = r"""
 typedef long long i64;
 typedef unsigned char u8;
 #define TX_R %(R)d
+#define TX_T %(T)d
 struct TxRowArgs { i64 N; int K; int pad; void* ptr[%(MAXOPS)d]; i64 rs[%(MAXOPS)d]; i64 cs[%(MAXOPS)d];
                    double* ws; unsigned int* counter; };
 __device__ __forceinline__ float tx_sigmoid(float x) { float z = expf(-fabsf(x)); return x >= 0.0f ? 1.0f / (1.0f + z) : z / (1.0f + z); }
@@ -265,6 +283,39 @@ template <class T> __device__ __forceinline__ void tx_wargmax(T& v, int& i) {
     if (take) { v = w; i = j; }
   }
 }
+// block-wide forms (one row per CTA, wide rows): warp trees, then every
+// warp combines the per-warp partials in the same fixed order
+template <class T> __device__ __forceinline__ T tx_bsum(T v) {
+  __shared__ T sh[32];
+  v = tx_wsum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  T r = (l < (int)(blockDim.x >> 5)) ? sh[l] : (T)0;
+  return tx_wsum(r);
+}
+template <class T> __device__ __forceinline__ T tx_bmax(T v) {
+  __shared__ T sh[32];
+  v = tx_wmax(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  T r = (l < (int)(blockDim.x >> 5)) ? sh[l] : sh[0];
+  return tx_wmax(r);
+}
+template <class T> __device__ __forceinline__ void tx_bargmax(T& v, int& i) {
+  __shared__ T shv[32];
+  __shared__ int shi[32];
+  tx_wargmax(v, i);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) { shv[w] = v; shi[w] = i; }
+  __syncthreads();
+  if (l < (int)(blockDim.x >> 5)) { v = shv[l]; i = shi[l]; } else { v = shv[0]; i = -1; }
+  tx_wargmax(v, i);
+}
 """
 
 
@@ -272,7 +323,11 @@ class _Gen:
     def __init__(self, grp: RowGroup, plan, fgraph):
         self.grp, self.plan, self.fg = grp, plan, fgraph
         self.N, self.K = grp.N, grp.K
-        self.R = (grp.K + 31) // 32
+        self.block = grp.K > MAX_K          # one row per CTA of WIDE_T threads
+        self.T = WIDE_T if self.block else 32
+        self.R = (grp.K + self.T - 1) // self.T
+        rs = "tx_b" if self.block else "tx_w"
+        self.rsum, self.rmax, self.rarg = rs + "sum", rs + "max", rs + "argmax"
         self.lines = []
         self.name = {}      # var id -> C identifier
         self.cls = {}       # var id -> class
@@ -309,11 +364,11 @@ class _Gen:
         p = f"((const {ct}*)a.ptr[{k}])"
         if cls == V:
             self.emit(f"{ct} {nm}[TX_R];")
-            self.emit(f"#pragma unroll\nfor (int j = 0; j < TX_R; ++j) {{ const int c = lane + 32 * j; "
+            self.emit(f"#pragma unroll\nfor (int j = 0; j < TX_R; ++j) {{ const int c = tc + TX_T * j; "
                       f"{nm}[j] = (active && c < K) ? {p}[row * a.rs[{k}] + (i64)c * a.cs[{k}]] : ({ct})0; }}")
         elif cls == C:
             self.emit(f"{ct} {nm}[TX_R];")
-            self.emit(f"#pragma unroll\nfor (int j = 0; j < TX_R; ++j) {{ const int c = lane + 32 * j; "
+            self.emit(f"#pragma unroll\nfor (int j = 0; j < TX_R; ++j) {{ const int c = tc + TX_T * j; "
                       f"{nm}[j] = (c < K) ? {p}[(i64)c * a.cs[{k}]] : ({ct})0; }}")
         elif cls == S:
             self.emit(f"const {ct} {nm} = active ? {p}[row * a.rs[{k}]] : ({ct})0;")
@@ -383,30 +438,30 @@ class _Gen:
         nm = f"t{len(self.name)}"
         if isinstance(op, Sum) and op.axes == (1,):
             self.emit(f"{ct} {nm} = 0;")
-            self.emit(f"#pragma unroll\nfor (int j = 0; j < TX_R; ++j) if (lane + 32 * j < K) {nm} += {xn}[j];")
-            self.emit(f"{nm} = tx_wsum({nm});")
+            self.emit(f"#pragma unroll\nfor (int j = 0; j < TX_R; ++j) if (tc + TX_T * j < K) {nm} += {xn}[j];")
+            self.emit(f"{nm} = {self.rsum}({nm});")
             self.name[o.id], self.cls[o.id], self.dt[o.id] = nm, S, o.type.dtype
         elif isinstance(op, Max) and op.axes == (1,):
             self.emit(f"{ct} {nm} = {xn}[0];")
-            self.emit(f"#pragma unroll\nfor (int j = 1; j < TX_R; ++j) if (lane + 32 * j < K) {{ {ct} w = {xn}[j]; "
+            self.emit(f"#pragma unroll\nfor (int j = 1; j < TX_R; ++j) if (tc + TX_T * j < K) {{ {ct} w = {xn}[j]; "
                       f"{nm} = ({nm} != {nm}) ? {nm} : ((w != w) ? w : (w > {nm} ? w : {nm})); }}")
-            self.emit(f"if (lane >= K) {nm} = -__int_as_float(0x7f800000);" if ct == "float" else f"if (lane >= K) {nm} = -__longlong_as_double(0x7ff0000000000000LL);")
-            self.emit(f"{nm} = tx_wmax({nm});")
+            self.emit(f"if (tc >= K) {nm} = -__int_as_float(0x7f800000);" if ct == "float" else f"if (tc >= K) {nm} = -__longlong_as_double(0x7ff0000000000000LL);")
+            self.emit(f"{nm} = {self.rmax}({nm});")
             self.name[o.id], self.cls[o.id], self.dt[o.id] = nm, S, o.type.dtype
         elif isinstance(op, (Argmax, ArgmaxOnehot)) and op.axes == (1,):
             iv, ii = f"{nm}_v", f"{nm}_i"
-            self.emit(f"{ct} {iv} = {xn}[0]; int {ii} = lane < K ? lane : -1;")
-            self.emit(f"#pragma unroll\nfor (int j = 1; j < TX_R; ++j) {{ const int c = lane + 32 * j; "
+            self.emit(f"{ct} {iv} = {xn}[0]; int {ii} = tc < K ? tc : -1;")
+            self.emit(f"#pragma unroll\nfor (int j = 1; j < TX_R; ++j) {{ const int c = tc + TX_T * j; "
                       f"if (c < K) {{ {ct} w = {xn}[j]; if ({ii} < 0 || w > {iv} || (w != w && {iv} == {iv})) "
                       f"{{ {iv} = w; {ii} = c; }} }} }}")
-            self.emit(f"tx_wargmax({iv}, {ii});")
+            self.emit(f"{self.rarg}({iv}, {ii});")
             if isinstance(op, Argmax):
                 self.emit(f"const i64 {nm} = (i64){ii};")
                 self.name[o.id], self.cls[o.id], self.dt[o.id] = nm, S, o.type.dtype
             else:
                 ot = C_TYPE[o.type.dtype]
                 self.emit(f"{ot} {nm}[TX_R];")
-                self.emit(f"#pragma unroll\nfor (int j = 0; j < TX_R; ++j) {nm}[j] = (lane + 32 * j == {ii}) ? "
+                self.emit(f"#pragma unroll\nfor (int j = 0; j < TX_R; ++j) {nm}[j] = (tc + TX_T * j == {ii}) ? "
                           f"({ot})1 : ({ot})0;")
                 self.name[o.id], self.cls[o.id], self.dt[o.id] = nm, V, o.type.dtype
         elif isinstance(op, Sum):  # sinks: reduce over the batch
@@ -415,13 +470,13 @@ class _Gen:
             if op.axes == (0,) and cin == V:
                 self.emit(f"{ct} {acc}[TX_R];")
                 self.emit(f"#pragma unroll\nfor (int j = 0; j < TX_R; ++j) {acc}[j] = "
-                          f"(active && lane + 32 * j < K) ? {xn}[j] : ({ct})0;")
+                          f"(active && tc + TX_T * j < K) ? {xn}[j] : ({ct})0;")
                 self.sinks.append((o, C, acc, x.type.dtype, self.K))
             else:
                 if cin == V:
                     self.emit(f"double {acc} = 0;")
-                    self.emit(f"#pragma unroll\nfor (int j = 0; j < TX_R; ++j) if (lane + 32 * j < K) {acc} += (double){xn}[j];")
-                    self.emit(f"{acc} = tx_wsum({acc});")
+                    self.emit(f"#pragma unroll\nfor (int j = 0; j < TX_R; ++j) if (tc + TX_T * j < K) {acc} += (double){xn}[j];")
+                    self.emit(f"{acc} = {self.rsum}({acc});")
                     self.emit(f"{acc} = active ? {acc} : 0.0;")
                 else:
                     self.emit(f"const double {acc} = active ? (double){xn} : 0.0;")
@@ -439,13 +494,13 @@ class _Gen:
             c = self.cls[vid]
             src = self.name[vid]
             if c == V:
-                self.emit(f"if (active) {{\n#pragma unroll\nfor (int j = 0; j < TX_R; ++j) {{ const int c = lane + 32 * j; "
+                self.emit(f"if (active) {{\n#pragma unroll\nfor (int j = 0; j < TX_R; ++j) {{ const int c = tc + TX_T * j; "
                           f"if (c < K) {p}[row * a.rs[{k}] + (i64)c * a.cs[{k}]] = ({ct}){src}[j]; }} }}")
             elif c == S:
-                self.emit(f"if (active && lane == 0) {p}[row * a.rs[{k}]] = ({ct}){src};")
+                self.emit(f"if (active && tc == 0) {p}[row * a.rs[{k}]] = ({ct}){src};")
             elif c == C:
-                self.emit(f"if (blockIdx.x == 0 && warp == 0) {{\n#pragma unroll\nfor (int j = 0; j < TX_R; ++j) "
-                          f"{{ const int c = lane + 32 * j; if (c < K) {p}[(i64)c * a.cs[{k}]] = ({ct}){src}[j]; }} }}")
+                self.emit(f"if (blockIdx.x == 0 && {'true' if self.block else 'warp == 0'}) {{\n#pragma unroll\nfor (int j = 0; j < TX_R; ++j) "
+                          f"{{ const int c = tc + TX_T * j; if (c < K) {p}[(i64)c * a.cs[{k}]] = ({ct}){src}[j]; }} }}")
             else:
                 self.emit(f"if (blockIdx.x == 0 && threadIdx.x == 0) {p}[0] = ({ct}){src};")
 
@@ -453,24 +508,35 @@ class _Gen:
         if not self.sinks:
             return 0
         total = sum(L for *_, L in self.sinks)
-        self.emit(f"__shared__ double sk_smem[8][{total}];")
         off = 0
         offs = []
-        for (o, c, acc, dt, L) in self.sinks:
-            offs.append(off)
-            if c == C:
-                self.emit(f"#pragma unroll\nfor (int j = 0; j < TX_R; ++j) {{ const int c = lane + 32 * j; "
-                          f"if (c < K) sk_smem[warp][{off} + c] = (double){acc}[j]; }}")
-            else:
-                self.emit(f"if (lane == 0) sk_smem[warp][{off}] = (double){acc};")
-            off += L
-        self.emit("__syncthreads();")
-        # CTA partial in fixed warp order, in the sink's own precision
-        self.emit(f"for (int e = threadIdx.x; e < {total}; e += blockDim.x) {{")
-        for (o, c, acc, dt, L), so in zip(self.sinks, offs):
-            self.emit(f"  if (e >= {so} && e < {so + L}) {{ double s = 0; for (int w = 0; w < 8; ++w) "
-                      f"s += sk_smem[w][e]; a.ws[(i64)blockIdx.x * {total} + e] = s; }}")
-        self.emit("}")
+        if self.block:
+            # one row per CTA: the CTA partial is the row's own contribution
+            for (o, c, acc, dt, L) in self.sinks:
+                offs.append(off)
+                if c == C:
+                    self.emit(f"#pragma unroll\nfor (int j = 0; j < TX_R; ++j) {{ const int c = tc + TX_T * j; "
+                              f"if (c < K) a.ws[(i64)blockIdx.x * {total} + {off} + c] = (double){acc}[j]; }}")
+                else:
+                    self.emit(f"if (tc == 0) a.ws[(i64)blockIdx.x * {total} + {off}] = (double){acc};")
+                off += L
+        else:
+            self.emit(f"__shared__ double sk_smem[8][{total}];")
+            for (o, c, acc, dt, L) in self.sinks:
+                offs.append(off)
+                if c == C:
+                    self.emit(f"#pragma unroll\nfor (int j = 0; j < TX_R; ++j) {{ const int c = tc + TX_T * j; "
+                              f"if (c < K) sk_smem[warp][{off} + c] = (double){acc}[j]; }}")
+                else:
+                    self.emit(f"if (lane == 0) sk_smem[warp][{off}] = (double){acc};")
+                off += L
+            self.emit("__syncthreads();")
+            # CTA partial in fixed warp order, in the sink's own precision
+            self.emit(f"for (int e = threadIdx.x; e < {total}; e += blockDim.x) {{")
+            for (o, c, acc, dt, L), so in zip(self.sinks, offs):
+                self.emit(f"  if (e >= {so} && e < {so + L}) {{ double s = 0; for (int w = 0; w < 8; ++w) "
+                          f"s += sk_smem[w][e]; a.ws[(i64)blockIdx.x * {total} + e] = s; }}")
+            self.emit("}")
         self.emit("__threadfence(); __syncthreads();")
         self.emit("__shared__ unsigned int sk_ticket; if (threadIdx.x == 0) sk_ticket = atomicAdd(a.counter, 1u);")
         self.emit("__syncthreads();")
@@ -479,7 +545,7 @@ class _Gen:
         # one warp per sink element (elements strided over the 8 warps): lanes
         # sum a fixed strided slice of the block partials, then a fixed xor
         # tree -> deterministic, and no CTA-wide barriers in the loop
-        self.emit(f"  for (int e = warp; e < {total}; e += 8) {{")
+        self.emit(f"  for (int e = warp; e < {total}; e += (int)(blockDim.x >> 5)) {{")
         self.emit("    double s = 0;")
         self.emit(f"    for (unsigned b = lane; b < gridDim.x; b += 32) s += __ldcg(a.ws + (i64)b * {total} + e);")
         self.emit("    s = tx_wsum(s);")
@@ -495,12 +561,17 @@ class _Gen:
         return total
 
     def source(self, body, total):
-        head = _PRELUDE % {"R": self.R, "MAXOPS": MAX_OPS}
-        return "\n".join([head, 'extern "C" __global__ void __launch_bounds__(256) tx_row(const TxRowArgs a) {',
-                          "const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;",
-                          "const i64 row = (i64)blockIdx.x * 8 + warp;",
-                          "const bool active = row < a.N;", "const int K = a.K;", "(void)lane;",
-                          "int* err = nullptr; (void)err;"]
+        head = _PRELUDE % {"R": self.R, "T": self.T, "MAXOPS": MAX_OPS}
+        if self.block:
+            pre = [f'extern "C" __global__ void __launch_bounds__({self.T}) tx_row(const TxRowArgs a) {{',
+                   "const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;",
+                   "const i64 row = (i64)blockIdx.x;", "const int tc = threadIdx.x;"]
+        else:
+            pre = ['extern "C" __global__ void __launch_bounds__(256) tx_row(const TxRowArgs a) {',
+                   "const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;",
+                   "const i64 row = (i64)blockIdx.x * 8 + warp;", "const int tc = lane;"]
+        return "\n".join([head] + pre + ["const bool active = row < a.N;", "const int K = a.K;",
+                                          "(void)lane; (void)warp; (void)tc;", "int* err = nullptr; (void)err;"]
                          + body + ["}"])
 
 
@@ -554,7 +625,8 @@ def emit_group(plan, grp: RowGroup, fgraph):
             args.rs[k], args.cs[k] = 0, st[-1]
         else:
             args.rs[k], args.cs[k] = 0, 1
-    grid = (grp.N + 7) // 8
+    grid = grp.N if gen.block else (grp.N + 7) // 8
+    threads = gen.T if gen.block else 256
     if total:
         ws = torch.zeros(grid * total * 8 + 256, dtype=torch.uint8, device="cuda")
         plan.keep.append(ws)
@@ -565,5 +637,5 @@ def emit_group(plan, grp: RowGroup, fgraph):
     plan.keep.append(args)
 
     def launch(stream):
-        lib.check(f(h, grid, 256, ap, stream))
+        lib.check(f(h, grid, threads, ap, stream))
     return launch, src

@@ -774,6 +774,7 @@ class StepPlan:
                             touch(self.lay[x.id], grp.last_pos)
 
         # ---- arena allocation with in-place reuse for elementwise kernels
+        deferred_ids = {n.id for grp in self.row_groups for n in grp.deferred}
         alloc = ArenaAllocator()
         live_at: dict[int, list] = {}
 
@@ -816,7 +817,10 @@ class StepPlan:
             w = self.ws.get(n.id)
             if w is not None:
                 w[0].offset = alloc.alloc(w[1])
-                alloc.release(w[0].offset, w[1])
+                # a node deferred past a row-fusion launch runs after its
+                # schedule slot: its scratch must not be handed on from here
+                if n.id not in deferred_ids:
+                    alloc.release(w[0].offset, w[1])
             for st in live_at.pop(i, []):
                 if fn.nan_guard is None and not fn.has_lazy:
                     # a guarded step keeps every value for its report; a lazy

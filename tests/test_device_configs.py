@@ -213,3 +213,33 @@ def test_narrow_grad_fusion_matches_unfused(B, H, K):
     for pa, pb in zip(ga["params"], gb["params"]):
         a, b = pa.get_value(), pb.get_value()
         assert np.linalg.norm(a - b) <= 1e-5 * max(np.linalg.norm(a), 1e-30), pa.name
+
+
+@pytest.mark.parametrize("N,K", [(20, 10000), (7, 3000), (300, 257), (64, 10240)])
+def test_wide_row_fusion_softmax_xent(N, K):
+    """Vocabulary-sized rows (one 1024-thread CTA per row): softmax +
+    cross-entropy forward and gradient, max / argmax outputs, against the
+    unfused graph (sums to reassociation, max / argmax bit-exact)."""
+    rng = np.random.default_rng(N + K)
+    z = T.matrix("z", dtype="float32")
+    y = T.matrix("y", dtype="float32")
+    m = T.max(z, axis=1)
+    e = T.exp(z - T.dimshuffle(m, (0, "x")))
+    p = e / T.dimshuffle(T.sum(e, axis=1), (0, "x"))
+    cost = -T.sum(y * T.log(p)) / float(N)
+    (gz,) = T.grad(cost, [z])
+    outs = [cost, gz, m, T.argmax(z, axis=1), T.sum(gz, axis=0)]
+    fa = T.compile([z, y], outs, row_fusion=False)
+    fb = T.compile([z, y], outs)
+    plan_groups = None
+    zv = (rng.standard_normal((N, K)) * 3).astype(np.float32)
+    zv[0, 5] = zv[0, K - 3] = 50.0  # a tie at the row maximum
+    yv = np.eye(K, dtype=np.float32)[rng.integers(0, K, N)]
+    a, b = fa(zv, yv), fb(zv, yv)
+    plan_groups = next(iter(fb._plans.values())).row_groups
+    assert plan_groups and any(g.K == K for g in plan_groups)
+    assert abs(a[0] - b[0]) <= 1e-5 * abs(a[0])
+    np.testing.assert_allclose(b[1], a[1], rtol=1e-5, atol=1e-8)
+    np.testing.assert_array_equal(b[2], a[2])
+    np.testing.assert_array_equal(b[3], a[3])
+    np.testing.assert_allclose(b[4], a[4], rtol=1e-4, atol=1e-7)
