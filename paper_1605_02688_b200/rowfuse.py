@@ -35,10 +35,22 @@ from .elemwise import Composite, Elemwise, kernel_compute_dtype
 from .reduce import Argmax, ArgmaxOnehot, Max, Sum
 
 MAX_K = 256          # warp-per-row form
-MAX_WIDE = 10240     # block-per-row form (1024 threads, <= 10 columns per thread)
-WIDE_T = 1024
+MAX_WIDE = 10240     # block-per-row form (<= 1024 threads, <= 10 columns per thread)
+WIDE_T_ENV = __import__('os').environ.get('TX_ROW_WIDE_T')
 MAX_OPS = 48
 V, S, C, U = "V", "S", "C", "U"
+
+
+def wide_threads(K):
+    """Threads per row of the block-per-row form: about 8 columns per thread
+    (register-resident rows; measured on softmax-xent fwd+bwd: K=1000 best at
+    256, K=4096 at 512, K=10000 at 1024)."""
+    if WIDE_T_ENV:
+        return int(WIDE_T_ENV)
+    t = 256
+    while t < 1024 and t * 8 < K:
+        t *= 2
+    return t
 
 
 def classify(shape, N, K):
@@ -323,8 +335,8 @@ class _Gen:
     def __init__(self, grp: RowGroup, plan, fgraph):
         self.grp, self.plan, self.fg = grp, plan, fgraph
         self.N, self.K = grp.N, grp.K
-        self.block = grp.K > MAX_K          # one row per CTA of WIDE_T threads
-        self.T = WIDE_T if self.block else 32
+        self.block = grp.K > MAX_K          # one row per CTA of wide_threads(K) threads
+        self.T = wide_threads(grp.K) if self.block else 32
         self.R = (grp.K + self.T - 1) // self.T
         rs = "tx_b" if self.block else "tx_w"
         self.rsum, self.rmax, self.rarg = rs + "sum", rs + "max", rs + "argmax"
