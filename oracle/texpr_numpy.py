@@ -236,7 +236,36 @@ def run_node(node, args):
         return [elemwise("mul", [z, args[2]])]
     if name == "dimshuffle":
         return [dimshuffle(args[0], op.pattern)]
+    if name == "subtensor":
+        return [subtensor(args[0], op.items)]
+    if name == "inc_subtensor":
+        return [inc_subtensor(args[0], args[1], op.items)]
+    if name == "join":
+        return [join(op.axis, args)]
     raise NotImplementedError(f"oracle has no kernel for op {name!r}")
+
+
+def _as_index(items):
+    """ops/shaping.py _as_index: ints stay, (start, stop, step) triples are slices."""
+    return tuple(i if isinstance(i, int) else slice(*i) for i in items)
+
+
+def subtensor(x, items):
+    """Subtensor.perform (ops/shaping.py:157-162): basic slicing, a view."""
+    return x[_as_index(items)]
+
+
+def inc_subtensor(target, value, items):
+    """IncSubtensor.perform (ops/shaping.py:238-242): a copy of target with
+    value added into the region."""
+    out = target.copy()
+    out[_as_index(items)] += value
+    return out
+
+
+def join(axis, xs):
+    """Join.perform (ops/shaping.py:416-420): np.concatenate along axis."""
+    return np.concatenate(xs, axis=axis)
 
 
 def evaluate(outputs, bindings):
