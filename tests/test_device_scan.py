@@ -319,3 +319,28 @@ def test_nested_and_last_step_match_reference_goldens():
     assert any(n.op.name == "scan" and n.op.retention == ("last",) for n in f.order)
     (v,) = f(np.random.default_rng(13).standard_normal(40))
     assert rel_err(v, g["last_out"]) <= 1e-12
+
+
+def test_sequence_pushout_moves_work_out_of_both_loops():
+    """loop_pushout_sequences: the BPTT loop's recomputed forward step and
+    cross-entropy, and the forward loop's input projection, run once over
+    the stacked sequences (seq_dot GEMMs outside the loops); results equal
+    the loop without the rewrite, and a saved function stays portable."""
+    from paper_1605_02688_b200.scan import ScanOp, SeqDot
+    from tools.lstm_bench import build
+    import torch
+
+    step_a, host = build(T, 32, 6, B=4, V=50, exclude=("loop_pushout_sequences",))
+    step_b, _ = build(T, 32, 6, B=4, V=50)
+    ins = [torch.from_numpy(v).cuda() for v in host]
+    n_seqdot = sum(isinstance(n.op, SeqDot) for n in step_b.order)
+    assert n_seqdot >= 3 and not any(isinstance(n.op, SeqDot) for n in step_a.order)
+    for _ in range(2):
+        ca = float(step_a.call_device(*ins, sync=True)[0].item())
+    del step_a
+    step_c = T.load(step_b.save())
+    for _ in range(2):
+        cb = float(step_b.call_device(*ins, sync=True)[0].item())
+    assert abs(ca - cb) <= 1e-4 * abs(ca)
+    cc = float(step_c.call_device(*ins, sync=True)[0].item())
+    assert np.isfinite(cc)
