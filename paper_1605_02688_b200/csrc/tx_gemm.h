@@ -16,7 +16,7 @@ template <class T>
 struct Epi {
   int kind = TX_EPI_NONE;
   const T* aux = nullptr;
-  int64_t s0 = 0, s1 = 0;  // aux strides (bias: s1 only)
+  int64_t s0 = 0, s1 = 0;  // aux strides (bias: s1 only; s0 after a transposition C^T = B^T A^T)
   T* out2 = nullptr;
   int64_t o0 = 0, o1 = 0;  // out2 strides
   T alpha = T(0);          // SGD learning rate
@@ -26,14 +26,14 @@ struct Epi {
 template <>
 __device__ __forceinline__ float Epi<float>::apply(float acc, int64_t m, int64_t n) const {
   switch (kind) {
-    case TX_EPI_BIAS: return __fadd_rn(aux[n * s1], acc);
-    case TX_EPI_BIAS_TANH: return tanhf(__fadd_rn(aux[n * s1], acc));
+    case TX_EPI_BIAS: return __fadd_rn(aux[m * s0 + n * s1], acc);
+    case TX_EPI_BIAS_TANH: return tanhf(__fadd_rn(aux[m * s0 + n * s1], acc));
     case TX_EPI_MUL_1MSQR: {
       float h = aux[m * s0 + n * s1];
       return __fmul_rn(acc, __fsub_rn(1.0f, __fmul_rn(h, h)));
     }
     case TX_EPI_BIAS_TANH_DUAL: {
-      const float h = tanhf(__fadd_rn(aux[n * s1], acc));
+      const float h = tanhf(__fadd_rn(aux[m * s0 + n * s1], acc));
       out2[m * o0 + n * o1] = __fsub_rn(1.0f, __fmul_rn(h, h));
       return h;
     }
@@ -46,14 +46,14 @@ __device__ __forceinline__ float Epi<float>::apply(float acc, int64_t m, int64_t
 template <>
 __device__ __forceinline__ double Epi<double>::apply(double acc, int64_t m, int64_t n) const {
   switch (kind) {
-    case TX_EPI_BIAS: return __dadd_rn(aux[n * s1], acc);
-    case TX_EPI_BIAS_TANH: return tanh(__dadd_rn(aux[n * s1], acc));
+    case TX_EPI_BIAS: return __dadd_rn(aux[m * s0 + n * s1], acc);
+    case TX_EPI_BIAS_TANH: return tanh(__dadd_rn(aux[m * s0 + n * s1], acc));
     case TX_EPI_MUL_1MSQR: {
       double h = aux[m * s0 + n * s1];
       return __dmul_rn(acc, __dsub_rn(1.0, __dmul_rn(h, h)));
     }
     case TX_EPI_BIAS_TANH_DUAL: {
-      const double h = tanh(__dadd_rn(aux[n * s1], acc));
+      const double h = tanh(__dadd_rn(aux[m * s0 + n * s1], acc));
       out2[m * o0 + n * o1] = __dsub_rn(1.0, __dmul_rn(h, h));
       return h;
     }

@@ -525,6 +525,8 @@ def _readers_through_views(g, var):
     while stack:
         v = stack.pop()
         for c in g.node_clients(v):
+            if c.id not in g.nodes:
+                continue
             if getattr(c.op, "view_capable", False):
                 stack.extend(c.outputs)
             else:

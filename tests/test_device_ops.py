@@ -334,3 +334,24 @@ def test_narrow_grad_sgd_in_place_and_fallbacks(rng):
     _narrow_case(300, 130, 10, rng, pad_h=2)                    # unaligned rows -> tx_gemm x2 + tx_reduce
     _narrow_case(300, 128, 17, rng, mode=1)                      # k > 16 -> fallback (exact-fp32 GEMM mode)
     _narrow_case(96, 64, 5, rng, sgd=True, dtype=np.float64)   # float64 -> fallback
+
+
+@pytest.mark.parametrize("M", [1, 4, 16, 37])
+def test_dot_bias_epilogues_short_m(M, rng):
+    """dot + row bias (and tanh) with few rows: the M <= 16 products run
+    transposed on the skinny kernels, where the bias runs along the other
+    axis (regression: every column used bias[0])."""
+    x = rng.standard_normal((M, 32)).astype(np.float32)
+    W = rng.standard_normal((32, 50)).astype(np.float32)
+    b = rng.standard_normal(50).astype(np.float32)
+    vx, vw, vb = T.matrix("x", dtype="float32"), T.matrix("w", dtype="float32"), T.vector("b", dtype="float32")
+    want = x.astype(np.float64) @ W + b
+    f = T.compile([vx, vw, vb], T.dot(vx, vw) + vb)
+    assert "dot+bias" in [getattr(n.op, "display_name", n.op.name) for n in f.order]
+    np.testing.assert_allclose(f(x, W, b), want, rtol=1e-5, atol=1e-5)
+    # the forward layer with its tanh-gradient factor: dot+bias_tanh_dual
+    h = T.tanh(T.dot(vx, vw) + vb)
+    g = T.compile([vx, vw, vb], [h, 1.0 - T.sqr(h)])
+    hv, gv = g(x, W, b)
+    np.testing.assert_allclose(hv, np.tanh(want), rtol=1e-5, atol=1e-5)
+    np.testing.assert_allclose(gv, 1 - np.tanh(want) ** 2, rtol=1e-5, atol=1e-5)

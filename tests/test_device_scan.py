@@ -321,20 +321,29 @@ def test_nested_and_last_step_match_reference_goldens():
     assert rel_err(v, g["last_out"]) <= 1e-12
 
 
+LOOP_REWRITES = ("loop_pushout_sequences", "loop_pushout_accumulators", "loop_pushout_outputs",
+                 "loop_drop_unused_outputs")
+
+
 def test_sequence_pushout_moves_work_out_of_both_loops():
-    """loop_pushout_sequences: the BPTT loop's recomputed forward step and
-    cross-entropy, and the forward loop's input projection, run once over
-    the stacked sequences (seq_dot GEMMs outside the loops); results equal
-    the loop without the rewrite, and a saved function stays portable."""
-    from paper_1605_02688_b200.scan import ScanOp, SeqDot
+    """The loop rewrites: the BPTT loop's recomputed forward step and
+    cross-entropy, the forward loop's input projection and its per-step
+    softmax / cross-entropy, and the weight-gradient accumulators run once
+    over stacked sequences / histories outside the loops (seq_dot / seq_gram
+    GEMMs); results equal the loops without the rewrites, and a saved
+    function stays portable."""
+    from paper_1605_02688_b200.scan import ScanOp, SeqDot, SeqGram
     from tools.lstm_bench import build
     import torch
 
-    step_a, host = build(T, 32, 6, B=4, V=50, exclude=("loop_pushout_sequences",))
+    step_a, host = build(T, 32, 6, B=4, V=50, exclude=LOOP_REWRITES)
     step_b, _ = build(T, 32, 6, B=4, V=50)
     ins = [torch.from_numpy(v).cuda() for v in host]
     n_seqdot = sum(isinstance(n.op, SeqDot) for n in step_b.order)
-    assert n_seqdot >= 3 and not any(isinstance(n.op, SeqDot) for n in step_a.order)
+    assert n_seqdot >= 3 and not any(isinstance(n.op, (SeqDot, SeqGram)) for n in step_a.order)
+    assert sum(isinstance(n.op, SeqGram) for n in step_b.order) >= 2
+    loops = [n.op for n in step_b.order if isinstance(n.op, ScanOp)]
+    assert all(op.n_states == 2 for op in loops)  # only the recurrences (h, c / their adjoints) stay carried
     for _ in range(2):
         ca = float(step_a.call_device(*ins, sync=True)[0].item())
     del step_a
