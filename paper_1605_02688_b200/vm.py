@@ -32,6 +32,7 @@ import numpy as np
 from . import codegen, native
 from .dtypes import ITEMSIZE, np_dtype
 from .elemwise import Composite, Elemwise, EwProgram
+from .shaping import IncSubtensor
 from .errors import (NotSupported, ShapeMismatch, TexprError, TypeMismatch,
                      UnderdeterminedOutputs)
 from .graph import Constant, FunctionGraph, Variable, clone_outputs
@@ -791,14 +792,22 @@ class StepPlan:
             if getattr(n.op, "view_capable", False):
                 continue
             taken = set()
-            inplace_ok = isinstance(n.op, (Elemwise, Composite)) and fn.nan_guard is None and not fn.has_lazy
+            is_inc = isinstance(n.op, IncSubtensor)
+            inplace_ok = (isinstance(n.op, (Elemwise, Composite)) or is_inc) and fn.nan_guard is None \
+                and not fn.has_lazy
             for o in n.outputs:
                 ol = self.lay[o.id]
                 st = ol.storage
                 if st.kind != "arena" or st.offset is not None:
                     continue
                 if inplace_ok:
-                    for x in n.inputs:
+                    # inc_subtensor updates its target in place when the target
+                    # dies here (the BPTT gate-gradient assembly: a chain of
+                    # region adds instead of a full copy per step)
+                    cands = n.inputs[:1] if is_inc else n.inputs
+                    if is_inc and self.lay[n.inputs[1].id].storage.root() is self.lay[n.inputs[0].id].storage.root():
+                        cands = []
+                    for x in cands:
                         xl = self.lay[x.id]
                         xs = xl.storage
                         if (xs.kind == "arena" and xs.alias is None and xs.offset is not None
