@@ -90,3 +90,40 @@ def test_loop_rewrites_last_step_and_pushout():
     fg = FunctionGraph([xs], [h3])
     _, log = run_preset(fg, "fast_run")
     assert log.count(rewrite="loop_pushout_invariants") == 0
+
+
+def test_loop_rewrites_move_work_out_of_lstm_loops():
+    """Graph-level check of the loop rewrites on the PTB LSTM training step
+    (no device): the forward loop keeps only h.Wh and the gate composite's
+    inputs, the BPTT loop only the adjoint recurrence; the input projections,
+    logits, softmax / cross-entropy and the weight-gradient accumulations run
+    outside as seq_dot / seq_gram products."""
+    from paper_1605_02688_b200.graph import FunctionGraph, Variable, ancestor_vars, clone_outputs
+    from paper_1605_02688_b200.rewrite import RewriteContext, run_preset
+    from paper_1605_02688_b200.scan import SeqDot, SeqGram
+    from paper_1605_02688_b200.shared import SharedVariable
+    from tools.lstm_bench import build
+    captured = {}
+    real = T.compile
+
+    def capture(inputs, outputs, updates=(), **kw):
+        captured["args"] = (inputs, outputs, updates)
+    T.compile = capture
+    try:
+        build(T, 16, 5, B=3, V=20)
+    finally:
+        T.compile = real
+    inputs, outputs, updates = captured["args"]
+    outs = list(outputs) + [u for _, u in updates]
+    shared = sorted({v for v in ancestor_vars(outs) if isinstance(v, SharedVariable)}, key=lambda v: v.id)
+    repl = {v: Variable(v.type, v.name) for v in list(inputs) + shared}
+    cloned, _ = clone_outputs(outs, repl)
+    fg = FunctionGraph([repl[v] for v in list(inputs) + shared], cloned)
+    run_preset(fg, "fast_run", ctx=RewriteContext(execution_bound=True))
+    nodes = fg.toposort()
+    loops = [n.op for n in nodes if isinstance(n.op, ScanOp)]
+    assert len(loops) == 2 and all(op.n_states == 2 for op in loops)
+    fwd = min(loops, key=lambda op: len(op._order))
+    assert sum(n.op.name == "dot" for n in fwd._order) == 1          # h . Wh only
+    assert sum(isinstance(n.op, SeqDot) for n in nodes) >= 3
+    assert sum(isinstance(n.op, SeqGram) for n in nodes) >= 2
