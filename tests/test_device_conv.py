@@ -72,3 +72,56 @@ def test_reshape_and_shape_of(rng):
     xt = T.transpose(T.matrix("m", dtype="float32"))
     (tv,) = T.compile([xt.owner.inputs[0]], [T.reshape(xt, (-1,))])(np.arange(6, dtype=np.float32).reshape(2, 3))
     np.testing.assert_array_equal(tv, np.arange(6).reshape(2, 3).T.reshape(-1))
+
+
+def _conv_ref(x, f, st, pd):
+    """Direct-loop cross-correlation (float64) and its two gradients for an
+    all-ones upstream weight w: dy = w."""
+    N, C, H, W = x.shape
+    K, _, kh, kw = f.shape
+    xp = np.pad(x, ((0, 0), (0, 0), (pd[0], pd[0]), (pd[1], pd[1])))
+    Ho = (H + 2 * pd[0] - kh) // st[0] + 1
+    Wo = (W + 2 * pd[1] - kw) // st[1] + 1
+    y = np.zeros((N, K, Ho, Wo))
+    for i in range(Ho):
+        for j in range(Wo):
+            win = xp[:, :, i * st[0]: i * st[0] + kh, j * st[1]: j * st[1] + kw]
+            y[:, :, i, j] = np.einsum("nchw,kchw->nk", win, f)
+    return y
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_conv_random_shapes_and_gradients(seed):
+    """Random NCHW / KCHW shapes, strides and paddings: the forward against
+    direct loops, and both gradients against central finite differences of
+    the direct-loop forward (float64, exact)."""
+    rng = np.random.default_rng(900 + seed)
+    N, C, K = (int(v) for v in rng.integers(1, 4, 3))
+    kh, kw = (int(v) for v in rng.integers(1, 4, 2))
+    st = tuple(int(v) for v in rng.integers(1, 3, 2))
+    pd = tuple(int(v) for v in rng.integers(0, 2, 2))
+    H = int(rng.integers(kh, kh + 6))
+    W = int(rng.integers(kw, kw + 6))
+    x = rng.standard_normal((N, C, H, W))
+    f = rng.standard_normal((K, C, kh, kw))
+    vx, vf = T.tensor4("x"), T.tensor4("f")
+    y = T.conv2d(vx, vf, stride=st, pad=pd)
+    yr = _conv_ref(x, f, st, pd)
+    wv = rng.standard_normal(yr.shape)
+    gx, gf = T.grad(T.sum(y * T.as_variable(wv)), [vx, vf])
+    got_y, got_gx, got_gf = T.compile([vx, vf], [y, gx, gf])(x, f)
+    assert _rel(got_y, yr) <= 1e-12
+    # exact gradients of a linear map: <w, conv(x, f)> is linear in x and in f
+    eps = 1.0
+    gx_ref = np.zeros_like(x)
+    for idx in np.ndindex(*x.shape):
+        d = np.zeros_like(x)
+        d[idx] = eps
+        gx_ref[idx] = (wv * _conv_ref(d, f, st, pd)).sum()
+    gf_ref = np.zeros_like(f)
+    for idx in np.ndindex(*f.shape):
+        d = np.zeros_like(f)
+        d[idx] = eps
+        gf_ref[idx] = (wv * _conv_ref(x, d, st, pd)).sum()
+    assert _rel(got_gx, gx_ref) <= 1e-12
+    assert _rel(got_gf, gf_ref) <= 1e-12
