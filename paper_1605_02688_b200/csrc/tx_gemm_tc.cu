@@ -571,17 +571,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
           if (E.kind != TX_EPI_NONE) {
             if (E.kind == TX_EPI_BIAS || E.kind == TX_EPI_BIAS_TANH) {
-              if (n + 32 <= p.N) {
+              if (n + 32 <= p.N && E.s1 == 1 && ((uintptr_t)E.aux & 15) == 0) {
 #pragma unroll
                 for (int i = 0; i < 32; i += 4) {
                   const float4 b4 = __ldg(reinterpret_cast<const float4*>(E.aux + n + i));
                   v[i] = __fadd_rn(b4.x, v[i]); v[i + 1] = __fadd_rn(b4.y, v[i + 1]);
                   v[i + 2] = __fadd_rn(b4.z, v[i + 2]); v[i + 3] = __fadd_rn(b4.w, v[i + 3]);
                 }
-              } else {
+              } else {  // ragged edge, or a strided / unaligned bias view
 #pragma unroll
                 for (int i = 0; i < 32; ++i)
-                  if (n + i < p.N) v[i] = __fadd_rn(E.aux[n + i], v[i]);
+                  if (n + i < p.N) v[i] = __fadd_rn(E.aux[(int64_t)(n + i) * E.s1], v[i]);
               }
               if (E.kind == TX_EPI_BIAS_TANH) {
 #pragma unroll

@@ -143,6 +143,17 @@ class DotEpilogue(Op):
 
     def check_runtime_shapes(self, node, shapes):
         Dot().check_runtime_shapes(node, shapes[:2])
+        # the replaced elementwise node's broadcast check (reference
+        # ops/base.py:132-163): a bias must match the product's last axis,
+        # an [M,N] operand its shape
+        (out,) = Dot().infer_shape(node, shapes[:2])[:1]
+        aux = tuple(shapes[2])
+        if self.kind in (EPI_BIAS, EPI_BIAS_TANH, EPI_BIAS_TANH_DUAL):
+            ok = len(aux) >= 1 and aux[-1] == out[-1] and all(d == 1 for d in aux[:-1])
+        else:
+            ok = aux == tuple(out)
+        if not ok:
+            raise ShapeMismatch(f"{self.display_name}: operand shape {aux} does not broadcast to {tuple(out)}")
 
     def infer_shape(self, node, input_shapes):
         (s,) = Dot().infer_shape(node, input_shapes[:2])

@@ -355,3 +355,25 @@ def test_dot_bias_epilogues_short_m(M, rng):
     hv, gv = g(x, W, b)
     np.testing.assert_allclose(hv, np.tanh(want), rtol=1e-5, atol=1e-5)
     np.testing.assert_allclose(gv, 1 - np.tanh(want) ** 2, rtol=1e-5, atol=1e-5)
+
+
+def test_dot_bias_strided_and_unaligned_bias(rng):
+    """The tensor-core epilogue with a bias that is a strided or unaligned
+    view (every other element of a vector, or a vector starting one element
+    into its buffer)."""
+    x = rng.standard_normal((256, 128)).astype(np.float32)
+    W = rng.standard_normal((128, 192)).astype(np.float32)
+    bb = rng.standard_normal(2 * 192 + 1).astype(np.float32)
+    vx, vw, vb = T.matrix("x", dtype="float32"), T.matrix("w", dtype="float32"), T.vector("bb", dtype="float32")
+    for sl, bview in ((slice(0, 2 * 192, 2), bb[: 2 * 192: 2]), (slice(1, 193, None), bb[1:193])):
+        f = T.compile([vx, vw, vb], T.dot(vx, vw) + T.subtensor(vb, (sl,)))
+        assert "dot+bias" in [getattr(n.op, "display_name", n.op.name) for n in f.order]
+        got = f(x, W, bb)
+        want = x.astype(np.float64) @ W + bview
+        bound = np.abs(x).astype(np.float64) @ np.abs(W)
+        assert np.all(np.abs(got - want) <= 2.0 ** -9 * bound + 1e-5)
+    # a bias of the wrong length fails like the unfused add would
+    from paper_1605_02688_b200.errors import ShapeMismatch
+    f = T.compile([vx, vw, vb], T.dot(vx, vw) + vb)
+    with pytest.raises(ShapeMismatch):
+        f(x, W, bb)
