@@ -125,3 +125,46 @@ def test_random_graphs_match_reference_algorithm(dt, rel, shape, n):
         want = ref(*vals)
         for g, w in zip(got, want):
             _check(g, w, rel)
+
+
+def _random_view_graph(seed, dt, n=48):
+    """Square operands so shape-preserving views mix freely: transposes,
+    reversed rows / columns (negative strides), comparisons and switch."""
+    from paper_1605_02688_b200.ops import flip0, subtensor
+    rng = np.random.default_rng(seed)
+    x, y, w = T.matrix("x", dtype=dt), T.matrix("y", dtype=dt), T.matrix("w", dtype=dt)
+    pool = [x, y, w]
+
+    def pick():
+        return pool[int(rng.integers(len(pool)))]
+    for _ in range(int(rng.integers(5, 12))):
+        r = rng.random()
+        if r < 0.2:
+            pool.append(T.dimshuffle(pick(), (1, 0)))
+        elif r < 0.32:
+            pool.append(flip0(pick()))
+        elif r < 0.42:
+            pool.append(subtensor(pick(), (slice(None), slice(None, None, -1))))
+        elif r < 0.62:
+            k = ("add", "mul", "sub", "maximum")[int(rng.integers(4))]
+            pool.append(make(k, [pick(), pick()]))
+        elif r < 0.72:
+            a, b = pick(), pick()
+            pool.append(make("switch", [make("gt", [a, b]), a, make("neg", [b])]))
+        elif r < 0.86:
+            pool.append(T.dot(pick(), pick()))
+        else:
+            pool.append(T.tanh(pick()) * T.dimshuffle(T.sum(pick(), axis=int(rng.integers(2))), (0, "x")))
+    outs = [pool[-1], T.sum(pool[int(rng.integers(3, len(pool)))], axis=0), T.max(pool[-1], axis=1)]
+    vals = [(rng.standard_normal((n, n)) / np.sqrt(n)).astype(dt) for _ in range(3)]
+    return [x, y, w], outs, vals
+
+
+@pytest.mark.parametrize("dt,rel", [("float64", 1e-9), ("float32", 4e-5)])
+def test_random_view_graphs_match_reference_algorithm(dt, rel):
+    for seed in range(40):
+        inputs, outs, vals = _random_view_graph(5000 + seed, dt)
+        got = T.compile(inputs, outs, gemm_mode="simt" if dt == "float32" else "auto")(*vals)
+        want = C.CpuFunction(T, inputs, outs)(*vals)
+        for g, w in zip(got, want):
+            _check(g, w, rel)
