@@ -92,6 +92,19 @@ G transposed(const G& g) {
 }
 
 }  // namespace
+
+int gemm_with_colsum(const tx_tensor* A, const tx_tensor* B, tx_tensor* C, const tx_epilogue* epi, int mode,
+                     float* partials, cudaStream_t st) {
+  G g;
+  int rc = build(A, B, C, epi, &g);
+  if (rc) return rc;
+  int path, kind;
+  choose(g, mode, &path, &kind);
+  if (path != PATH_TC || g.dtype != TX_F32 || g.M == 0 || g.N == 0 || g.K == 0) return TX_E_UNSUPPORTED;
+  g.colsum = partials;
+  return gemm_tc(g, nullptr, 0, st);
+}
+
 }  // namespace tx
 
 using namespace tx;

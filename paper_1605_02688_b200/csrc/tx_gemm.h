@@ -72,6 +72,7 @@ struct G {
   int64_t sam, sak, sbk, sbn, scm, scn;
   Epi<float> epi_f;
   Epi<double> epi_d;
+  float* colsum = nullptr;  // tcgen05 path only: [ceil(M/32)][N] column sums of C per 32-row block
 };
 
 enum { PATH_SIMT = 0, PATH_SKINNY = 1, PATH_TC = 2 };
@@ -84,6 +85,11 @@ int kred_splits(int64_t M, int64_t K);
 int gemm_tc_eligible(const G& g);
 int gemm_tc(const G& g, void* ws, size_t wsb, cudaStream_t st);
 size_t gemm_tc_workspace(const G& g);
+// C = A.B (+ epilogue) on the tcgen05 path with per-32-row-block column sums
+// of C into `partials` ([ceil(M/32)][N] fp32); TX_E_UNSUPPORTED when the
+// product does not take that path (caller reduces C separately)
+int gemm_with_colsum(const tx_tensor* A, const tx_tensor* B, tx_tensor* C, const tx_epilogue* epi, int mode,
+                     float* partials, cudaStream_t st);
 void choose_tile(const G& g, int* cg, int* bn);
 // C = epi(sum over splits of P[split][M][N]), fixed split order
 int splitk_finalize(const float* P, const G& g, int splits, cudaStream_t st);

@@ -251,6 +251,7 @@ struct TcParams {
   int tma_store;    // C written by TMA tile stores from swizzled smem staging
   int tma_aux;      // [M,N] epilogue operand read by TMA tile loads (CG = 2)
   int num_m, num_n, num_tiles;
+  float* colsum;    // optional: per-32-row-block column sums of the stored C, [ceil(M/32)][N]
   Epi<float> epi;
 };
 
@@ -632,6 +633,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           fence_async_smem();
           __syncwarp();
           if (lane == 0) tma_store_2d(&mapC, stg, n, row0);
+          if (p.colsum) {
+            // column sums of this 32 x 32 block from the swizzled staging tile
+            // (lane = column; conflict-free: the xor swizzle permutes banks)
+            float cs = 0.f;
+#pragma unroll 8
+            for (int r = 0; r < 32; ++r)
+              if (row0 + r < p.M) cs += stg[r * 32 + 4 * ((lane >> 2) ^ (r & 7)) + (lane & 3)];
+            if (n + lane < p.N) p.colsum[(int64_t)(row0 >> 5) * p.N + n + lane] = cs;
+          }
         }
         tc_fence_before();
         __syncwarp();
@@ -961,6 +971,8 @@ int gemm_tc(const G& g, void* ws, size_t wsb, cudaStream_t st) {
   tc_streamk(g, p.splits, &p.streamk, &sk_pieces, &sk_nc);
   if (p.streamk && (ws == nullptr || wsb < gemm_tc_workspace(g) || ((uintptr_t)ws & 15))) p.streamk = 0;
   p.epi = g.epi_f;
+  p.colsum = g.colsum;
+  if (p.colsum) p.splits = 1, p.kbs = p.num_kb, p.streamk = 0;  // every tile finished by its own epilogue
   p.dbg_nostore = getenv("TX_GEMM_DBG_NOSTORE") != nullptr;
   // TMA tile stores need a 16-byte aligned C with a 16-byte row pitch; the
   // dual-output epilogue (two stores per element) keeps the register path
@@ -979,6 +991,7 @@ int gemm_tc(const G& g, void* ws, size_t wsb, cudaStream_t st) {
     if (r != CUDA_SUCCESS) p.tma_store = 0;
   }
   if (p.streamk && !p.tma_store) p.streamk = 0;  // partial pieces need the TMA store path
+  if (p.colsum && !p.tma_store) return TX_E_UNSUPPORTED;  // the column sums read the staging tile
   CUtensorMap mp;
   memset(&mp, 0, sizeof(mp));
   if (p.splits > 1 || p.streamk) {

@@ -230,6 +230,23 @@ __global__ void __launch_bounds__(256) narrow_grad_finalize(const float* __restr
   else db[j * sdb] = v;
 }
 
+// db[j] = sum over the 32-row blocks of the dh GEMM's column sums, block order
+__global__ void colsum_finalize(const float* __restrict__ P, int S, int64_t H, float* __restrict__ db, int64_t sdb) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= H) return;
+  float v = 0.f;
+  int s = 0;
+  for (; s + 8 <= S; s += 8) {
+    float q[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) q[u] = __ldcs(P + (int64_t)(s + u) * H + j);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v += q[u];
+  }
+  for (; s < S; ++s) v += P[(int64_t)s * H + j];
+  db[j * sdb] = v;
+}
+
 struct NG {
   int64_t B, H, k;
   int S;  // slabs (CTAs along y)
@@ -316,13 +333,15 @@ int tx_narrow_grad_workspace(const tx_tensor* dz, const tx_tensor* wt, const tx_
     *bytes = (size_t)p.S * (size_t)p.H * (size_t)(p.k + 1) * 4 + 256;
     return TX_OK;
   }
-  // unfused: the three ops one after another share one workspace
+  // unfused: the three ops one after another share one workspace, plus the
+  // dh GEMM's per-32-row column sums when db is wanted (tcgen05 epilogue)
   size_t a = 0, b = 0, c = 0;
   tx_tensor ht = transposed2(*h);
   if ((rc = tx_gemm_workspace(dz, wt, dh, mode, &a))) return rc;
   if ((rc = tx_gemm_workspace(&ht, dz, gw, mode, &b))) return rc;
   if (db && db->data && (rc = tx_reduce_workspace(TX_SUM, dh, 1u, &c))) return rc;
-  *bytes = a > b ? (a > c ? a : c) : (b > c ? b : c);
+  const size_t colsum = (db && db->data) ? (size_t)((p.B + 31) / 32) * (size_t)p.H * 4 + 256 : 0;
+  *bytes = (a > b ? (a > c ? a : c) : (b > c ? b : c)) + colsum;
   return TX_OK;
 }
 
@@ -338,10 +357,26 @@ int tx_narrow_grad(const tx_tensor* dz, const tx_tensor* wt, const tx_tensor* h,
     memset(&e1, 0, sizeof(e1));
     e1.kind = TX_EPI_MUL_1MSQR;
     e1.aux = *h;
-    if ((rc = tx_gemm(dz, wt, dh, &e1, mode, ws, wsb, stream))) return rc;
+    // db from the dh GEMM's epilogue (column sums of the staged C tiles) when
+    // dh runs on the tensor cores: the [B, H] dh is not re-read
+    const size_t csb = want_db ? (size_t)((p.B + 31) / 32) * (size_t)p.H * 4 : 0;
+    bool db_done = false;
+    if (want_db && p.B > 0 && p.H > 0 && h->dtype == TX_F32 && !getenv("TX_NARROW_NO_COLSUM") && ws &&
+        wsb >= csb + 256) {
+      float* partials = (float*)(((uintptr_t)ws + wsb - csb) & ~(uintptr_t)15);
+      if ((uintptr_t)partials >= (uintptr_t)ws && gemm_with_colsum(dz, wt, dh, &e1, mode, partials, st) == TX_OK) {
+        const int64_t S = (p.B + 31) / 32;
+        colsum_finalize<<<(unsigned)((p.H + 255) / 256), 256, 0, st>>>(partials, (int)S, p.H, (float*)db->data,
+                                                                      db->strides[0]);
+        TX_CUDA(cudaGetLastError());
+        db_done = true;
+      }
+    }
+    const size_t wsg = want_db && wsb > csb + 256 ? wsb - csb - 256 : wsb;
+    if (!db_done && (rc = tx_gemm(dz, wt, dh, &e1, mode, ws, wsg, stream))) return rc;
     tx_tensor ht = transposed2(*h);
-    if ((rc = tx_gemm(&ht, dz, gw, gw_epi, mode, ws, wsb, stream))) return rc;
-    if (want_db) return tx_reduce(TX_SUM, dh, 1u, db, ws, wsb, stream);
+    if ((rc = tx_gemm(&ht, dz, gw, gw_epi, mode, ws, wsg, stream))) return rc;
+    if (want_db && !db_done) return tx_reduce(TX_SUM, dh, 1u, db, ws, wsg, stream);
     return TX_OK;
   }
   const size_t need = (size_t)p.S * (size_t)p.H * (size_t)(p.k + 1) * 4;

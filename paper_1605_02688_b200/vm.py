@@ -810,7 +810,14 @@ class StepPlan:
                     for x in cands:
                         xl = self.lay[x.id]
                         xs = xl.storage
-                        if (xs.kind == "arena" and xs.alias is None and xs.offset is not None
+                        # another operand reading the same storage through a
+                        # different view (x * x.T) would see elements this
+                        # kernel already overwrote: not in place
+                        clash = any(self.lay[y.id].storage.root() is xs.root()
+                                    and (self.lay[y.id].offset, self.lay[y.id].strides, self.lay[y.id].shape)
+                                    != (xl.offset, xl.strides, xl.shape)
+                                    for y in n.inputs if y is not x and y.id in self.lay)
+                        if (not clash and xs.kind == "arena" and xs.alias is None and xs.offset is not None
                                 and id(xs) not in taken and xs.last_use == i and xl.offset == 0
                                 and xl.shape == ol.shape and xl.dtype == ol.dtype and xl.contiguous()
                                 and xs.nbytes == st.nbytes):

@@ -384,3 +384,19 @@ def test_device_fault_leaves_updates_uncommitted():
     assert np.array_equal(s.get_value(), np.arange(6) + 3)
     f(np.full(6, 7, np.int64), np.full(6, 7, np.int64))
     assert np.array_equal(s.get_value(), np.arange(6) + 4)
+
+
+def test_elementwise_never_in_place_over_a_view_of_itself(rng):
+    """x * x.T where x dies at the product: writing the product into x's
+    buffer would race with the transposed reads (regression found by the
+    random view graphs; the result was run-to-run different)."""
+    a = T.matrix("a", dtype="float32")
+    b = T.matrix("b", dtype="float32")
+    d = T.dot(a, b)
+    f = T.compile([a, b], d * T.dimshuffle(d, (1, 0)), gemm_mode="simt")
+    av = rng.standard_normal((96, 96)).astype(np.float32)
+    bv = rng.standard_normal((96, 96)).astype(np.float32)
+    dv = av.astype(np.float64) @ bv
+    want = dv * dv.T
+    for _ in range(5):
+        np.testing.assert_allclose(f(av, bv), want, rtol=1e-4, atol=1e-3)
