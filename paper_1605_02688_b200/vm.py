@@ -33,6 +33,9 @@ from . import codegen, native
 from .dtypes import ITEMSIZE, np_dtype
 from .elemwise import Composite, Elemwise, EwProgram
 from .shaping import IncSubtensor
+
+# debugging aid (tests): TX_POISON=1 fills every arena / scratch buffer with NaN bytes
+_POISON = bool(__import__("os").environ.get("TX_POISON"))
 from .errors import (NotSupported, ShapeMismatch, TexprError, TypeMismatch,
                      UnderdeterminedOutputs)
 from .graph import Constant, FunctionGraph, Variable, clone_outputs
@@ -882,6 +885,8 @@ class StepPlan:
             self.arena = cur
         else:
             self.arena = t.empty(need, dtype=t.uint8, device="cuda")
+        if _POISON:
+            self.arena.fill_(0xFF)  # NaN / -1 everywhere: uninitialised reads show up in results
         base = self.arena.data_ptr()
         for lay in list(self.lay.values()) + [d for _, d in self.tail_copies]:
             r = lay.storage.root()
@@ -985,6 +990,8 @@ class StepPlan:
         t = _torch()
         nb = int(np.prod(shape, dtype=np.int64)) * ITEMSIZE[dtype]
         buf = t.empty(max(nb, ALIGN), dtype=t.uint8, device="cuda")
+        if _POISON:
+            buf.fill_(0xFF)
         self.keep.append(buf)
         st = Storage("scratch", nb, ptr=buf.data_ptr(), name="scratch")
         return Layout(st, 0, tuple(shape), contiguous_strides(tuple(shape)), dtype)
