@@ -782,6 +782,12 @@ class StepPlan:
         # ---- arena allocation with in-place reuse for elementwise kernels
         deferred_ids = {n.id for grp in self.row_groups for n in grp.deferred}
         alloc = ArenaAllocator()
+        # the zero-division flag is live for the whole step (cleared first,
+        # read last): placed before any liveness-based reuse, never released
+        if any(codegen.has_int_div(getattr(n.op, "program", None) or EwProgram.single(n.op.kernel, [x.type.dtype for x in n.inputs]))
+               for n in order if isinstance(n.op, (Elemwise, Composite))):
+            self.flag = Storage("arena", 4, name="flag")
+            self.flag.offset = alloc.alloc(4)
         live_at: dict[int, list] = {}
 
         def assign(st, step=INF):
@@ -852,10 +858,6 @@ class StepPlan:
         # any arena storage not yet placed (e.g. unused outputs)
         for lay in list(self.lay.values()):
             assign(lay.storage.root())
-        if any(codegen.has_int_div(getattr(n.op, "program", None) or EwProgram.single(n.op.kernel, [x.type.dtype for x in n.inputs]))
-               for n in order if isinstance(n.op, (Elemwise, Composite))):
-            self.flag = Storage("arena", 4, name="flag")
-            self.flag.offset = alloc.alloc(4)
         self.buckets = []  # (dtype, ptr, count, member vars)
         if partial_vars:
             from . import dp as _dp

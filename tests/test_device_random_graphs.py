@@ -168,3 +168,58 @@ def test_random_view_graphs_match_reference_algorithm(dt, rel):
         want = C.CpuFunction(T, inputs, outs)(*vals)
         for g, w in zip(got, want):
             _check(g, w, rel)
+
+
+def _random_int_graph(seed, dt, R=29, Cc=41):
+    """Integer expressions (bit-exact): add / sub / mul / maximum, floor
+    division by a non-zero divisor, comparisons into switch, row / column
+    sums and maxima, argmax."""
+    rng = np.random.default_rng(seed)
+    x, y, v = T.matrix("x", dtype=dt), T.matrix("y", dtype=dt), T.vector("v", dtype=dt)
+    mats, vecs = [x, y], [v]
+
+    def pick(pool):
+        return pool[int(rng.integers(len(pool)))]
+    for _ in range(int(rng.integers(5, 11))):
+        r = rng.random()
+        if r < 0.4:
+            k = ("add", "sub", "mul", "maximum")[int(rng.integers(4))]
+            b = pick(mats) if rng.random() < 0.7 else pick(vecs)
+            mats.append(make(k, [pick(mats), b]))
+        elif r < 0.55:
+            d = x if rng.random() < 0.5 else y   # small divisors: d*d + 1 cannot wrap to 0
+            mats.append(make("div", [pick(mats), make("add", [make("mul", [d, d]), T.as_variable(np.asarray(1, dtype=dt))])]))
+        elif r < 0.7:
+            a, b = pick(mats), pick(mats)
+            mats.append(make("switch", [make("le", [a, b]), a, make("neg", [b])]))
+        elif r < 0.85:
+            vecs.append((T.sum if rng.random() < 0.5 else T.max)(pick(mats), axis=0))
+        else:
+            mats.append(pick(mats) + T.dimshuffle(T.max(pick(mats), axis=1), (0, "x")))
+    outs = [mats[-1], vecs[-1], T.argmax(mats[-1], axis=int(rng.integers(2))), T.sum(mats[-1])]
+    vals = [rng.integers(-9, 10, (R, Cc)).astype(dt), rng.integers(-9, 10, (R, Cc)).astype(dt),
+            rng.integers(-9, 10, Cc).astype(dt)]
+    return [x, y, v], outs, vals
+
+
+@pytest.mark.parametrize("dt", ["int32", "int64"])
+def test_random_integer_graphs_bit_exact(dt):
+    for seed in range(30):
+        inputs, outs, vals = _random_int_graph(7000 + seed, dt)
+        got = T.compile(inputs, outs)(*vals)
+        want = C.CpuFunction(T, inputs, outs)(*vals)
+        for g, w in zip(got, want):
+            np.testing.assert_array_equal(np.asarray(g), np.asarray(w))
+
+
+def test_random_graphs_survive_save_and_load():
+    """A compiled random graph saved to a TXFN container and loaded back
+    computes the same values (portable form: device-only nodes expanded)."""
+    for seed in range(10):
+        inputs, outs, vals = _random_graph(1000 + seed, "float64")
+        f = T.compile(inputs, outs)
+        g = T.load(f.save())
+        for a, b in zip(f(*vals), g(*vals)):
+            a, b = np.asarray(a), np.asarray(b)
+            assert a.shape == b.shape
+            assert np.allclose(a, b, rtol=1e-12, atol=1e-12, equal_nan=True)

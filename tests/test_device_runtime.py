@@ -400,3 +400,17 @@ def test_elementwise_never_in_place_over_a_view_of_itself(rng):
     want = dv * dv.T
     for _ in range(5):
         np.testing.assert_allclose(f(av, bv), want, rtol=1e-4, atol=1e-3)
+
+
+def test_zero_division_flag_not_clobbered_by_reused_buffers():
+    """The device zero-division flag lives for the whole step; it used to be
+    placed after the liveness walk, in memory an intermediate later reused
+    (a // (c*c + 1) raised ZeroDivisionError; found by the random integer
+    graphs)."""
+    from paper_1605_02688_b200.elemwise import make
+    a, c = T.vector("a", dtype="int32"), T.vector("c", dtype="int32")
+    d = make("add", [make("mul", [c, c]), T.as_variable(np.asarray(1, dtype="int64"))])
+    av = np.arange(-5, 5, dtype=np.int32)
+    for preset in ("none", "fast_run"):
+        got = T.compile([a, c], make("div", [a, d]), preset=preset)(av, av)
+        np.testing.assert_array_equal(got, av.astype(np.int64) // (av.astype(np.int64) ** 2 + 1))
