@@ -324,7 +324,9 @@ class CompiledFunction:
         for s, u in self.updates:
             used_values[u.id] = used_values.get(u.id, 0) + 1
         for s, u in self.updates:
-            var = next(v for sh, v in self.shared_bindings if sh is s)
+            var = next((v for sh, v in self.shared_bindings if sh is s), None)
+            if var is None:
+                continue  # a target nothing reads: written back after the step
             p = u.owner
             if p is None or used_values[u.id] > 1 or u.id in outputs_set:
                 continue
@@ -705,13 +707,16 @@ class StepPlan:
         self.commits = []      # (src Layout, dst Layout)
         self.late_updates = [] # (shared, Layout) for shape-changing updates
         for s, u in fn.updates:
-            var = next(v for sh, v in fn.shared_bindings if sh is s)
+            var = next((v for sh, v in fn.shared_bindings if sh is s), None)
             ul = self.lay[u.id] if u.id in self.lay else self._const_layout(u)
-            slay = self.lay.get(var.id)
-            if slay is not None and ul.storage is slay.storage and ul.offset == 0:
+            slay = self.lay.get(var.id) if var is not None else None
+            if slay is not None and ul.storage is slay.storage and ul.offset == 0 \
+                    and ul.strides == slay.strides and ul.shape == slay.shape:
                 written.add(id(slay.storage))
                 continue  # written in place (or identity update)
             if slay is not None and ul.shape == slay.shape:
+                # (a value that is another view of the same storage -- A <- A.T
+                # -- is snapshotted below before the commit overwrites it)
                 self.commits.append((ul, slay))
                 written.add(id(slay.storage))
             else:
@@ -739,6 +744,15 @@ class StepPlan:
                 src = snap
             fixed.append((src, dst))
         self.commits = fixed
+        late = []
+        for sh, ul in self.late_updates:
+            if id(ul.storage) in written:  # e.g. B <- A while A is itself updated
+                nb = ul.numel * ITEMSIZE[ul.dtype]
+                snap = Layout(Storage("arena", nb, name="snap"), 0, ul.shape, contiguous_strides(ul.shape), ul.dtype)
+                self.tail_copies.append((ul, snap))
+                ul = snap
+            late.append((sh, ul))
+        self.late_updates = late
 
         # ---- liveness over storages
         def touch(lay_, step):

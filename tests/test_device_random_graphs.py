@@ -223,3 +223,49 @@ def test_random_graphs_survive_save_and_load():
             a, b = np.asarray(a), np.asarray(b)
             assert a.shape == b.shape
             assert np.allclose(a, b, rtol=1e-12, atol=1e-12, equal_nan=True)
+
+
+def test_random_update_graphs_match_reference_algorithm():
+    """Shared variables updated from random expressions of each other and of
+    the inputs (swaps, views of other shared values, in-place candidates,
+    outputs that read the old values), three calls, against the reference
+    algorithm's write-back-after-the-step semantics (runtime.py:415-421)."""
+    for seed in range(25):
+        rng = np.random.default_rng(8000 + seed)
+        n = 24
+        init = [rng.standard_normal((n, n)), rng.standard_normal((n, n)), rng.standard_normal(n)]
+
+        def build(vals):
+            A = T.shared(vals[0].copy(), name="A")
+            Bm = T.shared(vals[1].copy(), name="B")
+            v = T.shared(vals[2].copy(), name="v")
+            x = T.matrix("x")
+            pool = [A, Bm, x, T.dimshuffle(A, (1, 0)), Bm * 0.5]
+            r = np.random.default_rng(9000 + seed)
+
+            def pick():
+                return pool[int(r.integers(len(pool)))]
+            for _ in range(int(r.integers(2, 6))):
+                k = r.random()
+                if k < 0.4:
+                    pool.append(pick() + pick())
+                elif k < 0.7:
+                    pool.append(T.tanh(pick()) * 0.9)
+                else:
+                    pool.append(T.dot(pick(), pick()) * 0.1)
+            choices = [pool[int(r.integers(len(pool)))] for _ in range(2)]
+            ups = [(A, choices[0]), (Bm, A if r.random() < 0.4 else choices[1]),
+                   (v, v + T.sum(pool[-1], axis=0) * 0.01)]
+            outs = [T.sum(pool[-1]), A + 0.0]
+            return [x], outs, ups, (A, Bm, v)
+        xv = rng.standard_normal((n, n))
+        ins, outs, ups, sh_dev = build(init)
+        f = T.compile(ins, outs, updates=ups)
+        ins2, outs2, ups2, sh_ref = build(init)
+        ref = C.CpuFunction(T, ins2, outs2, ups2)
+        for _ in range(3):
+            got, want = f(xv), ref(xv)
+            for g, w in zip(got, want):
+                _check(g, w, 1e-9)
+        for s_dev, (s_ref, _) in zip(sh_dev, ups2):
+            _check(s_dev.get_value(), ref.value(s_ref), 1e-9)

@@ -414,3 +414,21 @@ def test_zero_division_flag_not_clobbered_by_reused_buffers():
     for preset in ("none", "fast_run"):
         got = T.compile([a, c], make("div", [a, d]), preset=preset)(av, av)
         np.testing.assert_array_equal(got, av.astype(np.int64) // (av.astype(np.int64) ** 2 + 1))
+
+
+def test_update_to_a_view_of_itself_and_unread_targets():
+    """A <- A.T (the update value is another view of the target's own
+    buffer: it used to be mistaken for an identity update and skipped),
+    B <- A (B read by nothing: it used to crash the scheduler), with the
+    reference's write-back-after-the-step semantics."""
+    a0 = np.arange(12.0).reshape(3, 4)[:, :3].copy()
+    A = T.shared(a0.copy(), name="A")
+    B = T.shared(np.zeros((3, 3)), name="B")
+    x = T.scalar("x")
+    f = T.compile([x], T.sum(A) * x, updates=[(A, T.dimshuffle(A, (1, 0))), (B, A)])
+    assert float(f(2.0)) == 2 * a0.sum()
+    np.testing.assert_array_equal(A.get_value(), a0.T)
+    np.testing.assert_array_equal(B.get_value(), a0)
+    f(1.0)
+    np.testing.assert_array_equal(A.get_value(), a0)
+    np.testing.assert_array_equal(B.get_value(), a0.T)
