@@ -803,8 +803,37 @@ using namespace tx;
 
 extern "C" {
 
+// Zero-size cases, before any planning (which divides by the extents):
+// returns 1 when there is nothing to launch.
+static int empty_case(int op, const tx_tensor& x, uint32_t mask, tx_tensor* y, cudaStream_t st, bool run, int* rc) {
+  int64_t red = 1, keep = 1;
+  for (int d = 0; d < x.ndim; ++d) ((mask >> d) & 1u ? red : keep) *= x.shape[d];
+  if (op == TX_ARGMAX_ONEHOT) keep *= red;  // the one-hot output has the input's shape
+  *rc = TX_OK;
+  if (red == 0 && op != TX_SUM) {           // NumPy raises for max / argmax over an empty axis
+    *rc = fail(TX_E_ARG, "zero-size reduction: max / argmax have no identity");  // (even for an empty result)
+    return 1;
+  }
+  if (keep == 0) return 1;                  // empty result: nothing to compute
+  if (red != 0) return 0;
+  if (run) {                                // sum over an empty axis is 0
+    if (!is_contiguous(*y)) {
+      *rc = fail(TX_E_UNSUPPORTED, "tx_reduce: empty-axis sum into a strided output");
+      return 1;
+    }
+    const cudaError_t e = cudaMemsetAsync(y->data, 0, (size_t)numel(*y) * itemsize(y->dtype), st);
+    if (e != cudaSuccess) *rc = cuda_fail(e, "cudaMemsetAsync");
+  }
+  return 1;
+}
+
 int tx_reduce_workspace(int op, const tx_tensor* x, uint32_t mask, size_t* bytes) {
   TX_CHECK(x && bytes, TX_E_ARG, "tx_reduce_workspace: null argument");
+  int erc;
+  if (mask && empty_case(op, *x, mask, nullptr, 0, false, &erc)) {
+    *bytes = 0;
+    return TX_OK;
+  }
   Plan p;
   int isz = itemsize(x->dtype);
   make_plan(op, *x, mask, isz < 4 ? 4 : isz, &p);
@@ -821,6 +850,8 @@ int tx_reduce(int op, const tx_tensor* x, uint32_t mask, tx_tensor* y, void* ws,
     }
     return tx_copy(x, y, stream);
   }
+  int erc;
+  if (empty_case(op, *x, mask, y, (cudaStream_t)stream, true, &erc)) return erc;
   return reduce_launch(op, *x, mask, *y, ws, wsb, (cudaStream_t)stream);
 }
 

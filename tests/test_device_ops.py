@@ -381,3 +381,21 @@ def test_dot_bias_strided_and_unaligned_bias(rng):
     f = T.compile([vx, vw, vb], T.dot(vx, vw) + vb)
     with pytest.raises(ShapeMismatch):
         f(x, W, bb)
+
+
+def test_reductions_over_empty_extents():
+    """Zero-size inputs: an empty result launches nothing, a sum over an
+    empty axis is 0, max / argmax over one raise (NumPy's ValueError in the
+    reference) -- the planner used to divide by the empty extent (SIGFPE)."""
+    from paper_1605_02688_b200.errors import TexprError
+    x = T.tensor3("x")
+    for shape in ((2, 33, 0), (5, 0, 33), (0, 0, 1)):
+        xv = np.zeros(shape)
+        s0, s1 = T.compile([x], [T.sum(x, axis=0), T.sum(x, axis=1)])(xv)
+        np.testing.assert_array_equal(s0, xv.sum(0))
+        np.testing.assert_array_equal(s1, xv.sum(1))
+        if 0 in (shape[1],):
+            with pytest.raises(Exception):
+                T.compile([x], T.max(x, axis=1))(xv)
+        else:
+            np.testing.assert_array_equal(T.compile([x], T.max(x, axis=1))(xv), xv.max(1))

@@ -269,3 +269,56 @@ def test_random_update_graphs_match_reference_algorithm():
                 _check(g, w, 1e-9)
         for s_dev, (s_ref, _) in zip(sh_dev, ups2):
             _check(s_dev.get_value(), ref.value(s_ref), 1e-9)
+
+
+def _random_edge_graph(seed):
+    """Rank-3 operands with broadcastable axes, ragged and empty extents,
+    reductions over axis pairs, outputs that are inputs or views of them."""
+    rng = np.random.default_rng(seed)
+    a, b, c = (int(v) for v in rng.choice([0, 2, 5, 33], 3))  # extent 1 only where declared broadcastable
+    x = T.tensor3("x")
+    y = T.tensor3("y", broadcastable=(False, True, False))       # [a, 1, c]
+    v = T.vector("v")                                             # [c]
+    pool = [x, y, v]
+
+    def pick():
+        return pool[int(rng.integers(len(pool)))]
+    for _ in range(int(rng.integers(3, 8))):
+        r = rng.random()
+        if r < 0.35:
+            k = ("add", "mul", "sub", "maximum")[int(rng.integers(4))]
+            pool.append(make(k, [pick(), pick()]))
+        elif r < 0.5:
+            pool.append(T.tanh(pick()))
+        elif r < 0.7:
+            src = pick()
+            if src.type.ndim == 3:
+                ax = [(0,), (1,), (2,), (0, 2), (1, 2), (0, 1, 2)][int(rng.integers(6))]
+                red = T.sum if rng.random() < 0.6 else T.max
+                pool.append(red(src, axis=ax) if len(ax) < 3 else red(src))
+        elif r < 0.85:
+            src = pick()
+            if src.type.ndim == 3:
+                pool.append(T.dimshuffle(src, (2, 0, 1)))
+        else:
+            pool.append(make("second", [pick(), T.as_variable(np.asarray(1.5))]))
+    outs = [pool[-1], x, T.dimshuffle(y, (0, 2, 1)), pool[int(rng.integers(len(pool)))]]
+    vals = [rng.standard_normal((a, b, c)), rng.standard_normal((a, 1, c)), rng.standard_normal(c)]
+    return [x, y, v], outs, vals
+
+
+def test_random_edge_graphs_match_reference_algorithm():
+    """Broadcastable and empty axes, axis-pair reductions, outputs aliasing
+    inputs: the device agrees with the reference algorithm or both raise
+    (max over an empty axis is an error in both)."""
+    for seed in range(60):
+        inputs, outs, vals = _random_edge_graph(11000 + seed)
+        try:
+            want = C.CpuFunction(T, inputs, outs)(*vals)
+        except (ValueError, Exception) as exc:  # noqa: B014 (the reference raises on empty max)
+            with pytest.raises(Exception):
+                T.compile(inputs, outs)(*vals)
+            continue
+        got = T.compile(inputs, outs)(*vals)
+        for g, w in zip(got, want):
+            _check(g, w, 1e-9)
