@@ -399,3 +399,33 @@ def test_reductions_over_empty_extents():
                 T.compile([x], T.max(x, axis=1))(xv)
         else:
             np.testing.assert_array_equal(T.compile([x], T.max(x, axis=1))(xv), xv.max(1))
+
+
+def test_empty_operands_everywhere():
+    """Zero-size operands through every kernel family: fused elementwise,
+    GEMMs with an empty M / N / K (K = 0 gives zeros), a softmax region over
+    zero rows, a loop over zero steps."""
+    x, w = T.matrix("x"), T.matrix("w")
+    e = T.tanh(x * 2.0 + 1.0) - x
+    m = T.max(x, axis=1)
+    p = T.exp(x - T.dimshuffle(m, (0, "x")))
+    sm = p / T.dimshuffle(T.sum(p, axis=1), (0, "x"))
+    f = T.compile([x, w], [e, T.dot(x, w), sm])
+    for xs, ws in (((0, 5), (5, 3)), ((4, 0), (0, 3)), ((4, 5), (5, 0))):
+        xv, wv = np.ones(xs), np.ones(ws)
+        if xs[1] == 0:
+            got = T.compile([x, w], [e, T.dot(x, w)])(xv, wv)
+            want = [np.tanh(xv * 2 + 1) - xv, xv @ wv]
+        else:
+            got = f(xv, wv)
+            ev = np.exp(xv - xv.max(1, keepdims=True)) if xv.size else xv
+            want = [np.tanh(xv * 2 + 1) - xv, xv @ wv, ev / ev.sum(1, keepdims=True) if xv.size else ev]
+        for g, wnt in zip(got, want):
+            assert g.shape == wnt.shape
+            np.testing.assert_allclose(g, wnt)
+    xs = T.matrix("xs")
+    h0 = T.vector("h0")
+    (hist,), (final,) = T.scan(lambda x_t, h: [T.tanh(x_t + h)], sequences=[xs], initial_states=[h0])
+    hv, fv = T.compile([xs, h0], [hist, final])(np.zeros((0, 3)), np.ones(3))
+    assert hv.shape == (0, 3)
+    np.testing.assert_array_equal(fv, np.ones(3))
