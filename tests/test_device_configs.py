@@ -215,7 +215,7 @@ def test_narrow_grad_fusion_matches_unfused(B, H, K):
         assert np.linalg.norm(a - b) <= 1e-5 * max(np.linalg.norm(a), 1e-30), pa.name
 
 
-@pytest.mark.parametrize("N,K", [(20, 10000), (7, 3000), (300, 257), (64, 10240)])
+@pytest.mark.parametrize("N,K", [(20, 10000), (7, 3000), (300, 257), (64, 10240), (300, 256), (50, 10241), (3, 2)])
 def test_wide_row_fusion_softmax_xent(N, K):
     """Vocabulary-sized rows (one 1024-thread CTA per row): softmax +
     cross-entropy forward and gradient, max / argmax outputs, against the
@@ -233,11 +233,12 @@ def test_wide_row_fusion_softmax_xent(N, K):
     fb = T.compile([z, y], outs)
     plan_groups = None
     zv = (rng.standard_normal((N, K)) * 3).astype(np.float32)
-    zv[0, 5] = zv[0, K - 3] = 50.0  # a tie at the row maximum
+    zv[0, min(5, K - 1)] = zv[0, max(K - 3, 0)] = 50.0  # a tie at the row maximum
     yv = np.eye(K, dtype=np.float32)[rng.integers(0, K, N)]
     a, b = fa(zv, yv), fb(zv, yv)
     plan_groups = next(iter(fb._plans.values())).row_groups
-    assert plan_groups and any(g.K == K for g in plan_groups)
+    from paper_1605_02688_b200.rowfuse import MAX_WIDE
+    assert bool(plan_groups and any(g.K == K for g in plan_groups)) == (2 <= K <= MAX_WIDE and N != K)
     assert abs(a[0] - b[0]) <= 1e-5 * abs(a[0])
     np.testing.assert_allclose(b[1], a[1], rtol=1e-5, atol=1e-8)
     np.testing.assert_array_equal(b[2], a[2])
