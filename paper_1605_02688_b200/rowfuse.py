@@ -29,6 +29,8 @@ from __future__ import annotations
 import ctypes
 import threading
 
+import numpy as np
+
 from . import codegen
 from .dtypes import C_TYPE, ITEMSIZE, is_float
 from .elemwise import Composite, Elemwise, kernel_compute_dtype
@@ -53,17 +55,29 @@ def wide_threads(K):
     return t
 
 
-def classify(shape, N, K):
+def classify(shape, lead, K):
+    """Class of a value in the row space lead + (K,): lead is (N,) for a
+    matrix of rows or (A, B) for a rank-3 tensor whose A*B rows are flattened."""
     shape = tuple(shape)
-    if shape == (N, K):
+    if isinstance(lead, int):
+        lead = (lead,)
+    r = len(lead)
+    if shape == lead + (K,):
         return V
-    if shape in ((N,), (N, 1)):
+    if shape in (lead, lead + (1,)):
         return S
-    if shape in ((K,), (1, K)):
+    if len(shape) <= r + 1 and shape[-1:] == (K,) and all(d == 1 for d in shape[:-1]):
         return C
-    if shape in ((), (1,), (1, 1)):
+    if all(d == 1 for d in shape):
         return U
     return None
+
+
+def _rows_flat(shape, strides, lead):
+    """Can a V / S value of a rank-3 row space be addressed with one row stride?"""
+    if len(lead) == 1:
+        return True
+    return len(shape) >= 2 and (shape[0] <= 1 or strides[0] == shape[1] * strides[1])
 
 
 def _combine(classes):
@@ -84,8 +98,10 @@ class RowArgs(ctypes.Structure):
 
 
 class RowGroup:
-    def __init__(self, N, K):
-        self.N, self.K = N, K
+    def __init__(self, lead, K):
+        self.lead = tuple(lead)
+        self.N, self.K = int(np.prod(self.lead)), K
+        self.row_axis = len(self.lead)
         self.members = []          # nodes (views included), schedule order
         self.member_ids = set()
         self.values = {}           # var id -> class, for every group-produced value
@@ -99,24 +115,42 @@ class RowGroup:
 
 # ---------------------------------------------------------------- grouping
 
-def _is_sink(n, shapes):
+def _is_sink(n, shapes, lead):
+    """A sum over the batch: all leading (row) axes of a row vector (-> a
+    column vector) or every axis (-> a scalar); of a row scalar, its row axes."""
     if not isinstance(n.op, Sum):
         return False
-    shp = shapes(n.inputs[0])
-    if len(shp) == 2 and n.op.axes in ((0,), (0, 1)):
+    shp, lead = tuple(shapes(n.inputs[0])), tuple(lead)
+    r = len(lead)
+    rows, every = tuple(range(r)), tuple(range(len(shp)))
+    if len(shp) == r + 1 and shp[:r] == lead:
+        return n.op.axes in (rows, every)
+    if shp in (lead, lead + (1,)):
+        return n.op.axes in (rows, every)
+    return False
+
+
+def _flat_ok(plan, v, grp):
+    """Rank-3 row spaces read every V / S operand through one row stride."""
+    if len(grp.lead) == 1 or v.id not in plan.lay:
         return True
-    return len(shp) == 1 and n.op.axes == (0,)
+    lay = plan.lay[v.id]
+    if classify(lay.shape, grp.lead, grp.K) not in (V, S):
+        return True
+    return _rows_flat(lay.shape, lay.strides, grp.lead)
 
 
-def _node_fits(n, grp, shapes, allowed_in):
+def _node_fits(n, grp, shapes, allowed_in, plan=None):
     """Can node n join group grp (given the values the group already has)?"""
     op = n.op
-    N, K = grp.N, grp.K
-    ins = [classify(shapes(x), N, K) for x in n.inputs]
-    outs = [classify(shapes(o), N, K) for o in n.outputs]
+    lead, K = grp.lead, grp.K
+    ins = [classify(shapes(x), lead, K) for x in n.inputs]
+    outs = [classify(shapes(o), lead, K) for o in n.outputs]
     if any(c is None for c in ins + outs):
         return False
     if any(x.id in grp.sink_vars for x in n.inputs):
+        return False
+    if plan is not None and not all(_flat_ok(plan, x, grp) for x in n.inputs):
         return False
     # (not necessarily connected: any row-space node whose inputs are ready
     # can run inside the group — fewer launches)
@@ -129,42 +163,44 @@ def _node_fits(n, grp, shapes, allowed_in):
             op.kernel == "div" and not is_float(kernel_compute_dtype("div", [x.type.dtype for x in n.inputs])))
         return not prog_has_int_div
     if isinstance(op, (Sum, Max, ArgmaxOnehot, Argmax)):
-        if op.axes == (1,) and ins[0] == V:
+        if op.axes == (grp.row_axis,) and ins[0] == V:
             return is_float(n.inputs[0].type.dtype)
-        if isinstance(op, Sum) and _is_sink(n, shapes) and ins[0] in (V, S):
+        if isinstance(op, Sum) and _is_sink(n, shapes, lead) and ins[0] in (V, S):
             # a wide row's column sums ([N, K] -> [K]) would be combined by a
             # single CTA; they stay a separate (parallel) column reduction
-            return not (grp.K > MAX_K and ins[0] == V and op.axes == (0,))
+            return not (grp.K > MAX_K and ins[0] == V and op.axes == tuple(range(len(lead))))
         return False
     return False
 
 
-def _seed(n, shapes, exclude_ids):
-    """A node that can open a group: a row reduction over [N, K] or an
-    elementwise node producing [N, K] (the logits' bias add), 2 <= K <= 256."""
+def _seed(n, shapes, exclude_ids, plan=None):
+    """A node that can open a group: a reduction over the last axis of an
+    [N, K] or [A, B, K] tensor, or an elementwise node producing one (the
+    logits' bias add), 2 <= K <= MAX_WIDE."""
     if n.id in exclude_ids:
         return None
     op = n.op
-    if isinstance(op, (Sum, Max, ArgmaxOnehot, Argmax)) and op.axes == (1,):
-        shp = shapes(n.inputs[0])
-        if not is_float(n.inputs[0].type.dtype):
+    if isinstance(op, (Sum, Max, ArgmaxOnehot, Argmax)):
+        shp = tuple(shapes(n.inputs[0]))
+        if op.axes != (len(shp) - 1,) or not is_float(n.inputs[0].type.dtype):
             return None
     elif isinstance(op, (Elemwise, Composite)):
-        shp = shapes(n.outputs[0])
+        shp = tuple(shapes(n.outputs[0]))
         if any(tuple(shapes(o)) != tuple(shp) for o in n.outputs):
             return None
         if isinstance(op, Composite) and codegen.has_int_div(op.program):
             return None
     else:
         return None
-    if len(shp) != 2:
+    if len(shp) not in (2, 3):
         return None
-    N, K = shp
-    if not (2 <= K <= MAX_WIDE) or N < 2 or N == K or N >= (1 << 31):
+    lead, K = shp[:-1], shp[-1]
+    N = int(np.prod(lead))
+    if not (2 <= K <= MAX_WIDE) or N < 2 or N >= (1 << 31) or K in lead or (len(lead) == 2 and N == K):
         return None
-    grp = RowGroup(N, K)
+    grp = RowGroup(lead, K)
     for x in n.inputs:
-        if classify(shapes(x), N, K) is None:
+        if classify(shapes(x), lead, K) is None or (plan is not None and not _flat_ok(plan, x, grp)):
             return None
     return grp
 
@@ -191,7 +227,8 @@ def find_groups(plan, order, fgraph, exclude_ids=()):
         # reductions; pure elementwise work on wide rows stays on the
         # 128-bit elementwise kernels
         if cur is not None and len(cur.launchable()) >= 2 and (cur.K <= MAX_K or any(
-                isinstance(n.op, (Sum, Max, ArgmaxOnehot, Argmax)) and n.op.axes == (1,) for n in cur.members)):
+                isinstance(n.op, (Sum, Max, ArgmaxOnehot, Argmax)) and n.op.axes == (cur.row_axis,)
+                for n in cur.members)):
             groups.append(cur)
         cur = None
         deferred_out.clear()
@@ -200,9 +237,9 @@ def find_groups(plan, order, fgraph, exclude_ids=()):
         grp.members.append(n)
         grp.member_ids.add(n.id)
         grp.last_pos = i
-        sink = _is_sink(n, shapes)
+        sink = _is_sink(n, shapes, grp.lead)
         for o in n.outputs:
-            grp.values[o.id] = classify(shapes(o), grp.N, grp.K)
+            grp.values[o.id] = classify(shapes(o), grp.lead, grp.K)
             if sink:
                 grp.sink_vars.add(o.id)
 
@@ -210,7 +247,7 @@ def find_groups(plan, order, fgraph, exclude_ids=()):
         reads_group = cur is not None and any(x.id in cur.values for x in n.inputs)
         reads_deferred = any(x.id in deferred_out for x in n.inputs)
         if cur is not None and not reads_deferred and n.id not in exclude_ids \
-                and _node_fits(n, cur, shapes, lambda x: True):
+                and _node_fits(n, cur, shapes, lambda x: True, plan):
             add(cur, n, i)
             continue
         if (reads_group or reads_deferred) and cur is not None and len(cur.launchable()) < 2:
@@ -225,7 +262,7 @@ def find_groups(plan, order, fgraph, exclude_ids=()):
             continue
         if reads_group or reads_deferred:
             close()
-        g = _seed(n, shapes, exclude_ids)
+        g = _seed(n, shapes, exclude_ids, plan)
         if g is not None:
             close()
             cur = g
@@ -369,7 +406,7 @@ class _Gen:
     def leaf(self, v):
         if v.id in self.name:
             return
-        cls = classify(self.shape(v), self.N, self.K)
+        cls = classify(self.shape(v), self.grp.lead, self.K)
         ct = C_TYPE[v.type.dtype]
         k = self.operand(v, "in")
         nm = f"L{k}"
@@ -448,19 +485,20 @@ class _Gen:
         ct = C_TYPE[x.type.dtype]
         xn = self.name[x.id]
         nm = f"t{len(self.name)}"
-        if isinstance(op, Sum) and op.axes == (1,):
+        ra = (self.grp.row_axis,)
+        if isinstance(op, Sum) and op.axes == ra:
             self.emit(f"{ct} {nm} = 0;")
             self.emit(f"#pragma unroll\nfor (int j = 0; j < TX_R; ++j) if (tc + TX_T * j < K) {nm} += {xn}[j];")
             self.emit(f"{nm} = {self.rsum}({nm});")
             self.name[o.id], self.cls[o.id], self.dt[o.id] = nm, S, o.type.dtype
-        elif isinstance(op, Max) and op.axes == (1,):
+        elif isinstance(op, Max) and op.axes == ra:
             self.emit(f"{ct} {nm} = {xn}[0];")
             self.emit(f"#pragma unroll\nfor (int j = 1; j < TX_R; ++j) if (tc + TX_T * j < K) {{ {ct} w = {xn}[j]; "
                       f"{nm} = ({nm} != {nm}) ? {nm} : ((w != w) ? w : (w > {nm} ? w : {nm})); }}")
             self.emit(f"if (tc >= K) {nm} = -__int_as_float(0x7f800000);" if ct == "float" else f"if (tc >= K) {nm} = -__longlong_as_double(0x7ff0000000000000LL);")
             self.emit(f"{nm} = {self.rmax}({nm});")
             self.name[o.id], self.cls[o.id], self.dt[o.id] = nm, S, o.type.dtype
-        elif isinstance(op, (Argmax, ArgmaxOnehot)) and op.axes == (1,):
+        elif isinstance(op, (Argmax, ArgmaxOnehot)) and op.axes == ra:
             iv, ii = f"{nm}_v", f"{nm}_i"
             self.emit(f"{ct} {iv} = {xn}[0]; int {ii} = tc < K ? tc : -1;")
             self.emit(f"#pragma unroll\nfor (int j = 1; j < TX_R; ++j) {{ const int c = tc + TX_T * j; "
@@ -479,7 +517,7 @@ class _Gen:
         elif isinstance(op, Sum):  # sinks: reduce over the batch
             cin = self.cls[x.id]
             acc = f"SK{len(self.sinks)}"
-            if op.axes == (0,) and cin == V:
+            if op.axes == tuple(range(len(self.grp.lead))) and cin == V:
                 self.emit(f"{ct} {acc}[TX_R];")
                 self.emit(f"#pragma unroll\nfor (int j = 0; j < TX_R; ++j) {acc}[j] = "
                           f"(active && tc + TX_T * j < K) ? {xn}[j] : ({ct})0;")
@@ -628,11 +666,12 @@ def emit_group(plan, grp: RowGroup, fgraph):
         t = plan.tx(lay)
         args.ptr[k] = t.data
         shp, st = lay.shape, lay.strides
-        cls = classify(shp, grp.N, grp.K)
+        cls = classify(shp, grp.lead, grp.K)
+        r = len(grp.lead)
         if cls == V:
-            args.rs[k], args.cs[k] = st[0], st[1]
+            args.rs[k], args.cs[k] = st[r - 1], st[r]      # rank-3: rows flattened (checked by _flat_ok)
         elif cls == S:
-            args.rs[k], args.cs[k] = st[0], 0
+            args.rs[k], args.cs[k] = st[r - 1], 0
         elif cls == C:
             args.rs[k], args.cs[k] = 0, st[-1]
         else:

@@ -244,3 +244,30 @@ def test_wide_row_fusion_softmax_xent(N, K):
     np.testing.assert_array_equal(b[2], a[2])
     np.testing.assert_array_equal(b[3], a[3])
     np.testing.assert_allclose(b[4], a[4], rtol=1e-4, atol=1e-7)
+
+
+@pytest.mark.parametrize("A,B,K", [(20, 20, 10000), (6, 7, 130), (3, 50, 257)])
+def test_rank3_row_fusion_softmax_xent(A, B, K):
+    """Softmax / cross-entropy over the last axis of an [A, B, K] tensor (the
+    stacked per-step logits the loop rewrites move out of an LSTM): the A*B
+    rows are one fused row space; results equal the unfused graph."""
+    rng = np.random.default_rng(A * B + K)
+    z = T.tensor3("z", dtype="float32")
+    y = T.tensor3("y", dtype="float32")
+    m = T.max(z, axis=2)
+    e = T.exp(z - T.dimshuffle(m, (0, 1, "x")))
+    p = e / T.dimshuffle(T.sum(e, axis=2), (0, 1, "x"))
+    cost = -T.sum(y * T.log(p)) / float(A * B)
+    (gz,) = T.grad(cost, [z])
+    outs = [cost, gz, m, T.argmax(z, axis=2)]
+    fa = T.compile([z, y], outs, row_fusion=False)
+    fb = T.compile([z, y], outs)
+    zv = (rng.standard_normal((A, B, K)) * 3).astype(np.float32)
+    yv = np.eye(K, dtype=np.float32)[rng.integers(0, K, (A, B))]
+    a, b = fa(zv, yv), fb(zv, yv)
+    groups = next(iter(fb._plans.values())).row_groups
+    assert any(g.lead == (A, B) and g.K == K for g in groups)
+    assert abs(a[0] - b[0]) <= 1e-5 * abs(a[0])
+    np.testing.assert_allclose(b[1], a[1], rtol=1e-5, atol=1e-8)
+    np.testing.assert_array_equal(b[2], a[2])
+    np.testing.assert_array_equal(b[3], a[3])
