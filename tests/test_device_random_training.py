@@ -80,3 +80,36 @@ def test_random_training_steps_match_reference_algorithm(mode, ctol, ptol):
         for (s, _), p in zip(ups, params):
             a, b = p.get_value(), ref.value(s)
             assert np.linalg.norm(a - b) <= ptol * max(np.linalg.norm(b), 1e-30), (seed, p.name)
+
+
+def test_random_training_steps_data_parallel_single_rank():
+    """The data-parallel path (sharding propagation, gradient buckets, NCCL
+    allreduce inside the captured step) on one rank gives the plain step's
+    results on random networks (row fusion off: then bit for bit)."""
+    import os
+
+    import torch.distributed as dist
+
+    from paper_1605_02688_b200.dp import DataParallel
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29541")
+    owns = not dist.is_initialized()
+    if owns:
+        dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        for seed in range(12):
+            ins, outs, ups, params, vals = _net(500 + seed)
+            init = [p.get_value() for p in params]
+            f = T.compile(ins, outs, updates=ups, row_fusion=False)
+            ca = [float(f(*vals)[0]) for _ in range(2)]
+            pa = [p.get_value() for p in params]
+            for p, v in zip(params, init):
+                p.set_value(v)
+            g = T.compile(ins, outs, updates=ups, row_fusion=False, data_parallel=DataParallel(world_size=1, rank=0))
+            cb = [float(g(*vals)[0]) for _ in range(2)]
+            assert ca == cb, (seed, ca, cb)
+            for p, a in zip(params, pa):
+                assert np.array_equal(p.get_value(), a), (seed, p.name)
+    finally:
+        if owns:
+            dist.destroy_process_group()
