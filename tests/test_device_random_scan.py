@@ -109,3 +109,33 @@ def test_random_loops_match_unrolled_reference(dt, b, d, rel, n, mode):
                 _close(g, w, rel)
             except AssertionError:
                 raise AssertionError(f"seed {300 + seed}: output {k} differs") from None
+
+
+def test_random_loops_forward_mode_matches_unrolled():
+    """R-operator (forward mode) through random loops -- the primal+tangent
+    loop of scan.py -- equals the R-operator of the unrolled graph."""
+    for seed in range(15):
+        rng = np.random.default_rng(600 + seed)
+        L = int(rng.integers(1, 6))
+        two, extra, body = _cell(rng)
+        xs = T.tensor3("xs")
+        h0, c0 = T.matrix("h0"), T.matrix("c0")
+        W, U, b = T.matrix("W"), T.matrix("U"), T.vector("b")
+        inits = [h0, c0] if two else [h0]
+        inv = [W, U, b]
+        outs, finals = T.scan(body, sequences=[xs], initial_states=inits, non_sequences=inv)
+        states = list(inits)
+        for t in range(L):
+            states = body(xs[t], *states, *inv)[: len(inits)]
+        dW, dxs = T.matrix("dW"), T.tensor3("dxs")
+        r_loop = T.rop([finals[0]], [W, xs], [dW, dxs])[0]
+        r_unr = T.rop([states[0]], [W, xs], [dW, dxs])[0]
+        ins = [xs] + inits + inv + [dW, dxs]
+        vals = [rng.standard_normal((L, B, D)), rng.standard_normal((B, D)) * 0.5]
+        if two:
+            vals.append(rng.standard_normal((B, D)) * 0.5)
+        vals += [rng.standard_normal((D, D)) / np.sqrt(D), rng.standard_normal((D, D)) / np.sqrt(D),
+                 rng.standard_normal(D) * 0.1, rng.standard_normal((D, D)), rng.standard_normal((L, B, D))]
+        got = T.compile(ins, r_loop)(*vals)
+        want = C.CpuFunction(T, ins, r_unr)(*vals)
+        _close(got, want)
