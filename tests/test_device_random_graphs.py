@@ -362,3 +362,25 @@ def test_random_lazy_conditionals():
         _check(f(np.int64(0), *vals), want_b, 1e-12)
         ran = {nid for nid, k in f.profile.node_calls.items() if k}
         assert ran, "the lazy walk recorded no node calls"
+
+
+def test_random_graphs_with_changing_shapes():
+    """One compiled function called with different row counts in turn (a
+    step plan per shape, cached and re-used out of order) agrees with the
+    reference algorithm every time."""
+    for seed in range(12):
+        inputs, outs, _ = _random_graph(1000 + seed, "float64")
+        f = T.compile(inputs, outs)
+        ref = C.CpuFunction(T, inputs, outs)
+        rng = np.random.default_rng(seed)
+        for R_ in (37, 5, 64, 37, 5, 1):
+            vals = [rng.standard_normal((R_, Cc)), rng.standard_normal((R_, Cc)),
+                    rng.standard_normal((Cc, Cc)) / np.sqrt(Cc), rng.standard_normal(Cc)]
+            try:
+                want = ref(*vals)
+            except Exception:
+                with pytest.raises(Exception):
+                    f(*vals)
+                continue
+            for g, w in zip(f(*vals), want):
+                _check(g, w, 1e-9)
