@@ -117,7 +117,9 @@ class CpuFunction:
         cloned, _ = clone_outputs(outs + uvals, repl)
         self.fg = FunctionGraph([repl[v] for v in full], cloned)
         # the reference has no GEMM epilogues: keep its node list
-        run_preset(self.fg, preset, exclude=tuple(exclude) + ("fuse_gemm_epilogue", "fuse_narrow_grad"))
+        run_preset(self.fg, preset, exclude=tuple(exclude) + (
+            "fuse_gemm_epilogue", "fuse_narrow_grad", "loop_pushout_sequences", "loop_pushout_accumulators",
+            "loop_pushout_outputs", "loop_drop_unused_outputs"))
         self.in_vars = [repl[v] for v in inputs]
         self.sh_vars = [repl[v] for v in found]
         self.n_out = len(outs)

@@ -384,3 +384,32 @@ def test_random_graphs_with_changing_shapes():
                 continue
             for g, w in zip(f(*vals), want):
                 _check(g, w, 1e-9)
+
+
+@pytest.mark.slow
+def test_random_elementwise_graphs_through_the_host_pipeline():
+    """Host-array calls large enough for the chunked H2D / kernel / D2H
+    pipeline (stream.py) on random element-wise graphs (ragged length, two
+    outputs): identical to the one-shot device call, and to the reference
+    algorithm."""
+    import torch
+    n = (17 << 20) + 12345
+    for seed in range(4):
+        rng = np.random.default_rng(12000 + seed)
+        a, b, c = (T.vector(nm, dtype="float32") for nm in "abc")
+        pool = [a, b, c]
+        for _ in range(int(rng.integers(3, 8))):
+            k = ("add", "mul", "sub", "maximum", "tanh", "sigmoid")[int(rng.integers(6))]
+            args = [pool[int(rng.integers(len(pool)))] for _ in range(1 if k in ("tanh", "sigmoid") else 2)]
+            pool.append(make(k, args))
+        outs = [pool[-1], pool[-2]]
+        f = T.compile([a, b, c], outs)
+        vals = [rng.standard_normal(n).astype(np.float32) for _ in range(3)]
+        host = f(*vals)
+        dev = [t.cpu().numpy() for t in f.call_device(*[torch.from_numpy(v).cuda() for v in vals], sync=True)]
+        for h, d in zip(host, dev):
+            np.testing.assert_array_equal(h, d)
+        idx = rng.integers(0, n, 4096)
+        want = C.CpuFunction(T, [a, b, c], outs)(*[v[idx] for v in vals])
+        for h, w in zip(host, want):
+            _check(h[idx], w, 1e-5)
