@@ -413,3 +413,25 @@ def test_random_elementwise_graphs_through_the_host_pipeline():
         want = C.CpuFunction(T, [a, b, c], outs)(*[v[idx] for v in vals])
         for h, w in zip(host, want):
             _check(h[idx], w, 1e-5)
+
+
+def test_random_graph_gradients_match_directional_differences():
+    """grad() of a random scalar cost (the reference's gradient rules,
+    autodiff.py / ops/*.py grad) executed on the device agrees with a central
+    difference of the device function along a random direction (float64)."""
+    for seed in range(15):
+        inputs, outs, vals = _random_graph(1000 + seed, "float64")
+        rng = np.random.default_rng(seed)
+        cost = T.sum(T.tanh(outs[0]) * T.as_variable(rng.standard_normal(vals[0].shape)))
+        floats = [v for v in inputs]
+        grads = T.grad(cost, floats, disconnected="zero")
+        fg = T.compile(inputs, grads)
+        fc = T.compile(inputs, cost)
+        g = fg(*vals)
+        d = [rng.standard_normal(v.shape) for v in vals]
+        h = 1e-6
+        plus = float(fc(*[v + h * dv for v, dv in zip(vals, d)]))
+        minus = float(fc(*[v - h * dv for v, dv in zip(vals, d)]))
+        fd = (plus - minus) / (2 * h)
+        an = sum(float((np.asarray(gi) * dv).sum()) for gi, dv in zip(g, d))
+        assert abs(fd - an) <= 1e-5 * max(1.0, abs(an)), (seed, fd, an)
