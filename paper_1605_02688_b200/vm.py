@@ -840,18 +840,22 @@ class StepPlan:
                                     and (self.lay[y.id].offset, self.lay[y.id].strides, self.lay[y.id].shape)
                                     != (xl.offset, xl.strides, xl.shape)
                                     for y in n.inputs if y is not x and y.id in self.lay)
-                        if (not clash and xs.kind == "arena" and xs.alias is None and xs.offset is not None
-                                and id(xs) not in taken and xs.last_use == i and xl.offset == 0
-                                and xl.shape == ol.shape and xl.dtype == ol.dtype and xl.contiguous()
-                                and xs.nbytes == st.nbytes):
+                        # chains are allowed (an in-place value that is itself
+                        # an alias): the buffer is the root's, and the value
+                        # and the root must both die at this node
+                        r = xs.root()
+                        if (not clash and r.kind == "arena" and r.offset is not None and xs.kind == "arena"
+                                and id(r) not in taken and xs.last_use == i and r.last_use == i
+                                and xl.offset == 0 and xl.shape == ol.shape and xl.dtype == ol.dtype
+                                and xl.contiguous() and xs.nbytes == st.nbytes and r.nbytes == st.nbytes):
                             st.alias = xs
-                            taken.add(id(xs))
-                            xs.last_use = max(xs.last_use, st.last_use)
+                            taken.add(id(r))
+                            r.last_use = max(r.last_use, st.last_use)
                             lst = live_at.get(i)
-                            if lst and xs in lst:
-                                lst.remove(xs)
-                            if xs.last_use < INF:
-                                live_at.setdefault(xs.last_use, []).append(xs)
+                            if lst and r in lst:
+                                lst.remove(r)
+                            if r.last_use < INF:
+                                live_at.setdefault(r.last_use, []).append(r)
                             break
                 if st.alias is None:
                     assign(st, i)
