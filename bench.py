@@ -176,7 +176,16 @@ def bench_ew_e2e(f, steps=5):
         out = f(*host)
     dt = (time.perf_counter() - t0) / steps
     assert out.shape == (EW_N,)
-    return dt, 4 * EW_N * 4, EW_N * 4
+    del host
+    # the reference's own call convention: pageable NumPy arrays in, NumPy out
+    rng = np.random.default_rng(2)
+    arrs = [rng.standard_normal(EW_N, dtype=np.float32) for _ in range(4)]
+    f(*arrs)
+    t0 = time.perf_counter()
+    for _ in range(max(2, steps // 2)):
+        out = f(*arrs)
+    dt_np = (time.perf_counter() - t0) / max(2, steps // 2)
+    return dt, 4 * EW_N * 4, EW_N * 4, dt_np
 
 
 def link_bandwidth(nbytes=1 << 30, reps=3):
@@ -228,6 +237,46 @@ def cpu_ew_baseline(T, C, budget_s=12.0, n=1 << 24):
     return {"value": round(EW_BYTES_PER_ELEM * n / med / 1e9, 3), "unit": "GB/s", "cores": 1, "kind": "port",
             "sample": f"{n} elements x {len(times)} reps of the reference's chunked Composite evaluation "
                       "(oracle/texpr_numpy.eval_composite_chunked, NumPy single-threaded ufuncs), kernel-only"}
+
+
+def attach_cpu_path(line, T, C, args):
+    """The reference's CPU path beside every config (rank 0, N=1 only): the
+    real reference from baseline/_ref when installed (tools/ref_bench.py),
+    else the oracle port for config 2 only."""
+    tab = None
+    if not args.no_cpu_table:
+        from tools import ref_bench
+        try:
+            tab = ref_bench.table(reps=5)
+        except Exception as e:  # pragma: no cover
+            tab = {"error": repr(e)[:300]}
+    if not tab or "error" in tab or "error" in tab.get("config2_ew_2p28", {"error": 1}):
+        line["cpu_baseline"] = cpu_ew_baseline(T, C)
+        if tab:
+            line["cpu_path"] = tab
+        return
+    host = tab["host"]
+    c2 = tab["config2_ew_2p28"]
+    line["cpu_baseline"] = {"value": c2["kernel"], "unit": "GB/s", "cores": 1, "kind": "reference",
+                            "sample": "full 2^28-element workload, texpr from baseline/_ref through its public API, "
+                                      "1 warm-up + median of 5 calls; kernel-only = sum of Profile.node_time "
+                                      "(NumPy elementwise is single-threaded)",
+                            "e2e_value": c2["e2e"], "host_cores": host["cpu_count"], "cpu_model": host["cpu_model"]}
+    line["cpu_path"] = tab
+    ex = line.get("extra", {})
+    pairs = (("mlp_b8192_1gpu", "config4_mlp_b8192"), ("mlp_dp_global65536", "config5_mlp_global65536"),
+             ("logreg_n600", "config1_logreg_n600"))
+    for ours, ref in pairs:
+        if isinstance(ex.get(ours), dict) and "e2e" in tab.get(ref, {}):
+            r = tab[ref]
+            ex[ours]["cpu_baseline"] = {"unit": r["unit"], "e2e": r["e2e"], "kernel": r["kernel"], "kind": "reference",
+                                        "cores": host["cpu_count"], "blas": host["blas"]}
+    if isinstance(ex.get("careduce_16384sq_GBs"), dict) and "sum_axis0" in tab.get("config3_careduce_16384sq", {}):
+        r = tab["config3_careduce_16384sq"]
+        ex["careduce_cpu_baseline"] = {k: {"e2e": v["e2e"], "kernel": v["kernel"]} for k, v in r.items()
+                                       if isinstance(v, dict)}
+        ex["careduce_cpu_baseline"]["unit"] = "GB/s"
+        ex["careduce_cpu_baseline"]["note"] = "the reference's argmax is ArgmaxOnehot (one-hot of the input's shape)"
 
 
 def bench_mlp(T, C, B, steps, warmup, lib_holder, dp=None, n_global=None):
@@ -330,10 +379,20 @@ def bench_reduce(T, C, steps, lib_holder):
 # ---------------------------------------------------------------- main
 
 def run_reference(args):
-    """--impl reference: the reference's CPU algorithm (oracle port) on the
-    same workload and metric, bounded samples per step."""
+    """--impl reference: the reference's own CPU path on the same workload and
+    metric.  The unmodified reference package from baseline/_ref, called
+    through its public API (texpr.compile + f(*host arrays)) on the full 2^28
+    config-2 workload: ``value`` is kernel-only (the sum of its
+    Profile.node_time, runtime.py:113-160), ``e2e`` the whole call including
+    its input/output copies (runtime.py:163-171, :412-417).  Without
+    baseline/_ref: the oracle port on a bounded 2^24 sample."""
     ws, rank, _ = dist_env()
     if rank != 0:
+        return
+    from tools import ref_bench
+    tx = ref_bench.load_reference()
+    if tx is not None:
+        run_reference_texpr(args, tx, ws)
         return
     import paper_1605_02688_b200 as T
     from oracle import configs as C
@@ -363,6 +422,62 @@ def run_reference(args):
     print(json.dumps(line))
 
 
+def self_launch(args) -> int:
+    """``--gpus N`` without a launcher: re-exec through torch.distributed.run
+    (one process per GPU over NCCL, rendezvous on 127.0.0.1).  Fails loudly
+    when fewer than N GPUs are visible (the reference arm runs on rank 0 only
+    and needs no GPU)."""
+    import socket
+    import subprocess
+    if args.impl == "ours":
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, found {have}", file=sys.stderr)
+            return 2
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def run_reference_texpr(args, tx, ws):
+    from tools import ref_bench
+    n = EW_N
+    a, bb, c, d = (tx.vector(k, dtype="float32") for k in "abcd")
+    f = tx.compile([a, bb, c, d], tx.sigmoid(a * bb + c) ** 2 - d, preset="fast_run")
+    ins = [np.random.default_rng(i).standard_normal(n, dtype=np.float32) for i in range(4)]
+    for _ in range(args.warmup):
+        f(*ins)
+    e2e, kern = [], []
+    for _ in range(args.steps):
+        k0 = sum(f.profile.node_time.values())
+        t0 = time.perf_counter()
+        f(*ins)
+        e2e.append(time.perf_counter() - t0)
+        kern.append(sum(f.profile.node_time.values()) - k0)
+    host = ref_bench.host_info()
+    v = EW_BYTES_PER_ELEM * n * args.steps / sum(kern) / 1e9
+    ve = EW_BYTES_PER_ELEM * n * args.steps / sum(e2e) / 1e9
+    line = {"metric": "fused-elemwise HBM GB/s", "value": round(v, 3), "unit": "GB/s", "impl": "reference",
+            "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(1e3 * sum(kern) / args.steps, 3), "higher_is_better": True, "dtype": "f32",
+            "data": "synthetic (NumPy default_rng, host)",
+            "config": {"workload": "config2: sigmoid(a*b+c)**2-d, 2^28 fp32 elements (full size)",
+                       "elements_per_step": n, "preset": "fast_run (one composite[5])"},
+            "cpu_baseline": {"value": round(v, 3), "unit": "GB/s", "cores": 1, "kind": "reference",
+                             "sample": f"full 2^28-element workload per step, texpr from baseline/_ref, "
+                                       f"kernel-only = sum of Profile.node_time",
+                             "host_cores": host["cpu_count"], "cpu_model": host["cpu_model"]},
+            "e2e": {"value": round(ve, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+                    "ms_per_step": round(1e3 * sum(e2e) / args.steps, 1),
+                    "path": "texpr CompiledFunction.__call__ with NumPy inputs (includes its input/output copies)"}}
+    print(json.dumps(line))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -370,8 +485,15 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--skip-extra", action="store_true")
+    ap.add_argument("--no-cpu-table", action="store_true",
+                    help="skip the reference CPU-path table (headline cpu_baseline falls back to the port sample)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
+    ws_env = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws_env != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws_env}")
     if args.impl == "reference":
         run_reference(args)
         return
@@ -420,11 +542,14 @@ def main():
     }
     if rank == 0:
         try:
-            dt, hb, db = bench_ew_e2e(f)
+            dt, hb, db, dt_np = bench_ew_e2e(f)
             line["e2e"] = {"value": round(bytes_step / dt / 1e9, 2), "unit": "GB/s", "h2d_bytes_per_step": hb,
                            "d2h_bytes_per_step": db, "ms_per_step": round(dt * 1e3, 2),
                            "path": "CompiledFunction.__call__ with pinned host torch tensors -> numpy result "
-                                   "(chunk-pipelined H2D / kernel / D2H, stream.py)"}
+                                   "(chunk-pipelined H2D / kernel / D2H, stream.py)",
+                           "numpy_pageable": {"value": round(bytes_step / dt_np / 1e9, 2), "unit": "GB/s",
+                                              "ms_per_step": round(dt_np * 1e3, 2),
+                                              "path": "CompiledFunction.__call__ with pageable NumPy inputs"}}
             try:
                 lk = link_bandwidth()
                 bound_s = max(hb / (lk["h2d_gbs"] * 1e9), db / (lk["d2h_gbs"] * 1e9))
@@ -435,7 +560,6 @@ def main():
                 line["e2e"]["link"] = {"error": repr(e)[:200]}
         except Exception as e:  # pragma: no cover
             line["e2e"] = {"error": repr(e)}
-        line["cpu_baseline"] = cpu_ew_baseline(T, C)
     del f, ins
     torch.cuda.empty_cache()
     if not args.skip_extra:
@@ -450,6 +574,10 @@ def main():
             extra["mlp_b8192_1gpu"] = {"samples_per_s": round(8192 / (med * 1e-3), 1), "ms_per_step": round(med, 3),
                                        "tflops": round(MLP_FLOP_PER_SAMPLE * 8192 / (med * 1e-3) / 1e12, 1),
                                        "frac_of_tf32_nominal_1130": round(MLP_FLOP_PER_SAMPLE * 8192 / (med * 1e-3) / 1e12 / TF32_NOMINAL, 3),
+                                       "frac_of_tf32_cublas_measured": (round(MLP_FLOP_PER_SAMPLE * 8192 / (med * 1e-3) / 1e12
+                                                                              / extra["tf32_cublas_tflops_8192cubed"], 3)
+                                                                        if isinstance(extra.get("tf32_cublas_tflops_8192cubed"), float) else None),
+                                       "precision": "tf32 tensor-core GEMMs (fp32 accumulate)",
                                        "cost_after": cost,
                                        "graph_nodes": len([1 for n in fm.order if not getattr(n.op, 'view_capable', False)]),
                                        "launches_per_step": kernel_launches(fm)}
@@ -491,6 +619,8 @@ def main():
         except Exception as e:
             extra["careduce_16384sq_GBs"] = {"error": repr(e)[:300]}
         line["extra"] = extra
+    if rank == 0 and ws == 1:
+        attach_cpu_path(line, T, C, args)
     if rank == 0:
         print(json.dumps(line))
     if ws > 1:

@@ -100,6 +100,10 @@ class Pipeline:
             if kind != "dev" or lay.shape[1:] != tuple(shape[1:]) or lay.shape[0] != rows:
                 raise _NotChunkable()
             self.out_specs.append(lay.dtype)
+        # an output that is an input variable (compile([x, y], [x, x*y])) is
+        # copied out of the slot's input buffer: the next H2D into that slot
+        # must then also wait for the D2H, not just for the compute
+        self.out_reads_input = any(lay.storage.root().kind == "input" for _, lay in self.slots[0].out_lays)
         # steady state keeps two result blocks per output in flight (the
         # caller's previous result + this call's); pin them now, not mid-stream
         for dt in self.out_specs:
@@ -137,6 +141,8 @@ class Pipeline:
             e_in, e_comp, e_out = self.ev[si]
             if self.used[si]:
                 lib.stream_wait_event(h2d, e_comp)      # slot inputs no longer read
+                if self.out_reads_input:
+                    lib.stream_wait_event(h2d, e_out)   # ... not even by the D2H
             for (st, nb), s, rb in zip(plan.host_inputs, src, in_rb):
                 if nb:
                     lib.memcpy(st.ptr, s + r0 * rb, n * rb, 0, h2d)
@@ -166,6 +172,12 @@ class Pipeline:
                 arr = arr.astype(np.bool_)
             res.append(arr)
         return res
+
+
+    def release(self):
+        self.lib.stream_sync(self.fn._stream)
+        for p in self.slots + ([self.tail] if self.tail else []):
+            p.release()
 
 
 class _NotChunkable(Exception):

@@ -25,6 +25,7 @@ from __future__ import annotations
 
 import threading
 import time
+from collections import OrderedDict
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -45,6 +46,8 @@ from .shared import SharedVariable, torch_dtype
 
 INF = 1 << 60
 ALIGN = 256
+# cached step plans per function (distinct shape signatures; LRU beyond this)
+MAX_PLANS = int(__import__("os").environ.get("TX_MAX_PLANS", "8"))
 
 
 def _torch():
@@ -103,7 +106,7 @@ class Profile:
 # storage & layouts
 
 class Storage:
-    __slots__ = ("kind", "nbytes", "offset", "ptr", "last_use", "alias", "name")
+    __slots__ = ("kind", "nbytes", "offset", "ptr", "last_use", "alias", "name", "owner")
 
     def __init__(self, kind, nbytes=0, ptr=None, name=""):
         self.kind = kind          # arena | input | shared | const
@@ -113,6 +116,7 @@ class Storage:
         self.last_use = -1
         self.alias = None
         self.name = name
+        self.owner = None         # torch tensor holding the memory, when plan-owned
 
     def root(self):
         s = self
@@ -273,12 +277,12 @@ class CompiledFunction:
         self.profile = Profile(stage_times=dict(rewrite_log.stage_times))
         self.has_lazy = False
         self._lock = threading.Lock()
-        self._plans: dict = {}
+        self._plans: OrderedDict = OrderedDict()   # shape key -> StepPlan, LRU, at most MAX_PLANS
         self._consts: dict[int, object] = {}
         self._stream = None
         self._comm_stream = None
         self._xfer = None
-        self._pipes: dict = {}
+        self._pipes: OrderedDict = OrderedDict()
         self.pipelined = True
         self.profile_nodes = False
         self._direct, self.order = self._schedule()
@@ -408,7 +412,10 @@ class CompiledFunction:
             if why is not None:
                 raise TypeMismatch(f"shared {s!r} holds a nonconforming value: {why}")
             shared_state.append((dev.data_ptr(), tuple(dev.shape), s.version))
-        key = (tuple((b.shape, b.dev_ptr) for b in binds), tuple(shared_state))
+        # plans are keyed on shapes (and the shared storages they bake in),
+        # never on the caller's input pointers: a fresh device tensor per call
+        # (a data loader) re-uses the plan through its input slots
+        key = (tuple((b.shape, b.dev_ptr is not None) for b in binds), tuple(shared_state))
         if self._value_keyed:
             vals = {}
             for i in self._value_keyed:
@@ -426,6 +433,12 @@ class CompiledFunction:
                 except _stream._NotChunkable:
                     pipe = False
                 self._pipes[key] = pipe
+                while len(self._pipes) > MAX_PLANS:
+                    old = self._pipes.pop(next(iter(self._pipes)))
+                    if old:
+                        old.release()
+            elif key in self._pipes:
+                self._pipes.move_to_end(key)
             if pipe:
                 outs = pipe.run(binds)
                 self.profile._pending += 1
@@ -433,9 +446,19 @@ class CompiledFunction:
                 self.profile.total_time += time.perf_counter() - t0
                 return outs[0] if self.single_output else outs
         plan = self._plans.get(key)
-        if plan is None:
+        if plan is not None and not plan.accepts(binds):
+            # the caller moved to new device buffers: replace the pointer-bound
+            # plan by one that copies device inputs into plan-owned slots
+            self._evict(key)
+            plan = StepPlan(self, lib, binds, key, slot_inputs=True)
+            self._plans[key] = plan
+        elif plan is None:
             plan = StepPlan(self, lib, binds, key)
             self._plans[key] = plan
+            while len(self._plans) > MAX_PLANS:
+                self._evict(next(iter(self._plans)))
+        else:
+            self._plans.move_to_end(key)
         stream = self._stream
         if self._events is None:
             self._events = (lib.event_create(), lib.event_create())
@@ -468,10 +491,25 @@ class CompiledFunction:
         else:
             outs = plan.download_outputs(stream)
         plan.check_flags()
-        plan.finish_updates()
+        if plan.finish_updates():
+            self._evict_stale()
         self.profile.call_count += 1
         self.profile.total_time += time.perf_counter() - t0
         return outs[0] if self.single_output else outs
+
+    def _evict(self, key):
+        """Drop one cached plan: wait for the function's stream (its arena is
+        handed back to the caching allocator), free its captured graphs.
+        Device outputs handed out earlier keep the arena alive themselves."""
+        plan = self._plans.pop(key, None)
+        if plan is not None:
+            plan.release(self._stream)
+
+    def _evict_stale(self):
+        """Plans baked against a shared storage that has since been replaced."""
+        live = {(s.device_tensor().data_ptr(), s.version) for s, _ in self.shared_bindings}
+        for key in [k for k in self._plans if any((p, v) not in live for p, _, v in k[1])]:
+            self._evict(key)
 
     # -- serialization (reference runtime.py:555-569) -------------------------
     def save(self) -> bytes:
@@ -493,8 +531,8 @@ class CompiledFunction:
         twin.profile = Profile(stage_times=dict(self.profile.stage_times), _order=self.profile._order)
         twin._events = None
         twin._lock = threading.Lock()
-        twin._plans = {}
-        twin._pipes = {}
+        twin._plans = OrderedDict()
+        twin._pipes = OrderedDict()
         twin._stream = None
         twin._comm_stream = None
         twin._xfer = None
@@ -595,12 +633,16 @@ def _bind_input(var, val) -> _Bind:
 # the step plan
 
 class StepPlan:
-    def __init__(self, fn: CompiledFunction, lib, binds, key, shared_arena=None, out_binds=None):
+    def __init__(self, fn: CompiledFunction, lib, binds, key, shared_arena=None, out_binds=None,
+                 slot_inputs=False):
         """``shared_arena``: a dict through which plans that never run
         concurrently (the unrolled steps of a loop, ``scan.py``) share one
         scratch arena allocation.  ``out_binds``: {var id: device pointer} --
         node outputs written straight into caller-owned memory (a loop's
-        history slot) instead of the arena."""
+        history slot) instead of the arena.  ``slot_inputs``: device inputs
+        are copied into plan-owned slots every call (reference
+        runtime.py:163-171 always copies) instead of being bound by pointer
+        into the captured graph."""
         self.fn, self.lib = fn, lib
         self.subplans = []                   # step plans of loops lowered into this plan
         self.values = dict(getattr(fn, "_bound_values", None) or {})  # var id -> host value (loop trip counts)
@@ -609,6 +651,10 @@ class StepPlan:
         self.lay: dict[int, Layout] = {}
         self.keep = []                       # torch tensors that must stay alive
         self.in_storage = []                 # (Storage, nbytes) for host-bound inputs
+        self.dev_slots = []                  # (Storage, nbytes) for slot-copied device inputs
+        self.slot_inputs = slot_inputs
+        # device pointers baked into the plan (None: host input or slot)
+        self.bound_ptrs = tuple(None if slot_inputs else b.dev_ptr for b in binds)
         self.ws: dict[int, tuple] = {}       # node id -> (Storage, nbytes)
         self.flag = None
         order = fn.order
@@ -618,14 +664,15 @@ class StepPlan:
         # ---- bound storages: inputs, shared, constants
         for var, b in zip(fn.input_vars, binds):
             nb = int(np.prod(b.shape, dtype=np.int64)) * ITEMSIZE[var.type.dtype]
-            if b.dev_ptr is not None:
+            if b.dev_ptr is not None and not slot_inputs:
                 st = Storage("input", nb, ptr=b.dev_ptr, name=var.name or "")
             else:
                 st = Storage("input", nb, name=var.name or "")
                 buf = t.empty(max(nb, 1), dtype=t.uint8, device="cuda")
                 self.keep.append(buf)
                 st.ptr = buf.data_ptr()
-                self.in_storage.append((st, nb))
+                st.owner = buf
+                (self.in_storage if b.dev_ptr is None else self.dev_slots).append((st, nb))
             self.lay[var.id] = Layout(st, 0, b.shape, contiguous_strides(b.shape), var.type.dtype)
         in_ids = {v.id for v in fn.input_vars}
         self.host_inputs = [(st, nb) for st, nb in self.in_storage]
@@ -634,6 +681,7 @@ class StepPlan:
             if var.id in self.lay:  # also declared as an explicit input
                 continue
             dev = s.device_tensor()
+            self.keep.append(dev)   # baked into the graph: outlives a shape-changing set_value
             st = Storage("shared", dev.numel() * dev.element_size(), ptr=dev.data_ptr(), name=s.name or "")
             self.shared_storage[id(s)] = st
             self.lay[var.id] = Layout(st, 0, tuple(dev.shape), contiguous_strides(tuple(dev.shape)), var.type.dtype)
@@ -1324,7 +1372,28 @@ class StepPlan:
         self.launches.append((None, launch))
 
     # -- execution --------------------------------------------------------------
+    def accepts(self, binds) -> bool:
+        """Whether this plan can run these inputs (same shapes are given by
+        the cache key): a pointer-bound plan only its own device buffers."""
+        return self.slot_inputs or all(p is None or p == b.dev_ptr for p, b in zip(self.bound_ptrs, binds))
+
+    def release(self, stream=None):
+        """Free the captured graphs (this plan's and its loops') once the
+        stream has drained; the arena goes back with the last reference."""
+        if stream is not None:
+            self.lib.stream_sync(stream)
+        for sp in self.subplans:
+            if hasattr(sp, "release"):
+                sp.release()
+        if self.graph is not None:
+            self.lib.graph_destroy(self.graph)
+            self.graph = None
+
     def upload_inputs(self, binds, stream):
+        if self.dev_slots:
+            devs = [b for b in binds if b.dev_ptr is not None]
+            for (st, nb), b in zip(self.dev_slots, devs):
+                self.lib.memcpy(st.ptr, b.dev_ptr, nb, 2, stream)
         hosts = [b for b in binds if b.dev_ptr is None]
         for (st, nb), b in zip(self.host_inputs, hosts):
             if nb == 0:
@@ -1421,8 +1490,9 @@ class StepPlan:
             if kind == "const":
                 outs.append(t.from_numpy(np.array(lay)).to("cuda"))
                 continue
-            outs.append(_torch_view(lay, self.tx(lay).data))
-        # the views alias plan-owned buffers at fixed addresses: build once
+            outs.append(_torch_view(lay, self.tx(lay).data, owner=self))
+        # the views alias plan-owned buffers at fixed addresses: build once;
+        # each keeps the plan (its arena) alive after an eviction
         self._dev_outs = tuple(outs)
         return outs
 
@@ -1440,9 +1510,10 @@ class StepPlan:
         if int(v.item()):
             raise ZeroDivisionError("integer division by zero")
 
-    def finish_updates(self):
+    def finish_updates(self) -> bool:
+        """Commit shape-changing updates (fresh shared storage); True if any."""
         if not self.late_updates:
-            return
+            return False
         t = _torch()
         self.lib.stream_sync(self.fn._stream)
         for s, ul in self.late_updates:
@@ -1450,26 +1521,29 @@ class StepPlan:
             with s._lock:
                 s._dev = view.clone()
                 s.version += 1
-        self.fn._plans.clear()
+        return True
 
 
-def _torch_view(lay: Layout, ptr: int):
+def _torch_view(lay: Layout, ptr: int, owner=None):
     """A torch tensor aliasing device memory at ``ptr`` with ``lay``'s geometry."""
     t = _torch()
     dt = torch_dtype(lay.dtype)
     if lay.numel == 0:
         return t.empty(lay.shape, dtype=dt, device="cuda")
     span = 1 + sum((s - 1) * st for s, st in zip(lay.shape, lay.strides))
-    return _wrap_device_pointer(ptr, span, dt).as_strided(lay.shape, lay.strides)
+    return _wrap_device_pointer(ptr, span, dt, owner).as_strided(lay.shape, lay.strides)
 
 
-def _wrap_device_pointer(ptr, numel, dtype):
+def _wrap_device_pointer(ptr, numel, dtype, owner=None):
     """Wrap raw device memory (owned by a plan's arena / shared storage) as a
-    torch tensor via __cuda_array_interface__ (no copy)."""
+    torch tensor via __cuda_array_interface__ (no copy).  torch keeps the
+    interface object alive with the storage, and it holds ``owner``."""
     t = _torch()
     typestr = {t.float32: "<f4", t.float64: "<f8", t.int32: "<i4", t.int64: "<i8", t.uint8: "|u1"}[dtype]
 
     class _CAI:
         __cuda_array_interface__ = {"shape": (int(numel),), "typestr": typestr, "data": (int(ptr), False),
                                     "version": 3, "strides": None}
-    return t.as_tensor(_CAI(), device="cuda")
+    cai = _CAI()
+    cai.owner = owner
+    return t.as_tensor(cai, device="cuda")

@@ -432,3 +432,91 @@ def test_update_to_a_view_of_itself_and_unread_targets():
     f(1.0)
     np.testing.assert_array_equal(A.get_value(), a0)
     np.testing.assert_array_equal(B.get_value(), a0.T)
+
+
+# -- step-plan cache (shape-keyed, bounded, pointer independent) ----------------
+
+def test_fresh_device_batches_reuse_one_plan_and_flat_memory():
+    """A data loader hands a new CUDA tensor every step: the MLP step keeps one
+    plan (device inputs copied into its slots), device memory stays flat and
+    every step equals the same step fed by host arrays."""
+    import torch
+    from oracle import configs as C
+    B, H = 128, 256
+    ga = C.build_mlp(T, B=B, H=H)
+    fa = T.compile(ga["inputs"], ga["outputs"], updates=ga["updates"])
+    gb = C.build_mlp(T, B=B, H=H)
+    fb = T.compile(gb["inputs"], gb["outputs"], updates=gb["updates"])
+    x, y = C.inputs_mlp(B=B, seed=3)
+    xd, yd = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+    mem = None
+    ring = []   # the loader keeps a few batches alive: addresses keep changing
+    for i in range(200):
+        xi, yi = torch.empty_like(xd), torch.empty_like(yd)
+        xi.copy_(xd)
+        yi.copy_(yd)
+        ring = (ring + [(xi, yi)])[-3:]
+        ca = float(fa.call_device(xi, yi, sync=True)[0].item())
+        if i % 40 == 0:
+            cb = float(fb(x, y)[0])
+            for _ in range(39 if i < 160 else 0):
+                fb(x, y)
+            assert ca == cb, (i, ca, cb)
+        del xi, yi
+        if i == 5:
+            torch.cuda.synchronize()
+            mem = torch.cuda.memory_allocated()
+    torch.cuda.synchronize()
+    assert len(fa._plans) == 1
+    assert next(iter(fa._plans.values())).slot_inputs
+    assert torch.cuda.memory_allocated() <= mem
+
+
+def test_plan_cache_is_bounded_lru():
+    from paper_1605_02688_b200 import vm
+    x = T.matrix("x", dtype="float32")
+    f = T.compile([x], [T.sum(T.exp(x), axis=1)])
+    outs = {}
+    for r in range(1, vm.MAX_PLANS + 5):
+        a = np.full((r, 3), 0.5, np.float32)
+        outs[r] = f(a)[0]
+        assert len(f._plans) <= vm.MAX_PLANS
+    for r, o in outs.items():
+        np.testing.assert_allclose(o, np.full(r, 3 * np.exp(np.float32(0.5)), np.float32), rtol=1e-6)
+
+
+def test_device_outputs_survive_plan_eviction():
+    """call_device returns views into the plan's arena; evicting the plan (a
+    shape-changing update, LRU) must not free memory the caller still holds."""
+    import torch
+    s = T.shared(np.zeros(4, np.float32), name="s")
+    x = T.vector("x", dtype="float32")
+    f = T.compile([x], [x * 2.0 + T.sum(s)], updates=[(s, T.join(0, s, s))])
+    a = torch.arange(6, dtype=torch.float32, device="cuda")
+    out = f.call_device(a, sync=True)
+    keep = out[0] if isinstance(out, (list, tuple)) else out
+    for r in range(2, 14):
+        f.call_device(torch.ones(r, device="cuda"), sync=True)
+        torch.empty(1 << 20, device="cuda").fill_(7.0)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(keep.cpu().numpy(), np.arange(6, dtype=np.float32) * 2.0)
+    assert len(f._plans) <= 1   # plans baked on the replaced storages were dropped
+
+
+def test_pipelined_identity_output_not_overwritten():
+    """compile([x, y], [x, x*y]) through the chunk pipeline: the first output is
+    copied out of the slot's input buffer, which the next H2D must not
+    overwrite early (stream.py slot reuse)."""
+    from paper_1605_02688_b200 import stream as S
+    x, y = T.vector("x", dtype="float32"), T.vector("y", dtype="float32")
+    f = T.compile([x, y], [x, x * y, x + y])
+    n = (S.MIN_BYTES // 4) + 12345
+    rng = np.random.default_rng(9)
+    a = rng.standard_normal(n).astype(np.float32)
+    b = rng.standard_normal(n).astype(np.float32)
+    for _ in range(3):
+        o0, o1, o2 = f(a, b)
+        assert _pipe_used(f)
+        np.testing.assert_array_equal(o0, a)
+        np.testing.assert_array_equal(o1, a * b)
+        np.testing.assert_array_equal(o2, a + b)

@@ -72,3 +72,24 @@ def test_saved_values_are_device_state():
     (s, _), = g.shared_bindings
     np.testing.assert_array_equal(s.get_value(), np.full((4, 3), 2.0, np.float32))
     assert float(g(np.ones((2, 4), np.float32))) == 2 * 3 * 4 * 2.0
+
+
+@pytest.mark.parametrize("reopt", [False, True])
+def test_data_parallel_step_resumes_from_checkpoint(reopt):
+    """A saved MLP step loads with data_parallel (no update fused into a
+    gradient GEMM, since gradients are partial sums until the allreduce) and
+    continues exactly like the data-parallel step it was saved from."""
+    from paper_1605_02688_b200.dp import DataParallel
+    B, H = 128, 256
+    x, y = C.inputs_mlp(B=B)
+    g = C.build_mlp(T, B=B, H=H)
+    f = T.compile(g["inputs"], g["outputs"], updates=g["updates"], data_parallel=DataParallel(world_size=1, rank=0))
+    f(x, y)
+    blob = f.save()
+    h = T.load(blob, force_reoptimize=reopt, data_parallel=DataParallel(world_size=1, rank=0))
+    assert h.shard is not None and len(h.shard.partial_vars) >= 6
+    c_orig, c_load = float(f(x, y)[0]), float(h(x, y)[0])
+    assert abs(c_orig - c_load) <= 1e-6 * abs(c_orig)
+    orig = {s.name: s.get_value() for s, _ in f.shared_bindings}
+    for s, _ in h.shared_bindings:
+        assert _rel(s.get_value(), orig[s.name]) <= 1e-6, s.name

@@ -10,4 +10,4 @@ for t in ${TESTS:-test_device_runtime test_device_ops test_device_configs}; do
 done
 if [ -n "$SMOKE" ]; then timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke exit $?" >> gpurun_out/summary.txt; fi
 if [ -n "$BENCH" ]; then timeout ${BTIMEOUT:-900} python bench.py $BENCH > gpurun_out/bench.log 2>&1; echo "bench exit $?" >> gpurun_out/summary.txt; fi
-tail -3 gpurun_out/*.log
+for f in gpurun_out/*.log; do echo "== $f"; tail -n 3 "$f"; done
