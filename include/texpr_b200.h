@@ -145,7 +145,11 @@ int tx_reduce(int op, const tx_tensor* x, uint32_t axes_mask, tx_tensor* y,
 enum {
   TX_GEMM_AUTO = 0,    /* tcgen05 TF32 where eligible                    */
   TX_GEMM_SIMT = 1,    /* force CUDA-core fp32/fp64 (exact fp32 products) */
-  TX_GEMM_TC = 2       /* force tcgen05 (error if the layout is ineligible) */
+  TX_GEMM_TC = 2,      /* force tcgen05 (error if the layout is ineligible) */
+  TX_GEMM_3XTF32 = 3   /* fp32-equivalent: as AUTO, but tcgen05 products run as
+                          big/small TF32 splits (3 products into one fp32
+                          accumulator, error ~2^-21 |A||B|) -- the reference's
+                          sgemm precision; needs tx_gemm_workspace() bytes */
 };
 /* Optional fused epilogue applied to the accumulator before the store. */
 /* Fused epilogues, applied per output element with IEEE round-to-nearest

@@ -73,6 +73,8 @@ struct G {
   Epi<float> epi_f;
   Epi<double> epi_d;
   float* colsum = nullptr;  // tcgen05 path only: [ceil(M/32)][N] column sums of C per 32-row block
+  int promo = 0;            // tcgen05 path only: k-blocks per accumulation-promotion chunk (0 = off) ...
+  int promo_first = 0;      // ... after a first chunk of this many k-blocks
 };
 
 enum { PATH_SIMT = 0, PATH_SKINNY = 1, PATH_TC = 2 };
@@ -89,7 +91,7 @@ size_t gemm_tc_workspace(const G& g);
 // of C into `partials` ([ceil(M/32)][N] fp32); TX_E_UNSUPPORTED when the
 // product does not take that path (caller reduces C separately)
 int gemm_with_colsum(const tx_tensor* A, const tx_tensor* B, tx_tensor* C, const tx_epilogue* epi, int mode,
-                     float* partials, cudaStream_t st);
+                     void* ws, size_t wsb, float* partials, cudaStream_t st);
 void choose_tile(const G& g, int* cg, int* bn);
 // C = epi(sum over splits of P[split][M][N]), fixed split order
 int splitk_finalize(const float* P, const G& g, int splits, cudaStream_t st);

@@ -252,8 +252,17 @@ struct TcParams {
   int tma_aux;      // [M,N] epilogue operand read by TMA tile loads (CG = 2)
   int num_m, num_n, num_tiles;
   float* colsum;    // optional: per-32-row-block column sums of the stored C, [ceil(M/32)][N]
+  int promo;        // PROMO kernels: k-blocks per TMEM accumulation chunk ...
+  int promo_first;  // ... after a first chunk of k-blocks [0, promo_first)
   Epi<float> epi;
 };
+
+// end of the accumulation chunk that starts at k-block kb (segment end kb1)
+__device__ __forceinline__ int chunk_end(const TcParams& p, int kb, int kb1) {
+  const int e = kb < p.promo_first ? p.promo_first
+                                   : p.promo_first + ((kb - p.promo_first) / p.promo + 1) * p.promo;
+  return min(e, kb1);
+}
 
 __device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int& mb, int& nb) {
   const int per_group = GROUP_M * num_n;
@@ -332,7 +341,17 @@ __device__ __forceinline__ bool seg_next(const TcParams& p, int c, int64_t& cur,
   return true;
 }
 
-template <int CG>
+// PROMO: accumulation promotion for the fp32-equivalent (3xTF32) mode.  The
+// tensor core adds each MMA's products into the fp32 TMEM accumulator with
+// round-toward-zero (measured: a bias of ~2^-24 |C| per instruction, growing
+// with K).  With PROMO the MMA warp restarts the accumulator at chunk
+// boundaries (chunk_end: one first chunk of p.promo_first k-blocks -- the
+// small cross terms, whose sum is ~2^-11 |C| and needs no promotion -- then
+// every p.promo k-blocks), cycling four 128-column TMEM buffers, and the
+// epilogue warps add each chunk into per-thread fp32 registers with
+// round-to-nearest: the round-toward-zero error is bounded by one short
+// chunk, not the whole K.
+template <int CG, bool PROMO>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                    const __grid_constant__ CUtensorMap mapC, const __grid_constant__ CUtensorMap mapX,
@@ -340,6 +359,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                    const __grid_constant__ CUtensorMap mapP, const TcParams p) {
   using K_ = Cfg<CG>;
   constexpr int STAGES = K_::STAGES;
+  constexpr int kEpiUnroll = PROMO ? 2 : 1;  // compile-time column-chunk index for the promoted sums
+  constexpr int kMaxJ = PROMO ? 2 : 4;       // 32-column chunks per epilogue thread (bn <= 128 with PROMO)
+  // TMEM accumulators: two 256-column buffers (tile i+1's MMAs overlap tile
+  // i's epilogue); PROMO (bn <= 128): four 128-column buffers, so the MMA
+  // warp runs up to three promotion chunks ahead of the epilogue
+  constexpr int NACC = PROMO ? 4 : 2;
+  constexpr int ACC_COLS = PROMO ? 128 : BN;
   const int bn = p.bn;
   const int BNL = bn / CG;  // B columns staged by this CTA
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -347,8 +373,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* full = (uint64_t*)(smem + K_::RING + K_::STAGING + K_::AUX_STAGING);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
-  uint64_t* tempty = tfull + 2;
-  uint64_t* auxbar = tempty + 2;                 // one per epilogue warp
+  uint64_t* tempty = tfull + 4;
+  uint64_t* auxbar = tempty + 4;                 // one per epilogue warp
   uint32_t* tmem_slot = (uint32_t*)(auxbar + EPI_WARPS);
 
   const int warp = threadIdx.x >> 5;
@@ -360,7 +386,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }
-    for (int b = 0; b < 2; ++b) { mbar_init(tfull + b, 1); mbar_init(tempty + b, EPI_WARPS * CG); }
+    for (int b = 0; b < NACC; ++b) { mbar_init(tfull + b, 1); mbar_init(tempty + b, EPI_WARPS * CG); }
     for (int w = 0; w < EPI_WARPS; ++w) mbar_init(auxbar + w, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -449,13 +475,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int it = 0;
       int64_t cur = seg_begin(p, cluster_id);
       Seg sg;
-      for (; seg_next(p, cluster_id, cur, sg); ++it) {
-        const int kb0 = sg.kb0, kb1 = sg.kb1;
-        const int buf = it & 1;
-        const uint32_t use = (uint32_t)(it >> 1);
+      while (seg_next(p, cluster_id, cur, sg)) {
+       for (int c0 = sg.kb0, c1; c0 < sg.kb1; c0 = c1, ++it) {
+        c1 = PROMO ? chunk_end(p, c0, sg.kb1) : sg.kb1;
+        const int kb0 = c0, kb1 = c1;
+        const int buf = it % NACC;
+        const uint32_t use = (uint32_t)(it / NACC);
         mbar_wait(tempty + buf, (use & 1) ^ 1);
         tc_fence_after();
-        const uint32_t tmem_d = tmem_base + (uint32_t)(buf * BN);  // buffers at 0 / 256 columns
+        const uint32_t tmem_d = tmem_base + (uint32_t)(buf * ACC_COLS);  // buffers at 0 / 256 (PROMO: 0/128/256/384)
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(full + stage, phase);
           tc_fence_after();
@@ -475,6 +503,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         if (lane == 0) umma_commit<CG>(tfull + buf);
         __syncwarp();
+       }
       }
     }
   } else {
@@ -498,14 +527,47 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tile_coords(sg.t, p.num_m, p.num_n, mb, nb);
       const int split = sg.piece;
       const bool partial = !sg.full;
-      const int buf = it & 1;
-      const uint32_t use = (uint32_t)(it >> 1);
+      const int q_ = warp & 3;
+      const int nchunks_ = bn / 32;
+      float acc[PROMO ? 2 : 1][32];
+      int nkc = 1;
+      if constexpr (PROMO) {
+        nkc = 0;
+        for (int c = sg.kb0; c < sg.kb1; c = chunk_end(p, c, sg.kb1)) ++nkc;
+      }
+      if constexpr (PROMO) {
+        // every chunk but the last: TMEM -> registers (RN adds), buffer released
+        for (int kc = 0; kc + 1 < nkc; ++kc, ++it) {
+          const int b_ = it % NACC;
+          mbar_wait(tfull + b_, (uint32_t)(it / NACC) & 1);
+          tc_fence_after();
+          const uint32_t ta = tmem_base + (uint32_t)(b_ * ACC_COLS) + ((uint32_t)(q_ * 32) << 16);
+#pragma unroll
+          for (int jj = 0; jj < kMaxJ; ++jj) {
+            const int ci = half + 2 * jj;
+            if (ci < nchunks_) {
+              float t[32];
+              tmem_ld32(ta + ci * 32, t);
+#pragma unroll
+              for (int i = 0; i < 32; ++i) acc[jj][i] = kc == 0 ? t[i] : __fadd_rn(acc[jj][i], t[i]);
+            }
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            if constexpr (CG == 1) mbar_arrive(tempty + b_);
+            else mbar_arrive_leader(tempty + b_);
+          }
+        }
+      }
+      const int buf = it % NACC;
+      const uint32_t use = (uint32_t)(it / NACC);
       mbar_wait(tfull + buf, use & 1);
       tc_fence_after();
       const int row0 = mb * BM * CG + (int)rank * BM + q * 32;
       const int row = row0 + lane;
       // 32-column chunks of the bn-wide accumulator, alternating between the two warps of a lane quarter
-      const uint32_t taddr = tmem_base + (uint32_t)(buf * BN) + ((uint32_t)(q * 32) << 16);
+      const uint32_t taddr = tmem_base + (uint32_t)(buf * ACC_COLS) + ((uint32_t)(q * 32) << 16);
       const int nchunks = bn / 32;
       float* crow = p.C + (int64_t)row * p.ldc;
       const bool row_ok = row < p.M;
@@ -515,8 +577,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         float* stg = reinterpret_cast<float*>(smem + K_::RING + (size_t)(warp - 2) * 4096);
         const float* xstg = reinterpret_cast<const float*>(smem + K_::RING + K_::STAGING + (size_t)(warp - 2) * 4096);
         uint64_t* xbar = auxbar + (warp - 2);
-#pragma unroll 1
-        for (int ci = half; ci < nchunks; ci += 2) {
+#pragma unroll kEpiUnroll
+        for (int jj = 0; jj < kMaxJ; ++jj) {
+          const int ci = half + 2 * jj;
+          if (ci >= nchunks) break;
           const int c = ci * 32;
           const int n = nb * bn + c;
           const bool live = !(row0 >= p.M || n >= p.N || p.dbg_nostore);
@@ -528,6 +592,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
           float v[32];
           tmem_ld32(taddr + c, v);
+          if constexpr (PROMO) {
+            if (nkc > 1) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] = __fadd_rn(acc[jj][i], v[i]);
+            }
+          }
           if (!live) continue;
           if (partial) {  // raw partial tile -> workspace [piece][M][N]; the reduction applies the epilogue
             if (lane == 0) tma_store_wait_read();
@@ -651,11 +721,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         continue;
       }
-#pragma unroll 1
-      for (int ci = half; ci < nchunks; ci += 2) {
+#pragma unroll kEpiUnroll
+      for (int jj = 0; jj < kMaxJ; ++jj) {
+        const int ci = half + 2 * jj;
+        if (ci >= nchunks) break;
         const int c = ci * 32;
         float v[32];
         tmem_ld32(taddr + c, v);
+        if constexpr (PROMO) {
+          if (nkc > 1) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = __fadd_rn(acc[jj][i], v[i]);
+          }
+        }
         const int n = nb * bn + c;
         if (!row_ok || n >= p.N || p.dbg_nostore) continue;
         if (vec_ok && n + 32 <= p.N) {
@@ -735,7 +813,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-static bool g_attr_set[3] = {false, false, false};
+static bool g_attr_set[2][3] = {{false, false, false}, {false, false, false}};
 
 static EncodeFn encode_fn() { return (EncodeFn)tmap_encoder(); }
 
@@ -836,6 +914,10 @@ void choose_tile(const G& g, int* cg_out, int* bn_out) {
   // would spend 16x the tensor time on padding -- use 32 / 64-wide tiles
   if (!bn_s && g.N <= 32) { bn = 32; cg = 1; }
   else if (!bn_s && g.N <= 64) bn = 64;
+  // promoted accumulation keeps a row's running sums in registers: at most
+  // 128 columns per tile (64 per epilogue thread within the 168-register cap
+  // that 10 warps on 4 sub-partitions leave)
+  if (g.promo && bn > 128) bn = 128;
   if (bn < 32 || bn > BN || bn % (32 * cg) != 0) bn = BN;
   *cg_out = cg;
   *bn_out = bn;
@@ -888,6 +970,15 @@ void tc_splitk(const G& g, int* splits, int* kbs) {
   const int num_kb = (int)((g.K + BK - 1) / BK);
   *splits = 1;
   *kbs = num_kb;
+  if (const char* fs = getenv("TX_GEMM_FORCE_SPLITS")) {  // diagnostics: accumulation-length experiments
+    const int want = atoi(fs);
+    if (want > 1 && g.N % 4 == 0) {
+      const int k = (num_kb + want - 1) / want;
+      *kbs = k;
+      *splits = (num_kb + k - 1) / k;
+      return;
+    }
+  }
   if (getenv("TX_GEMM_NO_SPLITK") || tiles * 2 > units || num_kb < 8 || g.N % 4 != 0) return;
   int64_t s = units / tiles;
   if (s > num_kb / 4) s = num_kb / 4;
@@ -1026,16 +1117,21 @@ int gemm_tc(const G& g, void* ws, size_t wsb, cudaStream_t st) {
   const int work = p.num_tiles * p.splits;
   const int nclusters = p.streamk ? units : (work < units ? work : units);
   p.nclusters = nclusters;
+  p.promo = g.promo > 0 && g.promo < p.num_kb ? g.promo : 0;
+  p.promo_first = p.promo ? (g.promo_first > 0 && g.promo_first < p.num_kb ? g.promo_first : 0) : 0;
+  const int pr = p.promo ? 1 : 0;
+  auto k1 = p.promo ? tc_gemm_kernel<1, true> : tc_gemm_kernel<1, false>;
+  auto k2 = p.promo ? tc_gemm_kernel<2, true> : tc_gemm_kernel<2, false>;
   if (cg == 1) {
-    if (!g_attr_set[1]) {
-      TX_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<1>::SMEM));
-      g_attr_set[1] = true;
+    if (!g_attr_set[pr][1]) {
+      TX_CUDA(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<1>::SMEM));
+      g_attr_set[pr][1] = true;
     }
-    tc_gemm_kernel<1><<<nclusters, NUM_THREADS, Cfg<1>::SMEM, st>>>(ma, mb, mc, mx, mae, mbe, mp, p);
+    k1<<<nclusters, NUM_THREADS, Cfg<1>::SMEM, st>>>(ma, mb, mc, mx, mae, mbe, mp, p);
   } else {
-    if (!g_attr_set[2]) {
-      TX_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<2>::SMEM));
-      g_attr_set[2] = true;
+    if (!g_attr_set[pr][2]) {
+      TX_CUDA(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<2>::SMEM));
+      g_attr_set[pr][2] = true;
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * nclusters, 1, 1);
@@ -1049,7 +1145,7 @@ int gemm_tc(const G& g, void* ws, size_t wsb, cudaStream_t st) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    TX_CUDA(cudaLaunchKernelEx(&cfg, tc_gemm_kernel<2>, ma, mb, mc, mx, mae, mbe, mp, p));
+    TX_CUDA(cudaLaunchKernelEx(&cfg, k2, ma, mb, mc, mx, mae, mbe, mp, p));
   }
   if (p.splits > 1) {
     TX_CUDA(cudaGetLastError());

@@ -364,7 +364,7 @@ int tx_narrow_grad(const tx_tensor* dz, const tx_tensor* wt, const tx_tensor* h,
     if (want_db && p.B > 0 && p.H > 0 && h->dtype == TX_F32 && !getenv("TX_NARROW_NO_COLSUM") && ws &&
         wsb >= csb + 256) {
       float* partials = (float*)(((uintptr_t)ws + wsb - csb) & ~(uintptr_t)15);
-      if ((uintptr_t)partials >= (uintptr_t)ws && gemm_with_colsum(dz, wt, dh, &e1, mode, partials, st) == TX_OK) {
+      if ((uintptr_t)partials >= (uintptr_t)ws && gemm_with_colsum(dz, wt, dh, &e1, mode, ws, wsb - csb - 256, partials, st) == TX_OK) {
         const int64_t S = (p.B + 31) / 32;
         colsum_finalize<<<(unsigned)((p.H + 255) / 256), 256, 0, st>>>(partials, (int)S, p.H, (float*)db->data,
                                                                       db->strides[0]);

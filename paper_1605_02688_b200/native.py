@@ -39,7 +39,7 @@ class TxEpilogue(ctypes.Structure):
 
 
 EPI_NONE, EPI_BIAS, EPI_BIAS_TANH, EPI_MUL_1MSQR, EPI_BIAS_TANH_DUAL, EPI_MUL_AUX, EPI_SGD = 0, 1, 2, 3, 4, 5, 6
-GEMM_AUTO, GEMM_SIMT, GEMM_TC = 0, 1, 2
+GEMM_AUTO, GEMM_SIMT, GEMM_TC, GEMM_3XTF32 = 0, 1, 2, 3
 
 
 def make_tensor(ptr: int, dtype: str, shape, strides) -> TxTensor:

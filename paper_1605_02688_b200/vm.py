@@ -270,7 +270,8 @@ class CompiledFunction:
         self.single_output = single_output
         self.allow_gc = allow_gc
         self.cuda_graph = cuda_graph
-        self.gemm_mode = {"auto": native.GEMM_AUTO, "simt": native.GEMM_SIMT, "tc": native.GEMM_TC}[gemm_mode]
+        self.gemm_mode = {"auto": native.GEMM_AUTO, "simt": native.GEMM_SIMT, "tc": native.GEMM_TC,
+                          "3xtf32": native.GEMM_3XTF32}[gemm_mode]
         self.dp = data_parallel
         self.nan_guard = nan_guard
         self.row_fusion = row_fusion and nan_guard is None

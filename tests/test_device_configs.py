@@ -271,3 +271,20 @@ def test_rank3_row_fusion_softmax_xent(A, B, K):
     np.testing.assert_allclose(b[1], a[1], rtol=1e-5, atol=1e-8)
     np.testing.assert_array_equal(b[2], a[2])
     np.testing.assert_array_equal(b[3], a[3])
+
+
+def test_mlp_full_size_3xtf32_three_steps_vs_oracle():
+    """Config 4 at full size (B=8192, H=4096) with fp32-equivalent tensor-core
+    GEMMs: three SGD steps within 1e-5 of the reference algorithm (cost rtol,
+    parameter relative L2) -- the precision the reference's sgemm has."""
+    B = 8192
+    g = C.build_mlp(T, B=B)
+    x, y = C.inputs_mlp(B=B)
+    step = T.compile(g["inputs"], g["outputs"], updates=g["updates"], gemm_mode="3xtf32")
+    gc = C.build_mlp(T, B=B)
+    cpu = C.CpuFunction(T, gc["inputs"], gc["outputs"], gc["updates"], exclude=("fuse_elemwise",))
+    for _ in range(3):
+        c_dev, c_ref = float(step(x, y)[0]), float(cpu(x, y)[0])
+        assert abs(c_dev - c_ref) <= 1e-5 * abs(c_ref), (c_dev, c_ref)
+    for i, (p, q) in enumerate(zip(g["params"], gc["params"])):
+        assert rel(p.get_value(), cpu.value(q)) <= 1e-5, i

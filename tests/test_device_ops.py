@@ -239,9 +239,49 @@ def _gemm_case(M, N, K, ta, tb, mode, rng):
                                    (129, 65, 33)])
 @pytest.mark.parametrize("ta,tb", [(False, False), (False, True), (True, False), (True, True)])
 def test_gemm_tcgen05_layouts(M, N, K, ta, tb, rng):
+    assert _gemm_path(M, N, K, ta, tb, 0) == _expected_path(M, N, K, ta, tb)
     got, want, bound = _gemm_case(M, N, K, ta, tb, "auto", rng)
     err = np.abs(got - want)
     assert np.all(err <= 2.0 ** -9 * bound + 1e-6), float((err / (bound + 1e-30)).max())
+
+
+def _gemm_path(M, N, K, ta, tb, mode):
+    """tx_gemm_path for the layouts _gemm_case builds (aligned dummy pointers)."""
+    from paper_1605_02688_b200 import native
+    lib = native.library()
+    mk = native.make_tensor
+    a = mk(256, "float32", (M, K), (1, M) if ta else (K, 1))
+    b = mk(256, "float32", (K, N), (1, K) if tb else (N, 1))
+    c = mk(256, "float32", (M, N), (N, 1))
+    return lib.gemm_path(a, b, c, mode)
+
+
+def _expected_path(M, N, K, ta, tb):
+    """The dispatch rule (tx_gemm.cu choose / gemm_tc_eligible) restated: a
+    regression that silently routes eligible products to SIMT fails here."""
+    if K <= 16 or N <= 16:
+        return 1                       # skinny (outer product / row dot / K reduction)
+    lead_a = M if ta else K
+    lead_b = K if tb else N
+    thin_ok = min(M, N) >= 64 or M * N * K >= (1 << 20)
+    if lead_a % 4 == 0 and lead_b % 4 == 0 and thin_ok:
+        return 2
+    return 1 if M <= 16 else 0         # C^T = B^T A^T makes M <= 16 a skinny N
+
+
+@pytest.mark.parametrize("M,N,K", [(256, 512, 256), (300, 520, 784), (784, 1024, 1000), (1024, 4096, 128), (352, 160, 96),
+                                   (20, 3000, 600), (700, 40, 1200), (20, 300, 8192), (64, 64, 20000),
+                                   (8192, 4096, 784), (129, 65, 33), (301, 517, 783)])
+@pytest.mark.parametrize("ta,tb", [(False, False), (False, True), (True, False), (True, True)])
+def test_gemm_3xtf32_layouts(M, N, K, ta, tb, rng):
+    """fp32-equivalent tensor-core products (gemm_mode="3xtf32"): every tcgen05
+    layout within 2^-20 |A||B| of the exact product, i.e. the
+    reference's sgemm precision class, and on the tcgen05 path -- also for
+    layouts the TF32 path cannot address (the split re-lays the operands)."""
+    assert _gemm_path(M, N, K, ta, tb, 3) == 2
+    got, want, bound = _gemm_case(M, N, K, ta, tb, "3xtf32", rng)
+    err = np.abs(got - want)
+    assert np.all(err <= 2.0 ** -20 * bound + 1e-7), float((err / (bound + 1e-30)).max())
 
 
 @pytest.mark.parametrize("M,N,K", [(8192, 10, 4096), (600, 10, 784), (8192, 4096, 10), (784, 10, 600),
