@@ -264,7 +264,9 @@ def attach_cpu_path(line, T, C, args):
                             "e2e_value": c2["e2e"], "host_cores": host["cpu_count"], "cpu_model": host["cpu_model"]}
     line["cpu_path"] = tab
     ex = line.get("extra", {})
-    pairs = (("mlp_b8192_1gpu", "config4_mlp_b8192"), ("mlp_dp_global65536", "config5_mlp_global65536"),
+    pairs = (("mlp_b8192_1gpu", "config4_mlp_b8192"), ("mlp_b8192_1gpu_3xtf32", "config4_mlp_b8192"),
+             ("mlp_b8192_1gpu_simt", "config4_mlp_b8192"), ("mlp_dp_global65536", "config5_mlp_global65536"),
+             ("mlp_dp_global65536_3xtf32", "config5_mlp_global65536"),
              ("logreg_n600", "config1_logreg_n600"))
     for ours, ref in pairs:
         if isinstance(ex.get(ours), dict) and "e2e" in tab.get(ref, {}):
@@ -279,10 +281,10 @@ def attach_cpu_path(line, T, C, args):
         ex["careduce_cpu_baseline"]["note"] = "the reference's argmax is ArgmaxOnehot (one-hot of the input's shape)"
 
 
-def bench_mlp(T, C, B, steps, warmup, lib_holder, dp=None, n_global=None):
+def bench_mlp(T, C, B, steps, warmup, lib_holder, dp=None, n_global=None, gemm_mode="auto"):
     import torch
     g = C.build_mlp(T, B=B, n_global=n_global)
-    f = T.compile(g["inputs"], g["outputs"], updates=g["updates"], data_parallel=dp)
+    f = T.compile(g["inputs"], g["outputs"], updates=g["updates"], data_parallel=dp, gemm_mode=gemm_mode)
     x, y = C.inputs_mlp(B=B, seed=1 + (dp.rank if dp else 0))
     xd, yd = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
     for _ in range(warmup):
@@ -585,21 +587,41 @@ def main():
         except Exception as e:
             extra["mlp_b8192_1gpu"] = {"error": repr(e)[:300]}
         torch.cuda.empty_cache()
-        try:
-            from paper_1605_02688_b200.dp import DataParallel
-            G = 65536
-            dp = DataParallel(world_size=ws, rank=rank)
-            fd, ms_d, cost_d = bench_mlp(T, C, G // ws, max(5, args.steps // 2), 3, lib_holder, dp=dp, n_global=G)
-            med = barrier_max(statistics.median(ms_d), ws)
-            extra["mlp_dp_global65536"] = {
-                "samples_per_s": round(G / (med * 1e-3), 1), "ms_per_step": round(med, 3), "n_gpus": ws,
-                "per_gpu_batch": G // ws, "scaling": "strong (fixed global batch)",
-                "tflops_total": round(MLP_FLOP_PER_SAMPLE * G / (med * 1e-3) / 1e12, 1),
-                "allreduce_buckets": len(fd._plans[next(iter(fd._plans))].buckets) if fd._plans else None,
-                "allreduce_bytes_per_step": 20037642 * 4 + 4, "cost_after": cost_d}
-            del fd
-        except Exception as e:
-            extra["mlp_dp_global65536"] = {"error": repr(e)[:300]}
+        # the same step at the reference's arithmetic precision (fp32 sgemm):
+        # 3xTF32 tensor-core GEMMs, and the CUDA-core fp32 FMA GEMMs
+        for mode, label in (("3xtf32", "3xtf32 tensor-core GEMMs (big/small TF32 split, promoted fp32 "
+                                        "accumulation; sgemm-class error)"),
+                            ("simt", "fp32 CUDA-core FMA GEMMs (exact fp32 products)")):
+            try:
+                fm, ms_m, cost = bench_mlp(T, C, 8192, 5, 3, lib_holder, gemm_mode=mode)
+                med = statistics.median(ms_m)
+                extra[f"mlp_b8192_1gpu_{mode}"] = {
+                    "samples_per_s": round(8192 / (med * 1e-3), 1), "ms_per_step": round(med, 3),
+                    "tflops": round(MLP_FLOP_PER_SAMPLE * 8192 / (med * 1e-3) / 1e12, 1), "precision": label,
+                    "cost_after": cost, "launches_per_step": kernel_launches(fm)}
+                del fm
+            except Exception as e:
+                extra[f"mlp_b8192_1gpu_{mode}"] = {"error": repr(e)[:300]}
+            torch.cuda.empty_cache()
+        from paper_1605_02688_b200.dp import DataParallel
+        for mode, key, label in (("auto", "mlp_dp_global65536", "tf32 tensor-core GEMMs (fp32 accumulate)"),
+                                 ("3xtf32", "mlp_dp_global65536_3xtf32", "3xtf32 tensor-core GEMMs (sgemm-class)")):
+            try:
+                G = 65536
+                dp = DataParallel(world_size=ws, rank=rank)
+                fd, ms_d, cost_d = bench_mlp(T, C, G // ws, max(5, args.steps // 2) if mode == "auto" else 5, 3,
+                                             lib_holder, dp=dp, n_global=G, gemm_mode=mode)
+                med = barrier_max(statistics.median(ms_d), ws)
+                extra[key] = {
+                    "samples_per_s": round(G / (med * 1e-3), 1), "ms_per_step": round(med, 3), "n_gpus": ws,
+                    "per_gpu_batch": G // ws, "scaling": "strong (fixed global batch)", "precision": label,
+                    "tflops_total": round(MLP_FLOP_PER_SAMPLE * G / (med * 1e-3) / 1e12, 1),
+                    "allreduce_buckets": len(fd._plans[next(iter(fd._plans))].buckets) if fd._plans else None,
+                    "allreduce_bytes_per_step": 20037642 * 4 + 4, "cost_after": cost_d}
+                del fd
+            except Exception as e:
+                extra[key] = {"error": repr(e)[:300]}
+            torch.cuda.empty_cache()
         torch.cuda.empty_cache()
         try:
             ms_l, e2e_l, nl = bench_logreg(T, C, 20, 5, lib_holder)

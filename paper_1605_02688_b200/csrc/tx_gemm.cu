@@ -85,18 +85,36 @@ __device__ __forceinline__ float tf32_rna(float x) {
 
 // x viewed as [outer][inner] (strides so, si) -> three planes of
 // y[plane * poff + o * ld + i]; plane `lo_plane` holds the small part.
-__global__ void tf32_split_kernel(const float* __restrict__ x, int64_t outer, int64_t inner, int64_t so, int64_t si,
-                                  float* __restrict__ y, int64_t ld, int64_t poff, int lo_plane) {
-  const int64_t n = outer * inner;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t o = e / inner, i = e - o * inner;
-    const float v = __ldcs(x + o * so + i * si);
-    float big = tf32_rna(v);
-    if (isinf(big) && !isinf(v)) big = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);  // no rounding to inf
-    const float small = isfinite(big) ? tf32_rna(__fsub_rn(v, big)) : 0.0f;
+__device__ __forceinline__ void split_one(float v, float& big, float& small) {
+  big = tf32_rna(v);
+  if (isinf(big) && !isinf(v)) big = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);  // no rounding to inf
+  small = isfinite(big) ? tf32_rna(__fsub_rn(v, big)) : 0.0f;
+}
+
+// grid: x over inner (4 elements per thread when V4), y (grid-stride) over outer
+template <bool V4>
+__global__ void __launch_bounds__(256) tf32_split_kernel(const float* __restrict__ x, int64_t outer, int64_t inner,
+                                                         int64_t so, int64_t si, float* __restrict__ y, int64_t ld,
+                                                         int64_t poff, int lo_plane) {
+  const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * (V4 ? 4 : 1);
+  if (i >= inner) return;
+  for (int64_t o = blockIdx.y; o < outer; o += gridDim.y) {
     float* d = y + o * ld + i;
+    if constexpr (V4) {  // si == 1, inner % 4 == 0, 16-byte aligned rows
+      const float4 v = __ldcs(reinterpret_cast<const float4*>(x + o * so + i));
+      float4 b, m;
+      split_one(v.x, b.x, m.x);
+      split_one(v.y, b.y, m.y);
+      split_one(v.z, b.z, m.z);
+      split_one(v.w, b.w, m.w);
 #pragma unroll
-    for (int j = 0; j < 3; ++j) d[j * poff] = j == lo_plane ? small : big;
+      for (int j = 0; j < 3; ++j) *reinterpret_cast<float4*>(d + j * poff) = j == lo_plane ? m : b;
+    } else {
+      float b, m;
+      split_one(__ldcs(x + o * so + i * si), b, m);
+#pragma unroll
+      for (int j = 0; j < 3; ++j) d[j * poff] = j == lo_plane ? m : b;
+    }
   }
 }
 
@@ -163,9 +181,16 @@ int split3_prepare(const G& g, void* ws, size_t wsb, cudaStream_t st, G* out, vo
   const int sms = sm_count();
   auto launch = [&](const float* x, int64_t outer, int64_t inner, int64_t so, int64_t si, float* y, int64_t ld,
                     int64_t poff, int lo) {
-    const int64_t n = outer * inner;
-    const int64_t blocks = std::min<int64_t>((n + 255) / 256, (int64_t)sms * 16);
-    tf32_split_kernel<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, st>>>(x, outer, inner, so, si, y, ld, poff, lo);
+    if (outer == 0 || inner == 0) return;
+    const bool v4 = si == 1 && inner % 4 == 0 && so % 4 == 0 && ld % 4 == 0 && poff % 4 == 0 &&
+                    ((uintptr_t)x & 15) == 0 && ((uintptr_t)y & 15) == 0;
+    const int64_t per = v4 ? 1024 : 256;
+    const int64_t bx = (inner + per - 1) / per;
+    // ~16 resident blocks per SM in total; rows grid-strided
+    const int64_t by = std::max<int64_t>(1, std::min<int64_t>(outer, std::min<int64_t>(65535, (int64_t)sms * 16 / bx + 1)));
+    dim3 grid((unsigned)bx, (unsigned)by);
+    if (v4) tf32_split_kernel<true><<<grid, 256, 0, st>>>(x, outer, inner, so, si, y, ld, poff, lo);
+    else tf32_split_kernel<false><<<grid, 256, 0, st>>>(x, outer, inner, so, si, y, ld, poff, lo);
   };
   // A' = [small | big | big], B' = [big ; small ; big]: the cross terms first
   launch((const float*)g.A, s.a_outer, s.a_inner, s.a_so, s.a_si, Ap, s.a_ld, s.a_poff, 0);

@@ -1,6 +1,6 @@
 """Short workload driver for ncu captures (never a bench number).
 
-    python tools/profile_run.py [--only ew|mlp|logreg|reduce] [--steps N]
+    python tools/profile_run.py [--only ew|mlp|logreg|reduce] [--steps N] [--gemm-mode auto|3xtf32|simt]
 """
 import argparse
 import os
@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--only", default="all")
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--B", type=int, default=8192)
+    ap.add_argument("--gemm-mode", default="auto")
     a = ap.parse_args()
     torch.cuda.set_device(0)
     if a.only in ("all", "ew"):
@@ -31,7 +32,7 @@ def main():
         del ins
     if a.only in ("all", "mlp"):
         g = C.build_mlp(T, B=a.B)
-        f = T.compile(g["inputs"], g["outputs"], updates=g["updates"])
+        f = T.compile(g["inputs"], g["outputs"], updates=g["updates"], gemm_mode=a.gemm_mode)
         x, y = C.inputs_mlp(B=a.B)
         xd, yd = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
         for _ in range(a.steps):
