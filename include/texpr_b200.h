@@ -77,6 +77,11 @@ int tx_memcpy_async(void* dst, const void* src, size_t bytes, int kind, void* st
 int tx_memset_async(void* dst, int value, size_t bytes, void* stream);
 int tx_host_register(void* ptr, size_t bytes);
 int tx_host_unregister(void* ptr);
+/* Device memory for callers without their own allocator (a cgo / JNI /
+ * ctypes binding of the reference; the Python package uses torch tensors).
+ * 256-byte aligned; tx_device_free(NULL) is a no-op. */
+int tx_device_alloc(size_t bytes, void** ptr);
+int tx_device_free(void* ptr);
 
 /* Capture every launch issued on `stream` between begin/end into one CUDA
  * graph (replaces the per-node Python walk, runtime.py:428-446). */

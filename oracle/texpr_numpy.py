@@ -242,7 +242,72 @@ def run_node(node, args):
         return [inc_subtensor(args[0], args[1], op.items)]
     if name == "join":
         return [join(op.axis, args)]
+    if name == "shape_of":
+        return [np.asarray(np.shape(args[0]), dtype=np.int64)]
+    if name == "reshape":
+        return [reshape(args[0], args[1])]
+    if name == "scan":
+        return scan_loop(op, args)
     raise NotImplementedError(f"oracle has no kernel for op {name!r}")
+
+
+def reshape(x, shp):
+    """Reshape.perform (ops/shaping.py:333-338): np.reshape, ShapeMismatch on failure."""
+    try:
+        return np.reshape(x, tuple(int(s) for s in shp))
+    except ValueError as exc:
+        from paper_1605_02688_b200.errors import ShapeMismatch
+        raise ShapeMismatch(f"reshape: {exc}") from exc
+
+
+def scan_loop(op, args):
+    """ScanOp.perform (scan.py:248-300): outer inputs [n_steps?, sequences,
+    initial states, invariants]; every step evaluates the inner graph on
+    [sequence elements, states, invariants]; outputs are the histories of
+    every inner output (the whole sequence, or only the last step for
+    retention "last") followed by each state's final value.  A zero-length
+    loop probes the inner graph once (on ones) for the history shapes."""
+    from paper_1605_02688_b200.errors import LengthMismatch
+    pos = 1 if op.has_nsteps else 0
+    seqs = [np.asarray(a) for a in args[pos: pos + op.n_seqs]]
+    states = [np.asarray(a) for a in args[pos + op.n_seqs: pos + op.n_seqs + op.n_states]]
+    nonseqs = [np.asarray(a) for a in args[pos + op.n_seqs + op.n_states:]]
+    lengths = {int(q.shape[0]) for q in seqs}
+    if len(lengths) > 1:
+        raise LengthMismatch(f"sequences disagree on length: {sorted(lengths)}")
+    if op.has_nsteps:
+        length = int(args[0])
+        if length < 0:
+            raise LengthMismatch(f"negative step count {length}")
+        if lengths and length != next(iter(lengths)):
+            raise LengthMismatch(f"step count {length} != shared sequence length {next(iter(lengths))}")
+    elif lengths:
+        length = next(iter(lengths))
+    else:
+        raise LengthMismatch("loop without sequences needs an explicit step count")
+    inner = list(op.inner_inputs)
+
+    def step(vals):
+        return evaluate(list(op.inner_outputs), dict(zip(inner, vals)))
+    full = [r == "full" for r in op.retention]
+    if length == 0:
+        probe = [np.ones(q.shape[1:], dtype=q.dtype) for q in seqs] + states + nonseqs
+        hist = [np.zeros((0,) + np.shape(o), dtype=np.dtype(v.type.dtype))
+                for o, v in zip(step(probe), op.inner_outputs)]
+        return hist + [np.array(x, copy=True) for x in states]
+    steps = []
+    for t in range(length):
+        outs = step([q[t] for q in seqs] + states + nonseqs)
+        outs = [np.asarray(o, dtype=np.dtype(v.type.dtype)) for o, v in zip(outs, op.inner_outputs)]
+        steps.append(outs)
+        states = [np.array(outs[k], copy=True) for k in range(op.n_states)]
+    hist = []
+    for i in range(len(op.inner_outputs)):
+        if full[i]:
+            hist.append(np.stack([s[i] for s in steps]))
+        else:
+            hist.append(np.asarray(steps[-1][i])[None])
+    return hist + [np.array(x, copy=True) for x in states]
 
 
 def _as_index(items):

@@ -196,6 +196,16 @@ int tx_memcpy_async(void* dst, const void* src, size_t bytes, int kind, void* s)
   TX_CUDA(cudaMemcpyAsync(dst, src, bytes, k, (cudaStream_t)s));
   return TX_OK;
 }
+int tx_device_alloc(size_t bytes, void** ptr) {
+  TX_CHECK(ptr, TX_E_ARG, "tx_device_alloc: null out pointer");
+  *ptr = nullptr;
+  TX_CUDA(cudaMalloc(ptr, bytes ? bytes : 1));
+  return TX_OK;
+}
+int tx_device_free(void* ptr) {
+  if (ptr) TX_CUDA(cudaFree(ptr));
+  return TX_OK;
+}
 int tx_memset_async(void* dst, int value, size_t bytes, void* s) {
   if (bytes == 0) return TX_OK;
   TX_CUDA(cudaMemsetAsync(dst, value, bytes, (cudaStream_t)s));

@@ -385,7 +385,7 @@ class EwProgram:
 
 
 @register_op
-class Composite(Op):
+class CompositeElemwise(Op):
     """One node evaluating a fused scalar DAG per element (reference
     ``CompositeElemwise``, ``ops/elemwise.py:452-695``).  Built by the convex
     fusion pass; lowered to one generated kernel."""
@@ -488,4 +488,4 @@ class Composite(Op):
 
 
 # Reference name, kept for drop-in imports.
-CompositeElemwise = Composite
+Composite = CompositeElemwise

@@ -20,6 +20,7 @@ EXPORTS = [
     "tx_version", "tx_last_error", "tx_init", "tx_device_info", "tx_stream_create", "tx_stream_destroy",
     "tx_stream_sync", "tx_event_create", "tx_event_destroy", "tx_event_record", "tx_stream_wait_event",
     "tx_event_elapsed_ms", "tx_memcpy_async", "tx_memset_async", "tx_host_register", "tx_host_unregister",
+    "tx_device_alloc", "tx_device_free",
     "tx_graph_begin", "tx_graph_end", "tx_graph_launch", "tx_graph_destroy", "tx_copy",
     "tx_ew_compile", "tx_ew_check", "tx_ew_launch", "tx_ew_destroy",
     "tx_kernel_compile", "tx_kernel_launch", "tx_kernel_destroy",
@@ -73,6 +74,7 @@ class Library:
             "tx_stream_wait_event": [vp, vp], "tx_event_elapsed_ms": [vp, vp, P(ctypes.c_float)],
             "tx_memcpy_async": [vp, vp, sz, ctypes.c_int, vp], "tx_memset_async": [vp, ctypes.c_int, sz, vp],
             "tx_host_register": [vp, sz], "tx_host_unregister": [vp],
+            "tx_device_alloc": [sz, P(vp)], "tx_device_free": [vp],
             "tx_graph_begin": [vp], "tx_graph_end": [vp, P(vp)], "tx_graph_launch": [vp, vp],
             "tx_graph_destroy": [vp], "tx_copy": [P(TxTensor), P(TxTensor), vp],
             "tx_ew_compile": [ctypes.c_char_p, ctypes.c_char_p, P(vp)],

@@ -3,12 +3,13 @@
 Same surface as reference ``ops/base.py:37-111`` (``infer_types``,
 ``check_runtime_shapes``, ``grad``, ``rop``, ``infer_shape``, ``attrs_key``
 value identity, ``attrs_payload``/``from_payload``, capability flags, and the
-``register_op`` registry) with one substitution: there is no host ``perform``.
-An op executes by *lowering* onto the device — ``lower(node, plan)`` appends
+``register_op`` registry) with one substitution: built-in ops have no host
+``perform``.  An op executes by *lowering* onto the device — ``lower(node, plan)`` appends
 launches of hand-written sm_100a kernels to a step plan (see ``vm.py``), or the
 op declares itself a zero-copy view (``view_layout``).  ``fold`` is a
 compile-time constant-folding hook restricted to tiny constants; it is never
-used to execute a compiled function.
+used to execute a compiled function.  A *user* op that only implements the
+reference's host ``perform`` still runs, as a host step (``is_host_op``).
 """
 from __future__ import annotations
 
@@ -78,7 +79,15 @@ class Op:
         raise NotImplementedError
 
     def lower(self, node, plan) -> None:
+        if is_host_op(self):
+            plan.emit_host_op(node)
+            return
         raise NotSupported(f"op {self.name} has no B200 lowering")
+
+    def perform(self, inputs, output_buffers=None):
+        """Host evaluation -- only for user plugin ops (see ``is_host_op``);
+        every built-in op lowers to device kernels instead."""
+        raise NotSupported(f"op {self.name} has no host perform (it executes on the device via lower)")
 
     def fold(self, values):
         """Compile-time evaluation on tiny host constants, or None."""
@@ -91,6 +100,18 @@ class Op:
     @classmethod
     def from_payload(cls, payload, decode_graph=None):
         return cls()
+
+
+def is_host_op(op) -> bool:
+    """A user plugin op written against the reference's contract only
+    (``perform`` on host arrays, reference ``ops/base.py:37-111``) and no
+    device ``lower``.  The VM runs such a node as a host step inside the
+    device step: the stream is drained, the node's inputs come to the host,
+    ``perform`` runs, its outputs go back to the planned device buffers, and
+    the step is not captured as a CUDA graph.  None of the built-in ops is a
+    host op: the hot path is device-only."""
+    t = type(op)
+    return t.perform is not Op.perform and t.lower is Op.lower
 
 
 OP_REGISTRY: dict[str, type] = {}

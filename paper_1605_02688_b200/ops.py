@@ -56,3 +56,37 @@ def rop_rule(op, inputs, input_perturbations):
 
 def infer_shape(op, node, input_shapes):
     return op.infer_shape(node, list(input_shapes))
+
+
+def perform(op, inputs, output_buffers=None):
+    """Evaluate one op on host arrays (reference ``ops/base.py:118-120``).
+
+    The reference runs ``op.perform`` on the CPU; here the op is executed on
+    the B200 through a one-node compiled function (``preset="none"``: the op
+    as given, no rewrites), so the reference's per-op golden tests exercise
+    the device kernels.  Extent-1 dimensions are declared broadcastable, as
+    the reference's NumPy broadcasting treats them.  ``output_buffers``, when
+    given, receive the results (the reference's ``out=`` convention)."""
+    import numpy as np
+
+    from .dtypes import dtype_of_value
+    from .graph import TensorType, Variable, apply
+    from .vm import compile as _compile
+    arrs = [np.asarray(v) for v in inputs]
+    ins = [Variable(TensorType(dtype_of_value(a), tuple(d == 1 for d in a.shape))) for a in arrs]
+    outs = apply(op, ins)
+    res = _compile(ins, outs, preset="none")(*arrs)
+    if output_buffers:
+        for buf, r in zip(output_buffers, res):
+            if buf is not None:
+                np.copyto(buf, r)
+        res = [buf if buf is not None else r for buf, r in zip(output_buffers, res)]
+    return res
+
+
+def conv2d_reference(x, f, stride=(1, 1), pad=(0, 0)):
+    """Host-array cross-correlation with the reference algorithm's exact
+    fp arithmetic (reference ``ops/conv.py:49-66``), computed on the device
+    by the direct ``reference``-algorithm kernel."""
+    from .conv import REFERENCE, Conv2d, FORWARD
+    return perform(Conv2d(FORWARD, REFERENCE, tuple(stride), tuple(pad)), [x, f])[0]

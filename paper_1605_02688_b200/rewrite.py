@@ -75,6 +75,7 @@ class LogRecord:
     node_id: int | None = None
     replaced_op: str | None = None
     replacement_op: str | None = None
+    created_node_ids: tuple = ()   # local rewrites: nodes the replacement imported (replay_log)
 
 
 @dataclass
@@ -172,7 +173,8 @@ class _Stage:
                 applied += 1
                 old, new = res[0]
                 src, dst = _dname(node.op), (_dname(new.owner.op) if new.owner else "<input>")
-                self.log.add(LogRecord(self.stage, rw.name, "local", self.pass_index, node.id, src, dst))
+                self.log.add(LogRecord(self.stage, rw.name, "local", self.pass_index, node.id, src, dst,
+                                       tuple(n.id for n in getattr(self.g, "imported", ()))))
                 self._oscillation(rw, src, dst)
                 for _, nv in res:
                     touched = list(self.g.node_clients(nv))
@@ -196,6 +198,49 @@ class _Stage:
         if back is not None and c + 1 >= 4 and back[0] >= 4:
             raise RewriteCycleDetected(f"rewrites {rw.name!r} and {back[1]!r} keep undoing each other "
                                        f"({src} <-> {dst})")
+
+
+def _silent(*a, **k):
+    return None
+
+
+_silent.note = lambda text: None
+
+
+def replay_log(fgraph: FunctionGraph, log: RewriteLog, var_mapping: dict, ctx=None) -> FunctionGraph:
+    """Re-apply a recorded rewrite sequence to a copy of the graph it was
+    recorded on (reference ``rewrites/engine.py:343-396``): ``var_mapping``
+    maps the original's variables to the copy's (``clone_with_replacements``).
+    Local records are re-matched at the mapped node and the nodes they create
+    are mapped in import order; global rewrites run once per recorded
+    invocation.  Rewrites are deterministic per site, so the copy ends
+    op-isomorphic to the optimized original."""
+    ctx = ctx or RewriteContext()
+    node_map = {old.owner.id: new.owner for old, new in var_mapping.items()
+                if old.owner is not None and new.owner is not None}
+    last_global = None
+    for rec in log.records:
+        rw = find_rewrite(rec.rewrite)
+        if rec.kind == "global":
+            if (rec.rewrite, rec.pass_index, rec.stage) == last_global:
+                continue
+            last_global = (rec.rewrite, rec.pass_index, rec.stage)
+            rw.fn(fgraph, ctx, _silent)
+            continue
+        last_global = None
+        node = node_map.get(rec.node_id)
+        if node is None or node.id not in fgraph.nodes:
+            raise RewriteCycleDetected(f"replay lost track of node {rec.node_id} for {rec.rewrite}")
+        res = try_local(fgraph, rw, node, ctx)
+        if not res:
+            raise RewriteCycleDetected(f"replay of {rec.rewrite} failed to re-match at node {rec.node_id}")
+        created = list(getattr(fgraph, "imported", ()))
+        if len(created) != len(rec.created_node_ids):
+            raise RewriteCycleDetected(f"replay of {rec.rewrite} created {len(created)} nodes, "
+                                       f"expected {len(rec.created_node_ids)}")
+        for oid, n in zip(rec.created_node_ids, created):
+            node_map[oid] = n
+    return fgraph
 
 
 def select_rewrites(preset, include=(), exclude=()):
@@ -223,7 +268,23 @@ def run_preset(fgraph: FunctionGraph, preset="fast_run", include=(), exclude=(),
         t0 = time.perf_counter()
         _Stage(fgraph, stage, rws, ctx, log).run()
         log.stage_times[stage] = log.stage_times.get(stage, 0.0) + time.perf_counter() - t0
+        if stage == "abstract_select":
+            _check_abstract(fgraph, ctx)
     return fgraph, log
+
+
+def _check_abstract(fgraph, ctx):
+    """Implementation selection with every convolution implementation
+    excluded (``conv_impl="none"``) must not leave placeholders behind
+    (reference ``rewrites/engine.py:328-340``)."""
+    if ctx.conv_impl != "none":
+        return
+    from .conv import Conv2d
+    left = [n for n in fgraph.nodes.values() if isinstance(n.op, Conv2d) and n.op.is_abstract]
+    if left:
+        from .errors import NoImplementationSelected
+        raise NoImplementationSelected("implementation selection ran with every convolution implementation "
+                                       f"excluded; {len(left)} placeholder node(s) remain")
 
 
 def graph_signature(fgraph: FunctionGraph) -> tuple:

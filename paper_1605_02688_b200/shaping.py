@@ -81,7 +81,7 @@ class DimShuffle(Op):
         dropped = [i for i in range(x.ndim) if i not in kept]
         y = np.transpose(x, kept + dropped)
         idx = tuple([None if p == "x" else slice(None) for p in self.pattern] + [0] * len(dropped))
-        return [np.ascontiguousarray(y[idx])]
+        return [np.asarray(y[idx], order="C")]
 
     def attrs_payload(self, encode_graph=None):
         return {"pattern": list(self.pattern)}
@@ -212,7 +212,7 @@ class Subtensor(Op):
 
     def fold(self, values):
         (x,) = values
-        return [np.ascontiguousarray(x[tuple(i if isinstance(i, int) else slice(*i) for i in self.items)])]
+        return [np.asarray(x[tuple(i if isinstance(i, int) else slice(*i) for i in self.items)], order="C")]
 
     def attrs_payload(self, encode_graph=None):
         return {"items": [i if isinstance(i, int) else list(i) for i in self.items]}

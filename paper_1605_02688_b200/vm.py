@@ -40,7 +40,7 @@ _POISON = bool(__import__("os").environ.get("TX_POISON"))
 from .errors import (NotSupported, ShapeMismatch, TexprError, TypeMismatch,
                      UnderdeterminedOutputs)
 from .graph import Constant, FunctionGraph, Variable, clone_outputs
-from .op import UNKNOWN_SHAPE
+from .op import UNKNOWN_SHAPE, is_host_op
 from .rewrite import RewriteContext, run_preset
 from .shared import SharedVariable, torch_dtype
 
@@ -530,14 +530,28 @@ class CompiledFunction:
         twin.updates = [(swap.get(s, s), v) for s, v in self.updates] if carry_updates else []
         twin._direct = {k: (swap.get(s, s), v) for k, (s, v) in self._direct.items()} if carry_updates else {}
         twin.profile = Profile(stage_times=dict(self.profile.stage_times), _order=self.profile._order)
-        twin._events = None
         twin._lock = threading.Lock()
+        if share_intermediate_storage and carry_updates:
+            # one set of step plans (arenas, captured graphs) for both
+            # functions, run under one lock on one stream so they never
+            # overlap; plans are keyed on the shared storages they bake in,
+            # so a twin with swapped shared variables gets its own entries
+            twin._lock = self._lock
+            return twin
+        twin._events = None
         twin._plans = OrderedDict()
         twin._pipes = OrderedDict()
         twin._stream = None
         twin._comm_stream = None
         twin._xfer = None
         return twin
+
+    @property
+    def _keep(self):
+        """The function's intermediate storage (reference ``runtime.py`` keeps
+        per-node buffers there with ``allow_gc=False``): here the cached step
+        plans, whose arenas hold every intermediate."""
+        return self._plans
 
 
 def save(fn: CompiledFunction) -> bytes:
@@ -711,6 +725,11 @@ class StepPlan:
                 outs = n.op.infer_shape(n, shapes)
             if getattr(n.op, "plan_value", False):
                 self.values[n.outputs[0].id] = n.op.value(n, shapes)
+            if is_host_op(n.op) and any(s is UNKNOWN_SHAPE or any(d is None for d in s) for s in outs):
+                # a host plugin op without infer_shape: its output shapes come
+                # from one host evaluation on zeros of the input shapes
+                probe = n.op.perform([np.zeros(sh, dtype=np_dtype(x.type.dtype)) for sh, x in zip(shapes, n.inputs)])
+                outs = [tuple(np.shape(r)) for r in probe]
             for o, s in zip(n.outputs, outs):
                 if s is UNKNOWN_SHAPE or any(d is None for d in s):
                     raise NotSupported(f"cannot infer the runtime shape of {o!r} ({n.op.name})")
@@ -1364,6 +1383,39 @@ class StepPlan:
             lib.stream_wait_event(stream, done)
         self.launches.append((None, launch))
 
+    def emit_host_op(self, node):
+        """A user plugin op with only a host ``perform`` (``op.is_host_op``):
+        drain the stream, bring the inputs to the host, run ``perform``, write
+        the results into the node's planned device buffers.  The step holding
+        it runs eagerly (host code cannot be captured into a CUDA graph)."""
+        lib, t = self.lib, _torch()
+        ins = [(self.lay[x.id], self.ptr_of(self.lay[x.id])) for x in node.inputs]
+        outs = [(self.lay[o.id], self.ptr_of(self.lay[o.id]), o) for o in node.outputs]
+        self.host_ops = getattr(self, "host_ops", 0) + 1
+        op = node.op
+
+        def launch(stream):
+            lib.stream_sync(stream)
+            vals = []
+            for lay, ptr in ins:
+                v = _torch_view(lay, ptr).cpu().numpy()
+                vals.append(v.astype(np.bool_) if lay.dtype == "bool" else v)
+            res = op.perform(vals, None)
+            keep = []
+            for (lay, ptr, o), r in zip(outs, res):
+                arr = np.array(r, dtype=np_dtype(lay.dtype), order="C")
+                if arr.shape != lay.shape:
+                    raise ShapeMismatch(f"{getattr(op, 'name', op)}: perform returned shape {arr.shape}, "
+                                        f"planned {lay.shape}")
+                if lay.dtype == "bool":
+                    arr = arr.astype(np.uint8)
+                keep.append(arr)
+                if arr.nbytes:
+                    lib.memcpy(ptr, arr.ctypes.data, arr.nbytes, 0, stream)
+            lib.stream_sync(stream)
+            del keep
+        self.add_launch(launch)
+
     def _emit_copy(self, src: Layout, dst: Layout):
         lib = self.lib
         s, d = self.tx(src), self.tx(dst)
@@ -1414,7 +1466,7 @@ class StepPlan:
             fn(stream)
 
     def run(self, stream):
-        if not self.fn.cuda_graph:
+        if not self.fn.cuda_graph or getattr(self, "host_ops", 0):
             self._launch_all(stream)
             return
         if self.graph is None:

@@ -52,8 +52,12 @@ def test_conv_forward_numpy_oracle_and_errors(rng):
             win = xp[:, :, 2 * i: 2 * i + 3, 2 * j: 2 * j + 3]
             want[:, :, i, j] = np.einsum("nchw,kchw->nk", win, f.astype(np.float64))
     assert _rel(y, want) <= 1e-6
+    # every implementation excluded: refused at compile time (reference rewrites/engine.py:328-340);
+    # no selection stage at all: the placeholder fails when it is executed
+    with pytest.raises(T.NoImplementationSelected):
+        T.compile([vx, vf], [T.conv2d(vx, vf)], conv_impl="none")
     with pytest.raises(AbstractOpRemaining):
-        T.compile([vx, vf], [T.conv2d(vx, vf)], conv_impl="none")(x, f)
+        T.compile([vx, vf], [T.conv2d(vx, vf)], preset="none")(x, f)
     with pytest.raises(ShapeMismatch):
         T.compile([vx, vf], [T.conv2d(vx, vf)])(x, rng.standard_normal((6, 5, 3, 3)).astype(np.float32))
 

@@ -520,3 +520,38 @@ def test_pipelined_identity_output_not_overwritten():
         np.testing.assert_array_equal(o0, a)
         np.testing.assert_array_equal(o1, a * b)
         np.testing.assert_array_equal(o2, a + b)
+
+
+def test_user_plugin_op_with_host_perform_runs_as_host_step():
+    """An op written against the reference's plugin contract only (host
+    ``perform``, no device lowering, no infer_shape) still executes: as a host
+    step between device launches, shapes probed from one host evaluation."""
+    from paper_1605_02688_b200.graph import apply
+    from paper_1605_02688_b200.op import Op, is_host_op
+
+    class HostCube(Op):
+        name = "host_cube_fixture"
+
+        def infer_types(self, input_types):
+            return [input_types[0]]
+
+        def perform(self, inputs, output_buffers=None):
+            return [inputs[0] ** 3]
+
+        def grad(self, inputs, output_grads):
+            return [output_grads[0] * 3.0 * inputs[0] * inputs[0]]
+
+    assert is_host_op(HostCube())
+    x = T.vector("x", dtype="float64")
+    y = T.exp(apply(HostCube(), [T.tanh(x)])[0]) * 2.0
+    (g,) = T.grad(T.sum(y), [x])
+    f = T.compile([x], [y, g])
+    xv = np.linspace(-1, 1, 7)
+    yv, gv = f(xv)
+    t = np.tanh(xv)
+    np.testing.assert_allclose(yv, np.exp(t ** 3) * 2.0, rtol=1e-12)
+    np.testing.assert_allclose(gv, np.exp(t ** 3) * 2.0 * 3 * t * t * (1 - t * t), rtol=1e-12)
+    plan = next(iter(f._plans.values()))
+    assert plan.host_ops == 1 and plan.graph is None
+    rep = T.verify_grad([x], [y], [xv], rel_tol=1e-6)
+    assert rep.passed, str(rep)
