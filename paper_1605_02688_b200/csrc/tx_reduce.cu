@@ -28,6 +28,7 @@
 #include <cstdlib>
 #include <climits>
 #include <cstring>
+#include <algorithm>
 #include <type_traits>
 
 #include "tx_common.h"
@@ -417,6 +418,44 @@ __global__ void __launch_bounds__(CT_THREADS) col_tma_kernel(const __grid_consta
   const int t = threadIdx.x;
   Acc<T, OP> a;
   a.init();
+  if constexpr (std::is_same<T, float>::value && (OP == TX_MAX || OP == TX_ARGMAX_INDEX || OP == TX_ARGMAX_ONEHOT)) {
+    // float max / argmax: the per-element compare-select is the issue-bound
+    // part of this kernel (sum: ~21% SM throughput, argmax: ~65%), so it is
+    // cut to the minimum: one unordered compare (take unless x <= v, which is
+    // also true for a NaN x) gated by v being a number (a NaN v is final), a
+    // 32-bit split-local row and two selects.  Rows arrive in increasing
+    // order: the first maximum and the first NaN win, exactly as the generic
+    // Acc::push (np.argmax / np.maximum.reduce, signed zeros included).
+    // v = -inf with row 0 as its index needs no "empty" sentinel: row 0 is
+    // taken unless it is -inf, in which case the first maximum IS row 0
+    // whenever nothing larger follows
+    float v = -INFINITY;
+    int vi = 0;
+    auto step = [&](float x, int row) {
+      const bool take = !(x <= v) & (v == v);
+      v = take ? x : v;
+      if constexpr (OP != TX_MAX) vi = take ? row : vi;
+    };
+    for (int i = 0; i < ntiles; ++i) {
+      const int s = i % CT_STAGES;
+      wait(full + s, (i / CT_STAGES) & 1);
+      const float* tile = reinterpret_cast<const float*>(tiles) + (size_t)s * CT_ROWS * CT_COLS;
+      const int rl = i * CT_ROWS;
+      const int nr = (int)min((int64_t)CT_ROWS, hi - (lo + rl));
+      if (nr == CT_ROWS) {
+#pragma unroll
+        for (int r = 0; r < CT_ROWS; ++r) step(tile[r * CT_COLS + t], rl + r);
+      } else {
+        for (int r = 0; r < nr; ++r) step(tile[r * CT_COLS + t], rl + r);
+      }
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sa32(empty + s)) : "memory");
+    }
+    if (ntiles > 0) {
+      a.v = v;
+      if constexpr (OP != TX_MAX) a.i = lo + vi;
+    }
+  } else {
   for (int i = 0; i < ntiles; ++i) {
     const int s = i % CT_STAGES;
     wait(full + s, (i / CT_STAGES) & 1);
@@ -431,6 +470,7 @@ __global__ void __launch_bounds__(CT_THREADS) col_tma_kernel(const __grid_consta
     }
     __syncwarp();
     if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sa32(empty + s)) : "memory");
+  }
   }
   const int64_t c = c0 + t;
   if (c >= K) return;
@@ -608,23 +648,27 @@ static void make_plan(int op, const tx_tensor& x, uint32_t mask, int itemsz, Pla
       col_splits_max = (int)splits;
       if (itemsz == 4 && ((uintptr_t)x.data & 15) == 0 && (rstride * 4) % 16 == 0 && rstride >= K &&
           R < (int64_t)INT32_MAX && K < (int64_t)INT32_MAX && tmap_encoder() && !getenv("TX_REDUCE_NO_TMA")) {
-        // one wave of 3 CTAs per SM (64 KB ring each)
+        // ~1.75 waves of 3 CTAs per SM (64 KB ring each): the second partial
+        // wave fills SMs whose first CTAs finish early (r02 A/B at 16384^2:
+        // 7 splits = 448 CTAs on 444 slots 190-194 us, 12 splits 174-179 us)
         p->form = COLTMA;
         const int64_t strips = (K + CT_COLS - 1) / CT_COLS;
-        int64_t want = (int64_t)sms * 3;
-        int64_t sp = (want + strips - 1) / strips;
+        int64_t want = (int64_t)sms * 3 * 7 / 4;
+        int64_t sp = want / strips;
         int64_t maxs = R / (4 * CT_ROWS);
         if (sp > maxs) sp = maxs;
         if (sp > 65535) sp = 65535;
         if (sp < 1) sp = 1;
+        if (const char* e = getenv("TX_REDUCE_COL_SPLITS")) sp = atoi(e);  // experiments
         p->splits = (int)sp;
       }
       {
         const int64_t strips = (K + CT_COLS - 1) / CT_COLS;
-        int64_t sp = ((int64_t)sms * 3 + strips - 1) / strips;
+        int64_t sp = std::max<int64_t>((int64_t)sms * 3 * 7 / 4 / strips, (int64_t)sms * 3 / strips + 1);
         int64_t maxs = R / (4 * CT_ROWS);
         if (sp > maxs) sp = maxs;
         if (sp > 65535) sp = 65535;
+        if (const char* e = getenv("TX_REDUCE_COL_SPLITS")) sp = atoi(e);
         if (sp > col_splits_max) col_splits_max = (int)sp;
       }
     } else if (R <= 512 && K >= 8) {
