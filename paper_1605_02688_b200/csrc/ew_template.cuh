@@ -73,10 +73,11 @@ __device__ __forceinline__ double tx_sigmoid(double x) {
 }
 template <class T> __device__ __forceinline__ T tx_sigmoid(T x) { return (T)tx_sigmoid((double)x); }
 
-// np.maximum: NaN in either operand propagates; ties keep the first operand
-__device__ __forceinline__ float tx_maximum(float a, float b) { return (a != a) ? a : (b != b) ? b : (a >= b ? a : b); }
-__device__ __forceinline__ double tx_maximum(double a, double b) { return (a != a) ? a : (b != b) ? b : (a >= b ? a : b); }
-template <class T> __device__ __forceinline__ T tx_maximum(T a, T b) { return a >= b ? a : b; }
+// np.maximum: NaN in either operand propagates (the first NaN if both); ties give the SECOND
+// operand ((a > b || isnan(a)) ? a : b), which decides the sign of a +0 / -0 tie
+__device__ __forceinline__ float tx_maximum(float a, float b) { return (a != a) ? a : (b != b) ? b : (a > b ? a : b); }
+__device__ __forceinline__ double tx_maximum(double a, double b) { return (a != a) ? a : (b != b) ? b : (a > b ? a : b); }
+template <class T> __device__ __forceinline__ T tx_maximum(T a, T b) { return a > b ? a : b; }
 
 __device__ __forceinline__ float tx_div(float a, float b, int*) { return a / b; }
 __device__ __forceinline__ double tx_div(double a, double b, int*) { return a / b; }

@@ -540,6 +540,26 @@ __global__ void gen_kernel(const T* __restrict__ x, int64_t K, int64_t R, GenMet
   if (OP == TX_SUM || OP == TX_MAX) out[o] = a.v; else out_idx[o] = a.i;
 }
 
+// max reductions: the sign of a zero maximum.  np.maximum.reduce keeps the
+// LATER operand on ties (reference ops/reductions.py:126, NumPy's
+// (a > b || isnan(a)) ? a : b), so a +0 / -0 tie resolves to the sign of the
+// last zero in index order.  The reduction kernels compute the maximum value
+// (any zero); this pass gives every zero result the sign of its range's last
+// zero, scanning backwards -- work only for outputs that are zero.
+template <class T>
+__global__ void max_zero_sign(const T* __restrict__ x, int64_t K, int64_t R, GenMeta m, T* __restrict__ out) {
+  const int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (o >= K || out[o] != T(0)) return;
+  int64_t base = 0, t = o;
+  for (int d = m.nk - 1; d >= 0; --d) { base += (t % m.kshape[d]) * m.kstride[d]; t /= m.kshape[d]; }
+  for (int64_t r = R - 1; r >= 0; --r) {
+    int64_t off = 0, u = r;
+    for (int d = m.nr - 1; d >= 0; --d) { off += (u % m.rshape[d]) * m.rstride[d]; u /= m.rshape[d]; }
+    const T e = x[base + off];
+    if (e == T(0)) { out[o] = e; return; }
+  }
+}
+
 // one-hot materialisation: y has x's shape; element is 1 where its flat
 // reduced index equals idx[flat kept index].
 template <class T>
@@ -785,6 +805,12 @@ static int run(const tx_tensor& x, uint32_t mask, tx_tensor& y, char* ws, size_t
     }
   }
   TX_CUDA(cudaGetLastError());
+  if constexpr (OP == TX_MAX && (std::is_same<T, float>::value || std::is_same<T, double>::value)) {
+    if (p.K > 0 && p.R > 0) {
+      max_zero_sign<T><<<(unsigned)((p.K + 127) / 128), 128, 0, st>>>(xp, p.K, p.R, p.gm, out);
+      TX_CUDA(cudaGetLastError());
+    }
+  }
   if (OP == TX_ARGMAX_ONEHOT) {
     T* yp = (T*)y.data;
     int64_t n = numel(y);

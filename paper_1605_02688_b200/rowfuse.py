@@ -304,9 +304,9 @@ template <class T> __device__ __forceinline__ T tx_sqrt(T x) { return (T)sqrt((d
 template <class T> __device__ __forceinline__ T tx_tanh(T x) { return (T)tanh((double)x); }
 template <class T> __device__ __forceinline__ T tx_sigmoid(T x) { return (T)tx_sigmoid((double)x); }
 template <class T> __device__ __forceinline__ T tx_pow(T a, T b) { if (b < 0) return (T)0; T r = 1; while (b) { if (b & 1) r *= a; a *= a; b >>= 1; } return r; }
-__device__ __forceinline__ float tx_maximum(float a, float b) { return (a != a) ? a : (b != b) ? b : (a >= b ? a : b); }
-__device__ __forceinline__ double tx_maximum(double a, double b) { return (a != a) ? a : (b != b) ? b : (a >= b ? a : b); }
-template <class T> __device__ __forceinline__ T tx_maximum(T a, T b) { return a >= b ? a : b; }
+__device__ __forceinline__ float tx_maximum(float a, float b) { return (a != a) ? a : (b != b) ? b : (a > b ? a : b); }
+__device__ __forceinline__ double tx_maximum(double a, double b) { return (a != a) ? a : (b != b) ? b : (a > b ? a : b); }
+template <class T> __device__ __forceinline__ T tx_maximum(T a, T b) { return a > b ? a : b; }
 __device__ __forceinline__ float tx_div(float a, float b, int*) { return a / b; }
 __device__ __forceinline__ double tx_div(double a, double b, int*) { return a / b; }
 __device__ __forceinline__ u8 tx_isnan(float a) { return a != a; }
@@ -497,6 +497,11 @@ class _Gen:
                       f"{nm} = ({nm} != {nm}) ? {nm} : ((w != w) ? w : (w > {nm} ? w : {nm})); }}")
             self.emit(f"if (tc >= K) {nm} = -__int_as_float(0x7f800000);" if ct == "float" else f"if (tc >= K) {nm} = -__longlong_as_double(0x7ff0000000000000LL);")
             self.emit(f"{nm} = {self.rmax}({nm});")
+            # a zero maximum takes the sign of the row's LAST zero (np.maximum.reduce
+            # keeps the later operand on ties, so +0/-0 ties resolve by position)
+            self.emit(f"if ({nm} == ({ct})0) {{ int zk = -1;\n#pragma unroll\nfor (int j = 0; j < TX_R; ++j) "
+                      f"{{ const int c = tc + TX_T * j; if (c < K && {xn}[j] == ({ct})0) zk = 2 * c + (signbit({xn}[j]) ? 1 : 0); }}\n"
+                      f"zk = {self.rmax}(zk); {nm} = (zk & 1) ? -({ct})0 : ({ct})0; }}")
             self.name[o.id], self.cls[o.id], self.dt[o.id] = nm, S, o.type.dtype
         elif isinstance(op, (Argmax, ArgmaxOnehot)) and op.axes == ra:
             iv, ii = f"{nm}_v", f"{nm}_i"

@@ -244,6 +244,14 @@ def test_wide_row_fusion_softmax_xent(N, K):
     np.testing.assert_array_equal(b[2], a[2])
     np.testing.assert_array_equal(b[3], a[3])
     np.testing.assert_allclose(b[4], a[4], rtol=1e-4, atol=1e-7)
+    # and against the reference algorithm itself (CPU oracle, same graph)
+    cpu = C.CpuFunction(T, [z, y], outs, exclude=("fuse_elemwise",))
+    o = cpu(zv, yv)
+    assert abs(b[0] - o[0]) <= 1e-5 * abs(o[0])
+    np.testing.assert_allclose(b[1], o[1], rtol=1e-5, atol=1e-8)
+    np.testing.assert_array_equal(b[2], o[2])
+    np.testing.assert_array_equal(b[3], o[3])
+    np.testing.assert_allclose(b[4], o[4], rtol=1e-4, atol=1e-7)
 
 
 @pytest.mark.parametrize("A,B,K", [(20, 20, 10000), (6, 7, 130), (3, 50, 257)])

@@ -42,6 +42,8 @@ def exact(got, want):
         assert np.array_equal(np.isnan(got), np.isnan(want))
         m = ~np.isnan(want)
         assert np.array_equal(got[m], want[m])
+        # bit-exact includes the sign of zero (== treats -0.0 and +0.0 as equal)
+        assert np.array_equal(np.signbit(got[m]), np.signbit(want[m]))
     else:
         assert np.array_equal(got, want)
 
@@ -469,3 +471,47 @@ def test_empty_operands_everywhere():
     hv, fv = T.compile([xs, h0], [hist, final])(np.zeros((0, 3)), np.ones(3))
     assert hv.shape == (0, 3)
     np.testing.assert_array_equal(fv, np.ones(3))
+
+
+@pytest.mark.parametrize("dt", ["float32", "float64"])
+def test_signed_zeros_bit_exact(dt):
+    """maximum / switch / second / neg / sub and the max reduction on +-0.0
+    (with ties, NaN and infinities around them) reproduce NumPy's sign of
+    zero (the reference's kernels, ops/elemwise.py:91-113, ops/reductions.py:126)."""
+    vals = np.array([0.0, -0.0, -0.0, 0.0, 1.0, -1.0, np.nan, np.inf, -np.inf, -0.0], dtype=dt)
+    a = np.array(np.meshgrid(vals, vals)[0].ravel(), dtype=dt)
+    b = np.array(np.meshgrid(vals, vals)[1].ravel(), dtype=dt)
+    c = (np.arange(a.size) % 3 == 0)
+    va, vb, vc = T.vector("a", dtype=dt), T.vector("b", dtype=dt), T.vector("c", dtype="bool")
+    for k in ("maximum", "sub", "add", "mul"):
+        exact(T.compile([va, vb], make(k, [va, vb]), preset="none")(a, b), O.elemwise(k, [a, b]))
+    exact(T.compile([va], make("neg", [va]), preset="none")(a), O.elemwise("neg", [a]))
+    exact(T.compile([vc, va, vb], make("switch", [vc, va, vb]), preset="none")(c, a, b),
+          O.elemwise("switch", [c, a, b]))
+    exact(T.compile([va, vb], make("second", [va, vb]), preset="none")(a, b), O.elemwise("second", [a, b]))
+    m = T.matrix("m", dtype=dt)
+    Z = np.array([[0.0, -0.0, 0.0], [-0.0, 0.0, -0.0], [-0.0, -0.0, -0.0], [0.0, 0.0, -0.0]] * 70, dtype=dt)
+    for ax in ((0,), (1,), None):
+        got = T.compile([m], T.max(m, axis=ax))(Z)
+        exact(got, O.reduce_max(Z, (0, 1) if ax is None else ax))
+
+
+@pytest.mark.parametrize("K", [3, 40, 700])
+def test_signed_zero_max_inside_row_fusion(K):
+    """The row max of a fused softmax region (rowfuse.py, warp- and
+    block-per-row forms) on rows whose maximum is +-0: the sign of the last
+    zero, as np.maximum.reduce gives."""
+    rng = np.random.default_rng(K)
+    z = -np.abs(rng.standard_normal((64, K))).astype(np.float32) - 1.0
+    for r in range(64):
+        cols = rng.choice(K, size=min(K, 1 + r % 3), replace=False)
+        z[r, cols] = np.where(rng.random(cols.size) < 0.5, np.float32(0.0), np.float32(-0.0))
+    v = T.matrix("z", dtype="float32")
+    m = T.max(v, axis=1)
+    e = T.exp(v - T.dimshuffle(m, (0, "x")))
+    p = e / T.dimshuffle(T.sum(e, axis=1), (0, "x"))
+    f = T.compile([v], [m, p])
+    got_m, got_p = f(z)
+    assert next(iter(f._plans.values())).row_groups, "expected a fused row region"
+    exact(got_m, O.reduce_max(z, (1,)))
+    np.testing.assert_allclose(got_p, T.compile([v], [p], row_fusion=False)(z)[0], rtol=1e-6, atol=1e-7)

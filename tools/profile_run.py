@@ -21,6 +21,8 @@ def main():
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--B", type=int, default=8192)
     ap.add_argument("--gemm-mode", default="auto")
+    ap.add_argument("--dp", action="store_true", help="MLP through the data-parallel path (1 rank)")
+    ap.add_argument("--n-global", type=int, default=None)
     a = ap.parse_args()
     torch.cuda.set_device(0)
     if a.only in ("all", "ew"):
@@ -31,8 +33,12 @@ def main():
             f.call_device(*ins, sync=True)
         del ins
     if a.only in ("all", "mlp"):
-        g = C.build_mlp(T, B=a.B)
-        f = T.compile(g["inputs"], g["outputs"], updates=g["updates"], gemm_mode=a.gemm_mode)
+        g = C.build_mlp(T, B=a.B, n_global=a.n_global)
+        dp = None
+        if a.dp:
+            from paper_1605_02688_b200.dp import DataParallel
+            dp = DataParallel(world_size=1, rank=0)
+        f = T.compile(g["inputs"], g["outputs"], updates=g["updates"], gemm_mode=a.gemm_mode, data_parallel=dp)
         x, y = C.inputs_mlp(B=a.B)
         xd, yd = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
         for _ in range(a.steps):
