@@ -266,7 +266,7 @@ def attach_cpu_path(line, T, C, args):
     ex = line.get("extra", {})
     pairs = (("mlp_b8192_1gpu", "config4_mlp_b8192"), ("mlp_b8192_1gpu_3xtf32", "config4_mlp_b8192"),
              ("mlp_b8192_1gpu_simt", "config4_mlp_b8192"), ("mlp_dp_global65536", "config5_mlp_global65536"),
-             ("mlp_dp_global65536_3xtf32", "config5_mlp_global65536"),
+             ("mlp_dp_global65536_3xtf32", "config5_mlp_global65536"), ("conv3x3_n32c64h56", "conv3x3_n32c64h56"),
              ("logreg_n600", "config1_logreg_n600"))
     for ours, ref in pairs:
         if isinstance(ex.get(ours), dict) and "e2e" in tab.get(ref, {}):
@@ -358,6 +358,27 @@ def bench_lstm(T, lib_holder, steps=10):
         out[name] = {"hidden": H, "steps": L, "batch": 20, "ms_per_batch": round(ms, 3),
                      "words_per_s": round(20 * L / (ms * 1e-3), 1)}
         del step, dev
+    return out
+
+
+def bench_conv(T, lib_holder, steps=10):
+    """Convolution layer training step (tools/ref_bench.conv_graph: 3x3, pad 1,
+    N=32 C=K=64 56x56, forward + grad_w + grad_x + SGD) at TF32 and 3xTF32."""
+    import torch
+    from tools import ref_bench as R
+    x, f0 = R.conv_inputs()
+    xd = torch.from_numpy(x).cuda()
+    lib = lib_holder()
+    out = {"shape": dict(R.CONV), "flop_per_step": R.CONV_FLOP}
+    for mode in ("auto", "3xtf32"):
+        ins, outs, ups = R.conv_graph(T, f0)
+        f = T.compile(ins, outs, updates=ups, gemm_mode=mode)
+        for _ in range(3):
+            f.call_device(xd)
+        ms = time_device_block(lambda: f.call_device(xd), lib, f._stream, steps)
+        out["tf32" if mode == "auto" else mode] = {"ms_per_step": round(ms, 3),
+                                                   "tflops": round(R.CONV_FLOP / (ms * 1e-3) / 1e12, 1)}
+        del f
     return out
 
 
@@ -630,6 +651,10 @@ def main():
                                     "e2e_us_per_step": round(e2e_l * 1e6, 1), "launches_per_step": nl}
         except Exception as e:
             extra["logreg_n600"] = {"error": repr(e)[:300]}
+        try:
+            extra["conv3x3_n32c64h56"] = bench_conv(T, lib_holder)
+        except Exception as e:
+            extra["conv3x3_n32c64h56"] = {"error": repr(e)[:300]}
         try:
             extra["lstm_ptb_words_per_s"] = bench_lstm(T, lib_holder)
         except Exception as e:

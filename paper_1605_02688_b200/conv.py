@@ -154,8 +154,7 @@ class Conv2d(Op):
             K, _, kh, kw = f.shape
             _, _, Ho, Wo = out.shape
             f = _contig(plan, f)
-            cols = plan.scratch((N * Ho * Wo, C * kh * kw), x.dtype)
-            self._im2col(plan, x, cols, kh, kw)
+            cols = self._cols(plan, node.inputs[0], x, N * Ho * Wo, C * kh * kw, kh, kw)
             fm = plan.view_of(f, (K, C * kh * kw), (C * kh * kw, 1), f.offset)
             colsT = plan.view_of(cols, (C * kh * kw, N * Ho * Wo), (1, C * kh * kw), 0)
             if N == 1:
@@ -168,6 +167,18 @@ class Conv2d(Op):
             return
         a, dy = plan.layout(node.inputs[0]), plan.layout(node.inputs[1])
         N, K, Ho, Wo = dy.shape
+        if (self.kind == GRAD_INPUTS and self.algo == GEMM and tuple(self.stride) == (1, 1)
+                and self.pad[0] < a.shape[2] and self.pad[1] < a.shape[3]):
+            # stride 1: the input gradient is the forward convolution of dy with
+            # the flipped, channel-transposed filters (pad k-1-p): im2col of dy
+            # and ONE GEMM straight into [N*H*W, C] -- no [N*Ho*Wo, C*kh*kw]
+            # gradient-of-columns matrix and no gather over it (col2im was 324 us
+            # of a 32x64x56x56 3x3 layer's step)
+            f = _contig(plan, a)
+            _, C, kh, kw = f.shape
+            _, _, H, W = out.shape
+            self._grad_inputs_as_conv(plan, f, _contig(plan, dy), out, N, K, C, H, W, kh, kw, mode)
+            return
         dyT = plan.scratch((K, N * Ho * Wo), dy.dtype)
         plan.emit_copy_layouts(plan.view_of(dy, (K, N, Ho * Wo), (dy.strides[1], dy.strides[0], 1), dy.offset)
                                if dy.contiguous() else _contig(plan, dy, (K, N, Ho * Wo), (1, 0, 2)),
@@ -175,8 +186,7 @@ class Conv2d(Op):
         if self.kind == GRAD_WEIGHTS:
             x = a
             _, C, kh, kw = out.shape
-            cols = plan.scratch((N * Ho * Wo, C * kh * kw), x.dtype)
-            self._im2col(plan, x, cols, kh, kw)
+            cols = self._cols(plan, node.inputs[0], x, N * Ho * Wo, C * kh * kw, kh, kw)
             plan.emit_gemm(dyT, cols, plan.view_of(out, (K, C * kh * kw), (C * kh * kw, 1), out.offset), mode)
             return
         f = _contig(plan, a)
@@ -193,9 +203,44 @@ class Conv2d(Op):
             lib.check(lib.lib.tx_col2im(dc, dx, win, Ho, Wo, stream))
         plan.add_launch(launch)
 
+    def _grad_inputs_as_conv(self, plan, f, dy4, out, N, K, C, H, W, kh, kw, mode):
+        # fr[(k, u, v), c] = f[k, c, kh-1-u, kw-1-v]: a negative-stride view copied contiguous
+        fr = plan.scratch((K, kh, kw, C), out.dtype)
+        plan.emit_copy_layouts(plan.view_of(f, (K, kh, kw, C), (C * kh * kw, -kw, -1, kh * kw),
+                                            f.offset + (kh - 1) * kw + (kw - 1)), fr)
+        ph, pw = kh - 1 - self.pad[0], kw - 1 - self.pad[1]
+        cols = plan.scratch((N * H * W, K * kh * kw), out.dtype)
+        lib = plan.lib
+        win = (__import__("ctypes").c_int * 6)(kh, kw, 1, 1, ph, pw)
+        td, tc = plan.tx(dy4), plan.tx(cols)
+
+        def launch(stream):
+            lib.check(lib.lib.tx_im2col(td, tc, win, stream))
+        plan.add_launch(launch)
+        # [N*H*W, K*kh*kw] . [K*kh*kw, C] -> [N*H*W, C], then to NCHW
+        res = plan.scratch((N * H * W, C), out.dtype)
+        plan.emit_gemm(cols, plan.view_of(fr, (K * kh * kw, C), (C, 1), 0), res, mode)
+        plan.emit_copy_layouts(plan.view_of(res, (N, C, H * W), (H * W * C, 1, C), 0),
+                               plan.view_of(out, (N, C, H * W), (C * H * W, H * W, 1), out.offset))
+
     def _win(self, kh, kw):
         import ctypes
         return (ctypes.c_int * 6)(kh, kw, self.stride[0], self.stride[1], self.pad[0], self.pad[1])
+
+    def _cols(self, plan, var, x, rows, ckk, kh, kw):
+        """The patch matrix of variable ``var`` (layout ``x``) for this window,
+        built once per step plan: a layer's forward and its weight gradient
+        read the same matrix (``var`` is live until the later of the two, so
+        its buffer is unchanged; keyed on the variable, not the address, which
+        the arena may hand to another tensor once ``var`` is dead)."""
+        cache = plan.__dict__.setdefault("_im2col_cache", {})
+        key = (var.id, x.shape, x.strides, kh, kw, tuple(self.stride), tuple(self.pad))
+        cols = cache.get(key)
+        if cols is None:
+            cols = plan.scratch((rows, ckk), x.dtype)
+            self._im2col(plan, x, cols, kh, kw)
+            cache[key] = cols
+        return cols
 
     def _im2col(self, plan, x, cols, kh, kw):
         lib = plan.lib

@@ -170,6 +170,42 @@ def config5(tx, reps, G=65536):
             "global_batch": G, "processes": 1, "note": "the reference has no data parallelism: one process"}
 
 
+CONV = dict(N=32, C=64, H=56, W=56, K=64, kh=3, kw=3, pad=(1, 1))
+
+
+def conv_graph(tx, shared_value, lr=1e-3):
+    """A 3x3 convolution layer's training step (SURVEY §8(f)3 shapes: a
+    ResNet conv2_x layer): forward, both gradients, SGD on the filters.
+    ``tx`` is either package (same spelling)."""
+    d = CONV
+    x = tx.tensor4("x", dtype=F32)
+    f = tx.shared(shared_value, name="f")
+    y = tx.conv2d(x, f, stride=(1, 1), pad=d["pad"])
+    cost = tx.sum(y * y) * 1e-6
+    gf, gx = tx.grad(cost, [f, x])
+    return [x], [cost, gx], [(f, f - lr * gf)]
+
+
+def conv_inputs():
+    d = CONV
+    r = np.random.default_rng(7)
+    x = r.standard_normal((d["N"], d["C"], d["H"], d["W"]), dtype=np.float32)
+    f = (r.standard_normal((d["K"], d["C"], d["kh"], d["kw"])) / np.sqrt(d["C"] * 9)).astype(np.float32)
+    return x, f
+
+
+CONV_FLOP = 3 * 2 * CONV["N"] * CONV["K"] * CONV["C"] * CONV["kh"] * CONV["kw"] * CONV["H"] * CONV["W"]
+
+
+def config_conv(tx, reps):
+    x, f0 = conv_inputs()
+    ins, outs, ups = conv_graph(tx, f0)
+    f = tx.compile(ins, outs, updates=ups, preset="fast_run", conv_impl="gemm")
+    e2e, k = _time(f, (x,), reps)
+    return {"unit": "TFLOP/s (fwd + grad_w + grad_x)", "e2e": CONV_FLOP / e2e / 1e12, "kernel": CONV_FLOP / k / 1e12,
+            "e2e_s": e2e, "kernel_s": k, "shape": dict(CONV)}
+
+
 def table(reps=5, only=None):
     """Every config's CPU-path throughput (end-to-end and kernel-only)."""
     tx = load_reference()
@@ -179,7 +215,7 @@ def table(reps=5, only=None):
            "calls": f"1 warm-up + median of {reps}", "host": host_info()}
     for name, fn in (("config1_logreg_n600", config1), ("config2_ew_2p28", config2),
                      ("config3_careduce_16384sq", config3), ("config4_mlp_b8192", config4),
-                     ("config5_mlp_global65536", config5)):
+                     ("config5_mlp_global65536", config5), ("conv3x3_n32c64h56", config_conv)):
         if only and name not in only:
             continue
         t0 = time.perf_counter()
