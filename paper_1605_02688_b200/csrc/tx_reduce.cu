@@ -806,7 +806,8 @@ static int run(const tx_tensor& x, uint32_t mask, tx_tensor& y, char* ws, size_t
   }
   TX_CUDA(cudaGetLastError());
   if constexpr (OP == TX_MAX && (std::is_same<T, float>::value || std::is_same<T, double>::value)) {
-    if (p.K > 0 && p.R > 0) {
+    static const bool off = getenv("TX_NO_MAX_ZERO_SIGN") != nullptr;  // A/B diagnostics only
+    if (p.K > 0 && p.R > 0 && !off) {
       max_zero_sign<T><<<(unsigned)((p.K + 127) / 128), 128, 0, st>>>(xp, p.K, p.R, p.gm, out);
       TX_CUDA(cudaGetLastError());
     }

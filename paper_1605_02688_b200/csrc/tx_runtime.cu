@@ -2,6 +2,8 @@
 // graph capture (the VM's replacement for the reference's per-node Python
 // loop, runtime.py:428-446), async copies and a strided copy kernel.
 #include <cuda_runtime.h>
+#include <algorithm>
+#include <cstdlib>
 
 #include <cstring>
 #include <mutex>
@@ -126,6 +128,8 @@ __global__ void __launch_bounds__(256) transpose_copy_kernel(const T* __restrict
 template <typename T>
 __global__ void __launch_bounds__(256) row_copy_kernel(const T* __restrict__ src, T* __restrict__ dst, TileMeta m,
                                                        int64_t nrows) {
+  // blockIdx.y: a 1024-element chunk of the row (4 independent copies per thread)
+  const int64_t i0 = (int64_t)blockIdx.y * 1024 + threadIdx.x;
   for (int64_t row = blockIdx.x; row < nrows; row += gridDim.x) {
     int64_t r = row, so = 0, dof = 0;
     for (int d = m.nb - 1; d >= 0; --d) {
@@ -134,7 +138,11 @@ __global__ void __launch_bounds__(256) row_copy_kernel(const T* __restrict__ src
       so += c * m.bs[d];
       dof += c * m.bd[d];
     }
-    for (int64_t i = threadIdx.x; i < m.sp; i += blockDim.x) dst[dof + i] = src[so + i];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t i = i0 + 256 * k;
+      if (i < m.sp) dst[dof + i] = src[so + i];
+    }
   }
 }
 
@@ -160,7 +168,10 @@ static int launch_copy(const tx_tensor* s, tx_tensor* d, cudaStream_t st) {
   if (sp.ndim == 0) {  // scalar
     m.v[0] = 1; m.v[1] = 0; m.v[2] = 0; sp.ndim = 1;
   }
-  if (sizeof(T) >= 4 && sp.ndim >= 2 && n >= (1 << 16)) {
+  static const bool generic_only = getenv("TX_COPY_GENERIC") != nullptr;  // A/B diagnostics
+  // (small copies -- the LSTM's per-step reorders -- stay on the generic
+  // kernel: its one-thread-per-element grid hides latency better there)
+  if (sizeof(T) >= 4 && sp.ndim >= 2 && n >= (1 << 21) && !generic_only) {
     int p = -1, q = -1;
     for (int i = 0; i < sp.ndim; ++i) {
       if (sp.strides[0][i] == 1 && sp.shape[i] > 1) p = i;
@@ -191,7 +202,8 @@ static int launch_copy(const tx_tensor* s, tx_tensor* d, cudaStream_t st) {
       }
     }
     const int last = sp.ndim - 1;
-    if (sp.strides[0][last] == 1 && sp.strides[1][last] == 1 && sp.shape[last] >= 64) {
+    if (sp.strides[0][last] == 1 && sp.strides[1][last] == 1 && sp.shape[last] >= 64 &&
+        (sp.shape[last] + 1023) / 1024 <= 65535) {
       TileMeta t;
       t.sp = sp.shape[last];
       t.nb = last;
@@ -203,8 +215,10 @@ static int launch_copy(const tx_tensor* s, tx_tensor* d, cudaStream_t st) {
         nrows *= sp.shape[i];
       }
       const int64_t cap = (int64_t)sm_count() * 16;
-      row_copy_kernel<T><<<(unsigned)(nrows < cap ? nrows : cap), 256, 0, st>>>((const T*)s->data, (T*)d->data, t,
-                                                                               nrows);
+      const int64_t gy = (t.sp + 1023) / 1024;
+      const int64_t gx = std::max<int64_t>(1, std::min<int64_t>(nrows, cap / std::max<int64_t>(gy, 1) + 1));
+      row_copy_kernel<T><<<dim3((unsigned)std::min<int64_t>(gx, 65535 * 16), (unsigned)std::min<int64_t>(gy, 65535)),
+                           256, 0, st>>>((const T*)s->data, (T*)d->data, t, nrows);
       TX_CUDA(cudaGetLastError());
       return TX_OK;
     }
