@@ -72,6 +72,8 @@ int tx_event_destroy(void* ev);
 int tx_event_record(void* ev, void* stream);
 int tx_stream_wait_event(void* stream, void* ev);
 int tx_event_elapsed_ms(void* start, void* stop, float* ms);
+/* Block the calling host thread until the event has completed. */
+int tx_event_sync(void* ev);
 /* kind: 0 H2D, 1 D2H, 2 D2D (all async on stream) */
 int tx_memcpy_async(void* dst, const void* src, size_t bytes, int kind, void* stream);
 int tx_memset_async(void* dst, int value, size_t bytes, void* stream);

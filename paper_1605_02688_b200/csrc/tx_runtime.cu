@@ -309,6 +309,7 @@ int tx_stream_wait_event(void* s, void* ev) {
   TX_CUDA(cudaStreamWaitEvent((cudaStream_t)s, (cudaEvent_t)ev, 0));
   return TX_OK;
 }
+int tx_event_sync(void* ev) { TX_CUDA(cudaEventSynchronize((cudaEvent_t)ev)); return TX_OK; }
 int tx_event_elapsed_ms(void* a, void* b, float* ms) {
   TX_CUDA(cudaEventElapsedTime(ms, (cudaEvent_t)a, (cudaEvent_t)b));
   return TX_OK;

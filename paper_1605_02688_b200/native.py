@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libtexpr_b2
 EXPORTS = [
     "tx_version", "tx_last_error", "tx_init", "tx_device_info", "tx_stream_create", "tx_stream_destroy",
     "tx_stream_sync", "tx_event_create", "tx_event_destroy", "tx_event_record", "tx_stream_wait_event",
-    "tx_event_elapsed_ms", "tx_memcpy_async", "tx_memset_async", "tx_host_register", "tx_host_unregister",
+    "tx_event_elapsed_ms", "tx_event_sync", "tx_memcpy_async", "tx_memset_async", "tx_host_register", "tx_host_unregister",
     "tx_device_alloc", "tx_device_free",
     "tx_graph_begin", "tx_graph_end", "tx_graph_launch", "tx_graph_destroy", "tx_copy",
     "tx_ew_compile", "tx_ew_check", "tx_ew_launch", "tx_ew_destroy",
@@ -72,6 +72,7 @@ class Library:
             "tx_stream_create": [P(vp)], "tx_stream_destroy": [vp], "tx_stream_sync": [vp],
             "tx_event_create": [P(vp)], "tx_event_destroy": [vp], "tx_event_record": [vp, vp],
             "tx_stream_wait_event": [vp, vp], "tx_event_elapsed_ms": [vp, vp, P(ctypes.c_float)],
+            "tx_event_sync": [vp],
             "tx_memcpy_async": [vp, vp, sz, ctypes.c_int, vp], "tx_memset_async": [vp, ctypes.c_int, sz, vp],
             "tx_host_register": [vp, sz], "tx_host_unregister": [vp],
             "tx_device_alloc": [sz, P(vp)], "tx_device_free": [vp],
@@ -139,6 +140,9 @@ class Library:
 
     def stream_wait_event(self, s, e):
         self.check(self.lib.tx_stream_wait_event(s, e))
+
+    def event_sync(self, e):
+        self.check(self.lib.tx_event_sync(e))
 
     def elapsed_ms(self, a, b) -> float:
         ms = ctypes.c_float()
