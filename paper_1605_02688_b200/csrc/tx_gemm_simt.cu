@@ -666,6 +666,41 @@ __global__ void __launch_bounds__(256) streamk_fixup_kernel(const float* __restr
   const int64_t n0 = (int64_t)nb * bn + (threadIdx.x & 63) * 4;
   const int64_t MN = M * N;
   const int npieces = c1 - c0 + 1;
+  // 128-bit form: the 4 adjacent columns of a thread as one float4 per piece
+  // (r01: the scalar form moved 36.8 MB in 28.7 us, 1.3 TB/s)
+  const bool v4 = scn == 1 && (scm & 3) == 0 && (N & 3) == 0 && ((uintptr_t)C & 15) == 0 && ((uintptr_t)P & 15) == 0 &&
+                  n0 + 4 <= N && n0 + 4 <= (int64_t)nb * bn + bn;
+  if (v4) {
+    float4 acc[4];
+    int64_t rows[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      rows[i] = (int64_t)mb * bm + (int64_t)blockIdx.y * 16 + (threadIdx.x >> 6) + 4 * i;
+      acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    const bool slab_ok = (int64_t)blockIdx.y * 16 < bm;
+    for (int q = 0; q < npieces; ++q) {  // pieces in k order; the 4 rows' loads are independent
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if (rows[i] < M && slab_ok) {
+          const float4 p = __ldcs(reinterpret_cast<const float4*>(P + q * MN + rows[i] * N + n0));
+          acc[i].x += p.x; acc[i].y += p.y; acc[i].z += p.z; acc[i].w += p.w;
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int64_t m = rows[i];
+      if (m >= M || !slab_ok) continue;
+      float4 o;
+      o.x = epi.apply(acc[i].x, m, n0);
+      o.y = epi.apply(acc[i].y, m, n0 + 1);
+      o.z = epi.apply(acc[i].z, m, n0 + 2);
+      o.w = epi.apply(acc[i].w, m, n0 + 3);
+      *reinterpret_cast<float4*>(C + m * scm + n0) = o;
+    }
+    return;
+  }
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int64_t m = (int64_t)mb * bm + (int64_t)blockIdx.y * 16 + (threadIdx.x >> 6) + 4 * i;
