@@ -555,3 +555,35 @@ def test_user_plugin_op_with_host_perform_runs_as_host_step():
     assert plan.host_ops == 1 and plan.graph is None
     rep = T.verify_grad([x], [y], [xv], rel_tol=1e-6)
     assert rep.passed, str(rep)
+
+
+def test_host_plugin_op_inside_a_loop_body():
+    """A perform-only plugin op inside a scan body: the loop's step plans and
+    the enclosing step run eagerly (no graph capture), results match."""
+    from paper_1605_02688_b200.graph import apply
+    from paper_1605_02688_b200.op import Op
+
+    class HostHalf(Op):
+        name = "host_half_fixture"
+
+        def infer_types(self, input_types):
+            return [input_types[0]]
+
+        def perform(self, inputs, output_buffers=None):
+            return [inputs[0] * 0.5]
+
+    xs = T.matrix("xs", dtype="float64")
+    h0 = T.vector("h0", dtype="float64")
+    hist, _ = T.scan(lambda x, h: apply(HostHalf(), [T.tanh(h + x)])[0], sequences=[xs], initial_states=[h0])
+    out = hist[0] if isinstance(hist, (list, tuple)) else hist
+    f = T.compile([xs, h0], [out])
+    xv = np.random.default_rng(1).standard_normal((5, 3))
+    got = f(xv, np.zeros(3))[0]
+    h, want = np.zeros(3), []
+    for t in range(5):
+        h = np.tanh(h + xv[t]) * 0.5
+        want.append(h)
+    np.testing.assert_allclose(got, np.array(want), rtol=1e-12)
+    for _ in range(2):
+        np.testing.assert_allclose(f(xv, np.zeros(3))[0], np.array(want), rtol=1e-12)
+    assert next(iter(f._plans.values())).graph is None
