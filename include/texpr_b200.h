@@ -131,6 +131,11 @@ enum { TX_SUM = 0, TX_MAX = 1, TX_ARGMAX_ONEHOT = 2, TX_ARGMAX_INDEX = 3 };
  * dcols -> dx[N,C,H,W] contiguous, each element the sum of its taps in
  * (u, v) order (deterministic).  The contractions are tx_gemm calls. */
 int tx_im2col(const tx_tensor* x, tx_tensor* cols, const int* win, void* stream);
+/* The same patch matrix with the columns in (u, v, c) order --
+ * cols[N*Ho*Wo, kh*kw*C] -- for a channel-contiguous input (x given as the
+ * [N,C,H,W] view of NHWC memory, channel stride 1): every gather and store
+ * is a run along c (128-bit when C % 4 == 0). */
+int tx_im2col_hwc(const tx_tensor* x, tx_tensor* cols, const int* win, void* stream);
 int tx_col2im(const tx_tensor* dcols, tx_tensor* dx, const int* win, int64_t Ho, int64_t Wo, void* stream);
 
 /* NaN guard (reference diagnostics.py:52-88 nan_guard_check, hooked per node

@@ -155,6 +155,11 @@ class Conv2d(Op):
             _, _, Ho, Wo = out.shape
             f = _contig(plan, f)
             cols = self._cols(plan, node.inputs[0], x, N * Ho * Wo, C * kh * kw, kh, kw)
+            if self.algo == GEMM:
+                # (u, v, c) patch order: the filters reordered to [K, kh, kw, C]
+                fr = plan.scratch((K, kh, kw, C), f.dtype)
+                plan.emit_copy_layouts(plan.view_of(f, (K, kh, kw, C), (C * kh * kw, kw, 1, kh * kw), f.offset), fr)
+                f = fr
             fm = plan.view_of(f, (K, C * kh * kw), (C * kh * kw, 1), f.offset)
             colsT = plan.view_of(cols, (C * kh * kw, N * Ho * Wo), (1, C * kh * kw), 0)
             if N == 1:
@@ -187,6 +192,12 @@ class Conv2d(Op):
             x = a
             _, C, kh, kw = out.shape
             cols = self._cols(plan, node.inputs[0], x, N * Ho * Wo, C * kh * kw, kh, kw)
+            if self.algo == GEMM:  # (u, v, c) patch order: dW as [K, kh, kw, C], then to [K, C, kh, kw]
+                gr = plan.scratch((K, kh, kw, C), out.dtype)
+                plan.emit_gemm(dyT, plan.view_of(cols, (N * Ho * Wo, C * kh * kw), (C * kh * kw, 1), 0),
+                               plan.view_of(gr, (K, C * kh * kw), (C * kh * kw, 1), 0), mode)
+                plan.emit_copy_layouts(plan.view_of(gr, (K, C, kh, kw), (C * kh * kw, 1, kw * C, C), 0), out)
+                return
             plan.emit_gemm(dyT, cols, plan.view_of(out, (K, C * kh * kw), (C * kh * kw, 1), out.offset), mode)
             return
         f = _contig(plan, a)
@@ -204,20 +215,23 @@ class Conv2d(Op):
         plan.add_launch(launch)
 
     def _grad_inputs_as_conv(self, plan, f, dy4, out, N, K, C, H, W, kh, kw, mode):
-        # fr[(k, u, v), c] = f[k, c, kh-1-u, kw-1-v]: a negative-stride view copied contiguous
-        fr = plan.scratch((K, kh, kw, C), out.dtype)
-        plan.emit_copy_layouts(plan.view_of(f, (K, kh, kw, C), (C * kh * kw, -kw, -1, kh * kw),
+        # fr[(u, v, k), c] = f[k, c, kh-1-u, kw-1-v]: a negative-stride view copied
+        # contiguous, in the (u, v, k) patch order of the channel-contiguous dy
+        fr = plan.scratch((kh, kw, K, C), out.dtype)
+        plan.emit_copy_layouts(plan.view_of(f, (kh, kw, K, C), (-kw, -1, C * kh * kw, kh * kw),
                                             f.offset + (kh - 1) * kw + (kw - 1)), fr)
         ph, pw = kh - 1 - self.pad[0], kw - 1 - self.pad[1]
+        Nn, Kk, Ho, Wo = dy4.shape
+        dyh = self._hwc(plan, None, dy4)
         cols = plan.scratch((N * H * W, K * kh * kw), out.dtype)
         lib = plan.lib
         win = (__import__("ctypes").c_int * 6)(kh, kw, 1, 1, ph, pw)
-        td, tc = plan.tx(dy4), plan.tx(cols)
+        td, tc = plan.tx(dyh), plan.tx(cols)
 
         def launch(stream):
-            lib.check(lib.lib.tx_im2col(td, tc, win, stream))
+            lib.check(lib.lib.tx_im2col_hwc(td, tc, win, stream))
         plan.add_launch(launch)
-        # [N*H*W, K*kh*kw] . [K*kh*kw, C] -> [N*H*W, C], then to NCHW
+        # [N*H*W, kh*kw*K] . [kh*kw*K, C] -> [N*H*W, C], then to NCHW
         res = plan.scratch((N * H * W, C), out.dtype)
         plan.emit_gemm(cols, plan.view_of(fr, (K * kh * kw, C), (C, 1), 0), res, mode)
         plan.emit_copy_layouts(plan.view_of(res, (N, C, H * W), (H * W * C, 1, C), 0),
@@ -234,13 +248,37 @@ class Conv2d(Op):
         its buffer is unchanged; keyed on the variable, not the address, which
         the arena may hand to another tensor once ``var`` is dead)."""
         cache = plan.__dict__.setdefault("_im2col_cache", {})
-        key = (var.id, x.shape, x.strides, kh, kw, tuple(self.stride), tuple(self.pad))
+        hwc = self.algo == GEMM
+        key = (var.id, x.shape, x.strides, kh, kw, tuple(self.stride), tuple(self.pad), hwc)
         cols = cache.get(key)
         if cols is None:
             cols = plan.scratch((rows, ckk), x.dtype)
-            self._im2col(plan, x, cols, kh, kw)
+            if hwc:
+                # (u, v, c) columns from a channel-contiguous copy of x: every
+                # gather and store runs along c, 128-bit (r02: the (c, u, v)
+                # gather over NCHW was L1-wavefront bound at 91 us for 231 MB)
+                xh = self._hwc(plan, var, x)
+                lib, win = plan.lib, self._win(kh, kw)
+                tx_, tc = plan.tx(xh), plan.tx(cols)
+
+                def launch(stream):
+                    lib.check(lib.lib.tx_im2col_hwc(tx_, tc, win, stream))
+                plan.add_launch(launch)
+            else:
+                self._im2col(plan, x, cols, kh, kw)
             cache[key] = cols
         return cols
+
+    def _hwc(self, plan, var, x):
+        """[N, C, H, W] view of a channel-contiguous (NHWC) copy of ``x`` (x
+        itself when its channel stride is already 1)."""
+        if x.strides[1] == 1:
+            return x
+        N, C, H, W = x.shape
+        dst = plan.scratch((N, H, W, C), x.dtype)
+        plan.emit_copy_layouts(plan.view_of(x, (N, H, W, C), (x.strides[0], x.strides[2], x.strides[3], x.strides[1]),
+                                            x.offset), dst)
+        return plan.view_of(dst, (N, C, H, W), (H * W * C, 1, W * C, C), 0)
 
     def _im2col(self, plan, x, cols, kh, kw):
         lib = plan.lib

@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <type_traits>
 
 #include "tx_common.h"
 
@@ -78,6 +79,48 @@ __global__ void __launch_bounds__(256) im2col_rows(const T* __restrict__ x, T* _
       T val = T(0);
       if (h >= 0 && h < g.H && w >= 0 && w < g.W) val = xc[sbase[rr] + (int64_t)h * g.xs[2] + (int64_t)w * g.xs[3]];
       out[(int64_t)rr * ckk] = val;
+    }
+  }
+}
+
+// (u, v, c) column order over a channel-contiguous input: thread t of the
+// CTA handles VEC consecutive channels of one (u, v) for 16 output pixels,
+// so loads and stores run along c (one 128-bit access per thread when VEC = 4).
+template <class T, int VEC>
+__global__ void __launch_bounds__(256) im2col_hwc_rows(const T* __restrict__ x, T* __restrict__ cols, ConvGeom g,
+                                                       int64_t rows) {
+  __shared__ int64_t sbase[IM2COL_RB];
+  __shared__ int sh0[IM2COL_RB], sw0[IM2COL_RB];
+  const int64_t row0 = (int64_t)blockIdx.x * IM2COL_RB;
+  if (threadIdx.x < IM2COL_RB) {
+    const int64_t row = row0 + threadIdx.x;
+    const int64_t n = row / (g.Ho * g.Wo), p = row - n * (g.Ho * g.Wo);
+    const int64_t i = p / g.Wo, j = p - i * g.Wo;
+    sbase[threadIdx.x] = n * g.xs[0];
+    sh0[threadIdx.x] = (int)(i * g.sh - g.ph);
+    sw0[threadIdx.x] = (int)(j * g.sw - g.pw);
+  }
+  __syncthreads();
+  const int C = (int)g.C;
+  const int ckk = C * g.kh * g.kw;
+  const int nr = (int)min((int64_t)IM2COL_RB, rows - row0);
+  using V = typename std::conditional<VEC == 4 && sizeof(T) == 4, float4, T>::type;
+  for (int col = threadIdx.x * VEC; col < ckk; col += blockDim.x * VEC) {
+    const int uv = col / C, c = col - uv * C;
+    const int u = uv / g.kw, v = uv - u * g.kw;
+    const T* xc = x + c;  // channel stride 1
+    T* out = cols + row0 * ckk + col;
+#pragma unroll 4
+    for (int rr = 0; rr < nr; ++rr) {
+      const int h = sh0[rr] + u, w = sw0[rr] + v;
+      const bool in = h >= 0 && h < g.H && w >= 0 && w < g.W;
+      const T* src = xc + sbase[rr] + (int64_t)h * g.xs[2] + (int64_t)w * g.xs[3];
+      if constexpr (VEC == 4 && sizeof(T) == 4) {
+        const float4 val = in ? *reinterpret_cast<const float4*>(src) : make_float4(0.f, 0.f, 0.f, 0.f);
+        *reinterpret_cast<float4*>(out + (int64_t)rr * ckk) = val;
+      } else {
+        out[(int64_t)rr * ckk] = in ? *src : T(0);
+      }
     }
   }
 }
@@ -157,6 +200,36 @@ int tx_im2col(const tx_tensor* x, tx_tensor* cols, const int* win, void* stream)
     im2col_kernel<double><<<(unsigned)grid_for(total), 256, 0, st>>>((const double*)x->data, (double*)cols->data, g, total);
   else
     return fail(TX_E_UNSUPPORTED, "tx_im2col: float32/float64 only");
+  TX_CUDA(cudaGetLastError());
+  return TX_OK;
+}
+
+int tx_im2col_hwc(const tx_tensor* x, tx_tensor* cols, const int* win, void* stream) {
+  TX_CHECK(x && cols && win && x->dtype == cols->dtype, TX_E_ARG, "tx_im2col_hwc: bad arguments");
+  TX_CHECK(cols->ndim == 2 && is_contiguous(*cols), TX_E_ARG, "tx_im2col_hwc: cols must be contiguous");
+  TX_CHECK(x->ndim == 4 && x->strides[1] == 1, TX_E_ARG, "tx_im2col_hwc: the channel dim must be contiguous");
+  ConvGeom g;
+  const int64_t Ho = (x->shape[2] + 2 * win[4] - win[0]) / win[2] + 1;
+  const int64_t Wo = (x->shape[3] + 2 * win[5] - win[1]) / win[3] + 1;
+  int rc = geom(x, win, Ho, Wo, &g);
+  if (rc) return rc;
+  TX_CHECK(cols->shape[0] == g.N * Ho * Wo && cols->shape[1] == g.C * g.kh * g.kw, TX_E_ARG,
+           "tx_im2col_hwc: cols shape");
+  TX_CHECK(g.C * g.kh * g.kw < (int64_t)INT32_MAX, TX_E_ARG, "tx_im2col_hwc: too many columns");
+  const int64_t rows = cols->shape[0];
+  if (rows == 0 || g.C == 0) return TX_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const unsigned rb = (unsigned)((rows + IM2COL_RB - 1) / IM2COL_RB);
+  const bool v4 = x->dtype == TX_F32 && g.C % 4 == 0 && ((uintptr_t)x->data & 15) == 0 &&
+                  ((uintptr_t)cols->data & 15) == 0 && g.xs[0] % 4 == 0 && g.xs[2] % 4 == 0 && g.xs[3] % 4 == 0;
+  if (v4)
+    im2col_hwc_rows<float, 4><<<rb, 256, 0, st>>>((const float*)x->data, (float*)cols->data, g, rows);
+  else if (x->dtype == TX_F32)
+    im2col_hwc_rows<float, 1><<<rb, 256, 0, st>>>((const float*)x->data, (float*)cols->data, g, rows);
+  else if (x->dtype == TX_F64)
+    im2col_hwc_rows<double, 1><<<rb, 256, 0, st>>>((const double*)x->data, (double*)cols->data, g, rows);
+  else
+    return fail(TX_E_UNSUPPORTED, "tx_im2col_hwc: float32/float64 only");
   TX_CUDA(cudaGetLastError());
   return TX_OK;
 }
