@@ -119,7 +119,7 @@ class CpuFunction:
         # the reference has no GEMM epilogues: keep its node list
         run_preset(self.fg, preset, exclude=tuple(exclude) + (
             "fuse_gemm_epilogue", "fuse_narrow_grad", "loop_pushout_sequences", "loop_pushout_accumulators",
-            "loop_pushout_outputs", "loop_drop_unused_outputs"))
+            "loop_pushout_outputs", "loop_drop_unused_outputs", "add_into_zero_inc", "loop_body_zero_inc_chains"))
         self.in_vars = [repl[v] for v in inputs]
         self.sh_vars = [repl[v] for v in found]
         self.n_out = len(outs)

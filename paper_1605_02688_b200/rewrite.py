@@ -387,6 +387,39 @@ def add_zero(fgraph, node, ctx):
     return None
 
 
+def _is_zeros(v) -> bool:
+    """A zero tensor: a zero constant or ``zeros_like`` (second(x, 0))."""
+    if isinstance(v, Constant):
+        return _all_eq(v, 0)
+    n = v.owner
+    return (n is not None and getattr(n.op, "kernel", None) == "second" and isinstance(n.inputs[1], Constant)
+            and _all_eq(n.inputs[1], 0))
+
+
+@register_rewrite("add_into_zero_inc", "canonicalize", "local")
+def add_into_zero_inc(fgraph, node, ctx):
+    """add(X, inc_subtensor(zeros, v, region)) -> inc_subtensor(X, v, region)
+    (B200-specific, not a reference rewrite).  ``grad`` of k slices of one
+    tensor -- the LSTM's four gates -- gives a sum of k region-embedded
+    gradients, each a full zero tensor plus a region; as a chain of
+    inc_subtensors the planner updates one buffer in place (k region adds)
+    instead of materialising k full tensors and summing them.  Values are
+    unchanged (X + 0 = X off the region) up to the sign of a -0.0 in X."""
+    from .shaping import IncSubtensor, inc_subtensor
+    if _kernel(node) != "add":
+        return None
+    out = node.outputs[0]
+    for i in (0, 1):
+        inc, other = node.inputs[i], node.inputs[1 - i]
+        n = inc.owner
+        if n is None or not isinstance(n.op, IncSubtensor) or not _is_zeros(n.inputs[0]):
+            continue
+        if other.type != out.type or inc.type != out.type or len(fgraph.node_clients(inc)) != 1:
+            continue
+        return [(out, inc_subtensor(other, n.inputs[1], n.op.items))]
+    return None
+
+
 @register_rewrite("mul_one", "canonicalize", "local")
 def mul_one(fgraph, node, ctx):
     if _kernel(node) != "mul":
