@@ -313,6 +313,122 @@ class IncSubtensor(Op):
         return cls(tuple(i if isinstance(i, int) else tuple(i) for i in payload["items"]))
 
 
+def _as_index(items):
+    return tuple(i if isinstance(i, int) else slice(*i) for i in items)
+
+
+@register_op
+class ZeroEmbed(Op):
+    """zeros of ``template``'s shape with each value added into its region:
+    ``inc_subtensor(...inc_subtensor(zeros_like(template), v0, r0)..., vk, rk)``
+    as one node (B200-specific; built by ``scan.loop_body_zero_embed`` from
+    the region-embedded gradient sums ``grad`` writes, e.g. the LSTM's four
+    gate gradients).  When the regions partition the output at plan time,
+    each value's producer writes straight into its region (``StepPlan``
+    places it) and the node costs nothing; otherwise it zero-fills and adds.
+    ``expand`` gives the reference-op chain for portable saves."""
+
+    name = "zero_embed"
+
+    def __init__(self, regions):
+        self.regions = tuple(tuple(_norm_item(i) for i in items) for items in regions)
+
+    @property
+    def display_name(self):
+        return f"zero_embed[{len(self.regions)}]"
+
+    def attrs_key(self):
+        return (self.regions,)
+
+    def infer_types(self, input_types):
+        target = input_types[0]
+        for items, value in zip(self.regions, input_types[1:]):
+            IncSubtensor(items).infer_types([target, value])
+        return [target]
+
+    def infer_shape(self, node, input_shapes):
+        return [input_shapes[0]]
+
+    def check_runtime_shapes(self, node, shapes):
+        for items, v in zip(self.regions, shapes[1:]):
+            IncSubtensor(items).check_runtime_shapes(node, [shapes[0], v])
+
+    def partition(self, shape):
+        """Whether the regions (at this concrete shape) are disjoint, cover the
+        whole tensor, and each value fills its region exactly."""
+        cover = np.zeros(shape, dtype=np.int32) if int(np.prod(shape, dtype=np.int64)) <= (1 << 22) else None
+        if cover is None:
+            return False
+        for items in self.regions:
+            cover[_as_index(items)] += 1
+        return bool(np.all(cover == 1))
+
+    def grad(self, inputs, output_grads):
+        (v,) = output_grads
+        out = [DISCONNECTED]
+        for items, x in zip(self.regions, inputs[1:]):
+            out.append(apply(Subtensor(items), [v])[0] if is_float(x.type.dtype) else DISCONNECTED)
+        return out
+
+    def rop(self, inputs, input_perturbations):
+        from .elemwise import zeros_like
+        dvs = input_perturbations[1:]
+        if all(d is None for d in dvs):
+            return [None]
+        acc = zeros_like(inputs[0])
+        for items, d in zip(self.regions, dvs):
+            if d is not None:
+                acc = inc_subtensor(acc, d, items)
+        return [acc]
+
+    def expand(self, inputs):
+        """The reference-op form: zeros_like(template) and a chain of inc_subtensors."""
+        from .elemwise import zeros_like
+        acc = zeros_like(inputs[0])
+        for items, v in zip(self.regions, inputs[1:]):
+            acc = inc_subtensor(acc, v, items)
+        return [acc]
+
+    def fold(self, values):
+        out = np.zeros(np.shape(values[0]), dtype=np.asarray(values[0]).dtype)
+        for items, v in zip(self.regions, values[1:]):
+            out[_as_index(items)] += v
+        return [out]
+
+    def lower(self, node, plan):
+        from .elemwise import EwProgram
+        out = node.outputs[0]
+        lo = plan.layout(out)
+        placed = plan.placed.get(node.id, ()) if hasattr(plan, "placed") else ()
+        part = self.partition(lo.shape)
+        if not part:
+            plan.emit_fill_zero(lo)
+        dt = out.type.dtype
+        for k, (items, v) in enumerate(zip(self.regions, node.inputs[1:])):
+            if k in placed:
+                continue  # its producer wrote the region already
+            lv = plan.layout(v)
+            shape, strides, off = _slice_geometry(items, lo.shape, lo.strides, lo.offset)
+            if 0 in shape:
+                continue
+            region = plan.view_of(lo, shape, strides, off)
+            vs = [0] * len(shape)
+            for j in range(1, len(lv.shape) + 1):
+                vs[-j] = 0 if lv.shape[-j] == 1 else lv.strides[-j]
+            if part:
+                plan.emit_copy_layouts(plan.view_of(lv, shape, tuple(vs), lv.offset), region)
+            else:
+                plan.emit_elementwise_tx(EwProgram.single("add", [dt, dt]), [plan.tx(region)],
+                                         [plan.tx(region), plan.tx(lv, shape, tuple(vs))])
+
+    def attrs_payload(self, encode_graph=None):
+        return {"regions": [[i if isinstance(i, int) else list(i) for i in items] for items in self.regions]}
+
+    @classmethod
+    def from_payload(cls, payload, decode_graph=None):
+        return cls(tuple(tuple(i if isinstance(i, int) else tuple(i) for i in items) for items in payload["regions"]))
+
+
 def inc_subtensor(target: Variable, value: Variable, items) -> Variable:
     return apply(IncSubtensor(items), [target, value])[0]
 

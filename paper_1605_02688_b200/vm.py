@@ -770,6 +770,37 @@ class StepPlan:
             if wsb:
                 self.ws[n.id] = (Storage("arena", wsb, name="ws"), wsb)
 
+        # ---- placement: a ZeroEmbed whose regions partition its output has
+        # each value's producer write straight into its region (the producer
+        # output becomes a strided view of the embed's storage): the LSTM BPTT
+        # body assembles dz from four gate gradients with no copies at all
+        self.placed = {}
+        placed_st = set()
+        if not fn.has_lazy and fn.nan_guard is None:
+            from .shaping import ZeroEmbed, _slice_geometry
+            out_ids = {v.id for v in g.outputs}
+            for n in order:
+                if not isinstance(n.op, ZeroEmbed):
+                    continue
+                lo = self.lay[n.outputs[0].id]
+                if lo.storage.kind not in ("arena", "bound") or not lo.contiguous() or not n.op.partition(lo.shape):
+                    continue
+                ks = set()
+                for k, (items, v) in enumerate(zip(n.op.regions, n.inputs[1:])):
+                    p = v.owner
+                    if (p is None or not isinstance(p.op, (Elemwise, Composite)) or v.id in out_ids
+                            or v.id in partial_ids or len(g.node_clients(v)) != 1 or v in n.inputs[k + 2:]
+                            or self.lay[v.id].storage.kind != "arena"):
+                        continue
+                    shape, strides, off = _slice_geometry(items, lo.shape, lo.strides, lo.offset)
+                    if tuple(shape) != tuple(self.lay[v.id].shape):
+                        continue
+                    self.lay[v.id] = Layout(lo.storage, off, shape, strides, v.type.dtype)
+                    ks.add(k)
+                if ks:
+                    self.placed[n.id] = ks
+                    placed_st.add(id(lo.storage))
+
         # ---- tail: output snapshots, contiguous copies, update commits
         written = set()
         self.commits = []      # (src Layout, dst Layout)
@@ -885,7 +916,7 @@ class StepPlan:
             taken = set()
             is_inc = isinstance(n.op, IncSubtensor)
             inplace_ok = (isinstance(n.op, (Elemwise, Composite)) or is_inc) and fn.nan_guard is None \
-                and not fn.has_lazy
+                and not fn.has_lazy and not any(id(self.lay[o.id].storage) in placed_st for o in n.outputs)
             for o in n.outputs:
                 ol = self.lay[o.id]
                 st = ol.storage
@@ -1126,6 +1157,18 @@ class StepPlan:
         return Layout(lay.storage, offset, shape, strides, lay.dtype)
 
     # -- emitters ---------------------------------------------------------------
+    def emit_fill_zero(self, lay: Layout):
+        """Zero a contiguous layout (memset) -- ZeroEmbed without a partition."""
+        lib = self.lib
+        nb = lay.numel * ITEMSIZE[lay.dtype]
+        if not lay.contiguous():
+            raise NotSupported("zero fill of a strided layout")
+        ptr = self.ptr_of(lay)
+
+        def launch(stream):
+            lib.memset(ptr, 0, nb, stream)
+        self.add_launch(launch)
+
     def emit_copy_layouts(self, src: Layout, dst: Layout):
         """Strided device copy src -> dst (same shape), attributed to the
         node being lowered."""

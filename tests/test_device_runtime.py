@@ -587,3 +587,35 @@ def test_host_plugin_op_inside_a_loop_body():
     for _ in range(2):
         np.testing.assert_allclose(f(xv, np.zeros(3))[0], np.array(want), rtol=1e-12)
     assert next(iter(f._plans.values())).graph is None
+
+
+@pytest.mark.parametrize("regions", [
+    (((None, None, None), (0, 3, None)), ((None, None, None), (3, 5, None)), ((None, None, None), (5, 8, None))),
+    (((None, None, None), (0, 3, None)), ((None, None, None), (5, 8, None))),            # a gap: zero-filled
+    (((None, None, None), (0, 5, None)), ((None, None, None), (3, 8, None))),            # overlap: summed
+])
+def test_zero_embed_placement_and_fallback(regions):
+    """ZeroEmbed (the LSTM's gate-gradient assembly): a partition has its
+    producers write straight into their regions; gaps and overlaps take the
+    zero-fill + add path.  Values equal the inc_subtensor chain over zeros."""
+    from paper_1605_02688_b200.graph import apply
+    from paper_1605_02688_b200.shaping import ZeroEmbed
+    x = T.matrix("x", dtype="float64")
+    vals = [T.matrix(f"v{k}", dtype="float64") for k in range(len(regions))]
+    ze = apply(ZeroEmbed(regions), [x] + [T.tanh(v) * 2.0 for v in vals])[0]
+    f = T.compile([x] + vals, [ze * 1.0 + 0.0])
+    rng = np.random.default_rng(3)
+    xv = rng.standard_normal((4, 8))
+    vv = [rng.standard_normal((4, r[1][1] - r[1][0])) for r in regions]
+    got = f(xv, *vv)[0]
+    want = np.zeros((4, 8))
+    for r, v in zip(regions, vv):
+        want[:, r[1][0]:r[1][1]] += np.tanh(v) * 2.0
+    np.testing.assert_allclose(got, want, rtol=1e-12, atol=1e-15)
+    plan = next(iter(f._plans.values()))
+    ze_nodes = [n for n in f.order if n.op.name == "zero_embed"]
+    assert ze_nodes
+    assert bool(plan.placed.get(ze_nodes[0].id)) == (len(regions) == 3)
+    # its portable (reference-op) form round-trips through a saved container
+    g = T.load(f.save())
+    np.testing.assert_allclose(g(xv, *vv)[0], want, rtol=1e-12, atol=1e-15)
