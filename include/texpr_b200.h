@@ -175,12 +175,15 @@ enum {
  *   SGD             C = w[m,n] - alpha * acc                sub(w, mul(lr, dot)): the SGD update of a
  *                                                           weight from its gradient GEMM (C may alias w) */
 enum { TX_EPI_NONE = 0, TX_EPI_BIAS = 1, TX_EPI_BIAS_TANH = 2, TX_EPI_MUL_1MSQR = 3, TX_EPI_BIAS_TANH_DUAL = 4,
-       TX_EPI_MUL_AUX = 5, TX_EPI_SGD = 6 };
+       TX_EPI_MUL_AUX = 5, TX_EPI_SGD = 6, TX_EPI_ADD_AUX_BIAS = 7 };
+/*   ADD_AUX_BIAS    C = b[n] + (g[m,n] + acc)                  add(b, add(g, dot)): a recurrent layer's
+ *                                                              pre-activation (input projection g) */
 typedef struct tx_epilogue {
   int32_t kind;
-  tx_tensor aux;  /* BIAS*: bias row [N]; MUL_* / SGD: [M,N] operand */
+  tx_tensor aux;  /* BIAS*: bias row [N]; MUL_* / SGD / ADD_AUX_BIAS: [M,N] operand */
   tx_tensor out2; /* BIAS_TANH_DUAL: second output [M,N] */
   double alpha;   /* SGD: the learning rate */
+  tx_tensor aux2; /* ADD_AUX_BIAS: bias row [N] */
 } tx_epilogue;
 int tx_gemm_workspace(const tx_tensor* A, const tx_tensor* B, const tx_tensor* C, int mode,
                       size_t* bytes);

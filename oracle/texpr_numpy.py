@@ -228,6 +228,8 @@ def run_node(node, args):
         return [dot(*args)]
     if name == "dot_epilogue":  # the device's fused form of dot + its consumer
         z = dot(args[0], args[1])
+        if op.kind == 7:
+            return [elemwise("add", [args[3], elemwise("add", [args[2], z])])]
         if op.kind == 1:
             return [elemwise("add", [args[2], z])]
         if op.kind == 4:

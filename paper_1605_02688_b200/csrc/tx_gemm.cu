@@ -35,9 +35,18 @@ int build(const tx_tensor* A, const tx_tensor* B, const tx_tensor* C, const tx_e
   g->scn = C->shape[1] == 1 ? 1 : C->strides[1];
   if (epi && epi->kind != TX_EPI_NONE) {
     TX_CHECK(epi->aux.dtype == A->dtype, TX_E_ARG, "tx_gemm: epilogue operand dtype");
-    TX_CHECK(epi->kind >= TX_EPI_BIAS && epi->kind <= TX_EPI_SGD, TX_E_ARG, "tx_gemm: unknown epilogue");
+    TX_CHECK(epi->kind >= TX_EPI_BIAS && epi->kind <= TX_EPI_ADD_AUX_BIAS, TX_E_ARG, "tx_gemm: unknown epilogue");
     int64_t s0 = 0, s1 = 0;
-    if (epi->kind == TX_EPI_MUL_1MSQR || epi->kind == TX_EPI_MUL_AUX || epi->kind == TX_EPI_SGD) {
+    if (epi->kind == TX_EPI_ADD_AUX_BIAS) {
+      const tx_tensor& b = epi->aux2;
+      TX_CHECK(b.dtype == A->dtype && b.ndim >= 1 && b.shape[b.ndim - 1] == g->N, TX_E_ARG,
+               "tx_gemm: ADD_AUX_BIAS bias must end in N");
+      g->epi_f.aux2 = (const float*)b.data;
+      g->epi_d.aux2 = (const double*)b.data;
+      g->epi_f.b1 = g->epi_d.b1 = b.shape[b.ndim - 1] == 1 ? 0 : b.strides[b.ndim - 1];
+    }
+    if (epi->kind == TX_EPI_MUL_1MSQR || epi->kind == TX_EPI_MUL_AUX || epi->kind == TX_EPI_SGD ||
+        epi->kind == TX_EPI_ADD_AUX_BIAS) {
       TX_CHECK(epi->aux.ndim == 2 && epi->aux.shape[0] == g->M && epi->aux.shape[1] == g->N, TX_E_ARG,
                "tx_gemm: epilogue operand must be [M,N]");
       s0 = epi->aux.strides[0];
@@ -238,6 +247,8 @@ G transposed(const G& g) {
   std::swap(t.epi_d.s0, t.epi_d.s1);
   std::swap(t.epi_f.o0, t.epi_f.o1);
   std::swap(t.epi_d.o0, t.epi_d.o1);
+  std::swap(t.epi_f.b0, t.epi_f.b1);
+  std::swap(t.epi_d.b0, t.epi_d.b1);
   return t;
 }
 

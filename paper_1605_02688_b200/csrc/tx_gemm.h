@@ -20,6 +20,8 @@ struct Epi {
   T* out2 = nullptr;
   int64_t o0 = 0, o1 = 0;  // out2 strides
   T alpha = T(0);          // SGD learning rate
+  const T* aux2 = nullptr; // ADD_AUX_BIAS: the bias row
+  int64_t b0 = 0, b1 = 0;  // its strides (b1 along n; swapped with C^T = B^T A^T)
   __device__ __forceinline__ T apply(T acc, int64_t m, int64_t n) const;
 };
 
@@ -39,6 +41,7 @@ __device__ __forceinline__ float Epi<float>::apply(float acc, int64_t m, int64_t
     }
     case TX_EPI_MUL_AUX: return __fmul_rn(acc, aux[m * s0 + n * s1]);
     case TX_EPI_SGD: return __fsub_rn(aux[m * s0 + n * s1], __fmul_rn(alpha, acc));
+    case TX_EPI_ADD_AUX_BIAS: return __fadd_rn(aux2[m * b0 + n * b1], __fadd_rn(aux[m * s0 + n * s1], acc));
   }
   return acc;
 }
@@ -59,6 +62,7 @@ __device__ __forceinline__ double Epi<double>::apply(double acc, int64_t m, int6
     }
     case TX_EPI_MUL_AUX: return __dmul_rn(acc, aux[m * s0 + n * s1]);
     case TX_EPI_SGD: return __dsub_rn(aux[m * s0 + n * s1], __dmul_rn(alpha, acc));
+    case TX_EPI_ADD_AUX_BIAS: return __dadd_rn(aux2[m * b0 + n * b1], __dadd_rn(aux[m * s0 + n * s1], acc));
   }
   return acc;
 }

@@ -658,6 +658,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
                 for (int i = 0; i < 32; ++i) v[i] = tanhf(v[i]);
               }
+            } else if (E.kind == TX_EPI_ADD_AUX_BIAS) {  // b[n] + (g[m,n] + acc), per element
+              if (row_ok) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                  if (n + i < p.N) v[i] = E.apply(v[i], row, n + i);
+              }
             } else if (row_ok && !(CG == 2 && p.tma_aux) && E.kind == TX_EPI_SGD) {
               if (n + 32 <= p.N && E.s1 == 1 && (E.s0 % 4) == 0 && ((uintptr_t)E.aux & 15) == 0) {
                 const float* g = E.aux + (int64_t)row * E.s0 + n;
@@ -756,6 +762,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     __fsub_rn(1.0f, __fmul_rn(v[i], v[i])), __fsub_rn(1.0f, __fmul_rn(v[i + 1], v[i + 1])),
                     __fsub_rn(1.0f, __fmul_rn(v[i + 2], v[i + 2])), __fsub_rn(1.0f, __fmul_rn(v[i + 3], v[i + 3])));
             }
+          } else if (E.kind == TX_EPI_ADD_AUX_BIAS) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = E.apply(v[i], row, n + i);
           } else if (E.kind == TX_EPI_SGD) {
             const float* g = E.aux + (int64_t)row * E.s0 + n;
 #pragma unroll

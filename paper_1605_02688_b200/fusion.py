@@ -213,6 +213,23 @@ def _match_bias_tanh_dual(prog, z_idx):
     return float(prog.consts[r3[0][1]][1]) == 1.0
 
 
+def _match_add_aux_bias(prog, z_idx):
+    """{t0 = add(g, z); t1 = add(b, t0)} with output t1, g a second [M,N]
+    operand and b a row: a recurrent layer's pre-activation
+    (x-projection + h.W + bias).  Returns (g index, b index) or None."""
+    nodes = prog.nodes
+    if len(nodes) != 2 or len(prog.in_dtypes) != 3 or prog.outputs != (("node", 1),):
+        return None
+    (k0, r0, _), (k1, r1, _) = nodes
+    if k0 != "add" or k1 != "add" or ("in", z_idx) not in r0 or ("node", 0) not in r1:
+        return None
+    g = [r for r in r0 if r != ("in", z_idx)]
+    b = [r for r in r1 if r != ("node", 0)]
+    if len(g) != 1 or len(b) != 1 or g[0][0] != "in" or b[0][0] != "in" or g[0][1] == b[0][1]:
+        return None
+    return g[0][1], b[0][1]
+
+
 def _sole_dot_client(fgraph, z, Dot):
     """z = dot(a, b) feeding exactly one consumer (and not a graph output)."""
     if z.owner is None or not isinstance(z.owner.op, Dot) or fgraph.is_output(z):
@@ -364,7 +381,7 @@ def _fuse_narrow_grads(fgraph, emit) -> int:
 
 @register_rewrite("fuse_gemm_epilogue", "abstract_select", "global")
 def fuse_gemm_epilogue(fgraph, ctx, emit) -> int:
-    from .linalg import EPI_BIAS, EPI_BIAS_TANH_DUAL, EPI_MUL_AUX, Dot, DotEpilogue
+    from .linalg import EPI_ADD_AUX_BIAS, EPI_BIAS, EPI_BIAS_TANH_DUAL, EPI_MUL_AUX, Dot, DotEpilogue
     applied = _fuse_tanh_layers(fgraph, emit) + _fuse_sgd_updates(fgraph, ctx, emit)
     for d in list(fgraph.toposort()):
         if d.id not in fgraph.nodes or not isinstance(d.op, Dot):
@@ -379,7 +396,14 @@ def fuse_gemm_epilogue(fgraph, ctx, emit) -> int:
         if len(clients) != 1 or len(fgraph.clients[z]) != 1:
             continue
         c = clients[0]
-        kind, aux = None, None
+        kind, aux, extra = None, None, []
+        if isinstance(c.op, Composite) and len(c.inputs) == 3 and z in c.inputs and c.inputs.count(z) == 1:
+            m = _match_add_aux_bias(c.op.program, c.inputs.index(z))
+            if m is not None:
+                g, bias = c.inputs[m[0]], c.inputs[m[1]]
+                if (g.type.dtype == bias.type.dtype == z.type.dtype and g.type.broadcastable == (False, False)
+                        and bias.type.ndim == 1 and not bias.type.broadcastable[0]):
+                    kind, aux, extra = EPI_ADD_AUX_BIAS, g, [bias]
         if isinstance(c.op, Composite) and len(c.inputs) == 2 and z in c.inputs:
             zi = c.inputs.index(z)
             other = c.inputs[1 - zi]
@@ -396,7 +420,7 @@ def fuse_gemm_epilogue(fgraph, ctx, emit) -> int:
                 kind, aux = EPI_BIAS, other
         if kind is None:
             continue
-        outs = apply(DotEpilogue(kind), [a, b, aux])
+        outs = apply(DotEpilogue(kind), [a, b, aux] + extra)
         if [o.type for o in outs] != [o.type for o in c.outputs]:
             continue
         fgraph.replace_all(list(zip(c.outputs, outs)), "fuse_gemm_epilogue")

@@ -93,8 +93,10 @@ def dot(a: Variable, b: Variable) -> Variable:
 
 # epilogue kinds (include/texpr_b200.h TX_EPI_*)
 EPI_BIAS, EPI_BIAS_TANH, EPI_MUL_1MSQR, EPI_BIAS_TANH_DUAL, EPI_MUL_AUX, EPI_SGD = 1, 2, 3, 4, 5, 6
+EPI_ADD_AUX_BIAS = 7
 _EPI_NAMES = {EPI_BIAS: "bias", EPI_BIAS_TANH: "bias_tanh", EPI_MUL_1MSQR: "mul_1msqr",
-              EPI_BIAS_TANH_DUAL: "bias_tanh_dual", EPI_MUL_AUX: "mul_aux", EPI_SGD: "sgd"}
+              EPI_BIAS_TANH_DUAL: "bias_tanh_dual", EPI_MUL_AUX: "mul_aux", EPI_SGD: "sgd",
+              EPI_ADD_AUX_BIAS: "add_aux_bias"}
 
 
 @register_op
@@ -112,6 +114,8 @@ class DotEpilogue(Op):
       mul_aux         out = (a.b) * aux
       sgd             out = aux - alpha * (a.b)      (a weight's SGD update from its gradient GEMM;
                                                       the output may be written in place over aux)
+      add_aux_bias    out = bias[n] + (aux + a.b)    (inputs a, b, aux, bias: a recurrent
+                                                      pre-activation with its input projection)
     """
 
     name = "dot_epilogue"
@@ -135,7 +139,7 @@ class DotEpilogue(Op):
         return (self.kind, self.alpha, self.alpha_dtype)
 
     def infer_types(self, input_types):
-        a, b, aux = input_types
+        a, b, aux = input_types[:3]
         (t,) = Dot().infer_types([a, b])
         if self.kind == EPI_BIAS_TANH_DUAL:
             return [t, t]
@@ -152,6 +156,9 @@ class DotEpilogue(Op):
             ok = len(aux) >= 1 and aux[-1] == out[-1] and all(d == 1 for d in aux[:-1])
         else:
             ok = aux == tuple(out)
+        if ok and self.kind == EPI_ADD_AUX_BIAS:
+            bias = tuple(shapes[3])
+            ok = len(bias) >= 1 and bias[-1] == out[-1] and all(d == 1 for d in bias[:-1])
         if not ok:
             raise ShapeMismatch(f"{self.display_name}: operand shape {aux} does not broadcast to {tuple(out)}")
 
@@ -168,8 +175,10 @@ class DotEpilogue(Op):
         same scalar operations in the same order as the epilogue -- used to
         save portable graphs (``serialize.portable_outputs``)."""
         from .elemwise import make
-        a, b, aux = inputs
+        a, b, aux = inputs[:3]
         z = dot(a, b)
+        if self.kind == EPI_ADD_AUX_BIAS:
+            return [make("add", [inputs[3], make("add", [aux, z])])]
         if self.kind == EPI_BIAS:
             return [make("add", [aux, z])]
         if self.kind == EPI_BIAS_TANH:
@@ -192,6 +201,8 @@ class DotEpilogue(Op):
         epi.kind = self.kind
         epi.aux = plan.tx(node.inputs[2])
         epi.alpha = self.alpha
+        if self.kind == EPI_ADD_AUX_BIAS:
+            epi.aux2 = plan.tx(node.inputs[3])
         if self.kind == EPI_BIAS_TANH_DUAL:
             epi.out2 = plan.tx(node.outputs[1])
         plan.emit_dot(node, epilogue=epi)

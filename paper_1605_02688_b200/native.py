@@ -36,10 +36,12 @@ class TxTensor(ctypes.Structure):
 
 
 class TxEpilogue(ctypes.Structure):
-    _fields_ = [("kind", ctypes.c_int32), ("aux", TxTensor), ("out2", TxTensor), ("alpha", ctypes.c_double)]
+    _fields_ = [("kind", ctypes.c_int32), ("aux", TxTensor), ("out2", TxTensor), ("alpha", ctypes.c_double),
+                ("aux2", TxTensor)]
 
 
 EPI_NONE, EPI_BIAS, EPI_BIAS_TANH, EPI_MUL_1MSQR, EPI_BIAS_TANH_DUAL, EPI_MUL_AUX, EPI_SGD = 0, 1, 2, 3, 4, 5, 6
+EPI_ADD_AUX_BIAS = 7
 GEMM_AUTO, GEMM_SIMT, GEMM_TC, GEMM_3XTF32 = 0, 1, 2, 3
 
 

@@ -519,3 +519,23 @@ def test_signed_zero_max_inside_row_fusion(K):
     assert next(iter(f._plans.values())).row_groups, "expected a fused row region"
     exact(got_m, np.maximum.accumulate(z, axis=1)[:, -1])
     np.testing.assert_allclose(got_p, T.compile([v], [p], row_fusion=False)(z)[0], rtol=1e-6, atol=1e-7)
+
+
+@pytest.mark.parametrize("M,N,K", [(8, 64, 32), (20, 800, 200), (20, 2400, 600), (300, 520, 784)])
+def test_dot_add_aux_bias_epilogue_bit_exact(M, N, K, rng):
+    """x.W + g + b (a recurrent pre-activation with its input projection g):
+    fused into the GEMM epilogue as b + (g + acc) -- the same two IEEE adds
+    as the unfused composite, so the result is bit-identical on every path
+    (transposed skinny M <= 16, thin tcgen05 tiles, the regular tiles)."""
+    x = rng.standard_normal((M, K)).astype(np.float32)
+    W = rng.standard_normal((K, N)).astype(np.float32)
+    g = rng.standard_normal((M, N)).astype(np.float32)
+    b = rng.standard_normal(N).astype(np.float32)
+    vx, vw = T.matrix("x", dtype="float32"), T.matrix("w", dtype="float32")
+    vg, vb = T.matrix("g", dtype="float32"), T.vector("b", dtype="float32")
+    expr = (vg + T.dot(vx, vw)) + vb
+    f = T.compile([vx, vw, vg, vb], expr)
+    assert "dot+add_aux_bias" in [getattr(n.op, "display_name", n.op.name) for n in f.order]
+    u = T.compile([vx, vw, vg, vb], expr, exclude=("fuse_gemm_epilogue",))
+    assert "dot+add_aux_bias" not in [getattr(n.op, "display_name", n.op.name) for n in u.order]
+    np.testing.assert_array_equal(f(x, W, g, b), u(x, W, g, b))
