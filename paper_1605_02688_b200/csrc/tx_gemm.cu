@@ -231,6 +231,10 @@ void choose(const G& g, int mode, int* path, int* kind) {
   if (g.K <= 16) { *path = PATH_SKINNY; *kind = SK_OUTER; return; }
   if (g.N <= 16 && g.sak == 1) { *path = PATH_SKINNY; *kind = SK_ROWDOT; return; }
   if (g.N <= 16 && g.sam == 1) { *path = PATH_SKINNY; *kind = SK_KRED; return; }
+  static const bool no_smallm = getenv("TX_GEMM_NO_SMALLM") != nullptr;
+  if (mode == TX_GEMM_AUTO && g.M <= SMALLM_MAX_M && g.N * g.K <= SMALLM_MAX_NK && !no_smallm) {
+    *path = PATH_SKINNY; *kind = SK_SMALLM; return;
+  }
   if (gemm_tc_eligible(g) == TX_OK) { *path = PATH_TC; return; }
   *path = PATH_SIMT;
 }

@@ -82,7 +82,12 @@ struct G {
 };
 
 enum { PATH_SIMT = 0, PATH_SKINNY = 1, PATH_TC = 2 };
-enum { SK_ROWDOT = 0, SK_OUTER = 1, SK_KRED = 2 };
+enum { SK_ROWDOT = 0, SK_OUTER = 1, SK_KRED = 2, SK_SMALLM = 3 };
+// AUTO-mode products with M <= SMALLM_MAX_M and a B of at most SMALLM_MAX_NK
+// elements take the SIMT small-M kernel (beyond that B streams from HBM and
+// the tensor cores' FLOP headroom wins)
+constexpr int SMALLM_MAX_M = 32;
+constexpr int64_t SMALLM_MAX_NK = 1LL << 21;
 
 int gemm_simt(const G& g, cudaStream_t st);
 int gemm_skinny(const G& g, int kind, void* ws, size_t wsb, cudaStream_t st);

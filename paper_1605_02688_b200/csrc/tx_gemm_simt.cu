@@ -4,6 +4,7 @@
 //
 // Replaces np.dot for those shapes (reference ops/linalg.py:42-62); the
 // tensor-core path for large fp32 problems is tx_gemm_tc.cu.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <cstdlib>
 
@@ -624,6 +625,210 @@ static int launch_kred(const G& g, void* ws, size_t wsb, cudaStream_t st) {
   return TX_OK;
 }
 
+
+// ------------------------------------------------ M <= 32: few rows, any N, K
+// The recurrent products of an unrolled scan (h.W_h, dz.W_h^T: M = the
+// minibatch, 20 in the LSTM configs) are too thin for a 128-row tcgen05 tile:
+// the tensor-core kernel's fixed cost (TMEM allocation, barrier set-up, one
+// k-block pipeline fill, TMEM drain) was ~10 us per launch on [20 x 800 x 200].
+// Here one CTA owns 32 output columns (one per lane) and a K range; its 8
+// warps take interleaved groups of 8 k-rows.  A is staged per 256-row piece
+// in shared memory as [m][k] rows (16-byte cp.async when A is K-contiguous),
+// read back as broadcast float4s along k, so the accumulator count is M
+// rounded up to 4 (no padding to a tile).  Every load of a piece (this
+// warp's <= 4 B groups: 128-byte coalesced rows for N-major B, two 16-byte
+// vectors per lane for K-major B) is issued before its first use.  The K
+// range is split over a thread-block cluster (<= 8 CTAs); the column blocks'
+// partials are summed by rank 0 through distributed shared memory in rank
+// order and the fused epilogue is applied: one launch, deterministic, exact
+// fp32 FMAs (tighter than the TF32 tensor-core path it replaces).
+constexpr int SMM_THREADS = 256;
+constexpr int SMM_KP = 128;       // k rows per staged A piece
+constexpr int SMM_KPP = SMM_KP + 4;  // row pitch (16-byte aligned; spreads the transposing stage's banks)
+
+__device__ __forceinline__ void cp_async_zfill(void* smem, const void* gmem, int bytes, int valid) {
+  if (bytes == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
+                 "l"(gmem), "r"(valid) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
+                 "l"(gmem), "r"(valid) : "memory");
+}
+
+// BMODE 0: N-major B (sbn == 1); 1: K-major B, 16-byte vectors; 2: generic strides.
+// AK: A K-contiguous with 16-byte aligned rows (16-byte staging).
+template <int MT, int BMODE, bool AK>
+__global__ void __launch_bounds__(SMM_THREADS, 2) smallm_kernel(const float* __restrict__ A, const float* __restrict__ B,
+                                                               float* __restrict__ C, int M, int N, int64_t K,
+                                                               int64_t sam, int64_t sak, int64_t sbk, int64_t sbn,
+                                                               int64_t scm, int64_t scn, Epi<float> epi, int64_t kchunk) {
+  constexpr int STAGE = MT * SMM_KPP, RED = 8 * MT * 32;
+  __shared__ __align__(16) float smem[STAGE > RED ? STAGE : RED];
+  __shared__ float part[MT * 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n0 = blockIdx.x * 32;
+  const int n = n0 + lane;
+  const bool nok = n < N;
+  const int64_t klo = (int64_t)blockIdx.y * kchunk;
+  const int64_t khi = klo + kchunk < K ? klo + kchunk : K;
+  float acc[MT];
+#pragma unroll
+  for (int m = 0; m < MT; ++m) acc[m] = 0.f;
+  auto load_b = [&](int64_t k, int avail, float (&b)[8]) {  // k rows [k, k + 8) of column n (zero past `avail`)
+    if (BMODE == 1 && avail >= 8 && nok) {
+      const float4* bp = reinterpret_cast<const float4*>(B + (int64_t)n * sbn + k);
+      const float4 u = __ldg(bp), w = __ldg(bp + 1);
+      b[0] = u.x; b[1] = u.y; b[2] = u.z; b[3] = u.w; b[4] = w.x; b[5] = w.y; b[6] = w.z; b[7] = w.w;
+    } else {
+      const float* bp = B + k * sbk + (BMODE == 0 ? (int64_t)n : (int64_t)n * sbn);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) b[i] = (i < avail && nok) ? __ldg(bp + i * sbk) : 0.f;
+    }
+  };
+  const int g0 = warp * 8;
+  for (int64_t p0 = klo; p0 < khi; p0 += SMM_KP) {
+    const int rows = (int)(khi - p0 < SMM_KP ? khi - p0 : SMM_KP);
+    const int rows8 = (rows + 7) & ~7;  // whole 8-row groups; k in [rows, rows8) stage as zeros
+    float bq[SMM_KP / 64][8];
+#pragma unroll
+    for (int q = 0; q < SMM_KP / 64; ++q)
+      if (g0 + 64 * q < rows) load_b(p0 + g0 + 64 * q, rows - g0 - 64 * q, bq[q]);
+    __syncthreads();  // the previous piece is consumed
+    if (AK) {  // 16-byte chunks of A rows: MT x SMM_KP / 4 chunks
+#pragma unroll
+      for (int u = 0; u < (MT * SMM_KP / 4 + SMM_THREADS - 1) / SMM_THREADS; ++u) {
+        const int e = tid + u * SMM_THREADS;
+        const int m = e / (SMM_KP / 4), c = (e % (SMM_KP / 4)) * 4;
+        if (m < M && c < rows8) {
+          const int valid = rows - c >= 4 ? 16 : (rows > c ? (rows - c) * 4 : 0);
+          cp_async_zfill(smem + m * SMM_KPP + c, valid ? A + (int64_t)m * sam + p0 + c : A, 16, valid);
+        }
+      }
+    } else {
+#pragma unroll 4
+      for (int u = 0; u < MT * SMM_KP / SMM_THREADS; ++u) {
+        const int e = tid + u * SMM_THREADS;
+        int r, m;
+        if (sam == 1) { r = e / MT; m = e - r * MT; }  // A M-contiguous: m fastest
+        else { m = e / SMM_KP; r = e % SMM_KP; }       // k fastest
+        if (m < M && r < rows8) {
+          const bool ok = r < rows;
+          cp_async_zfill(smem + m * SMM_KPP + r, ok ? A + (int64_t)m * sam + (p0 + r) * sak : A, 4, ok ? 4 : 0);
+        }
+      }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < SMM_KP / 64; ++q) {
+      const int g = g0 + 64 * q;
+      if (g >= rows) break;
+#pragma unroll
+      for (int m = 0; m < MT; ++m) {
+        const float4* a4 = reinterpret_cast<const float4*>(smem + m * SMM_KPP + g);
+        const float4 u = a4[0], w = a4[1];
+        float a = acc[m];
+        a = fmaf(u.x, bq[q][0], a); a = fmaf(u.y, bq[q][1], a); a = fmaf(u.z, bq[q][2], a); a = fmaf(u.w, bq[q][3], a);
+        a = fmaf(w.x, bq[q][4], a); a = fmaf(w.y, bq[q][5], a); a = fmaf(w.z, bq[q][6], a); a = fmaf(w.w, bq[q][7], a);
+        acc[m] = a;
+      }
+    }
+  }
+  // warps -> CTA partial (fixed warp order)
+  __syncthreads();
+#pragma unroll
+  for (int m = 0; m < MT; ++m) smem[(warp * MT + m) * 32 + lane] = acc[m];
+  __syncthreads();
+  for (int e = tid; e < MT * 32; e += SMM_THREADS) {
+    float v = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) v += smem[w * MT * 32 + e];
+    part[e] = v;
+  }
+  namespace cg = cooperative_groups;
+  const int cs = (int)gridDim.y;
+  if (cs > 1) {
+    cg::cluster_group cl = cg::this_cluster();
+    cl.sync();
+    if (cl.block_rank() == 0) {
+#pragma unroll 1
+      for (int e = tid; e < MT * 32; e += SMM_THREADS) {
+        const int m = e >> 5, c = n0 + (e & 31);
+        if (m >= M || c >= N) continue;
+        float v = part[e];
+        for (int r = 1; r < cs; ++r) v += cl.map_shared_rank(part, r)[e];
+        C[(int64_t)m * scm + (int64_t)c * scn] = epi.kind != TX_EPI_NONE ? epi.apply(v, m, c) : v;
+      }
+    }
+    cl.sync();  // the other ranks' partials stay resident until rank 0 has read them
+    return;
+  }
+  __syncthreads();
+#pragma unroll 1
+  for (int e = tid; e < MT * 32; e += SMM_THREADS) {
+    const int m = e >> 5, c = n0 + (e & 31);
+    if (m >= M || c >= N) continue;
+    const float v = part[e];
+    C[(int64_t)m * scm + (int64_t)c * scn] = epi.kind != TX_EPI_NONE ? epi.apply(v, m, c) : v;
+  }
+}
+
+template <int MT, int BMODE, bool AK>
+static int launch_smallm_t(const G& g, int cs, int64_t kchunk, cudaStream_t st) {
+  const unsigned strips = (unsigned)((g.N + 31) / 32);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(strips, (unsigned)cs, 1);
+  cfg.blockDim = dim3(SMM_THREADS, 1, 1);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 1;
+  attr[0].val.clusterDim.y = (unsigned)cs;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  TX_CUDA(cudaLaunchKernelEx(&cfg, smallm_kernel<MT, BMODE, AK>, (const float*)g.A, (const float*)g.B, (float*)g.C,
+                             (int)g.M, (int)g.N, g.K, g.sam, g.sak, g.sbk, g.sbn, g.scm, g.scn, g.epi_f, kchunk));
+  return TX_OK;
+}
+
+template <int MT, int BMODE>
+static int launch_smallm_b(const G& g, int cs, int64_t kchunk, cudaStream_t st) {
+  const bool ak = g.sak == 1 && g.sam % 4 == 0 && ((uintptr_t)g.A & 15) == 0;
+  return ak ? launch_smallm_t<MT, BMODE, true>(g, cs, kchunk, st) : launch_smallm_t<MT, BMODE, false>(g, cs, kchunk, st);
+}
+
+template <int MT>
+static int launch_smallm_m(const G& g, int cs, int64_t kchunk, cudaStream_t st) {
+  if (g.sbn == 1) return launch_smallm_b<MT, 0>(g, cs, kchunk, st);
+  if (g.sbk == 1 && g.sbn % 4 == 0 && ((uintptr_t)g.B & 15) == 0) return launch_smallm_b<MT, 1>(g, cs, kchunk, st);
+  return launch_smallm_b<MT, 2>(g, cs, kchunk, st);
+}
+
+static int launch_smallm(const G& g, cudaStream_t st) {
+  // cluster split of K: about two CTAs per SM overall while every warp keeps
+  // >= 32 k-rows (its fixed costs -- staging, reduction -- stay amortised)
+  const int64_t strips = (g.N + 31) / 32;
+  int64_t cs = (2 * (int64_t)sm_count() + strips - 1) / strips;
+  if (cs > 8) cs = 8;
+  if (cs > g.K / 256) cs = g.K / 256;
+  if (cs < 1) cs = 1;
+  int64_t kchunk = (g.K + cs - 1) / cs;
+  kchunk = (kchunk + 7) / 8 * 8;  // pieces start 32-byte aligned along k
+  cs = (g.K + kchunk - 1) / kchunk;
+  switch ((g.M + 3) / 4) {
+    case 1: return launch_smallm_m<4>(g, (int)cs, kchunk, st);
+    case 2: return launch_smallm_m<8>(g, (int)cs, kchunk, st);
+    case 3: return launch_smallm_m<12>(g, (int)cs, kchunk, st);
+    case 4: return launch_smallm_m<16>(g, (int)cs, kchunk, st);
+    case 5: return launch_smallm_m<20>(g, (int)cs, kchunk, st);
+    case 6: return launch_smallm_m<24>(g, (int)cs, kchunk, st);
+    case 7: return launch_smallm_m<28>(g, (int)cs, kchunk, st);
+    default: return launch_smallm_m<32>(g, (int)cs, kchunk, st);
+  }
+}
+
 }  // namespace
 
 int kred_splits(int64_t M, int64_t K) {
@@ -765,6 +970,8 @@ int gemm_skinny(const G& g, int kind, void* ws, size_t wsb, cudaStream_t st) {
       TX_WIDTHS(CASE)
 #undef CASE
     }
+  } else if (kind == SK_SMALLM) {
+    return launch_smallm(g, st);
   } else {
     switch ((int)g.N) {
 #define CASE(w) case w: return launch_kred<w>(g, ws, wsb, st);

@@ -213,6 +213,9 @@ def _match_bias_tanh_dual(prog, z_idx):
     return float(prog.consts[r3[0][1]][1]) == 1.0
 
 
+_NO_AUX_BIAS = bool(__import__("os").environ.get("TX_FUSE_NO_AUX_BIAS"))  # A/B diagnostic
+
+
 def _match_add_aux_bias(prog, z_idx):
     """{t0 = add(g, z); t1 = add(b, t0)} with output t1, g a second [M,N]
     operand and b a row: a recurrent layer's pre-activation
@@ -397,7 +400,8 @@ def fuse_gemm_epilogue(fgraph, ctx, emit) -> int:
             continue
         c = clients[0]
         kind, aux, extra = None, None, []
-        if isinstance(c.op, Composite) and len(c.inputs) == 3 and z in c.inputs and c.inputs.count(z) == 1:
+        if isinstance(c.op, Composite) and len(c.inputs) == 3 and z in c.inputs and c.inputs.count(z) == 1 \
+                and not _NO_AUX_BIAS:
             m = _match_add_aux_bias(c.op.program, c.inputs.index(z))
             if m is not None:
                 g, bias = c.inputs[m[0]], c.inputs[m[1]]

@@ -263,6 +263,8 @@ def _expected_path(M, N, K, ta, tb):
     regression that silently routes eligible products to SIMT fails here."""
     if K <= 16 or N <= 16:
         return 1                       # skinny (outer product / row dot / K reduction)
+    if M <= 32 and N * K <= 1 << 21:
+        return 1                       # few rows: the SIMT small-M kernel (tx_gemm_simt.cu smallm_kernel)
     lead_a = M if ta else K
     lead_b = K if tb else N
     thin_ok = min(M, N) >= 64 or M * N * K >= (1 << 20)
@@ -284,6 +286,41 @@ def test_gemm_3xtf32_layouts(M, N, K, ta, tb, rng):
     got, want, bound = _gemm_case(M, N, K, ta, tb, "3xtf32", rng)
     err = np.abs(got - want)
     assert np.all(err <= 2.0 ** -20 * bound + 1e-7), float((err / (bound + 1e-30)).max())
+
+
+@pytest.mark.parametrize("M,N,K", [(20, 800, 200), (20, 200, 800), (1, 33, 17), (7, 1000, 65), (16, 64, 4096),
+                                   (32, 200, 10000), (20, 3000, 600), (31, 129, 257), (17, 20, 100000)])
+@pytest.mark.parametrize("ta,tb", [(False, False), (False, True), (True, False), (True, True)])
+def test_gemm_small_m(M, N, K, ta, tb, rng):
+    """M <= 32 (an unrolled scan's recurrent products): the SIMT small-M
+    kernel, every operand layout (N-major, K-major and strided B; both A
+    layouts), the cluster split of K (up to 8 CTAs summed through distributed
+    shared memory) and ragged column strips -- exact fp32 FMAs."""
+    assert _gemm_path(M, N, K, ta, tb, 0) == 1
+    got, want, bound = _gemm_case(M, N, K, ta, tb, "auto", rng)
+    assert np.all(np.abs(got - want) <= 1e-5 * bound + 1e-6), float((np.abs(got - want) / (bound + 1e-30)).max())
+
+
+def test_gemm_small_m_strided_and_epilogues(rng):
+    """Strided (non-unit) operand views and every fused epilogue kind on the
+    small-M path, against the unfused graph (bit-exact: the same product
+    followed by the same IEEE round-to-nearest epilogue arithmetic)."""
+    M, N, K = 20, 200, 150
+    x = rng.standard_normal((M, 2 * K)).astype(np.float32)
+    w = rng.standard_normal((K, 3 * N)).astype(np.float32)
+    g = rng.standard_normal((M, N)).astype(np.float32)
+    bias = rng.standard_normal(N).astype(np.float32)
+    vx, vw = T.matrix("x", dtype="float32"), T.matrix("w", dtype="float32")
+    vg, vb = T.matrix("g", dtype="float32"), T.vector("b", dtype="float32")
+    z = T.dot(vx[:, ::2], vw[:, ::3])
+    outs = [z, T.tanh(z + vb), z * vg, z * (1.0 - vg * vg), (vg + z) + vb]
+    fused = T.compile([vx, vw, vg, vb], outs)(x, w, g, bias)
+    plain = T.compile([vx, vw, vg, vb], outs, exclude=("fuse_gemm_epilogue",))(x, w, g, bias)
+    want = x[:, ::2].astype(np.float64) @ w[:, ::3].astype(np.float64)
+    bound = np.abs(x[:, ::2]).astype(np.float64) @ np.abs(w[:, ::3]).astype(np.float64)
+    assert np.all(np.abs(fused[0] - want) <= 1e-5 * bound + 1e-6)
+    for a, b in zip(fused, plain):
+        np.testing.assert_array_equal(a, b)
 
 
 @pytest.mark.parametrize("M,N,K", [(8192, 10, 4096), (600, 10, 784), (8192, 4096, 10), (784, 10, 600),
