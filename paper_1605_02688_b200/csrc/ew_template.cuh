@@ -182,6 +182,7 @@ __device__ __forceinline__ V4<T> tx_ld4b(const T* p, i64 s1) {
 #ifdef TX_KERNELS
 
 extern "C" __global__ void __launch_bounds__(256) tx_ew_flat(const TxEwArgs a) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic dependent launch (tx_common.h)
   TX_PTRS
   int* err = a.err;
   (void)err;
@@ -222,17 +223,39 @@ extern "C" __global__ void __launch_bounds__(256) tx_ew_flat(const TxEwArgs a) {
   }
 }
 
-// rank <= 2: shape[0] rows x shape[1] cols; operand k uses strides[k][0..1]
+// Row-major forms: shape[1] columns (operand column stride strides[k][1]) by
+// rows = e0 * e1 * e2, the row index split into up to three coordinates
+// (c0 < e0 = shape[0], stride strides[k][0]; c1 < e1 = shape[2], strides[k][2];
+// c2 < e2 = shape[3], strides[k][3]; ndim = 2, 3 or 4).  Rank-3/4 spaces
+// that do not collapse to 2-D (a reversed-time view, a [T]-vector broadcast
+// over [T, B, V]) keep the contiguous, vectorised column loop; the row
+// coordinates cost two integer divisions per row, not per element as in
+// tx_ew_nd.
+#define TX_ROWS_DECL                                       \
+  const int e0 = (int)a.shape[0];                          \
+  const int e1 = a.ndim >= 3 ? (int)a.shape[2] : 1;        \
+  const int e2 = a.ndim >= 4 ? (int)a.shape[3] : 1;        \
+  const int rows = e0 * e1 * e2;
+#define TX_ROW_COORDS                                      \
+  int c0 = row, c1 = 0, c2 = 0;                            \
+  if (a.ndim > 2) {                                        \
+    c0 = row % e0;                                         \
+    const int t_ = row / e0;                               \
+    c1 = t_ % e1;                                          \
+    c2 = t_ / e1;                                          \
+  }
 extern "C" __global__ void __launch_bounds__(256) tx_ew_2d(const TxEwArgs a) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic dependent launch (tx_common.h)
   TX_PTRS
   int* err = a.err;
   (void)err;
-  const int rows = (int)a.shape[0];
+  TX_ROWS_DECL
   const int cols = (int)a.shape[1];
   const int col = blockIdx.x * blockDim.x + threadIdx.x;
   if (col >= cols) return;
   for (int row = blockIdx.y; row < rows; row += gridDim.y) {
-#define OFF(k) ((i64)row * a.strides[k][0] + (i64)col * a.strides[k][1])
+    TX_ROW_COORDS
+#define OFF(k) ((i64)c0 * a.strides[k][0] + (i64)c1 * a.strides[k][2] + (i64)c2 * a.strides[k][3] + (i64)col * a.strides[k][1])
 #define IN(k) p##k[OFF(TX_IN_SLOT(k))]
 #define OUT(k, val) q##k[OFF(k)] = (val)
     TX_BODY
@@ -246,16 +269,18 @@ extern "C" __global__ void __launch_bounds__(256) tx_ew_2d(const TxEwArgs a) {
 // rank-2 with the contiguous dim vectorised: every operand has column stride
 // 0 or 1 and 16 B-aligned rows; 4 columns per thread, one row per grid.y step.
 extern "C" __global__ void __launch_bounds__(256) tx_ew_2dv(const TxEwArgs a) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic dependent launch (tx_common.h)
   TX_PTRS
   int* err = a.err;
   (void)err;
-  const int rows = (int)a.shape[0];
+  TX_ROWS_DECL
   const int cols4 = (int)(a.shape[1] >> 2);
   const int c4 = blockIdx.x * blockDim.x + threadIdx.x;
   if (c4 >= cols4) return;
   const i64 col = (i64)c4 << 2;
   for (int row = blockIdx.y; row < rows; row += gridDim.y) {
-#define OFF(k) ((i64)row * a.strides[k][0] + col * a.strides[k][1])
+    TX_ROW_COORDS
+#define OFF(k) ((i64)c0 * a.strides[k][0] + (i64)c1 * a.strides[k][2] + (i64)c2 * a.strides[k][3] + col * a.strides[k][1])
     TX_VDECL
     TX_VLOAD2D
 #pragma unroll
@@ -272,6 +297,7 @@ extern "C" __global__ void __launch_bounds__(256) tx_ew_2dv(const TxEwArgs a) {
 }
 
 extern "C" __global__ void __launch_bounds__(256) tx_ew_nd(const TxEwArgs a) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic dependent launch (tx_common.h)
   TX_PTRS
   int* err = a.err;
   (void)err;

@@ -4,6 +4,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <string>
+#include <utility>
 
 #include "../../include/texpr_b200.h"
 
@@ -68,6 +69,34 @@ struct Space {
 void collapse(int ndim, const int64_t* shape, int nops, const int64_t (*strides)[TX_MAX_RANK], Space* out);
 
 int sm_count();
+
+// ---------------------------------------------- programmatic dependent launch
+// Every kernel of the library starts with TX_GRID_WAIT() (griddepcontrol.wait:
+// returns once the preceding kernel in the stream has completed and its
+// writes are visible; immediately when there is none) and is launched with
+// the programmatic-stream-serialization attribute, so a kernel's launch and
+// CTA rasterisation overlap the tail of its predecessor -- inside captured
+// CUDA graphs too.  The chains of small dependent kernels (an unrolled scan's
+// bodies, the logistic-regression step) are launch-latency bound; this is
+// the gap it closes.  TX_NO_PDL=1 launches plainly (A/B).
+#define TX_GRID_WAIT() asm volatile("griddepcontrol.wait;" ::: "memory")
+bool pdl_enabled();
+
+template <class... KArgs, class... Args>
+inline cudaError_t launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                          Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 // cuTensorMapEncodeTiled through the runtime's driver entry point (nullptr
 // when no driver is present); shared by the GEMM and reduction TMA paths
 void* tmap_encoder();

@@ -25,6 +25,7 @@ struct ConvGeom {
 
 template <class T>
 __global__ void im2col_kernel(const T* __restrict__ x, T* __restrict__ cols, ConvGeom g, int64_t total) {
+  TX_GRID_WAIT();
   const int64_t ckk = g.C * g.kh * g.kw;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t row = e / ckk, col = e - row * ckk;
@@ -53,6 +54,7 @@ constexpr int IM2COL_RB = 16;
 template <class T>
 __global__ void __launch_bounds__(256) im2col_rows(const T* __restrict__ x, T* __restrict__ cols, ConvGeom g,
                                                    int64_t rows) {
+  TX_GRID_WAIT();
   __shared__ int64_t sbase[IM2COL_RB];
   __shared__ int sh0[IM2COL_RB], sw0[IM2COL_RB];
   const int64_t row0 = (int64_t)blockIdx.x * IM2COL_RB;
@@ -89,6 +91,7 @@ __global__ void __launch_bounds__(256) im2col_rows(const T* __restrict__ x, T* _
 template <class T, int VEC>
 __global__ void __launch_bounds__(256) im2col_hwc_rows(const T* __restrict__ x, T* __restrict__ cols, ConvGeom g,
                                                        int64_t rows) {
+  TX_GRID_WAIT();
   __shared__ int64_t sbase[IM2COL_RB];
   __shared__ int sh0[IM2COL_RB], sw0[IM2COL_RB];
   const int64_t row0 = (int64_t)blockIdx.x * IM2COL_RB;
@@ -127,6 +130,7 @@ __global__ void __launch_bounds__(256) im2col_hwc_rows(const T* __restrict__ x, 
 
 template <class T>
 __global__ void col2im_kernel(const T* __restrict__ dcols, T* __restrict__ dx, ConvGeom g, int64_t total) {
+  TX_GRID_WAIT();
   const int64_t ckk = g.C * g.kh * g.kw;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     int64_t t = e;
@@ -191,13 +195,13 @@ int tx_im2col(const tx_tensor* x, tx_tensor* cols, const int* win, void* stream)
   const bool by_rows = g.C * g.kh * g.kw < (int64_t)INT32_MAX && !getenv("TX_IM2COL_FLAT");
   const unsigned rb = (unsigned)((rows + IM2COL_RB - 1) / IM2COL_RB);
   if (x->dtype == TX_F32 && by_rows)
-    im2col_rows<float><<<rb, 256, 0, st>>>((const float*)x->data, (float*)cols->data, g, rows);
+    ::tx::launch(im2col_rows<float>, dim3(rb), dim3(256), 0, st, (const float*)x->data, (float*)cols->data, g, rows);
   else if (x->dtype == TX_F64 && by_rows)
-    im2col_rows<double><<<rb, 256, 0, st>>>((const double*)x->data, (double*)cols->data, g, rows);
+    ::tx::launch(im2col_rows<double>, dim3(rb), dim3(256), 0, st, (const double*)x->data, (double*)cols->data, g, rows);
   else if (x->dtype == TX_F32)
-    im2col_kernel<float><<<(unsigned)grid_for(total), 256, 0, st>>>((const float*)x->data, (float*)cols->data, g, total);
+    ::tx::launch(im2col_kernel<float>, dim3((unsigned)grid_for(total)), dim3(256), 0, st, (const float*)x->data, (float*)cols->data, g, total);
   else if (x->dtype == TX_F64)
-    im2col_kernel<double><<<(unsigned)grid_for(total), 256, 0, st>>>((const double*)x->data, (double*)cols->data, g, total);
+    ::tx::launch(im2col_kernel<double>, dim3((unsigned)grid_for(total)), dim3(256), 0, st, (const double*)x->data, (double*)cols->data, g, total);
   else
     return fail(TX_E_UNSUPPORTED, "tx_im2col: float32/float64 only");
   TX_CUDA(cudaGetLastError());
@@ -223,11 +227,11 @@ int tx_im2col_hwc(const tx_tensor* x, tx_tensor* cols, const int* win, void* str
   const bool v4 = x->dtype == TX_F32 && g.C % 4 == 0 && ((uintptr_t)x->data & 15) == 0 &&
                   ((uintptr_t)cols->data & 15) == 0 && g.xs[0] % 4 == 0 && g.xs[2] % 4 == 0 && g.xs[3] % 4 == 0;
   if (v4)
-    im2col_hwc_rows<float, 4><<<rb, 256, 0, st>>>((const float*)x->data, (float*)cols->data, g, rows);
+    ::tx::launch(im2col_hwc_rows<float, 4>, dim3(rb), dim3(256), 0, st, (const float*)x->data, (float*)cols->data, g, rows);
   else if (x->dtype == TX_F32)
-    im2col_hwc_rows<float, 1><<<rb, 256, 0, st>>>((const float*)x->data, (float*)cols->data, g, rows);
+    ::tx::launch(im2col_hwc_rows<float, 1>, dim3(rb), dim3(256), 0, st, (const float*)x->data, (float*)cols->data, g, rows);
   else if (x->dtype == TX_F64)
-    im2col_hwc_rows<double, 1><<<rb, 256, 0, st>>>((const double*)x->data, (double*)cols->data, g, rows);
+    ::tx::launch(im2col_hwc_rows<double, 1>, dim3(rb), dim3(256), 0, st, (const double*)x->data, (double*)cols->data, g, rows);
   else
     return fail(TX_E_UNSUPPORTED, "tx_im2col_hwc: float32/float64 only");
   TX_CUDA(cudaGetLastError());
@@ -246,9 +250,9 @@ int tx_col2im(const tx_tensor* dcols, tx_tensor* dx, const int* win, int64_t Ho,
   if (total == 0) return TX_OK;
   cudaStream_t st = (cudaStream_t)stream;
   if (dx->dtype == TX_F32)
-    col2im_kernel<float><<<(unsigned)grid_for(total), 256, 0, st>>>((const float*)dcols->data, (float*)dx->data, g, total);
+    ::tx::launch(col2im_kernel<float>, dim3((unsigned)grid_for(total)), dim3(256), 0, st, (const float*)dcols->data, (float*)dx->data, g, total);
   else if (dx->dtype == TX_F64)
-    col2im_kernel<double><<<(unsigned)grid_for(total), 256, 0, st>>>((const double*)dcols->data, (double*)dx->data, g, total);
+    ::tx::launch(col2im_kernel<double>, dim3((unsigned)grid_for(total)), dim3(256), 0, st, (const double*)dcols->data, (double*)dx->data, g, total);
   else
     return fail(TX_E_UNSUPPORTED, "tx_col2im: float32/float64 only");
   TX_CUDA(cudaGetLastError());

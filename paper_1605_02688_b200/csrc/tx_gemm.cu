@@ -105,6 +105,7 @@ template <bool V4>
 __global__ void __launch_bounds__(256) tf32_split_kernel(const float* __restrict__ x, int64_t outer, int64_t inner,
                                                          int64_t so, int64_t si, float* __restrict__ y, int64_t ld,
                                                          int64_t poff, int lo_plane) {
+  TX_GRID_WAIT();
   const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * (V4 ? 4 : 1);
   if (i >= inner) return;
   for (int64_t o = blockIdx.y; o < outer; o += gridDim.y) {
@@ -198,8 +199,8 @@ int split3_prepare(const G& g, void* ws, size_t wsb, cudaStream_t st, G* out, vo
     // ~16 resident blocks per SM in total; rows grid-strided
     const int64_t by = std::max<int64_t>(1, std::min<int64_t>(outer, std::min<int64_t>(65535, (int64_t)sms * 16 / bx + 1)));
     dim3 grid((unsigned)bx, (unsigned)by);
-    if (v4) tf32_split_kernel<true><<<grid, 256, 0, st>>>(x, outer, inner, so, si, y, ld, poff, lo);
-    else tf32_split_kernel<false><<<grid, 256, 0, st>>>(x, outer, inner, so, si, y, ld, poff, lo);
+    if (v4) ::tx::launch(tf32_split_kernel<true>, dim3(grid), dim3(256), 0, st, x, outer, inner, so, si, y, ld, poff, lo);
+    else ::tx::launch(tf32_split_kernel<false>, dim3(grid), dim3(256), 0, st, x, outer, inner, so, si, y, ld, poff, lo);
   };
   // A' = [small | big | big], B' = [big ; small ; big]: the cross terms first
   launch((const float*)g.A, s.a_outer, s.a_inner, s.a_so, s.a_si, Ap, s.a_ld, s.a_poff, 0);

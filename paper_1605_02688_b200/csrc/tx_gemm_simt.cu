@@ -25,6 +25,7 @@ template <class T>
 __global__ void __launch_bounds__(256) simt_gemm(const T* __restrict__ A, const T* __restrict__ B, T* __restrict__ C,
                                                 int64_t M, int64_t N, int64_t K, int64_t sam, int64_t sak,
                                                 int64_t sbk, int64_t sbn, int64_t scm, int64_t scn, Epi<T> epi) {
+  TX_GRID_WAIT();
   __shared__ T As[16][64 + 1];
   __shared__ T Bs[16][64 + 1];
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
@@ -84,6 +85,7 @@ template <int NN, int R>
 __global__ void __launch_bounds__(256) rowdot_kernel(const float* __restrict__ A, const float* __restrict__ B,
                                                     float* __restrict__ C, int64_t M, int N, int64_t K, int64_t sam,
                                                     int64_t sbk, int64_t sbn, int64_t scm, int64_t scn, Epi<float> epi) {
+  TX_GRID_WAIT();
   __shared__ __align__(16) float Bt[NN][RD_KC];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t row0 = ((int64_t)blockIdx.x * 8 + warp) * R;
@@ -182,6 +184,7 @@ __global__ void __launch_bounds__(R >= 8 ? 256 : 512) rowdot_full_kernel(const f
                                                          float* __restrict__ C, int64_t M, int N, int64_t K,
                                                          int64_t sam, int64_t sbk, int64_t sbn, int64_t scm,
                                                          int64_t scn, Epi<float> epi) {
+  TX_GRID_WAIT();
   extern __shared__ __align__(16) float Bs[];  // [K][NN], or Bt [NN][Kp] when TRANS
   const int64_t total = K * NN;
   const int64_t Kp = ((K + 31) & ~(int64_t)31) + 4;
@@ -296,6 +299,7 @@ __global__ void __launch_bounds__(256) outer_kernel(const float* __restrict__ A,
                                                    float* __restrict__ C, int64_t M, int64_t N, int K, int64_t sam,
                                                    int64_t sak, int64_t sbk, int64_t sbn, int64_t scm, int64_t scn,
                                                    Epi<float> epi) {
+  TX_GRID_WAIT();
   __shared__ float As[32][KK];
   const int64_t m0 = (int64_t)blockIdx.y * 32;
   const int64_t n0 = ((int64_t)blockIdx.x * 256 + threadIdx.x) * 4;
@@ -378,6 +382,7 @@ template <int NN>
 __global__ void __launch_bounds__(KR_THREADS) kred_kernel(const float* __restrict__ A, const float* __restrict__ B,
                                                          float* __restrict__ P, int64_t M, int N, int64_t K,
                                                          int64_t sak, int64_t sbk, int64_t sbn, int splits) {
+  TX_GRID_WAIT();
   __shared__ float Bs[KR_KC][NN];
   const int64_t m0 = ((int64_t)blockIdx.x * KR_THREADS + threadIdx.x) * 4;
   const int64_t chunk = (K + splits - 1) / splits;
@@ -459,6 +464,7 @@ template <int NN>
 __global__ void __launch_bounds__(KR_THREADS) kred_ring_kernel(const float* __restrict__ A, const float* __restrict__ B,
                                                               float* __restrict__ P, int64_t M, int N, int64_t K,
                                                               int64_t sak, int64_t sbk, int64_t sbn, int splits) {
+  TX_GRID_WAIT();
   extern __shared__ __align__(16) float4 kr_smem[];
   float4* ring = kr_smem;                                                  // [KR_S*KR_RU][KR_THREADS]
   float* Bs = reinterpret_cast<float*>(kr_smem + KR_S * KR_RU * KR_THREADS);  // [chunk][NN]
@@ -524,6 +530,7 @@ __global__ void __launch_bounds__(KR_THREADS) kred_ring_kernel(const float* __re
 // flight per thread (the adds stay in order, so the result is deterministic)
 __global__ void kred_finalize(const float* __restrict__ P, float* __restrict__ C, int64_t M, int N, int splits,
                               int64_t scm, int64_t scn, Epi<float> epi) {
+  TX_GRID_WAIT();
   int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t MN = M * N;
   if (e >= MN) return;
@@ -557,7 +564,7 @@ static int launch_rowdot_full(const G& g, int threads, size_t smem, cudaStream_t
   const int per_sm = (int)(RDF_MAX_SMEM / (smem + 1024)) > 0 ? (int)(RDF_MAX_SMEM / (smem + 1024)) : 1;
   const int64_t cap = (int64_t)sm_count() * (per_sm < 4 ? per_sm : 4);
   if (blocks > cap) blocks = cap;
-  rowdot_full_kernel<NN, R, TRANS><<<(unsigned)blocks, threads, smem, st>>>((const float*)g.A, (const float*)g.B, (float*)g.C,
+  ::tx::launch(rowdot_full_kernel<NN, R, TRANS>, dim3((unsigned)blocks), dim3(threads), smem, st, (const float*)g.A, (const float*)g.B, (float*)g.C,
                                                                      g.M, (int)g.N, g.K, g.sam, g.sbk, g.sbn, g.scm,
                                                                      g.scn, g.epi_f);
   TX_CUDA(cudaGetLastError());
@@ -585,11 +592,11 @@ static int launch_rowdot(const G& g, cudaStream_t st) {
   }
   if (g.M >= 4096) {
     unsigned blocks = (unsigned)((g.M + 31) / 32);
-    rowdot_kernel<NN, 4><<<blocks, 256, 0, st>>>((const float*)g.A, (const float*)g.B, (float*)g.C, g.M, (int)g.N,
+    ::tx::launch(rowdot_kernel<NN, 4>, dim3(blocks), dim3(256), 0, st, (const float*)g.A, (const float*)g.B, (float*)g.C, g.M, (int)g.N,
                                                  g.K, g.sam, g.sbk, g.sbn, g.scm, g.scn, g.epi_f);
   } else {
     unsigned blocks = (unsigned)((g.M + 7) / 8);
-    rowdot_kernel<NN, 1><<<blocks, 256, 0, st>>>((const float*)g.A, (const float*)g.B, (float*)g.C, g.M, (int)g.N,
+    ::tx::launch(rowdot_kernel<NN, 1>, dim3(blocks), dim3(256), 0, st, (const float*)g.A, (const float*)g.B, (float*)g.C, g.M, (int)g.N,
                                                  g.K, g.sam, g.sbk, g.sbn, g.scm, g.scn, g.epi_f);
   }
   TX_CUDA(cudaGetLastError());
@@ -599,7 +606,7 @@ static int launch_rowdot(const G& g, cudaStream_t st) {
 template <int KK>
 static int launch_outer(const G& g, cudaStream_t st) {
   dim3 grid((unsigned)((g.N + 1023) / 1024), (unsigned)((g.M + 31) / 32));
-  outer_kernel<KK><<<grid, 256, 0, st>>>((const float*)g.A, (const float*)g.B, (float*)g.C, g.M, g.N, (int)g.K, g.sam,
+  ::tx::launch(outer_kernel<KK>, dim3(grid), dim3(256), 0, st, (const float*)g.A, (const float*)g.B, (float*)g.C, g.M, g.N, (int)g.K, g.sam,
                                          g.sak, g.sbk, g.sbn, g.scm, g.scn, g.epi_f);
   TX_CUDA(cudaGetLastError());
   return TX_OK;
@@ -613,13 +620,13 @@ static int launch_kred(const G& g, void* ws, size_t wsb, cudaStream_t st) {
   const int64_t chunk = (g.K + splits - 1) / splits;
   const size_t smem = (size_t)KR_S * KR_RU * KR_THREADS * 16 + (size_t)chunk * NN * 4;
   if (g.M % 4 == 0 && g.sak % 4 == 0 && ((uintptr_t)g.A & 15) == 0 && smem <= 48 * 1024) {
-    kred_ring_kernel<NN><<<grid, KR_THREADS, smem, st>>>((const float*)g.A, (const float*)g.B, (float*)ws, g.M,
+    ::tx::launch(kred_ring_kernel<NN>, dim3(grid), dim3(KR_THREADS), smem, st, (const float*)g.A, (const float*)g.B, (float*)ws, g.M,
                                                          (int)g.N, g.K, g.sak, g.sbk, g.sbn, splits);
   } else
-  kred_kernel<NN><<<grid, KR_THREADS, 0, st>>>((const float*)g.A, (const float*)g.B, (float*)ws, g.M, (int)g.N, g.K, g.sak,
+  ::tx::launch(kred_kernel<NN>, dim3(grid), dim3(KR_THREADS), 0, st, (const float*)g.A, (const float*)g.B, (float*)ws, g.M, (int)g.N, g.K, g.sak,
                                         g.sbk, g.sbn, splits);
   int64_t tot = g.M * g.N;
-  kred_finalize<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>((const float*)ws, (float*)g.C, g.M, (int)g.N, splits,
+  ::tx::launch(kred_finalize, dim3((unsigned)((tot + 255) / 256)), dim3(256), 0, st, (const float*)ws, (float*)g.C, g.M, (int)g.N, splits,
                                                               g.scm, g.scn, g.epi_f);
   TX_CUDA(cudaGetLastError());
   return TX_OK;
@@ -662,6 +669,7 @@ __global__ void __launch_bounds__(SMM_THREADS, 2) smallm_kernel(const float* __r
                                                                float* __restrict__ C, int M, int N, int64_t K,
                                                                int64_t sam, int64_t sak, int64_t sbk, int64_t sbn,
                                                                int64_t scm, int64_t scn, Epi<float> epi, int64_t kchunk) {
+  TX_GRID_WAIT();
   constexpr int STAGE = MT * SMM_KPP, RED = 8 * MT * 32;
   __shared__ __align__(16) float smem[STAGE > RED ? STAGE : RED];
   __shared__ float part[MT * 32];
@@ -781,13 +789,15 @@ static int launch_smallm_t(const G& g, int cs, int64_t kchunk, cudaStream_t st) 
   cfg.blockDim = dim3(SMM_THREADS, 1, 1);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = 1;
   attr[0].val.clusterDim.y = (unsigned)cs;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
   TX_CUDA(cudaLaunchKernelEx(&cfg, smallm_kernel<MT, BMODE, AK>, (const float*)g.A, (const float*)g.B, (float*)g.C,
                              (int)g.M, (int)g.N, g.K, g.sam, g.sak, g.sbk, g.sbn, g.scm, g.scn, g.epi_f, kchunk));
   return TX_OK;
@@ -857,6 +867,7 @@ __global__ void __launch_bounds__(256) streamk_fixup_kernel(const float* __restr
                                                            int64_t M, int64_t N, int64_t scm, int64_t scn,
                                                            Epi<float> epi, int num_m, int num_n, int bm, int bn,
                                                            int num_kb, int NC, int group_m, int base) {
+  TX_GRID_WAIT();
   const int num_tiles = num_m * num_n;
   const int64_t U2 = (int64_t)(num_tiles - base) * num_kb;
   const int rt = blockIdx.x;
@@ -929,7 +940,7 @@ int streamk_fixup(const float* P, const G& g, int num_m, int num_n, int bm, int 
   if (num_tiles == base) return TX_OK;
   TX_CHECK(bn <= 256, TX_E_ARG, "streamk_fixup: tile too wide");
   dim3 grid((unsigned)(num_tiles - base), (unsigned)((bm + 15) / 16));
-  streamk_fixup_kernel<<<grid, 256, 0, st>>>(P, (float*)g.C, g.M, g.N, g.scm, g.scn, g.epi_f, num_m, num_n, bm, bn,
+  ::tx::launch(streamk_fixup_kernel, dim3(grid), dim3(256), 0, st, P, (float*)g.C, g.M, g.N, g.scm, g.scn, g.epi_f, num_m, num_n, bm, bn,
                                              num_kb, nclusters, group_m, base);
   TX_CUDA(cudaGetLastError());
   return TX_OK;
@@ -937,7 +948,7 @@ int streamk_fixup(const float* P, const G& g, int num_m, int num_n, int bm, int 
 
 int splitk_finalize(const float* P, const G& g, int splits, cudaStream_t st) {
   const int64_t tot = g.M * g.N;
-  kred_finalize<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(P, (float*)g.C, g.M, (int)g.N, splits, g.scm, g.scn,
+  ::tx::launch(kred_finalize, dim3((unsigned)((tot + 255) / 256)), dim3(256), 0, st, P, (float*)g.C, g.M, (int)g.N, splits, g.scm, g.scn,
                                                               g.epi_f);
   TX_CUDA(cudaGetLastError());
   return TX_OK;
@@ -946,10 +957,10 @@ int splitk_finalize(const float* P, const G& g, int splits, cudaStream_t st) {
 int gemm_simt(const G& g, cudaStream_t st) {
   dim3 grid((unsigned)((g.N + 63) / 64), (unsigned)((g.M + 63) / 64));
   if (g.dtype == TX_F32)
-    simt_gemm<float><<<grid, 256, 0, st>>>((const float*)g.A, (const float*)g.B, (float*)g.C, g.M, g.N, g.K, g.sam,
+    ::tx::launch(simt_gemm<float>, dim3(grid), dim3(256), 0, st, (const float*)g.A, (const float*)g.B, (float*)g.C, g.M, g.N, g.K, g.sam,
                                            g.sak, g.sbk, g.sbn, g.scm, g.scn, g.epi_f);
   else
-    simt_gemm<double><<<grid, 256, 0, st>>>((const double*)g.A, (const double*)g.B, (double*)g.C, g.M, g.N, g.K,
+    ::tx::launch(simt_gemm<double>, dim3(grid), dim3(256), 0, st, (const double*)g.A, (const double*)g.B, (double*)g.C, g.M, g.N, g.K,
                                             g.sam, g.sak, g.sbk, g.sbn, g.scm, g.scn, g.epi_d);
   TX_CUDA(cudaGetLastError());
   return TX_OK;

@@ -389,6 +389,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                    const __grid_constant__ CUtensorMap mapC, const __grid_constant__ CUtensorMap mapX,
                    const __grid_constant__ CUtensorMap mapAe, const __grid_constant__ CUtensorMap mapBe,
                    const __grid_constant__ CUtensorMap mapP, const TcParams p) {
+  TX_GRID_WAIT();
   using K_ = Cfg<CG>;
   constexpr int STAGES = K_::STAGES;
   constexpr int kEpiUnroll = PROMO ? 2 : 1;  // compile-time column-chunk index for the promoted sums
@@ -1163,7 +1164,7 @@ int gemm_tc(const G& g, void* ws, size_t wsb, cudaStream_t st) {
       TX_CUDA(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<1>::SMEM));
       g_attr_set[pr][1] = true;
     }
-    k1<<<nclusters, NUM_THREADS, Cfg<1>::SMEM, st>>>(ma, mb, mc, mx, mae, mbe, mp, p);
+    ::tx::launch(k1, dim3(nclusters), dim3(NUM_THREADS), Cfg<1>::SMEM, st, ma, mb, mc, mx, mae, mbe, mp, p);
   } else {
     if (!g_attr_set[pr][2]) {
       TX_CUDA(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<2>::SMEM));
@@ -1174,13 +1175,15 @@ int gemm_tc(const G& g, void* ws, size_t wsb, cudaStream_t st) {
     cfg.blockDim = dim3(NUM_THREADS, 1, 1);
     cfg.dynamicSmemBytes = Cfg<2>::SMEM;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = 2;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
     TX_CUDA(cudaLaunchKernelEx(&cfg, k2, ma, mb, mc, mx, mae, mbe, mp, p));
   }
   if (p.splits > 1) {

@@ -84,6 +84,7 @@ __global__ void __launch_bounds__(NG_THREADS, (NK <= 10 ? 2 : 1)) narrow_grad_ke
     const float* __restrict__ dz, int64_t sz0, int64_t sz1, const float* __restrict__ wt, int64_t swk, int64_t swh,
     const float* __restrict__ h, int64_t sh0, float* __restrict__ dh, int64_t sd0, float* __restrict__ Pg,
     int64_t B, int64_t H, int64_t rows_per) {
+  TX_GRID_WAIT();
   constexpr int KP = (NK + 3) & ~3;  // dz row pitch in smem (zero padded)
   constexpr int NQ = (NK + 1) / 2;   // k pairs
   constexpr int RING = NG_S * NG_RU;
@@ -210,6 +211,7 @@ __global__ void __launch_bounds__(NG_THREADS, (NK <= 10 ? 2 : 1)) narrow_grad_ke
 __global__ void __launch_bounds__(256) narrow_grad_finalize(const float* __restrict__ P, int S, int64_t H, int NK,
                                                            float* __restrict__ gw, int64_t sg0, int64_t sg1,
                                                            Epi<float> epi, float* __restrict__ db, int64_t sdb) {
+  TX_GRID_WAIT();
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t HK1 = H * (NK + 1);
   if (e >= HK1) return;
@@ -232,6 +234,7 @@ __global__ void __launch_bounds__(256) narrow_grad_finalize(const float* __restr
 
 // db[j] = sum over the 32-row blocks of the dh GEMM's column sums, block order
 __global__ void colsum_finalize(const float* __restrict__ P, int S, int64_t H, float* __restrict__ db, int64_t sdb) {
+  TX_GRID_WAIT();
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j >= H) return;
   float v = 0.f;
@@ -310,7 +313,7 @@ int launch(const NG& p, const tx_tensor* dz, const tx_tensor* wt, const tx_tenso
     attr = true;
   }
   dim3 grid((unsigned)((p.H + 4 * NG_THREADS - 1) / (4 * NG_THREADS)), (unsigned)p.S);
-  narrow_grad_kernel<NK><<<grid, NG_THREADS, smem, st>>>(
+  ::tx::launch(narrow_grad_kernel<NK>, dim3(grid), dim3(NG_THREADS), smem, st, 
       (const float*)dz->data, dz->strides[0], dz->strides[1], (const float*)wt->data, wt->strides[0], wt->strides[1],
       (const float*)h->data, h->strides[0], (float*)dh->data, dh->strides[0], Pg, p.B, p.H, p.rows_per);
   TX_CUDA(cudaGetLastError());
@@ -366,7 +369,7 @@ int tx_narrow_grad(const tx_tensor* dz, const tx_tensor* wt, const tx_tensor* h,
       float* partials = (float*)(((uintptr_t)ws + wsb - csb) & ~(uintptr_t)15);
       if ((uintptr_t)partials >= (uintptr_t)ws && gemm_with_colsum(dz, wt, dh, &e1, mode, ws, wsb - csb - 256, partials, st) == TX_OK) {
         const int64_t S = (p.B + 31) / 32;
-        colsum_finalize<<<(unsigned)((p.H + 255) / 256), 256, 0, st>>>(partials, (int)S, p.H, (float*)db->data,
+        ::tx::launch(colsum_finalize, dim3((unsigned)((p.H + 255) / 256)), dim3(256), 0, st, partials, (int)S, p.H, (float*)db->data,
                                                                       db->strides[0]);
         TX_CUDA(cudaGetLastError());
         db_done = true;
@@ -401,7 +404,7 @@ int tx_narrow_grad(const tx_tensor* dz, const tx_tensor* wt, const tx_tensor* h,
     epi.alpha = (float)gw_epi->alpha;
   }
   const int64_t tot = p.H * (p.k + 1);
-  narrow_grad_finalize<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
+  ::tx::launch(narrow_grad_finalize, dim3((unsigned)((tot + 255) / 256)), dim3(256), 0, st, 
       Pg, p.S, p.H, (int)p.k, (float*)gw->data, gw->strides[0], gw->strides[1], epi,
       want_db ? (float*)db->data : nullptr, want_db ? db->strides[0] : 0);
   TX_CUDA(cudaGetLastError());

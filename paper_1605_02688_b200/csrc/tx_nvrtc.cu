@@ -9,6 +9,8 @@
 #include <cuda_runtime.h>
 #include <nvrtc.h>
 
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -25,6 +27,7 @@ struct Drv {
   CUresult (*moduleGetFunction)(CUfunction*, CUmodule, const char*) = nullptr;
   CUresult (*launchKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
                            CUstream, void**, void**) = nullptr;
+  CUresult (*launchKernelEx)(const CUlaunchConfig*, CUfunction, void**, void**) = nullptr;  // optional
   CUresult (*occupancy)(int*, CUfunction, int, size_t) = nullptr;
   CUresult (*getErrorString)(CUresult, const char**) = nullptr;
   bool ok = false;
@@ -50,9 +53,32 @@ static const Drv& drv() {
            entry("cuModuleGetFunction", &d.moduleGetFunction) && entry("cuLaunchKernel", &d.launchKernel) &&
            entry("cuOccupancyMaxActiveBlocksPerMultiprocessor", &d.occupancy) &&
            entry("cuGetErrorString", &d.getErrorString);
+    if (!entry("cuLaunchKernelEx", &d.launchKernelEx)) d.launchKernelEx = nullptr;
     g_drv = d;
   });
   return g_drv;
+}
+
+// cuLaunchKernel, as a programmatic dependent launch when the kernel opens
+// with griddepcontrol.wait (every generated kernel of this library does;
+// tx_common.h TX_GRID_WAIT)
+static CUresult launch_drv(CUfunction fn, unsigned gx, unsigned gy, unsigned gz, unsigned bx, unsigned by, unsigned bz,
+                           unsigned smem, CUstream st, void** params, bool waits) {
+  const Drv& d = drv();
+  if (!waits || !d.launchKernelEx || !pdl_enabled())
+    return d.launchKernel(fn, gx, gy, gz, bx, by, bz, smem, st, params, nullptr);
+  CUlaunchAttribute attr[1];
+  attr[0].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
+  attr[0].value.programmaticStreamSerializationAllowed = 1;
+  CUlaunchConfig cfg;
+  memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDimX = gx; cfg.gridDimY = gy; cfg.gridDimZ = gz;
+  cfg.blockDimX = bx; cfg.blockDimY = by; cfg.blockDimZ = bz;
+  cfg.sharedMemBytes = smem;
+  cfg.hStream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return d.launchKernelEx(&cfg, fn, params, nullptr);
 }
 
 static int drv_fail(CUresult r, const char* what) {
@@ -147,6 +173,7 @@ int tx_ew_compile(const char* source, const char* name, void** out) {
 struct GenKernel {
   CUmodule mod = nullptr;
   CUfunction fn = nullptr;
+  bool waits = false;  // the source opens with griddepcontrol.wait: launched as a programmatic dependent
 };
 
 int tx_kernel_compile(const char* source, const char* name, const char* entry, void** out) {
@@ -156,6 +183,7 @@ int tx_kernel_compile(const char* source, const char* name, const char* entry, v
   int rc = nvrtc_compile(source, name, &cubin);
   if (rc) return rc;
   GenKernel* k = new GenKernel();
+  k->waits = strstr(source, "griddepcontrol.wait") != nullptr;
   CUresult r = d.moduleLoadData(&k->mod, cubin.data());
   if (r != CUDA_SUCCESS) { delete k; return drv_fail(r, "cuModuleLoadData"); }
   if ((r = d.moduleGetFunction(&k->fn, k->mod, entry)) != CUDA_SUCCESS) {
@@ -171,7 +199,7 @@ int tx_kernel_launch(void* h, unsigned grid, unsigned block, void* args, void* s
   GenKernel* k = (GenKernel*)h;
   TX_CHECK(k && drv().ok, TX_E_ARG, "tx_kernel_launch: invalid handle");
   void* params[] = {args};
-  CUresult r = drv().launchKernel(k->fn, grid, 1, 1, block, 1, 1, 0, (cudaStream_t)stream, params, nullptr);
+  CUresult r = launch_drv(k->fn, grid, 1, 1, block, 1, 1, 0, (cudaStream_t)stream, params, k->waits);
   if (r != CUDA_SUCCESS) return drv_fail(r, "cuLaunchKernel(generated)");
   return TX_OK;
 }
@@ -256,7 +284,7 @@ int tx_ew_launch(void* h, int n_out, int n_in, const tx_tensor* ops, int* err_fl
     int64_t cap = (int64_t)sms * k->occ_flat;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
-    r = d.launchKernel(k->flat, (unsigned)blocks, 1, 1, 256, 1, 1, 0, s, params, nullptr);
+    r = launch_drv(k->flat, (unsigned)blocks, 1, 1, 256, 1, 1, 0, s, params, true);
     if (r != CUDA_SUCCESS) return drv_fail(r, "cuLaunchKernel(tx_ew_flat)");
     return TX_OK;
   }
@@ -264,7 +292,16 @@ int tx_ew_launch(void* h, int n_out, int n_in, const tx_tensor* ops, int* err_fl
   for (int i = 0; i < sp.ndim; ++i) a.shape[i] = sp.shape[i];
   for (int op = 0; op < nops; ++op)
     for (int i = 0; i < sp.ndim; ++i) a.strides[op][i] = sp.strides[op][i];
-  if (sp.ndim <= 2 && a.n < (int64_t)1 << 31) {
+  if (sp.ndim >= 3 && sp.ndim <= 4 && a.n < (int64_t)1 << 31 && !getenv("TX_EW_NO_ROWS")) {
+    // row-major form (ew_template.cuh TX_ROW_COORDS): [0] inner row dim,
+    // [1] columns, [2] / [3] outer row dims
+    const int nd = sp.ndim;
+    const int map[4] = {nd - 2, nd - 1, nd - 3, nd - 4};
+    for (int i = 0; i < 4; ++i) a.shape[i] = i < nd ? sp.shape[map[i]] : 1;
+    for (int op = 0; op < nops; ++op)
+      for (int i = 0; i < 4; ++i) a.strides[op][i] = i < nd ? sp.strides[op][map[i]] : 0;
+  }
+  if (sp.ndim <= 4 && a.n < (int64_t)1 << 31 && (sp.ndim <= 2 || !getenv("TX_EW_NO_ROWS"))) {
     if (sp.ndim == 1) {  // treat as one row
       a.shape[1] = a.shape[0];
       a.shape[0] = 1;
@@ -272,25 +309,27 @@ int tx_ew_launch(void* h, int n_out, int n_in, const tx_tensor* ops, int* err_fl
     } else if (sp.ndim == 0) {
       a.shape[0] = a.shape[1] = 1;
     }
-    int64_t rows = a.shape[0], cols = a.shape[1];
+    int64_t rows = a.shape[0] * (sp.ndim >= 3 ? a.shape[2] : 1) * (sp.ndim >= 4 ? a.shape[3] : 1), cols = a.shape[1];
     // vectorised variant: column strides in {0,1}, outputs contiguous along
     // columns, rows 16 B aligned for every vector-loaded operand
     bool v2 = (cols % 4 == 0);
     for (int op = 0; op < nops && v2; ++op) {
-      const int64_t s1 = a.strides[op][1], s0 = a.strides[op][0];
+      const int64_t s1 = a.strides[op][1];
       const int isz = itemsize(ops[op].dtype);
       const uintptr_t pa = (uintptr_t)ops[op].data;
       if (op < n_out && s1 != 1) v2 = false;
       if (s1 != 0 && s1 != 1) v2 = false;
       if (s1 == 1) {
         const int64_t need = isz == 1 ? 4 : 16;
-        if ((pa % need) || ((s0 * isz) % need)) v2 = false;
+        if ((pa % need) || ((a.strides[op][0] * isz) % need) || ((a.strides[op][2] * isz) % need) ||
+            ((a.strides[op][3] * isz) % need))
+          v2 = false;
       }
     }
     if (v2) {
       unsigned gx = (unsigned)((cols / 4 + 255) / 256);
       int64_t gy = rows < 65535 ? rows : 65535;
-      r = d.launchKernel(k->k2dv, gx, (unsigned)gy, 1, 256, 1, 1, 0, s, params, nullptr);
+      r = launch_drv(k->k2dv, gx, (unsigned)gy, 1, 256, 1, 1, 0, s, params, true);
       if (r != CUDA_SUCCESS) return drv_fail(r, "cuLaunchKernel(tx_ew_2dv)");
       return TX_OK;
     }
@@ -300,14 +339,24 @@ int tx_ew_launch(void* h, int n_out, int n_in, const tx_tensor* ops, int* err_fl
     if (gy > want) gy = want;
     if (gy > 65535) gy = 65535;
     if (gy < 1) gy = 1;
-    r = d.launchKernel(k->k2d, gx, (unsigned)gy, 1, 256, 1, 1, 0, s, params, nullptr);
+    r = launch_drv(k->k2d, gx, (unsigned)gy, 1, 256, 1, 1, 0, s, params, true);
     if (r != CUDA_SUCCESS) return drv_fail(r, "cuLaunchKernel(tx_ew_2d)");
     return TX_OK;
+  }
+  static const bool trace = getenv("TX_EW_TRACE_ND") != nullptr;  // diagnostics: which launches take the N-d path
+  if (trace) {
+    fprintf(stderr, "tx_ew_nd: n=%lld ndim=%d shape", (long long)a.n, sp.ndim);
+    for (int i = 0; i < sp.ndim; ++i) fprintf(stderr, " %lld", (long long)sp.shape[i]);
+    for (int op = 0; op < nops; ++op) {
+      fprintf(stderr, " | op%d", op);
+      for (int i = 0; i < sp.ndim; ++i) fprintf(stderr, " %lld", (long long)sp.strides[op][i]);
+    }
+    fprintf(stderr, "\n");
   }
   int64_t blocks = (a.n + 255) / 256;
   int64_t cap = (int64_t)sms * k->occ_nd;
   if (blocks > cap) blocks = cap;
-  r = d.launchKernel(k->knd, (unsigned)blocks, 1, 1, 256, 1, 1, 0, s, params, nullptr);
+  r = launch_drv(k->knd, (unsigned)blocks, 1, 1, 256, 1, 1, 0, s, params, true);
   if (r != CUDA_SUCCESS) return drv_fail(r, "cuLaunchKernel(tx_ew_nd)");
   return TX_OK;
 }

@@ -161,6 +161,7 @@ __global__ void __launch_bounds__(kThreads, (OP == TX_ARGMAX_INDEX || OP == TX_A
                                                       int64_t es, int splits, T* __restrict__ out,
                                                       long long* __restrict__ out_idx, T* __restrict__ pv,
                                                       long long* __restrict__ pi) {
+  TX_GRID_WAIT();
   const int64_t row = blockIdx.y + (int64_t)blockIdx.z * gridDim.y;
   if (row >= rows) return;
   // split chunks are a multiple of 4 elements so every split of an aligned
@@ -275,6 +276,7 @@ __global__ void __launch_bounds__(kThreads, (OP == TX_ARGMAX_INDEX || OP == TX_A
 template <class T, int OP>
 __global__ void __launch_bounds__(kThreads) row_warp_kernel(const T* __restrict__ x, int64_t rows, int64_t R, int64_t rs,
                                                            int64_t es, T* __restrict__ out, long long* __restrict__ out_idx) {
+  TX_GRID_WAIT();
   const int64_t row = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= rows) return;
@@ -295,6 +297,7 @@ template <class T, int OP>
 __global__ void __launch_bounds__(kThreads) finalize_splits(int64_t rows, int splits, const T* __restrict__ pv,
                                                            const long long* __restrict__ pi, T* __restrict__ out,
                                                            long long* __restrict__ out_idx) {
+  TX_GRID_WAIT();
   const int64_t row = blockIdx.x;
   Acc<T, OP> a;
   a.init();
@@ -318,6 +321,7 @@ __global__ void __launch_bounds__(kThreads) col_kernel(const T* __restrict__ x, 
                                                       int splits, bool vec, T* __restrict__ out,
                                                       long long* __restrict__ out_idx, T* __restrict__ pv,
                                                       long long* __restrict__ pi) {
+  TX_GRID_WAIT();
   const int64_t c0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (c0 >= K) return;
   const int64_t chunk = (R + splits - 1) / splits;
@@ -374,6 +378,7 @@ __global__ void __launch_bounds__(CT_THREADS) col_tma_kernel(const __grid_consta
                                                             int64_t K, int splits, T* __restrict__ out,
                                                             long long* __restrict__ out_idx, T* __restrict__ pv,
                                                             long long* __restrict__ pi) {
+  TX_GRID_WAIT();
   extern __shared__ __align__(128) uint8_t ct_smem[];
   T* tiles = reinterpret_cast<T*>(ct_smem);  // [STAGES][ROWS][COLS]
   uint64_t* full = reinterpret_cast<uint64_t*>(ct_smem + (size_t)CT_STAGES * CT_ROWS * CT_COLS * sizeof(T));
@@ -488,6 +493,7 @@ template <class T, int OP>
 __global__ void __launch_bounds__(256) finalize_cols(int64_t K, int splits, const T* __restrict__ pv,
                                                     const long long* __restrict__ pi, T* __restrict__ out,
                                                     long long* __restrict__ out_idx) {
+  TX_GRID_WAIT();
   __shared__ T sv[8][32];
   __shared__ long long si[8][32];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
@@ -526,6 +532,7 @@ struct GenMeta {
 template <class T, int OP>
 __global__ void gen_kernel(const T* __restrict__ x, int64_t K, int64_t R, GenMeta m, T* __restrict__ out,
                            long long* __restrict__ out_idx) {
+  TX_GRID_WAIT();
   int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (o >= K) return;
   int64_t base = 0, t = o;
@@ -548,6 +555,7 @@ __global__ void gen_kernel(const T* __restrict__ x, int64_t K, int64_t R, GenMet
 // zero, scanning backwards -- work only for outputs that are zero.
 template <class T>
 __global__ void max_zero_sign(const T* __restrict__ x, int64_t K, int64_t R, GenMeta m, T* __restrict__ out) {
+  TX_GRID_WAIT();
   const int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (o >= K || out[o] != T(0)) return;
   int64_t base = 0, t = o;
@@ -564,6 +572,7 @@ __global__ void max_zero_sign(const T* __restrict__ x, int64_t K, int64_t R, Gen
 // reduced index equals idx[flat kept index].
 template <class T>
 __global__ void onehot_kernel(T* __restrict__ y, int64_t n, GenMeta m, const long long* __restrict__ idx) {
+  TX_GRID_WAIT();
   // m.kshape/kstride hold y's FULL shape and a per-dim role: kstride[d] = 1 kept, 0 reduced
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
     int64_t t = e, ki = 0, ri = 0, kmul = 1, rmul = 1, off = 0;
@@ -580,6 +589,7 @@ __global__ void onehot_kernel(T* __restrict__ y, int64_t n, GenMeta m, const lon
 
 template <class T>
 __global__ void onehot_rows(T* __restrict__ y, int64_t rows, int64_t R, const long long* __restrict__ idx) {
+  TX_GRID_WAIT();
   // y contiguous [rows, R]
   const int64_t n = rows * R;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
@@ -590,6 +600,7 @@ __global__ void onehot_rows(T* __restrict__ y, int64_t rows, int64_t R, const lo
 
 template <class T>
 __global__ void onehot_cols(T* __restrict__ y, int64_t R, int64_t K, const long long* __restrict__ idx) {
+  TX_GRID_WAIT();
   // y contiguous [R, K]; idx per column
   const int64_t n = R * K;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
@@ -754,24 +765,24 @@ static int run(const tx_tensor& x, uint32_t mask, tx_tensor& y, char* ws, size_t
       unsigned gy = (unsigned)(rows < 65535 ? rows : 65535);
       unsigned gz = (unsigned)((rows + gy - 1) / gy);
       dim3 grid((unsigned)p.splits, gy, gz);
-      row_kernel<T, OP><<<grid, kThreads, 0, st>>>(xp, rows, p.R, p.ks, p.es, p.splits, out, out_idx, pv, pi);
+      ::tx::launch(row_kernel<T, OP>, dim3(grid), dim3(kThreads), 0, st, xp, rows, p.R, p.ks, p.es, p.splits, out, out_idx, pv, pi);
       if (p.splits > 1)
-        finalize_splits<T, OP><<<(unsigned)rows, kThreads, 0, st>>>(rows, p.splits, pv, pi, out, out_idx);
+        ::tx::launch(finalize_splits<T, OP>, dim3((unsigned)rows), dim3(kThreads), 0, st, rows, p.splits, pv, pi, out, out_idx);
       break;
     }
     case ROWWARP: {
       int64_t rows = p.K;
       unsigned blocks = (unsigned)((rows + (kThreads / 32) - 1) / (kThreads / 32));
-      row_warp_kernel<T, OP><<<blocks, kThreads, 0, st>>>(xp, rows, p.R, p.ks, p.es, out, out_idx);
+      ::tx::launch(row_warp_kernel<T, OP>, dim3(blocks), dim3(kThreads), 0, st, xp, rows, p.R, p.ks, p.es, out, out_idx);
       break;
     }
     case COL: {
       bool vec = ((uintptr_t)xp & 15) == 0 && (p.rs % 4) == 0;
       unsigned gx = (unsigned)((p.K + 4 * kThreads - 1) / (4 * kThreads));
       dim3 grid(gx, (unsigned)p.splits);
-      col_kernel<T, OP><<<grid, kThreads, 0, st>>>(xp, p.R, p.K, p.rs, p.splits, vec, out, out_idx, pv, pi);
+      ::tx::launch(col_kernel<T, OP>, dim3(grid), dim3(kThreads), 0, st, xp, p.R, p.K, p.rs, p.splits, vec, out, out_idx, pv, pi);
       if (p.splits > 1)
-        finalize_cols<T, OP><<<(unsigned)((p.K + 31) / 32), 256, 0, st>>>(p.K, p.splits, pv, pi, out, out_idx);
+        ::tx::launch(finalize_cols<T, OP>, dim3((unsigned)((p.K + 31) / 32)), dim3(256), 0, st, p.K, p.splits, pv, pi, out, out_idx);
       break;
     }
     case COLTMA: {
@@ -794,13 +805,13 @@ static int run(const tx_tensor& x, uint32_t mask, tx_tensor& y, char* ws, size_t
         attr = true;
       }
       dim3 grid((unsigned)((p.K + CT_COLS - 1) / CT_COLS), (unsigned)p.splits);
-      col_tma_kernel<T, OP><<<grid, CT_THREADS, CT_SMEM, st>>>(map, p.R, p.K, p.splits, out, out_idx, pv, pi);
+      ::tx::launch(col_tma_kernel<T, OP>, dim3(grid), dim3(CT_THREADS), CT_SMEM, st, map, p.R, p.K, p.splits, out, out_idx, pv, pi);
       if (p.splits > 1)
-        finalize_cols<T, OP><<<(unsigned)((p.K + 31) / 32), 256, 0, st>>>(p.K, p.splits, pv, pi, out, out_idx);
+        ::tx::launch(finalize_cols<T, OP>, dim3((unsigned)((p.K + 31) / 32)), dim3(256), 0, st, p.K, p.splits, pv, pi, out, out_idx);
       break;
     }
     case GEN: {
-      gen_kernel<T, OP><<<(unsigned)((p.K + 127) / 128), 128, 0, st>>>(xp, p.K, p.R, p.gm, out, out_idx);
+      ::tx::launch(gen_kernel<T, OP>, dim3((unsigned)((p.K + 127) / 128)), dim3(128), 0, st, xp, p.K, p.R, p.gm, out, out_idx);
       break;
     }
   }
@@ -808,7 +819,7 @@ static int run(const tx_tensor& x, uint32_t mask, tx_tensor& y, char* ws, size_t
   if constexpr (OP == TX_MAX && (std::is_same<T, float>::value || std::is_same<T, double>::value)) {
     static const bool off = getenv("TX_NO_MAX_ZERO_SIGN") != nullptr;  // A/B diagnostics only
     if (p.K > 0 && p.R > 0 && !off) {
-      max_zero_sign<T><<<(unsigned)((p.K + 127) / 128), 128, 0, st>>>(xp, p.K, p.R, p.gm, out);
+      ::tx::launch(max_zero_sign<T>, dim3((unsigned)((p.K + 127) / 128)), dim3(128), 0, st, xp, p.K, p.R, p.gm, out);
       TX_CUDA(cudaGetLastError());
     }
   }
@@ -824,9 +835,9 @@ static int run(const tx_tensor& x, uint32_t mask, tx_tensor& y, char* ws, size_t
       if (mask & (1u << d)) { if (first_r < 0) first_r = d; last_r = d; ++nred; }
     bool block_contig = nred > 0 && (last_r - first_r + 1) == nred;
     if (ycont && block_contig && last_r == x.ndim - 1) {
-      onehot_rows<T><<<(unsigned)blocks, 256, 0, st>>>(yp, p.K, p.R, onehot_idx);
+      ::tx::launch(onehot_rows<T>, dim3((unsigned)blocks), dim3(256), 0, st, yp, p.K, p.R, onehot_idx);
     } else if (ycont && block_contig && first_r == 0) {
-      onehot_cols<T><<<(unsigned)blocks, 256, 0, st>>>(yp, p.R, p.K, onehot_idx);
+      ::tx::launch(onehot_cols<T>, dim3((unsigned)blocks), dim3(256), 0, st, yp, p.R, p.K, onehot_idx);
     } else {
       GenMeta m;
       m.nk = y.ndim;
@@ -835,7 +846,7 @@ static int run(const tx_tensor& x, uint32_t mask, tx_tensor& y, char* ws, size_t
         m.kstride[d] = (mask & (1u << d)) ? 0 : 1;
         m.rstride[d] = y.strides[d];
       }
-      onehot_kernel<T><<<(unsigned)blocks, 256, 0, st>>>(yp, n, m, onehot_idx);
+      ::tx::launch(onehot_kernel<T>, dim3((unsigned)blocks), dim3(256), 0, st, yp, n, m, onehot_idx);
     }
     TX_CUDA(cudaGetLastError());
   }

@@ -28,6 +28,11 @@ int sm_count() {
   return g_sm_count;
 }
 
+bool pdl_enabled() {
+  static const bool on = getenv("TX_NO_PDL") == nullptr;
+  return on;
+}
+
 void collapse(int ndim, const int64_t* shape, int nops, const int64_t (*strides)[TX_MAX_RANK], Space* out) {
   // drop extent-1 dims
   int64_t sh[TX_MAX_RANK];
@@ -67,6 +72,7 @@ struct CopyMeta {
 template <typename T>
 __global__ void strided_copy_kernel_p(const T* __restrict__ src, T* __restrict__ dst, int64_t n, int nd,
                                       CopyMeta m) {
+  TX_GRID_WAIT();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     int64_t r = i, so = 0, dof = 0;
     for (int d = nd - 1; d >= 0; --d) {
@@ -97,6 +103,7 @@ struct TileMeta {
 template <typename T>
 __global__ void __launch_bounds__(256) transpose_copy_kernel(const T* __restrict__ src, T* __restrict__ dst, TileMeta m,
                                                              int64_t nbatch) {
+  TX_GRID_WAIT();
   __shared__ T tile[32][33];
   const int64_t p0 = (int64_t)blockIdx.y * 32, q0 = (int64_t)blockIdx.x * 32;
   for (int64_t b = blockIdx.z; b < nbatch; b += gridDim.z) {
@@ -128,6 +135,7 @@ __global__ void __launch_bounds__(256) transpose_copy_kernel(const T* __restrict
 template <typename T>
 __global__ void __launch_bounds__(256) row_copy_kernel(const T* __restrict__ src, T* __restrict__ dst, TileMeta m,
                                                        int64_t nrows) {
+  TX_GRID_WAIT();
   // blockIdx.y: a 1024-element chunk of the row (4 independent copies per thread)
   const int64_t i0 = (int64_t)blockIdx.y * 1024 + threadIdx.x;
   for (int64_t row = blockIdx.x; row < nrows; row += gridDim.x) {
@@ -196,7 +204,7 @@ static int launch_copy(const tx_tensor* s, tx_tensor* d, cudaStream_t st) {
       dim3 grid((unsigned)((t.sq + 31) / 32), (unsigned)((t.sp + 31) / 32),
                 (unsigned)(nbatch < 65535 ? nbatch : 65535));
       if (grid.y <= 65535) {
-        transpose_copy_kernel<T><<<grid, dim3(32, 8), 0, st>>>((const T*)s->data, (T*)d->data, t, nbatch);
+        ::tx::launch(transpose_copy_kernel<T>, dim3(grid), dim3(dim3(32, 8)), 0, st, (const T*)s->data, (T*)d->data, t, nbatch);
         TX_CUDA(cudaGetLastError());
         return TX_OK;
       }
@@ -217,8 +225,7 @@ static int launch_copy(const tx_tensor* s, tx_tensor* d, cudaStream_t st) {
       const int64_t cap = (int64_t)sm_count() * 16;
       const int64_t gy = (t.sp + 1023) / 1024;
       const int64_t gx = std::max<int64_t>(1, std::min<int64_t>(nrows, cap / std::max<int64_t>(gy, 1) + 1));
-      row_copy_kernel<T><<<dim3((unsigned)std::min<int64_t>(gx, 65535 * 16), (unsigned)std::min<int64_t>(gy, 65535)),
-                           256, 0, st>>>((const T*)s->data, (T*)d->data, t, nrows);
+      ::tx::launch(row_copy_kernel<T>, dim3(dim3((unsigned)std::min<int64_t>(gx, 65535 * 16), (unsigned)std::min<int64_t>(gy, 65535))), dim3(256), 0, st, (const T*)s->data, (T*)d->data, t, nrows);
       TX_CUDA(cudaGetLastError());
       return TX_OK;
     }
@@ -227,7 +234,7 @@ static int launch_copy(const tx_tensor* s, tx_tensor* d, cudaStream_t st) {
   int64_t blocks = (n + threads - 1) / threads;
   int64_t cap = (int64_t)sm_count() * 8;
   if (blocks > cap) blocks = cap;
-  strided_copy_kernel_p<T><<<(unsigned)blocks, threads, 0, st>>>((const T*)s->data, (T*)d->data, n, sp.ndim, m);
+  ::tx::launch(strided_copy_kernel_p<T>, dim3((unsigned)blocks), dim3(threads), 0, st, (const T*)s->data, (T*)d->data, n, sp.ndim, m);
   TX_CUDA(cudaGetLastError());
   return TX_OK;
 }
@@ -236,6 +243,7 @@ static int launch_copy(const tx_tensor* s, tx_tensor* d, cudaStream_t st) {
 template <typename T>
 __global__ void check_values_kernel(const T* __restrict__ x, int64_t n, int nd, CopyMeta m, uint32_t* flags,
                                     int slot, int mode, double big) {
+  TX_GRID_WAIT();
   uint32_t bits = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     int64_t r = i, off = 0;
@@ -382,9 +390,9 @@ int tx_check_values(const tx_tensor* x, uint32_t* flags, int slot, int mode, dou
   if (blocks > cap) blocks = cap;
   cudaStream_t st = (cudaStream_t)s;
   if (x->dtype == TX_F32)
-    check_values_kernel<float><<<(unsigned)blocks, 256, 0, st>>>((const float*)x->data, n, nd, m, flags, slot, mode, big);
+    ::tx::launch(check_values_kernel<float>, dim3((unsigned)blocks), dim3(256), 0, st, (const float*)x->data, n, nd, m, flags, slot, mode, big);
   else
-    check_values_kernel<double><<<(unsigned)blocks, 256, 0, st>>>((const double*)x->data, n, nd, m, flags, slot, mode, big);
+    ::tx::launch(check_values_kernel<double>, dim3((unsigned)blocks), dim3(256), 0, st, (const double*)x->data, n, nd, m, flags, slot, mode, big);
   TX_CUDA(cudaGetLastError());
   return TX_OK;
 }

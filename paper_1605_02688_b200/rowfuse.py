@@ -43,6 +43,11 @@ MAX_OPS = 48
 V, S, C, U = "V", "S", "C", "U"
 
 
+# every generated kernel waits for its stream predecessor first: the launch is
+# programmatic (tx_nvrtc.cu launch_drv; tx_common.h TX_GRID_WAIT)
+_GRID_WAIT = 'asm volatile("griddepcontrol.wait;" ::: "memory");'
+
+
 def wide_threads(K):
     """Threads per row of the block-per-row form: about 8 columns per thread
     (register-resident rows; measured on softmax-xent fwd+bwd: K=1000 best at
@@ -619,10 +624,12 @@ class _Gen:
         head = _PRELUDE % {"R": self.R, "T": self.T, "MAXOPS": MAX_OPS}
         if self.block:
             pre = [f'extern "C" __global__ void __launch_bounds__({self.T}) tx_row(const TxRowArgs a) {{',
+                   _GRID_WAIT,
                    "const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;",
                    "const i64 row = (i64)blockIdx.x;", "const int tc = threadIdx.x;"]
         else:
             pre = ['extern "C" __global__ void __launch_bounds__(256) tx_row(const TxRowArgs a) {',
+                   _GRID_WAIT,
                    "const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;",
                    "const i64 row = (i64)blockIdx.x * 8 + warp;", "const int tc = lane;"]
         return "\n".join([head] + pre + ["const bool active = row < a.N;", "const int K = a.K;",

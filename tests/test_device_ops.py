@@ -89,6 +89,35 @@ def test_broadcast_composite(golden):
     close(f(golden["bc_X"], golden["bc_r"], golden["bc_col"]), golden["bc_out"], 1e-5, 1e-6)
 
 
+def test_elementwise_rank3_rank4_row_forms(rng):
+    """Rank-3/4 iteration spaces that do not collapse to 2-D -- a time-reversed
+    view and a [T]-vector broadcast over [T, B, V] (the LSTM loss layer), a
+    4-D mix of broadcasts -- take the row-major kernels with per-row
+    coordinates (ew_template.cuh TX_ROW_COORDS), vectorised and scalar:
+    bit-identical to NumPy float32 arithmetic."""
+    Tn, B, V = 5, 6, 36
+    X = rng.standard_normal((Tn, B, V)).astype(np.float32)
+    Y = rng.standard_normal((Tn, B, V)).astype(np.float32)
+    t = rng.standard_normal(Tn).astype(np.float32)
+    m = rng.standard_normal((Tn, B)).astype(np.float32)
+    vX, vY = T.tensor3("X", dtype="float32"), T.tensor3("Y", dtype="float32")
+    vt, vm = T.vector("t", dtype="float32"), T.matrix("m", dtype="float32")
+    expr = (vX[::-1] + T.dimshuffle(vt, (0, "x", "x"))) * vY - T.dimshuffle(vm, (0, 1, "x"))
+    f = T.compile([vX, vY, vt, vm], expr)
+    want = (X[::-1] + t[:, None, None]) * Y - m[:, :, None]
+    exact(f(X, Y, t, m), want)
+    # odd row length: the scalar row form
+    exact(f(X[:, :, :35].copy(), Y[:, :, :35].copy(), t, m), (X[::-1, :, :35] + t[:, None, None]) * Y[:, :, :35] - m[:, :, None])
+    # rank 4: [A, B, C, D] with a [A, 1, C, 1] and a [1, B, 1, D] operand
+    A4 = rng.standard_normal((3, 4, 5, 8)).astype(np.float32)
+    p = rng.standard_normal((3, 5)).astype(np.float32)
+    q = rng.standard_normal((4, 8)).astype(np.float32)
+    vA = T.tensor4("A", dtype="float32")
+    vp, vq = T.matrix("p", dtype="float32"), T.matrix("q", dtype="float32")
+    g = T.compile([vA, vp, vq], vA * T.dimshuffle(vp, (0, "x", 1, "x")) + T.dimshuffle(vq, ("x", 0, "x", 1)))
+    exact(g(A4, p, q), A4 * p[:, None, :, None] + q[None, :, None, :])
+
+
 def test_config2_expression_fused(golden):
     r7 = np.random.default_rng(7)
     ins = [r7.standard_normal(40000, dtype=np.float32) for _ in range(4)]
