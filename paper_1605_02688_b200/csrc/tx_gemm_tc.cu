@@ -247,6 +247,7 @@ struct TcParams {
   int nclusters;    // clusters of the launch (stream-K partition)
   int bn;           // N tile of this launch (<= BN, multiple of 32): chosen per shape against wave quantisation
   int stage_tx;     // TMA bytes landing per stage on the leader's barrier
+  int group_m;      // M-tiles per raster group (operand panels shared in L2 by concurrently running tiles)
   int dbg_nostore;  // diagnostics only (TX_GEMM_DBG_NOSTORE): epilogue drains TMEM without storing
   int tma_store;    // C written by TMA tile stores from swizzled smem staging
   int tma_aux;      // [M,N] epilogue operand read by TMA tile loads (CG = 2)
@@ -264,11 +265,11 @@ __device__ __forceinline__ int chunk_end(const TcParams& p, int kb, int kb1) {
   return min(e, kb1);
 }
 
-__device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int& mb, int& nb) {
-  const int per_group = GROUP_M * num_n;
+__device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int group_m, int& mb, int& nb) {
+  const int per_group = group_m * num_n;
   const int g = t / per_group;
-  const int first = g * GROUP_M;
-  const int gsz = min(num_m - first, GROUP_M);
+  const int first = g * group_m;
+  const int gsz = min(num_m - first, group_m);
   const int r = t - g * per_group;
   mb = first + r % gsz;
   nb = r / gsz;
@@ -452,7 +453,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       Seg sg;
       while (seg_next(p, cluster_id, cur, sg)) {
         int mb, nb;
-        tile_coords(sg.t, p.num_m, p.num_n, mb, nb);
+        tile_coords(sg.t, p.num_m, p.num_n, p.group_m, mb, nb);
         const int kb0 = sg.kb0, kb1 = sg.kb1;
         const int m0 = mb * BM * CG + (int)rank * BM;   // this CTA's rows
         const int n0 = nb * bn + (int)rank * BNL;       // this CTA's half of B
@@ -557,7 +558,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     Seg sg;
     for (; seg_next(p, cluster_id, cur, sg); ++it) {
       int mb, nb;
-      tile_coords(sg.t, p.num_m, p.num_n, mb, nb);
+      tile_coords(sg.t, p.num_m, p.num_n, p.group_m, mb, nb);
       const int split = sg.piece;
       const bool partial = !sg.full;
       const int q_ = warp & 3;
@@ -1102,6 +1103,8 @@ int gemm_tc(const G& g, void* ws, size_t wsb, cudaStream_t st) {
   p.colsum = g.colsum;
   if (p.colsum) p.splits = 1, p.kbs = p.num_kb, p.streamk = 0;  // every tile finished by its own epilogue
   p.dbg_nostore = getenv("TX_GEMM_DBG_NOSTORE") != nullptr;
+  static const int group_env = getenv("TX_GEMM_GROUP_M") ? atoi(getenv("TX_GEMM_GROUP_M")) : 0;
+  p.group_m = group_env > 0 ? group_env : GROUP_M;
   // TMA tile stores need a 16-byte aligned C with a 16-byte row pitch; the
   // dual-output epilogue (two stores per element) keeps the register path
   CUtensorMap mc;
@@ -1192,7 +1195,7 @@ int gemm_tc(const G& g, void* ws, size_t wsb, cudaStream_t st) {
   }
   if (p.streamk) {
     TX_CUDA(cudaGetLastError());
-    return streamk_fixup((const float*)ws, g, p.num_m, p.num_n, BM * cg, bn, p.num_kb, nclusters, GROUP_M, st);
+    return streamk_fixup((const float*)ws, g, p.num_m, p.num_n, BM * cg, bn, p.num_kb, nclusters, p.group_m, st);
   }
   TX_CUDA(cudaGetLastError());
   return TX_OK;
