@@ -36,6 +36,17 @@ def main():
         va, vb = T.matrix("a", dtype=f32), T.matrix("b", dtype=f32)
         for mode in ("auto", "3xtf32", "simt"):
             T.compile([va, vb], T.dot(va, vb), gemm_mode=mode, cuda_graph=False)(A, B)
+    # r02 small-M kernel: every B layout, the cluster split of K (DSMEM reduction), an epilogue
+    for (M, N, K, tb) in ((20, 200, 800, False), (7, 96, 1000, True), (20, 800, 200, False)):
+        A = rng.standard_normal((M, K)).astype(np.float32)
+        B = rng.standard_normal((N, K) if tb else (K, N)).astype(np.float32)
+        bias = rng.standard_normal(N).astype(np.float32)
+        va, vb, vc = T.matrix("a", dtype=f32), T.matrix("b", dtype=f32), T.vector("c", dtype=f32)
+        T.compile([va, vb, vc], T.tanh(T.dot(va, T.transpose(vb) if tb else vb) + vc), cuda_graph=False)(A, B, bias)
+    # r02 rank-3 row-major elementwise form (reversed view, [T] broadcast)
+    v3, vt = T.tensor3("X3", dtype=f32), T.vector("t", dtype=f32)
+    T.compile([v3, vt], (v3[::-1] + T.dimshuffle(vt, (0, "x", "x"))) * 2.0, cuda_graph=False)(
+        rng.standard_normal((5, 6, 36)).astype(np.float32), rng.standard_normal(5).astype(np.float32))
     # training steps: logistic regression (row fusion, skinny GEMMs) and a small MLP
     # (fused epilogues, narrow-grad, stream-K), TF32 and 3xTF32
     gl = C.build_logreg(T)
