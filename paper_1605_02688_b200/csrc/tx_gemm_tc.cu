@@ -233,6 +233,18 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// 8 TMEM columns of this warp's 32 lanes (the promoted-accumulation drains:
+// the running sums already hold 128 registers per thread)
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+
 struct TcParams {
   float* C;
   int64_t ldc;
@@ -364,7 +376,7 @@ __device__ __noinline__ float epi_apply_edge(const Epi<float>& E, float v, int r
 // epilogue past the instruction cache: 79 us vs 11 us on the LSTM's
 // [20 x 800 x 200] GEMM); 128-bit loads when both operands are unit-stride
 // and aligned.
-__device__ __forceinline__ void add_aux_bias32(const Epi<float>& E, int row, int n, int N, float (&v)[32]) {
+__device__ __forceinline__ void add_aux_bias32(const Epi<float>& E, int row, int n, int N, float* v) {
   const float* g = E.aux + (int64_t)row * E.s0;
   const float* b = E.aux2 + (int64_t)row * E.b0;
   if (n + 32 <= N && E.s1 == 1 && E.b1 == 1 && (((uintptr_t)(g + n) | (uintptr_t)(b + n)) & 15) == 0) {
@@ -393,13 +405,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   TX_GRID_WAIT();
   using K_ = Cfg<CG>;
   constexpr int STAGES = K_::STAGES;
-  constexpr int kEpiUnroll = PROMO ? 2 : 1;  // compile-time column-chunk index for the promoted sums
-  constexpr int kMaxJ = PROMO ? 2 : 4;       // 32-column chunks per epilogue thread (bn <= 128 with PROMO)
-  // TMEM accumulators: two 256-column buffers (tile i+1's MMAs overlap tile
-  // i's epilogue); PROMO (bn <= 128): four 128-column buffers, so the MMA
-  // warp runs up to three promotion chunks ahead of the epilogue
-  constexpr int NACC = PROMO ? 4 : 2;
-  constexpr int ACC_COLS = PROMO ? 128 : BN;
+  constexpr int kEpiUnroll = PROMO ? 4 : 1;  // compile-time column-chunk index for the promoted sums
+  constexpr int kMaxJ = 4;                   // 32-column chunks per epilogue thread
+  // TMEM accumulators: two 256-column buffers (tile i+1's MMAs -- PROMO: the
+  // next promotion chunk's -- overlap the epilogue's drain of the other)
+  constexpr int NACC = 2;
+  constexpr int ACC_COLS = BN;
   const int bn = p.bn;
   const int BNL = bn / CG;  // B columns staged by this CTA
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -563,7 +574,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const bool partial = !sg.full;
       const int q_ = warp & 3;
       const int nchunks_ = bn / 32;
-      float acc[PROMO ? 2 : 1][32];
+      float acc[PROMO ? kMaxJ : 1][32];  // PROMO: the row's running fp32 sums, 128 registers at bn = 256
       int nkc = 1;
       if constexpr (PROMO) {
         nkc = 0;
@@ -580,10 +591,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           for (int jj = 0; jj < kMaxJ; ++jj) {
             const int ci = half + 2 * jj;
             if (ci < nchunks_) {
-              float t[32];
-              tmem_ld32(ta + ci * 32, t);
 #pragma unroll
-              for (int i = 0; i < 32; ++i) acc[jj][i] = kc == 0 ? t[i] : __fadd_rn(acc[jj][i], t[i]);
+              for (int s8 = 0; s8 < 4; ++s8) {
+                float t[8];
+                tmem_ld8(ta + ci * 32 + s8 * 8, t);
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                  acc[jj][8 * s8 + i] = kc == 0 ? t[i] : __fadd_rn(acc[jj][8 * s8 + i], t[i]);
+              }
             }
           }
           tc_fence_before();
@@ -624,13 +639,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               tma_load_2d((void*)xstg, &mapX, xbar, n, row0);
             }
           }
-          float v[32];
-          tmem_ld32(taddr + c, v);
-          if constexpr (PROMO) {
-            if (nkc > 1) {
+          float vloc[32];
+          float* v = vloc;
+          if constexpr (PROMO) {  // last chunk added into the running sums in place (8 columns at a time)
 #pragma unroll
-              for (int i = 0; i < 32; ++i) v[i] = __fadd_rn(acc[jj][i], v[i]);
+            for (int s8 = 0; s8 < 4; ++s8) {
+              float t[8];
+              tmem_ld8(taddr + c + s8 * 8, t);
+#pragma unroll
+              for (int i = 0; i < 8; ++i) acc[jj][8 * s8 + i] = nkc > 1 ? __fadd_rn(acc[jj][8 * s8 + i], t[i]) : t[i];
             }
+            v = acc[jj];
+          } else {
+            tmem_ld32(taddr + c, vloc);
           }
           if (!live) continue;
           if (partial) {  // raw partial tile -> workspace [piece][M][N]; the reduction applies the epilogue
@@ -762,13 +783,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int ci = half + 2 * jj;
         if (ci >= nchunks) break;
         const int c = ci * 32;
-        float v[32];
-        tmem_ld32(taddr + c, v);
+        float vloc[32];
+        float* v = vloc;
         if constexpr (PROMO) {
-          if (nkc > 1) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = __fadd_rn(acc[jj][i], v[i]);
+          for (int s8 = 0; s8 < 4; ++s8) {
+            float t[8];
+            tmem_ld8(taddr + c + s8 * 8, t);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) acc[jj][8 * s8 + i] = nkc > 1 ? __fadd_rn(acc[jj][8 * s8 + i], t[i]) : t[i];
           }
+          v = acc[jj];
+        } else {
+          tmem_ld32(taddr + c, vloc);
         }
         const int n = nb * bn + c;
         if (!row_ok || n >= p.N || p.dbg_nostore) continue;
@@ -952,10 +979,12 @@ void choose_tile(const G& g, int* cg_out, int* bn_out) {
   // would spend 16x the tensor time on padding -- use 32 / 64-wide tiles
   if (!bn_s && g.N <= 32) { bn = 32; cg = 1; }
   else if (!bn_s && g.N <= 64) bn = 64;
-  // promoted accumulation keeps a row's running sums in registers: at most
-  // 128 columns per tile (64 per epilogue thread within the 168-register cap
-  // that 10 warps on 4 sub-partitions leave)
-  if (g.promo && bn > 128) bn = 128;
+  // promoted accumulation keeps a row's running sums in registers (128 per
+  // epilogue thread at bn = 256, drained 8 TMEM columns at a time to stay
+  // inside the 168-register cap that 10 warps on 4 sub-partitions leave);
+  // TX_3X_BN128=1 restores the r02a 128-column promoted tile (A/B)
+  static const bool bn128 = getenv("TX_3X_BN128") != nullptr;
+  if (g.promo && bn > 128 && bn128) bn = 128;
   if (bn < 32 || bn > BN || bn % (32 * cg) != 0) bn = BN;
   *cg_out = cg;
   *bn_out = bn;
