@@ -823,6 +823,19 @@ static int launch_smallm(const G& g, cudaStream_t st) {
   int64_t cs = (2 * (int64_t)sm_count() + strips - 1) / strips;
   if (cs > 8) cs = 8;
   if (cs > g.K / 256) cs = g.K / 256;
+  // small products (B of <= 2^18 elements) are latency-bound: one staged
+  // piece per CTA where the cluster allows, i.e. fewer serial load rounds
+  // (LSTM small 797 -> 765 us per batch; the medium model's larger products
+  // keep the rule above, 1816 vs 1937 us).  TX_SMALLM_CS=0/1/k+1 for A/B.
+  static const int rule_env = getenv("TX_SMALLM_CS") ? atoi(getenv("TX_SMALLM_CS")) : -1;
+  const int rule = rule_env >= 0 ? rule_env : (g.N * g.K <= (1 << 18) ? 1 : 0);
+  if (rule == 1) {
+    cs = (g.K + SMM_KP - 1) / SMM_KP;
+    if (cs > 8) cs = 8;
+    while (cs > 1 && strips * cs > 4 * (int64_t)sm_count()) --cs;
+  } else if (rule > 1) {
+    cs = rule - 1;
+  }
   if (cs < 1) cs = 1;
   int64_t kchunk = (g.K + cs - 1) / cs;
   kchunk = (kchunk + 7) / 8 * 8;  // pieces start 32-byte aligned along k
