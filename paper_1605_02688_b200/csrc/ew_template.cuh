@@ -182,7 +182,7 @@ __device__ __forceinline__ V4<T> tx_ld4b(const T* p, i64 s1) {
 #ifdef TX_KERNELS
 
 extern "C" __global__ void __launch_bounds__(256) tx_ew_flat(const TxEwArgs a) {
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic dependent launch (tx_common.h)
+  asm volatile("griddepcontrol.wait;\n\tgriddepcontrol.launch_dependents;" ::: "memory");  // programmatic dependent launch (tx_common.h)
   TX_PTRS
   int* err = a.err;
   (void)err;
@@ -245,7 +245,7 @@ extern "C" __global__ void __launch_bounds__(256) tx_ew_flat(const TxEwArgs a) {
     c2 = t_ / e1;                                          \
   }
 extern "C" __global__ void __launch_bounds__(256) tx_ew_2d(const TxEwArgs a) {
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic dependent launch (tx_common.h)
+  asm volatile("griddepcontrol.wait;\n\tgriddepcontrol.launch_dependents;" ::: "memory");  // programmatic dependent launch (tx_common.h)
   TX_PTRS
   int* err = a.err;
   (void)err;
@@ -269,7 +269,7 @@ extern "C" __global__ void __launch_bounds__(256) tx_ew_2d(const TxEwArgs a) {
 // rank-2 with the contiguous dim vectorised: every operand has column stride
 // 0 or 1 and 16 B-aligned rows; 4 columns per thread, one row per grid.y step.
 extern "C" __global__ void __launch_bounds__(256) tx_ew_2dv(const TxEwArgs a) {
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic dependent launch (tx_common.h)
+  asm volatile("griddepcontrol.wait;\n\tgriddepcontrol.launch_dependents;" ::: "memory");  // programmatic dependent launch (tx_common.h)
   TX_PTRS
   int* err = a.err;
   (void)err;
@@ -297,7 +297,7 @@ extern "C" __global__ void __launch_bounds__(256) tx_ew_2dv(const TxEwArgs a) {
 }
 
 extern "C" __global__ void __launch_bounds__(256) tx_ew_nd(const TxEwArgs a) {
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic dependent launch (tx_common.h)
+  asm volatile("griddepcontrol.wait;\n\tgriddepcontrol.launch_dependents;" ::: "memory");  // programmatic dependent launch (tx_common.h)
   TX_PTRS
   int* err = a.err;
   (void)err;

@@ -74,12 +74,13 @@ int sm_count();
 // Every kernel of the library starts with TX_GRID_WAIT() (griddepcontrol.wait:
 // returns once the preceding kernel in the stream has completed and its
 // writes are visible; immediately when there is none) and is launched with
-// the programmatic-stream-serialization attribute, so a kernel's launch and
-// CTA rasterisation overlap the tail of its predecessor -- inside captured
-// CUDA graphs too.  The chains of small dependent kernels (an unrolled scan's
+// the programmatic-stream-serialization attribute; right after the wait it
+// releases its own dependents (griddepcontrol.launch_dependents), so the next
+// kernel's CTAs are launched and resident while this one runs and start the
+// moment it completes -- inside captured CUDA graphs too.  The chains of small dependent kernels (an unrolled scan's
 // bodies, the logistic-regression step) are launch-latency bound; this is
 // the gap it closes.  TX_NO_PDL=1 launches plainly (A/B).
-#define TX_GRID_WAIT() asm volatile("griddepcontrol.wait;" ::: "memory")
+#define TX_GRID_WAIT() asm volatile("griddepcontrol.wait;\n\tgriddepcontrol.launch_dependents;" ::: "memory")
 bool pdl_enabled();
 
 template <class... KArgs, class... Args>

@@ -45,7 +45,7 @@ V, S, C, U = "V", "S", "C", "U"
 
 # every generated kernel waits for its stream predecessor first: the launch is
 # programmatic (tx_nvrtc.cu launch_drv; tx_common.h TX_GRID_WAIT)
-_GRID_WAIT = 'asm volatile("griddepcontrol.wait;" ::: "memory");'
+_GRID_WAIT = 'asm volatile("griddepcontrol.wait;\\n\\tgriddepcontrol.launch_dependents;" ::: "memory");'
 
 
 def wide_threads(K):
