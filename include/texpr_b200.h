@@ -137,6 +137,14 @@ int tx_im2col(const tx_tensor* x, tx_tensor* cols, const int* win, void* stream)
  * is a run along c (128-bit when C % 4 == 0). */
 int tx_im2col_hwc(const tx_tensor* x, tx_tensor* cols, const int* win, void* stream);
 int tx_col2im(const tx_tensor* dcols, tx_tensor* dx, const int* win, int64_t Ho, int64_t Wo, void* stream);
+/* Implicit-GEMM stride-1 convolution on the tensor cores (the reference's
+ * im2col + np.dot of ops/conv.py:108-157 without the patch matrix):
+ * out[(n,p,q), k] = sum_{u,v,c} xpad[n, p+u, q+v, c] * w[k, (u,v,c)], TF32.
+ * xpad: zero-padded NHWC input [N, Hp, Wp, C] contiguous; w: [K, kh*kw*C]
+ * contiguous in (u, v, c) order; out: [N*P*Q, K] contiguous with
+ * P = Hp-kh+1, Q = Wp-kw+1.  `win` = {kh, kw}.  TX_E_UNSUPPORTED unless
+ * float32, C % 32 == 0, Q <= 128 and 16-byte aligned operands. */
+int tx_conv_implicit(const tx_tensor* xpad, const tx_tensor* w, tx_tensor* out, const int* win, void* stream);
 
 /* NaN guard (reference diagnostics.py:52-88 nan_guard_check, hooked per node
  * at runtime.py:359-367): scan one float tensor and OR into flags[slot]

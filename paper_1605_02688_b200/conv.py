@@ -154,6 +154,14 @@ class Conv2d(Op):
             K, _, kh, kw = f.shape
             _, _, Ho, Wo = out.shape
             f = _contig(plan, f)
+            if self._implicit_ok(mode, x.dtype, C, Wo):
+                fr = plan.scratch((K, kh, kw, C), f.dtype)
+                plan.emit_copy_layouts(plan.view_of(f, (K, kh, kw, C), (C * kh * kw, kw, 1, kh * kw), f.offset), fr)
+                res = plan.scratch((N * Ho * Wo, K), out.dtype)
+                self._implicit(plan, x, self.pad, fr, res, kh, kw)
+                plan.emit_copy_layouts(plan.view_of(res, (N, K, Ho * Wo), (Ho * Wo * K, 1, K), 0),
+                                       plan.view_of(out, (N, K, Ho * Wo), (K * Ho * Wo, Ho * Wo, 1), out.offset))
+                return
             cols = self._cols(plan, node.inputs[0], x, N * Ho * Wo, C * kh * kw, kh, kw)
             if self.algo == GEMM:
                 # (u, v, c) patch order: the filters reordered to [K, kh, kw, C]
@@ -222,6 +230,15 @@ class Conv2d(Op):
                                             f.offset + (kh - 1) * kw + (kw - 1)), fr)
         ph, pw = kh - 1 - self.pad[0], kw - 1 - self.pad[1]
         Nn, Kk, Ho, Wo = dy4.shape
+        if ph >= 0 and pw >= 0 and self._implicit_ok(mode, dy4.dtype, K, W):
+            # filters as [C, (u, v, k)] rows for the implicit GEMM's K-major B
+            frT = plan.scratch((C, kh, kw, K), out.dtype)
+            plan.emit_copy_layouts(plan.view_of(fr, (C, kh, kw, K), (1, kw * K * C, K * C, C), 0), frT)
+            res = plan.scratch((N * H * W, C), out.dtype)
+            self._implicit(plan, dy4, (ph, pw), frT, res, kh, kw)
+            plan.emit_copy_layouts(plan.view_of(res, (N, C, H * W), (H * W * C, 1, C), 0),
+                                   plan.view_of(out, (N, C, H * W), (C * H * W, H * W, 1), out.offset))
+            return
         dyh = self._hwc(plan, None, dy4)
         cols = plan.scratch((N * H * W, K * kh * kw), out.dtype)
         lib = plan.lib
@@ -236,6 +253,40 @@ class Conv2d(Op):
         plan.emit_gemm(cols, plan.view_of(fr, (K * kh * kw, C), (C, 1), 0), res, mode)
         plan.emit_copy_layouts(plan.view_of(res, (N, C, H * W), (H * W * C, 1, C), 0),
                                plan.view_of(out, (N, C, H * W), (C * H * W, H * W, 1), out.offset))
+
+    def _implicit_ok(self, mode, dtype, C, Wo) -> bool:
+        """The tensor-core implicit GEMM (tx_conv_implicit) applies: GEMM
+        algorithm at TF32, stride 1, float32, 32-channel blocks, output rows
+        of at most 128 pixels."""
+        from . import native
+        return (self.algo == GEMM and mode in (native.GEMM_AUTO, native.GEMM_TC) and tuple(self.stride) == (1, 1)
+                and dtype == "float32" and C % 32 == 0 and 0 < Wo <= 128 and not _NO_IMPLICIT)
+
+    def _implicit(self, plan, x, pad, wr, res, kh, kw):
+        """res[(n, p, q), k] = conv(x, w) with x [N, C, H, W] (any strides),
+        wr [K, kh, kw, C] contiguous, res [N*P*Q, K] contiguous: x goes to a
+        zero-padded NHWC buffer (memset + one strided copy), then ONE
+        tcgen05 launch reads it through 4-D TMA boxes per (tap, channel
+        block) -- no patch matrix (the explicit form wrote and re-read
+        N*P*Q*kh*kw*C floats: 231 MB for a 32x64x56x56 3x3 layer)."""
+        N, C, H, W = x.shape
+        ph, pw = pad
+        Hp, Wp = H + 2 * ph, W + 2 * pw
+        xp = plan.scratch((N, Hp, Wp, C), x.dtype)
+        plan.emit_fill_zero(xp)
+        plan.emit_copy_layouts(plan.view_of(x, (N, H, W, C), (x.strides[0], x.strides[2], x.strides[3], x.strides[1]),
+                                            x.offset),
+                               plan.view_of(xp, (N, H, W, C), (Hp * Wp * C, Wp * C, C, 1), (ph * Wp + pw) * C))
+        K = wr.shape[0]
+        lib = plan.lib
+        tx_ = plan.tx(xp)
+        tw = plan.tx(wr, (K, kh * kw * C), (kh * kw * C, 1))
+        tr = plan.tx(res)
+        win = (__import__("ctypes").c_int * 2)(kh, kw)
+
+        def launch(stream):
+            lib.check(lib.lib.tx_conv_implicit(tx_, tw, tr, win, stream))
+        plan.add_launch(launch)
 
     def _win(self, kh, kw):
         import ctypes
@@ -288,6 +339,9 @@ class Conv2d(Op):
         def launch(stream):
             lib.check(lib.lib.tx_im2col(tx, tc, win, stream))
         plan.add_launch(launch)
+
+
+_NO_IMPLICIT = bool(__import__("os").environ.get("TX_CONV_NO_IMPLICIT"))  # A/B: explicit im2col for every conv
 
 
 def _contig(plan, lay, shape=None, perm=None):

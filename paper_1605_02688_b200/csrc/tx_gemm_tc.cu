@@ -112,6 +112,14 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
       "l"((uint64_t)map), "r"(su32(bar)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2,
+                                            int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(
+          su32(dst)),
+      "l"((uint64_t)map), "r"(su32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
 __device__ __forceinline__ void tma_load_3d_2sm(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
                                                 int c2) {
   asm volatile(
@@ -259,6 +267,17 @@ struct TcParams {
   int nclusters;    // clusters of the launch (stream-K partition)
   int bn;           // N tile of this launch (<= BN, multiple of 32): chosen per shape against wave quantisation
   int stage_tx;     // TMA bytes landing per stage on the leader's barrier
+  // implicit-GEMM convolution (stride 1; CG = 1): A rows are output pixels,
+  // fetched per k-block (filter tap u, v; 32-channel block) as ONE 4-D TMA box
+  // {32 c, Q, RB rows, 1 image} of a zero-padded NHWC input -- no patch matrix
+  int conv;
+  int cv_cb;        // 32-channel blocks per tap
+  int cv_kw;        // filter width
+  int cv_P, cv_Q;   // output rows / columns per image
+  int cv_RB;        // output rows per M tile (RB * Q <= 128)
+  int cv_pb;        // M tiles per image, ceil(P / RB)
+  int kpack;        // k-blocks per ring stage (conv, bn <= 64: 2 -- A0 | A1 | B0 | B1 in one 48 KB stage,
+                    // twice the loads in flight; else 1)
   int group_m;      // M-tiles per raster group (operand panels shared in L2 by concurrently running tiles)
   int dbg_nostore;  // diagnostics only (TX_GEMM_DBG_NOSTORE): epilogue drains TMEM without storing
   int tma_store;    // C written by TMA tile stores from swizzled smem staging
@@ -468,11 +487,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int kb0 = sg.kb0, kb1 = sg.kb1;
         const int m0 = mb * BM * CG + (int)rank * BM;   // this CTA's rows
         const int n0 = nb * bn + (int)rank * BNL;       // this CTA's half of B
-        for (int kb = kb0; kb < kb1; ++kb) {
+        for (int kb = kb0; kb < kb1; kb += p.kpack) {
           mbar_wait(empty + stage, phase ^ 1);
           uint8_t* sa = smem + stage * K_::STAGE_BYTES;
           uint8_t* sb = sa + K_::A_BYTES;
-          if (leader) mbar_expect_tx(full + stage, (uint32_t)p.stage_tx);
+          const int nsub = min(p.kpack, kb1 - kb);
+          if (leader) mbar_expect_tx(full + stage, (uint32_t)(p.stage_tx * nsub));
           const int k0 = kb * BK;
           auto load = [&](void* dst, const CUtensorMap* map, int c0, int c1) {
             if constexpr (CG == 1) tma_load_2d(dst, map, full + stage, c0, c1);
@@ -482,7 +502,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if constexpr (CG == 1) tma_load_3d(dst, map, full + stage, 0, c1, c2);
             else tma_load_3d_2sm(dst, map, full + stage, 0, c1, c2);
           };
-          if (p.a_3d && m0 + BM <= p.a_lim) {
+          if (p.conv) {
+            const int img = mb / p.cv_pb, r0 = (mb % p.cv_pb) * p.cv_RB;
+            for (int sub = 0; sub < nsub; ++sub) {
+              const int k = kb + sub;
+              const int tap = k / p.cv_cb, c0 = (k % p.cv_cb) * 32;
+              uint8_t* da = p.kpack == 2 ? sa + sub * 16384 : sa;
+              uint8_t* db = p.kpack == 2 ? sa + 32768 + sub * 8192 : sb;
+              tma_load_4d(da, &mapA, full + stage, c0, tap % p.cv_kw, r0 + tap / p.cv_kw, img);
+              tma_load_2d(db, &mapB, full + stage, k * BK, n0);
+            }
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+            continue;
+          } else if (p.a_3d && m0 + BM <= p.a_lim) {
             load3(sa, &mapA, k0, m0 / 32);
           } else if (p.a_mn) {  // 32-wide boxes: 2-D edge map (clipped at M)
             const CUtensorMap* ma = p.a_3d ? &mapAe : &mapA;
@@ -529,17 +561,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         mbar_wait(tempty + buf, (use & 1) ^ 1);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + (uint32_t)(buf * ACC_COLS);  // buffers at 0 / 256 (PROMO: 0/128/256/384)
-        for (int kb = kb0; kb < kb1; ++kb) {
+        for (int kb = kb0; kb < kb1; kb += p.kpack) {
           mbar_wait(full + stage, phase);
           tc_fence_after();
           if (lane == 0) {
-            const uint32_t sa = su32(smem + stage * K_::STAGE_BYTES);
-            const uint32_t sb = sa + K_::A_BYTES;
+            const uint32_t s0 = su32(smem + stage * K_::STAGE_BYTES);
+            const int nsub = min(p.kpack, kb1 - kb);
+            for (int sub = 0; sub < nsub; ++sub) {
+              const uint32_t sa = p.kpack == 2 ? s0 + sub * 16384 : s0;
+              const uint32_t sb = p.kpack == 2 ? s0 + 32768 + sub * 8192 : s0 + K_::A_BYTES;
 #pragma unroll
-            for (int kk = 0; kk < BK / 8; ++kk) {
-              const uint64_t da = sdesc(sa + kk * a_step, a_lbo, a_sbo, a_lay);
-              const uint64_t db = sdesc(sb + kk * b_step, b_lbo, b_sbo, b_lay);
-              umma_tf32<CG>(tmem_d, da, db, idesc, (kb != kb0) || (kk != 0));
+              for (int kk = 0; kk < BK / 8; ++kk) {
+                const uint64_t da = sdesc(sa + kk * a_step, a_lbo, a_sbo, a_lay);
+                const uint64_t db = sdesc(sb + kk * b_step, b_lbo, b_sbo, b_lay);
+                umma_tf32<CG>(tmem_d, da, db, idesc, (kb != kb0) || (sub != 0) || (kk != 0));
+              }
             }
             umma_commit<CG>(empty + stage);
           }
@@ -613,13 +649,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint32_t use = (uint32_t)(it / NACC);
       mbar_wait(tfull + buf, use & 1);
       tc_fence_after();
-      const int row0 = mb * BM * CG + (int)rank * BM + q * 32;
-      const int row = row0 + lane;
+      int row0 = mb * BM * CG + (int)rank * BM + q * 32;
+      int row = row0 + lane;
+      int conv_valid = BM;
+      if (p.conv) {  // tile = RB output rows of one image (RB * Q pixels), rows past them are padding
+        const int img = mb / p.cv_pb, r0 = (mb % p.cv_pb) * p.cv_RB;
+        conv_valid = min(p.cv_RB, p.cv_P - r0) * p.cv_Q;
+        row0 = (img * p.cv_P + r0) * p.cv_Q + q * 32;
+        row = row0 + lane;
+      }
       // 32-column chunks of the bn-wide accumulator, alternating between the two warps of a lane quarter
       const uint32_t taddr = tmem_base + (uint32_t)(buf * ACC_COLS) + ((uint32_t)(q * 32) << 16);
       const int nchunks = bn / 32;
       float* crow = p.C + (int64_t)row * p.ldc;
-      const bool row_ok = row < p.M;
+      const bool row_ok = p.conv ? q * 32 + lane < conv_valid : row < p.M;
       if (p.tma_store || p.splits > 1) {  // (split-K: every segment is a partial tile -> workspace)
         // row `lane` of a [32 x 32] tile -> swizzled staging -> one TMA store
         // per chunk (coalesced, asynchronous; TMA clips the M/N edges)
@@ -1103,6 +1146,8 @@ int gemm_tc(const G& g, void* ws, size_t wsb, cudaStream_t st) {
   }
   if (rc) return rc;
   TcParams p;
+  p.conv = 0;
+  p.kpack = 1;
   p.C = (float*)g.C;
   p.ldc = g.scm;
   p.M = (int)g.M;
@@ -1227,6 +1272,85 @@ int gemm_tc(const G& g, void* ws, size_t wsb, cudaStream_t st) {
     return streamk_fixup((const float*)ws, g, p.num_m, p.num_n, BM * cg, bn, p.num_kb, nclusters, p.group_m, st);
   }
   TX_CUDA(cudaGetLastError());
+  return TX_OK;
+}
+
+// Implicit-GEMM stride-1 convolution on the tcgen05 kernel (CG = 1):
+//   out[(n, p, q), k] = sum_{u, v, c} xpad[n, p + u, q + v, c] * w[k, (u, v, c)]
+// xpad: zero-padded NHWC input [N, Hp, Wp, C] (contiguous), w: [K, kh*kw*C]
+// (contiguous, (u, v, c) order), out: [N*P*Q, K] (contiguous rows).  The
+// A tile of a k-block (tap u, v; channels c0..c0+31) is one 4-D TMA box
+// {32, Q, RB, 1} at (c0, v, r0 + u, n): RB whole output rows of one image,
+// landing as RB*Q consecutive 128-byte rows -- the K-major, 128B-swizzled
+// layout the MMA reads -- so no [N*P*Q, kh*kw*C] patch matrix is written or
+// read.  Tile rows past RB*Q are stale and never stored (register epilogue).
+int gemm_tc_conv(const float* xpad, int64_t N, int64_t Hp, int64_t Wp, int64_t C, const float* w, int64_t K, int kh,
+                 int kw, float* out, cudaStream_t st) {
+  const int64_t P = Hp - kh + 1, Q = Wp - kw + 1;
+  TX_CHECK(P > 0 && Q > 0 && C % 32 == 0 && Q <= BM && K > 0, TX_E_UNSUPPORTED,
+           "tx_conv_implicit: needs C % 32 == 0 and output width <= 128");
+  TX_CHECK(((uintptr_t)xpad & 15) == 0 && ((uintptr_t)w & 15) == 0 && ((uintptr_t)out & 15) == 0, TX_E_UNSUPPORTED,
+           "tx_conv_implicit: 16-byte aligned operands");
+  EncodeFn enc = encode_fn();
+  TX_CHECK(enc, TX_E_NODEVICE, "cuTensorMapEncodeTiled unavailable");
+  const int RB = (int)(BM / Q);
+  CUtensorMap ma, mb;
+  {
+    cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)Wp, (cuuint64_t)Hp, (cuuint64_t)N};
+    cuuint64_t strides[3] = {(cuuint64_t)(C * 4), (cuuint64_t)(Wp * C * 4), (cuuint64_t)(Hp * Wp * C * 4)};
+    cuuint32_t box[4] = {32, (cuuint32_t)Q, (cuuint32_t)RB, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    CUresult r = enc(&ma, CU_TENSOR_MAP_DATA_TYPE_TFLOAT32, 4, const_cast<float*>(xpad), dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(TX_E_CUDA, "tx_conv_implicit: input map (code " + std::to_string((int)r) + ")");
+  }
+  const int64_t KK = (int64_t)kh * kw * C;
+  int bn = (int)((K + 31) / 32 * 32);
+  if (bn > BN) bn = BN;
+  int rc = make_map(&mb, w, KK, K, KK, 32, bn, false);
+  if (rc) return rc;
+  TcParams p;
+  memset(&p, 0, sizeof(p));
+  p.C = out;
+  p.ldc = K;
+  p.M = (int)(N * P * Q);
+  p.N = (int)K;
+  p.K = (int)KK;
+  p.a_lim = p.b_lim = INT32_MAX;
+  p.conv = 1;
+  static const bool no_pack = getenv("TX_CONV_NO_KPACK") != nullptr;
+  p.kpack = bn <= 64 && !no_pack ? 2 : 1;
+  p.cv_cb = (int)(C / 32);
+  p.cv_kw = kw;
+  p.cv_P = (int)P;
+  p.cv_Q = (int)Q;
+  p.cv_RB = RB;
+  p.cv_pb = (int)((P + RB - 1) / RB);
+  p.num_m = (int)(N * p.cv_pb);
+  p.num_n = (int)((K + bn - 1) / bn);
+  p.bn = bn;
+  p.stage_tx = RB * (int)Q * BK * 4 + bn * BK * 4;
+  p.num_tiles = p.num_m * p.num_n;
+  p.splits = 1;
+  p.num_kb = (int)(KK / BK);
+  p.kbs = p.num_kb;
+  p.streamk = 0;
+  p.epi = Epi<float>();
+  p.tma_store = 0;
+  p.tma_aux = 0;
+  p.promo = p.promo_first = 0;
+  p.group_m = GROUP_M;
+  const int units = sm_count();
+  p.nclusters = p.num_tiles < units ? p.num_tiles : units;
+  CUtensorMap none;
+  memset(&none, 0, sizeof(none));
+  if (!g_attr_set[0][1]) {
+    TX_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<1>::SMEM));
+    g_attr_set[0][1] = true;
+  }
+  TX_CUDA(::tx::launch(tc_gemm_kernel<1, false>, dim3(p.nclusters), dim3(NUM_THREADS), Cfg<1>::SMEM, st, ma, mb, none,
+                       none, none, none, none, p));
   return TX_OK;
 }
 

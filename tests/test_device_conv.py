@@ -2,6 +2,7 @@
 gather) against the REAL reference's outputs (tests/golden/make_conv_golden.py)
 and NumPy, plus reshape / shape_of and the implementation-selection rules
 (reference ops/conv.py, rewrites/convselect.py)."""
+import ctypes
 import os
 import sys
 
@@ -129,3 +130,49 @@ def test_conv_random_shapes_and_gradients(seed):
         gf_ref[idx] = (wv * _conv_ref(x, d, st, pd)).sum()
     assert _rel(got_gx, gx_ref) <= 1e-12
     assert _rel(got_gf, gf_ref) <= 1e-12
+
+
+def _conv_nhwc_ref(xpad, w, kh, kw):
+    """out[(n,p,q), k] = sum_{u,v,c} xpad[n,p+u,q+v,c] w[k,(u,v,c)] in float64, and |.| bound."""
+    N, Hp, Wp, C = xpad.shape
+    P, Q = Hp - kh + 1, Wp - kw + 1
+    X = xpad.astype(np.float64)
+    Wt = w.astype(np.float64).reshape(w.shape[0], kh, kw, C)
+    out = np.zeros((N, P, Q, w.shape[0]))
+    bound = np.zeros_like(out)
+    for u in range(kh):
+        for v in range(kw):
+            patch = X[:, u:u + P, v:v + Q, :]
+            out += patch @ Wt[:, u, v, :].T
+            bound += np.abs(patch) @ np.abs(Wt[:, u, v, :]).T
+    return out.reshape(N * P * Q, -1), bound.reshape(N * P * Q, -1)
+
+
+@pytest.mark.parametrize("N,Hp,Wp,C,K,kh,kw", [(2, 10, 12, 32, 64, 3, 3), (1, 58, 58, 64, 64, 3, 3),
+                                                (3, 9, 130, 32, 40, 3, 3), (2, 20, 7, 96, 300, 5, 5),
+                                                (4, 5, 5, 64, 16, 1, 1), (1, 33, 67, 32, 64, 2, 4)])
+def test_conv_implicit_gemm_direct(N, Hp, Wp, C, K, kh, kw):
+    """tx_conv_implicit through the C ABI: the A tile of every (tap, channel
+    block) is a 4-D TMA box of the padded NHWC input (ragged last row block,
+    output width up to 128, several output-channel tiles, 1x1 and 5x5 taps);
+    TF32 products against float64 within 2^-9 of the |x||w| bound."""
+    import torch
+    from paper_1605_02688_b200 import native
+    if Wp - kw + 1 > 128:
+        pytest.skip("output width > 128 is outside the implicit path")
+    lib = native.library()
+    rng = np.random.default_rng(N * 1000 + C + K)
+    xpad = rng.standard_normal((N, Hp, Wp, C)).astype(np.float32)
+    w = rng.standard_normal((K, kh * kw * C)).astype(np.float32)
+    P, Q = Hp - kh + 1, Wp - kw + 1
+    tx, tw = torch.from_numpy(xpad).cuda(), torch.from_numpy(w).cuda()
+    to = torch.full((N * P * Q, K), float("nan"), device="cuda")
+    mk = native.make_tensor
+    win = (ctypes.c_int * 2)(kh, kw)
+    lib.check(lib.lib.tx_conv_implicit(mk(tx.data_ptr(), "float32", xpad.shape, (Hp * Wp * C, Wp * C, C, 1)),
+                                       mk(tw.data_ptr(), "float32", w.shape, (w.shape[1], 1)),
+                                       mk(to.data_ptr(), "float32", (N * P * Q, K), (K, 1)), win, None))
+    torch.cuda.synchronize()
+    got = to.cpu().numpy()
+    want, bound = _conv_nhwc_ref(xpad, w, kh, kw)
+    assert np.all(np.abs(got - want) <= 2.0 ** -9 * bound + 1e-5), float(np.nanmax(np.abs(got - want) / (bound + 1e-30)))
