@@ -73,6 +73,12 @@ def main():
         rng.standard_normal((9, 64)).astype(np.float32), np.zeros(64, np.float32))
     # convolution
     vx, vf = T.tensor4("x", dtype=f32), T.tensor4("f", dtype=f32)
+    # r02b implicit-GEMM convolution (stride 1, 32-channel blocks): forward and both gradients
+    xi = rng.standard_normal((2, 32, 9, 11)).astype(np.float32)
+    fi = rng.standard_normal((8, 32, 3, 3)).astype(np.float32)
+    yi = T.conv2d(vx, vf, stride=(1, 1), pad=(1, 1))
+    gfi, gxi = T.grad(T.sum(yi * yi), [vf, vx])
+    T.compile([vx, vf], [yi, gfi, gxi], cuda_graph=False, conv_impl="gemm")(xi, fi)
     T.compile([vx, vf], [T.conv2d(vx, vf, stride=(2, 2), pad=(1, 1))], cuda_graph=False)(
         rng.standard_normal((2, 3, 11, 9)).astype(np.float32), rng.standard_normal((4, 3, 3, 3)).astype(np.float32))
     print("sanitize tour done")
