@@ -549,6 +549,39 @@ __global__ void kred_finalize(const float* __restrict__ P, float* __restrict__ C
   C[m * scm + n * scn] = epi.apply(v, m, n);
 }
 
+// Many splits (the skinny K reductions: up to 1024 partials of a few
+// thousand outputs): 32 outputs per CTA, the splits interleaved over its 8
+// warps, partials added in warp order (deterministic) -- 8x the loads in
+// flight of one thread walking every split.
+__global__ void __launch_bounds__(256) kred_finalize_wide(const float* __restrict__ P, float* __restrict__ C,
+                                                          int64_t M, int N, int splits, int64_t scm, int64_t scn,
+                                                          Epi<float> epi) {
+  TX_GRID_WAIT();
+  __shared__ float part[8][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t MN = M * N;
+  const int64_t e = blockIdx.x * 32LL + lane;
+  float v = 0.f;
+  if (e < MN) {
+    int s = w;
+    for (; s + 24 < splits; s += 32) {
+      const float q0 = __ldcs(P + (int64_t)s * MN + e), q1 = __ldcs(P + (int64_t)(s + 8) * MN + e);
+      const float q2 = __ldcs(P + (int64_t)(s + 16) * MN + e), q3 = __ldcs(P + (int64_t)(s + 24) * MN + e);
+      v += q0; v += q1; v += q2; v += q3;
+    }
+    for (; s < splits; s += 8) v += P[(int64_t)s * MN + e];
+  }
+  part[w][lane] = v;
+  __syncthreads();
+  if (w != 0 || e >= MN) return;
+  float t = part[0][lane];
+#pragma unroll
+  for (int u = 1; u < 8; ++u) t += part[u][lane];
+  const int64_t m = e / N;
+  const int n = (int)(e - m * N);
+  C[m * scm + n * scn] = epi.apply(t, m, n);
+}
+
 template <int NN, int R, bool TRANS = false>
 static int launch_rowdot_full(const G& g, int threads, size_t smem, cudaStream_t st) {
   static bool attr = false;
@@ -626,6 +659,10 @@ static int launch_kred(const G& g, void* ws, size_t wsb, cudaStream_t st) {
   ::tx::launch(kred_kernel<NN>, dim3(grid), dim3(KR_THREADS), 0, st, (const float*)g.A, (const float*)g.B, (float*)ws, g.M, (int)g.N, g.K, g.sak,
                                         g.sbk, g.sbn, splits);
   int64_t tot = g.M * g.N;
+  if (splits >= 32)
+    ::tx::launch(kred_finalize_wide, dim3((unsigned)((tot + 31) / 32)), dim3(256), 0, st, (const float*)ws, (float*)g.C, g.M,
+                 (int)g.N, splits, g.scm, g.scn, g.epi_f);
+  else
   ::tx::launch(kred_finalize, dim3((unsigned)((tot + 255) / 256)), dim3(256), 0, st, (const float*)ws, (float*)g.C, g.M, (int)g.N, splits,
                                                               g.scm, g.scn, g.epi_f);
   TX_CUDA(cudaGetLastError());
