@@ -273,6 +273,11 @@ def attach_cpu_path(line, T, C, args):
             r = tab[ref]
             ex[ours]["cpu_baseline"] = {"unit": r["unit"], "e2e": r["e2e"], "kernel": r["kernel"], "kind": "reference",
                                         "cores": host["cpu_count"], "blas": host["blas"]}
+    if isinstance(ex.get("lstm_ptb_words_per_s"), dict) and "small" in tab.get("lstm_ptb", {}):
+        r = tab["lstm_ptb"]
+        ex["lstm_ptb_words_per_s"]["cpu_baseline"] = {
+            "unit": "words/s", "kind": "reference", "cores": host["cpu_count"],
+            **{m: {"e2e": r[m]["e2e"], "kernel": r[m]["kernel"]} for m in ("small", "medium") if m in r}}
     if isinstance(ex.get("careduce_16384sq_GBs"), dict) and "sum_axis0" in tab.get("config3_careduce_16384sq", {}):
         r = tab["config3_careduce_16384sq"]
         ex["careduce_cpu_baseline"] = {k: {"e2e": v["e2e"], "kernel": v["kernel"]} for k, v in r.items()

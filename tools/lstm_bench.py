@@ -20,7 +20,10 @@ CONFIGS = {"small": (200, 20), "medium": (600, 40)}
 
 
 def build(T, H, L, B=20, V=10000, lr=0.1, seed=0, exclude=()):
-    from paper_1605_02688_b200.ops import dimshuffle, subtensor
+    """``T`` is this package or the reference ``texpr`` (same spelling)."""
+    import importlib
+    ops = importlib.import_module(T.__name__ + ".ops")
+    dimshuffle, subtensor = ops.dimshuffle, ops.subtensor
     rng = np.random.default_rng(seed)
     f32 = "float32"
 

@@ -206,6 +206,18 @@ def config_conv(tx, reps):
             "e2e_s": e2e, "kernel_s": k, "shape": dict(CONV)}
 
 
+def config_lstm(tx, reps):
+    """The PTB LSTM language-model step (tools/lstm_bench.py: scan over T steps,
+    softmax-xent per step, BPTT, SGD) on the reference's CPU path."""
+    from tools.lstm_bench import CONFIGS, build
+    out = {"unit": "words/s"}
+    for name, (H, L) in CONFIGS.items():
+        f, args = build(tx, H, L, exclude=("fuse_elemwise",))
+        e2e, k = _time(f, args, max(2, reps // 2))
+        out[name] = {"e2e": 20 * L / e2e, "kernel": 20 * L / k, "e2e_s": e2e, "kernel_s": k, "hidden": H, "steps": L}
+    return out
+
+
 def table(reps=5, only=None):
     """Every config's CPU-path throughput (end-to-end and kernel-only)."""
     tx = load_reference()
@@ -215,7 +227,8 @@ def table(reps=5, only=None):
            "calls": f"1 warm-up + median of {reps}", "host": host_info()}
     for name, fn in (("config1_logreg_n600", config1), ("config2_ew_2p28", config2),
                      ("config3_careduce_16384sq", config3), ("config4_mlp_b8192", config4),
-                     ("config5_mlp_global65536", config5), ("conv3x3_n32c64h56", config_conv)):
+                     ("config5_mlp_global65536", config5), ("conv3x3_n32c64h56", config_conv),
+                     ("lstm_ptb", config_lstm)):
         if only and name not in only:
             continue
         t0 = time.perf_counter()
