@@ -141,8 +141,9 @@ int tx_col2im(const tx_tensor* dcols, tx_tensor* dx, const int* win, int64_t Ho,
  * im2col + np.dot of ops/conv.py:108-157 without the patch matrix):
  * out[(n,p,q), k] = sum_{u,v,c} xpad[n, p+u, q+v, c] * w[k, (u,v,c)], TF32.
  * xpad: zero-padded NHWC input [N, Hp, Wp, C] contiguous; w: [K, kh*kw*C]
- * contiguous in (u, v, c) order; out: [N*P*Q, K] contiguous with
- * P = Hp-kh+1, Q = Wp-kw+1.  `win` = {kh, kw}.  TX_E_UNSUPPORTED unless
+ * contiguous in (u, v, c) order; out: [N*P*Q, K] (NHWC rows) or
+ * [N, K, P, Q] (NCHW), contiguous, with P = Hp-kh+1, Q = Wp-kw+1.
+ * `win` = {kh, kw}.  TX_E_UNSUPPORTED unless
  * float32, C % 32 == 0, Q <= 128 and 16-byte aligned operands. */
 int tx_conv_implicit(const tx_tensor* xpad, const tx_tensor* w, tx_tensor* out, const int* win, void* stream);
 

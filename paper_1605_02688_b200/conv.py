@@ -157,6 +157,9 @@ class Conv2d(Op):
             if self._implicit_ok(mode, x.dtype, C, Wo):
                 fr = plan.scratch((K, kh, kw, C), f.dtype)
                 plan.emit_copy_layouts(plan.view_of(f, (K, kh, kw, C), (C * kh * kw, kw, 1, kh * kw), f.offset), fr)
+                if out.contiguous():  # the epilogue stores NCHW directly
+                    self._implicit(plan, x, self.pad, fr, out, kh, kw)
+                    return
                 res = plan.scratch((N * Ho * Wo, K), out.dtype)
                 self._implicit(plan, x, self.pad, fr, res, kh, kw)
                 plan.emit_copy_layouts(plan.view_of(res, (N, K, Ho * Wo), (Ho * Wo * K, 1, K), 0),
@@ -234,6 +237,9 @@ class Conv2d(Op):
             # filters as [C, (u, v, k)] rows for the implicit GEMM's K-major B
             frT = plan.scratch((C, kh, kw, K), out.dtype)
             plan.emit_copy_layouts(plan.view_of(fr, (C, kh, kw, K), (1, kw * K * C, K * C, C), 0), frT)
+            if out.contiguous():  # the epilogue stores NCHW directly
+                self._implicit(plan, dy4, (ph, pw), frT, out, kh, kw)
+                return
             res = plan.scratch((N * H * W, C), out.dtype)
             self._implicit(plan, dy4, (ph, pw), frT, res, kh, kw)
             plan.emit_copy_layouts(plan.view_of(res, (N, C, H * W), (H * W * C, 1, C), 0),
@@ -263,8 +269,8 @@ class Conv2d(Op):
                 and dtype == "float32" and C % 32 == 0 and 0 < Wo <= 128 and not _NO_IMPLICIT)
 
     def _implicit(self, plan, x, pad, wr, res, kh, kw):
-        """res[(n, p, q), k] = conv(x, w) with x [N, C, H, W] (any strides),
-        wr [K, kh, kw, C] contiguous, res [N*P*Q, K] contiguous: x goes to a
+        """res = conv(x, w) with x [N, C, H, W] (any strides), wr [K, kh, kw,
+        C] contiguous, res [N*P*Q, K] or [N, K, P, Q] contiguous: x goes to a
         zero-padded NHWC buffer (memset + one strided copy), then ONE
         tcgen05 launch reads it through 4-D TMA boxes per (tap, channel
         block) -- no patch matrix (the explicit form wrote and re-read

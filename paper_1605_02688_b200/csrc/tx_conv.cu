@@ -268,16 +268,19 @@ extern "C" int tx_conv_implicit(const tx_tensor* xpad, const tx_tensor* w, tx_te
   TX_CHECK(xpad && w && out && win, TX_E_ARG, "tx_conv_implicit: bad arguments");
   TX_CHECK(xpad->dtype == TX_F32 && w->dtype == TX_F32 && out->dtype == TX_F32, TX_E_UNSUPPORTED,
            "tx_conv_implicit: float32 only");
-  TX_CHECK(xpad->ndim == 4 && is_contiguous(*xpad) && w->ndim == 2 && is_contiguous(*w) && out->ndim == 2 &&
-               is_contiguous(*out),
-           TX_E_ARG, "tx_conv_implicit: contiguous xpad[N,Hp,Wp,C], w[K,kh*kw*C], out[N*P*Q,K]");
+  TX_CHECK(xpad->ndim == 4 && is_contiguous(*xpad) && w->ndim == 2 && is_contiguous(*w) &&
+               (out->ndim == 2 || out->ndim == 4) && is_contiguous(*out),
+           TX_E_ARG, "tx_conv_implicit: contiguous xpad[N,Hp,Wp,C], w[K,kh*kw*C], out[N*P*Q,K] or [N,K,P,Q]");
   const int kh = win[0], kw = win[1];
   const int64_t N = xpad->shape[0], Hp = xpad->shape[1], Wp = xpad->shape[2], C = xpad->shape[3];
   const int64_t K = w->shape[0];
   TX_CHECK(kh >= 1 && kw >= 1 && w->shape[1] == (int64_t)kh * kw * C, TX_E_ARG, "tx_conv_implicit: filter shape");
-  TX_CHECK(out->shape[0] == N * (Hp - kh + 1) * (Wp - kw + 1) && out->shape[1] == K, TX_E_ARG,
-           "tx_conv_implicit: output shape");
-  if (out->shape[0] == 0) return TX_OK;
+  const int64_t P = Hp - kh + 1, Q = Wp - kw + 1;
+  const bool nchw = out->ndim == 4;
+  TX_CHECK(nchw ? (out->shape[0] == N && out->shape[1] == K && out->shape[2] == P && out->shape[3] == Q)
+                : (out->shape[0] == N * P * Q && out->shape[1] == K),
+           TX_E_ARG, "tx_conv_implicit: output shape");
+  if (N * P * Q == 0) return TX_OK;
   return gemm_tc_conv((const float*)xpad->data, N, Hp, Wp, C, (const float*)w->data, K, kh, kw, (float*)out->data,
-                      (cudaStream_t)stream);
+                      nchw ? 1 : 0, (cudaStream_t)stream);
 }

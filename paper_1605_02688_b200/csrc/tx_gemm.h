@@ -98,7 +98,7 @@ int gemm_tc(const G& g, void* ws, size_t wsb, cudaStream_t st);
 size_t gemm_tc_workspace(const G& g);
 // implicit-GEMM stride-1 convolution (tx_conv_implicit)
 int gemm_tc_conv(const float* xpad, int64_t N, int64_t Hp, int64_t Wp, int64_t C, const float* w, int64_t K, int kh,
-                 int kw, float* out, cudaStream_t st);
+                 int kw, float* out, int out_nchw, cudaStream_t st);
 // C = A.B (+ epilogue) on the tcgen05 path with per-32-row-block column sums
 // of C into `partials` ([ceil(M/32)][N] fp32); TX_E_UNSUPPORTED when the
 // product does not take that path (caller reduces C separately)

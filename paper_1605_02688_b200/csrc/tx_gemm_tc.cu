@@ -276,6 +276,7 @@ struct TcParams {
   int cv_P, cv_Q;   // output rows / columns per image
   int cv_RB;        // output rows per M tile (RB * Q <= 128)
   int cv_pb;        // M tiles per image, ceil(P / RB)
+  int cv_nchw;      // store C as [N, K, P, Q] (per output channel, a tile's pixels are one contiguous run)
   int kpack;        // k-blocks per ring stage (conv, bn <= 64: 2 -- A0 | A1 | B0 | B1 in one 48 KB stage,
                     // twice the loads in flight; else 1)
   int group_m;      // M-tiles per raster group (operand panels shared in L2 by concurrently running tiles)
@@ -652,11 +653,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int row0 = mb * BM * CG + (int)rank * BM + q * 32;
       int row = row0 + lane;
       int conv_valid = BM;
+      int64_t nchw_base = 0;  // conv NCHW store: &C[img, 0, pixel of this lane]
       if (p.conv) {  // tile = RB output rows of one image (RB * Q pixels), rows past them are padding
         const int img = mb / p.cv_pb, r0 = (mb % p.cv_pb) * p.cv_RB;
         conv_valid = min(p.cv_RB, p.cv_P - r0) * p.cv_Q;
         row0 = (img * p.cv_P + r0) * p.cv_Q + q * 32;
         row = row0 + lane;
+        nchw_base = (int64_t)img * p.N * (p.cv_P * p.cv_Q) + r0 * p.cv_Q + q * 32 + lane;
       }
       // 32-column chunks of the bn-wide accumulator, alternating between the two warps of a lane quarter
       const uint32_t taddr = tmem_base + (uint32_t)(buf * ACC_COLS) + ((uint32_t)(q * 32) << 16);
@@ -842,6 +845,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         const int n = nb * bn + c;
         if (!row_ok || n >= p.N || p.dbg_nostore) continue;
+        if (p.cv_nchw) {  // channel n + i of this lane's pixel: lanes store 32 consecutive pixels (128 B)
+          const int64_t pq = (int64_t)p.cv_P * p.cv_Q;
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (n + i < p.N) p.C[nchw_base + (int64_t)(n + i) * pq] = v[i];
+          continue;
+        }
         if (vec_ok && n + 32 <= p.N) {
           if (E.kind == TX_EPI_BIAS || E.kind == TX_EPI_BIAS_TANH || E.kind == TX_EPI_BIAS_TANH_DUAL) {
 #pragma unroll
@@ -1147,6 +1157,7 @@ int gemm_tc(const G& g, void* ws, size_t wsb, cudaStream_t st) {
   if (rc) return rc;
   TcParams p;
   p.conv = 0;
+  p.cv_nchw = 0;
   p.kpack = 1;
   p.C = (float*)g.C;
   p.ldc = g.scm;
@@ -1285,7 +1296,7 @@ int gemm_tc(const G& g, void* ws, size_t wsb, cudaStream_t st) {
 // layout the MMA reads -- so no [N*P*Q, kh*kw*C] patch matrix is written or
 // read.  Tile rows past RB*Q are stale and never stored (register epilogue).
 int gemm_tc_conv(const float* xpad, int64_t N, int64_t Hp, int64_t Wp, int64_t C, const float* w, int64_t K, int kh,
-                 int kw, float* out, cudaStream_t st) {
+                 int kw, float* out, int out_nchw, cudaStream_t st) {
   const int64_t P = Hp - kh + 1, Q = Wp - kw + 1;
   TX_CHECK(P > 0 && Q > 0 && C % 32 == 0 && Q <= BM && K > 0, TX_E_UNSUPPORTED,
            "tx_conv_implicit: needs C % 32 == 0 and output width <= 128");
@@ -1319,6 +1330,7 @@ int gemm_tc_conv(const float* xpad, int64_t N, int64_t Hp, int64_t Wp, int64_t C
   p.K = (int)KK;
   p.a_lim = p.b_lim = INT32_MAX;
   p.conv = 1;
+  p.cv_nchw = out_nchw;
   static const bool no_pack = getenv("TX_CONV_NO_KPACK") != nullptr;
   p.kpack = bn <= 64 && !no_pack ? 2 : 1;
   p.cv_cb = (int)(C / 32);

@@ -176,3 +176,10 @@ def test_conv_implicit_gemm_direct(N, Hp, Wp, C, K, kh, kw):
     got = to.cpu().numpy()
     want, bound = _conv_nhwc_ref(xpad, w, kh, kw)
     assert np.all(np.abs(got - want) <= 2.0 ** -9 * bound + 1e-5), float(np.nanmax(np.abs(got - want) / (bound + 1e-30)))
+    # the same product stored straight into an NCHW output
+    t4 = torch.full((N, K, P, Q), float("nan"), device="cuda")
+    lib.check(lib.lib.tx_conv_implicit(mk(tx.data_ptr(), "float32", xpad.shape, (Hp * Wp * C, Wp * C, C, 1)),
+                                       mk(tw.data_ptr(), "float32", w.shape, (w.shape[1], 1)),
+                                       mk(t4.data_ptr(), "float32", (N, K, P, Q), (K * P * Q, P * Q, Q, 1)), win, None))
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(t4.cpu().numpy(), got.reshape(N, P, Q, K).transpose(0, 3, 1, 2))
