@@ -158,10 +158,10 @@ class Conv2d(Op):
                 fr = plan.scratch((K, kh, kw, C), f.dtype)
                 plan.emit_copy_layouts(plan.view_of(f, (K, kh, kw, C), (C * kh * kw, kw, 1, kh * kw), f.offset), fr)
                 if out.contiguous():  # the epilogue stores NCHW directly
-                    self._implicit(plan, x, self.pad, fr, out, kh, kw)
+                    self._implicit(plan, x, self.pad, fr, out, kh, kw, var=node.inputs[0])
                     return
                 res = plan.scratch((N * Ho * Wo, K), out.dtype)
-                self._implicit(plan, x, self.pad, fr, res, kh, kw)
+                self._implicit(plan, x, self.pad, fr, res, kh, kw, var=node.inputs[0])
                 plan.emit_copy_layouts(plan.view_of(res, (N, K, Ho * Wo), (Ho * Wo * K, 1, K), 0),
                                        plan.view_of(out, (N, K, Ho * Wo), (K * Ho * Wo, Ho * Wo, 1), out.offset))
                 return
@@ -268,7 +268,7 @@ class Conv2d(Op):
         return (self.algo == GEMM and mode in (native.GEMM_AUTO, native.GEMM_TC) and tuple(self.stride) == (1, 1)
                 and dtype == "float32" and C % 32 == 0 and 0 < Wo <= 128 and not _NO_IMPLICIT)
 
-    def _implicit(self, plan, x, pad, wr, res, kh, kw):
+    def _implicit(self, plan, x, pad, wr, res, kh, kw, var=None):
         """res = conv(x, w) with x [N, C, H, W] (any strides), wr [K, kh, kw,
         C] contiguous, res [N*P*Q, K] or [N, K, P, Q] contiguous: x goes to a
         zero-padded NHWC buffer (memset + one strided copy), then ONE
@@ -278,11 +278,7 @@ class Conv2d(Op):
         N, C, H, W = x.shape
         ph, pw = pad
         Hp, Wp = H + 2 * ph, W + 2 * pw
-        xp = plan.scratch((N, Hp, Wp, C), x.dtype)
-        plan.emit_fill_zero(xp)
-        plan.emit_copy_layouts(plan.view_of(x, (N, H, W, C), (x.strides[0], x.strides[2], x.strides[3], x.strides[1]),
-                                            x.offset),
-                               plan.view_of(xp, (N, H, W, C), (Hp * Wp * C, Wp * C, C, 1), (ph * Wp + pw) * C))
+        xp = self._padded_nhwc(plan, var, x, pad)
         K = wr.shape[0]
         lib = plan.lib
         tx_ = plan.tx(xp)
@@ -293,6 +289,26 @@ class Conv2d(Op):
         def launch(stream):
             lib.check(lib.lib.tx_conv_implicit(tx_, tw, tr, win, stream))
         plan.add_launch(launch)
+
+    def _padded_nhwc(self, plan, var, x, pad):
+        """Zero-padded NHWC copy of ``x`` ([N, Hp, Wp, C]), built once per step
+        plan per (variable, padding): the layer's weight gradient gathers its
+        patch matrix from the same buffer (see ``_cols``)."""
+        N, C, H, W = x.shape
+        ph, pw = pad
+        Hp, Wp = H + 2 * ph, W + 2 * pw
+        cache = plan.__dict__.setdefault("_xpad_cache", {})
+        key = None if var is None else (var.id, x.shape, x.strides, ph, pw)
+        if key is not None and key in cache:
+            return cache[key]
+        xp = plan.scratch((N, Hp, Wp, C), x.dtype)
+        plan.emit_fill_zero(xp)
+        plan.emit_copy_layouts(plan.view_of(x, (N, H, W, C), (x.strides[0], x.strides[2], x.strides[3], x.strides[1]),
+                                            x.offset),
+                               plan.view_of(xp, (N, H, W, C), (Hp * Wp * C, Wp * C, C, 1), (ph * Wp + pw) * C))
+        if key is not None:
+            cache[key] = xp
+        return xp
 
     def _win(self, kh, kw):
         import ctypes
@@ -313,9 +329,17 @@ class Conv2d(Op):
             if hwc:
                 # (u, v, c) columns from a channel-contiguous copy of x: every
                 # gather and store runs along c, 128-bit (r02: the (c, u, v)
-                # gather over NCHW was L1-wavefront bound at 91 us for 231 MB)
-                xh = self._hwc(plan, var, x)
+                # gather over NCHW was L1-wavefront bound at 91 us for 231 MB);
+                # the forward's zero-padded NHWC copy when the implicit GEMM
+                # built one (window padding 0 over it: the same columns)
+                xp = plan.__dict__.get("_xpad_cache", {}).get((var.id, x.shape, x.strides, self.pad[0], self.pad[1]))
                 lib, win = plan.lib, self._win(kh, kw)
+                if xp is not None:
+                    N_, Hp, Wp, C_ = xp.shape
+                    xh = plan.view_of(xp, (N_, C_, Hp, Wp), (Hp * Wp * C_, 1, Wp * C_, C_), 0)
+                    win = (__import__("ctypes").c_int * 6)(kh, kw, self.stride[0], self.stride[1], 0, 0)
+                else:
+                    xh = self._hwc(plan, var, x)
                 tx_, tc = plan.tx(xh), plan.tx(cols)
 
                 def launch(stream):
