@@ -137,6 +137,9 @@ int tx_im2col(const tx_tensor* x, tx_tensor* cols, const int* win, void* stream)
  * is a run along c (128-bit when C % 4 == 0). */
 int tx_im2col_hwc(const tx_tensor* x, tx_tensor* cols, const int* win, void* stream);
 int tx_col2im(const tx_tensor* dcols, tx_tensor* dx, const int* win, int64_t Ho, int64_t Wo, void* stream);
+/* x[N,C,H,W] (any strides) -> y[N, H+2*pad[0], W+2*pad[1], C] contiguous,
+ * zero borders: the implicit GEMM's input, in one pass. */
+int tx_pad_nhwc(const tx_tensor* x, tx_tensor* y, const int* pad, void* stream);
 /* Implicit-GEMM stride-1 convolution on the tensor cores (the reference's
  * im2col + np.dot of ops/conv.py:108-157 without the patch matrix):
  * out[(n,p,q), k] = sum_{u,v,c} xpad[n, p+u, q+v, c] * w[k, (u,v,c)], TF32.

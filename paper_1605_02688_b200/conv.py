@@ -302,10 +302,13 @@ class Conv2d(Op):
         if key is not None and key in cache:
             return cache[key]
         xp = plan.scratch((N, Hp, Wp, C), x.dtype)
-        plan.emit_fill_zero(xp)
-        plan.emit_copy_layouts(plan.view_of(x, (N, H, W, C), (x.strides[0], x.strides[2], x.strides[3], x.strides[1]),
-                                            x.offset),
-                               plan.view_of(xp, (N, H, W, C), (Hp * Wp * C, Wp * C, C, 1), (ph * Wp + pw) * C))
+        lib = plan.lib
+        tx_, tp = plan.tx(x), plan.tx(xp)
+        pads = (__import__("ctypes").c_int * 2)(ph, pw)
+
+        def launch(stream):  # one pass: transposed interior + zero borders
+            lib.check(lib.lib.tx_pad_nhwc(tx_, tp, pads, stream))
+        plan.add_launch(launch)
         if key is not None:
             cache[key] = xp
         return xp

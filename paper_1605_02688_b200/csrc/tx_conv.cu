@@ -167,6 +167,45 @@ int geom(const tx_tensor* x4, const int* win, int64_t Ho, int64_t Wo, ConvGeom* 
   return TX_OK;
 }
 
+// x[N, C, H, W] (any strides) -> y[N, Hp, Wp, C] contiguous with zero borders
+// (the implicit GEMM's input).  One CTA per padded row (n, hp): the row's
+// C x W interior goes through a shared tile in channel blocks of 32 (reads
+// run along w, writes along c: both coalesced), border pixels and rows are
+// written as zeros in the same pass (no separate memset).
+constexpr int PAD_CB = 32;
+template <class T>
+__global__ void __launch_bounds__(256) pad_nhwc_kernel(const T* __restrict__ x, T* __restrict__ y, int64_t N, int64_t C,
+                                                       int64_t H, int64_t W, int ph, int pw, int64_t xs0, int64_t xs1,
+                                                       int64_t xs2, int64_t xs3) {
+  TX_GRID_WAIT();
+  extern __shared__ __align__(16) unsigned char pad_smem[];
+  T* tile = reinterpret_cast<T*>(pad_smem);  // [PAD_CB][W + 1]
+  const int64_t Hp = H + 2 * ph, Wp = W + 2 * pw;
+  const int64_t n = blockIdx.x / Hp, hp = blockIdx.x % Hp;
+  const int64_t h = hp - ph;
+  T* yrow = y + (n * Hp + hp) * Wp * C;
+  if (h < 0 || h >= H) {
+    for (int64_t e = threadIdx.x; e < Wp * C; e += blockDim.x) yrow[e] = T(0);
+    return;
+  }
+  // lane along w (reads) / along c (writes), warp along the other axis: no
+  // per-element division, 128-byte runs on both sides
+  const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const T* xrow = x + n * xs0 + h * xs2;
+  for (int64_t c0 = 0; c0 < C; c0 += PAD_CB) {
+    const int cb = (int)(C - c0 < PAD_CB ? C - c0 : PAD_CB);
+    __syncthreads();
+    for (int c = wq; c < cb; c += nw)
+      for (int64_t w = lane; w < W; w += 32) tile[c * (W + 1) + w] = xrow[(c0 + c) * xs1 + w * xs3];
+    __syncthreads();
+    if (lane < cb)
+      for (int64_t wp = wq; wp < Wp; wp += nw) {
+        const int64_t w = wp - pw;
+        yrow[wp * C + c0 + lane] = (w >= 0 && w < W) ? tile[lane * (W + 1) + w] : T(0);
+      }
+  }
+}
+
 int64_t grid_for(int64_t n) {
   int64_t b = (n + 255) / 256;
   const int64_t cap = (int64_t)sm_count() * 16;
@@ -206,6 +245,32 @@ int tx_im2col(const tx_tensor* x, tx_tensor* cols, const int* win, void* stream)
   else
     return fail(TX_E_UNSUPPORTED, "tx_im2col: float32/float64 only");
   TX_CUDA(cudaGetLastError());
+  return TX_OK;
+}
+
+int tx_pad_nhwc(const tx_tensor* x, tx_tensor* y, const int* pad, void* stream) {
+  TX_CHECK(x && y && pad && x->dtype == y->dtype && x->ndim == 4 && y->ndim == 4 && is_contiguous(*y), TX_E_ARG,
+           "tx_pad_nhwc: x[N,C,H,W], contiguous y[N,H+2ph,W+2pw,C]");
+  const int64_t N = x->shape[0], C = x->shape[1], H = x->shape[2], W = x->shape[3];
+  const int ph = pad[0], pw = pad[1];
+  TX_CHECK(ph >= 0 && pw >= 0 && y->shape[0] == N && y->shape[1] == H + 2 * ph && y->shape[2] == W + 2 * pw &&
+               y->shape[3] == C,
+           TX_E_ARG, "tx_pad_nhwc: output shape");
+  const int64_t rows = N * (H + 2 * ph);
+  if (rows == 0 || C == 0 || W == 0) return TX_OK;
+  TX_CHECK(rows < (1LL << 31), TX_E_UNSUPPORTED, "tx_pad_nhwc: too many rows");
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t smem = (size_t)PAD_CB * (W + 1) * itemsize(x->dtype);
+  TX_CHECK(smem <= 48 * 1024, TX_E_UNSUPPORTED, "tx_pad_nhwc: rows wider than the shared tile");
+  if (x->dtype == TX_F32)
+    TX_CUDA(::tx::launch(pad_nhwc_kernel<float>, dim3((unsigned)rows), dim3(256), smem, st, (const float*)x->data,
+                         (float*)y->data, N, C, H, W, ph, pw, x->strides[0], x->strides[1], x->strides[2], x->strides[3]));
+  else if (x->dtype == TX_F64)
+    TX_CUDA(::tx::launch(pad_nhwc_kernel<double>, dim3((unsigned)rows), dim3(256), smem, st, (const double*)x->data,
+                         (double*)y->data, N, C, H, W, ph, pw, x->strides[0], x->strides[1], x->strides[2],
+                         x->strides[3]));
+  else
+    return fail(TX_E_UNSUPPORTED, "tx_pad_nhwc: float32/float64 only");
   return TX_OK;
 }
 

@@ -24,7 +24,7 @@ EXPORTS = [
     "tx_graph_begin", "tx_graph_end", "tx_graph_launch", "tx_graph_destroy", "tx_copy",
     "tx_ew_compile", "tx_ew_check", "tx_ew_launch", "tx_ew_destroy",
     "tx_kernel_compile", "tx_kernel_launch", "tx_kernel_destroy",
-    "tx_reduce_workspace", "tx_reduce", "tx_check_values", "tx_im2col", "tx_im2col_hwc", "tx_col2im", "tx_conv_implicit",
+    "tx_reduce_workspace", "tx_reduce", "tx_check_values", "tx_im2col", "tx_im2col_hwc", "tx_col2im", "tx_conv_implicit", "tx_pad_nhwc",
     "tx_gemm_workspace", "tx_gemm", "tx_gemm_path", "tx_narrow_grad_workspace", "tx_narrow_grad",
     "tx_nccl_unique_id", "tx_nccl_init", "tx_nccl_allreduce_sum", "tx_nccl_destroy",
 ]
@@ -90,6 +90,7 @@ class Library:
             "tx_im2col": [P(TxTensor), P(TxTensor), P(ctypes.c_int), vp],
             "tx_im2col_hwc": [P(TxTensor), P(TxTensor), P(ctypes.c_int), vp],
             "tx_conv_implicit": [P(TxTensor), P(TxTensor), P(TxTensor), P(ctypes.c_int), vp],
+            "tx_pad_nhwc": [P(TxTensor), P(TxTensor), P(ctypes.c_int), vp],
             "tx_col2im": [P(TxTensor), P(TxTensor), P(ctypes.c_int), i64, i64, vp],
             "tx_reduce": [ctypes.c_int, P(TxTensor), ctypes.c_uint32, P(TxTensor), vp, sz, vp],
             "tx_gemm_workspace": [P(TxTensor), P(TxTensor), P(TxTensor), ctypes.c_int, P(sz)],

@@ -183,3 +183,26 @@ def test_conv_implicit_gemm_direct(N, Hp, Wp, C, K, kh, kw):
                                        mk(t4.data_ptr(), "float32", (N, K, P, Q), (K * P * Q, P * Q, Q, 1)), win, None))
     torch.cuda.synchronize()
     np.testing.assert_array_equal(t4.cpu().numpy(), got.reshape(N, P, Q, K).transpose(0, 3, 1, 2))
+
+
+@pytest.mark.parametrize("N,C,H,W,ph,pw", [(2, 64, 7, 9, 1, 1), (1, 40, 5, 130, 0, 2), (3, 3, 4, 4, 2, 0)])
+def test_pad_nhwc_direct(N, C, H, W, ph, pw):
+    """tx_pad_nhwc: NCHW (here a strided, sliced view) -> zero-padded NHWC in
+    one pass, bit-exact against NumPy (channel blocks of 32 with a ragged
+    last block, borders zeroed without a memset)."""
+    import torch
+    from paper_1605_02688_b200 import native
+    lib = native.library()
+    rng = np.random.default_rng(C + W)
+    big = rng.standard_normal((N, C, H, W + 3)).astype(np.float32)
+    xs = big[:, :, :, 1:W + 1]
+    tb = torch.from_numpy(big).cuda()
+    ty = torch.full((N, H + 2 * ph, W + 2 * pw, C), float("nan"), device="cuda")
+    mk = native.make_tensor
+    tx = mk(tb.data_ptr() + 4, "float32", (N, C, H, W), (C * H * (W + 3), H * (W + 3), W + 3, 1))
+    pads = (ctypes.c_int * 2)(ph, pw)
+    lib.check(lib.lib.tx_pad_nhwc(tx, mk(ty.data_ptr(), "float32", tuple(ty.shape), tuple(ty.stride())), pads, None))
+    torch.cuda.synchronize()
+    want = np.zeros((N, H + 2 * ph, W + 2 * pw, C), np.float32)
+    want[:, ph:ph + H, pw:pw + W, :] = xs.transpose(0, 2, 3, 1)
+    np.testing.assert_array_equal(ty.cpu().numpy(), want)
