@@ -206,3 +206,26 @@ def test_pad_nhwc_direct(N, C, H, W, ph, pw):
     want = np.zeros((N, H + 2 * ph, W + 2 * pw, C), np.float32)
     want[:, ph:ph + H, pw:pw + W, :] = xs.transpose(0, 2, 3, 1)
     np.testing.assert_array_equal(ty.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("shape,pad,ks", [((2, 32, 9, 11), (1, 1), 3), ((3, 64, 12, 7), (2, 1), 5),
+                                          ((1, 32, 6, 130), (0, 0), 3), ((2, 96, 5, 5), (0, 0), 1)])
+def test_conv_trio_implicit_vs_exact(shape, pad, ks):
+    """The stride-1, 32-channel-block layers take the implicit-GEMM forward
+    and input gradient (and the weight gradient's patch matrix from the padded
+    NHWC buffer): forward and both gradients within TF32 tolerance of the
+    exact fp32 CUDA-core lowering (conv_impl="reference")."""
+    rng = np.random.default_rng(sum(shape) + ks)
+    N, C, H, W = shape
+    K = 64 if C > 64 else (32 if ks != 5 else 24)   # K % 32 == 0: the input gradient is implicit too
+    x = rng.standard_normal(shape).astype(np.float32)
+    f = (rng.standard_normal((K, C, ks, min(ks, 3))) / np.sqrt(C * ks * 3)).astype(np.float32)
+    vx, vf = T.tensor4("x", dtype="float32"), T.tensor4("f", dtype="float32")
+    y = T.conv2d(vx, vf, stride=(1, 1), pad=pad)
+    gf, gx = T.grad(T.sum(y * y), [vf, vx])
+    outs = {}
+    for impl in ("gemm", "reference"):
+        outs[impl] = T.compile([vx, vf], [y, gf, gx], conv_impl=impl)(x, f)
+    for a, b in zip(outs["gemm"], outs["reference"]):
+        assert a.shape == b.shape
+        assert _rel(a, b) <= 3e-3, _rel(a, b)
