@@ -120,6 +120,16 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, u
       "l"((uint64_t)map), "r"(su32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
       : "memory");
 }
+// one 2-D box landing at the same shared-memory offset in every CTA of `mask`
+// (each CTA's own barrier at `bar`'s offset counts the bytes)
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                               uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(su32(dst)),
+      "l"((uint64_t)map), "r"(su32(bar)), "r"(c0), "r"(c1), "h"(mask)
+      : "memory");
+}
 __device__ __forceinline__ void tma_load_3d_2sm(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
                                                 int c2) {
   asm volatile(
@@ -199,6 +209,13 @@ __device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t a, uint64_t 
 
 // tcgen05.commit: arrive (once) on a barrier when all prior MMAs of this
 // thread complete; CG = 2 multicasts the arrive to both CTAs of the pair.
+// single-CTA MMAs done: arrive on the barrier at `bar`'s offset in every CTA of `mask`
+__device__ __forceinline__ void umma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                   su32(bar)),
+               "h"(mask)
+               : "memory");
+}
 template <int CG>
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   if constexpr (CG == 1) {
@@ -279,6 +296,8 @@ struct TcParams {
   int cv_nchw;      // store C as [N, K, P, Q] (per output channel, a tile's pixels are one contiguous run)
   int kpack;        // k-blocks per ring stage (conv, bn <= 64: 2 -- A0 | A1 | B0 | B1 in one 48 KB stage,
                     // twice the loads in flight; else 1)
+  int mcast;        // CG = 1 only: clusters of `mcast` CTAs along N sharing one A panel (MN-major A), each
+                    // loading 1/mcast of its 32-row atoms and multicasting them to all (1 = off)
   int group_m;      // M-tiles per raster group (operand panels shared in L2 by concurrently running tiles)
   int dbg_nostore;  // diagnostics only (TX_GEMM_DBG_NOSTORE): epilogue drains TMEM without storing
   int tma_store;    // C written by TMA tile stores from swizzled smem staging
@@ -450,7 +469,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int num_clusters = gridDim.x / CG;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }
+    for (int s = 0; s < STAGES; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, p.mcast > 1 ? p.mcast : 1); }
     for (int b = 0; b < NACC; ++b) { mbar_init(tfull + b, 1); mbar_init(tempty + b, EPI_WARPS * CG); }
     for (int w = 0; w < EPI_WARPS; ++w) mbar_init(auxbar + w, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -469,9 +488,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   }
   tc_fence_before();
-  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
+  if (CG == 2 || p.mcast > 1) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  const uint32_t mrank = CG == 1 && p.mcast > 1 ? cluster_rank() : 0;  // rank within the multicast cluster
+  const uint16_t mmask = (uint16_t)((1u << (p.mcast > 1 ? p.mcast : 1)) - 1u);
   const int num_kb = (p.K + BK - 1) / BK;
 
   if (warp == 0) {
@@ -485,6 +506,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       while (seg_next(p, cluster_id, cur, sg)) {
         int mb, nb;
         tile_coords(sg.t, p.num_m, p.num_n, p.group_m, mb, nb);
+      if (p.mcast > 1) { mb = (sg.t / p.mcast) % p.num_m; nb = (sg.t / (p.mcast * p.num_m)) * p.mcast + sg.t % p.mcast; }
+        if (p.mcast > 1) { mb = (sg.t / p.mcast) % p.num_m; nb = (sg.t / (p.mcast * p.num_m)) * p.mcast + sg.t % p.mcast; }
         const int kb0 = sg.kb0, kb1 = sg.kb1;
         const int m0 = mb * BM * CG + (int)rank * BM;   // this CTA's rows
         const int n0 = nb * bn + (int)rank * BNL;       // this CTA's half of B
@@ -515,6 +538,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
             if (++stage == STAGES) { stage = 0; phase ^= 1; }
             continue;
+          } else if (CG == 1 && p.mcast > 1) {  // this CTA's share of the A panel's 32-row atoms, to every CTA
+            for (int j = (int)mrank; j < BM / 32; j += p.mcast)
+              tma_load_2d_mc(sa + j * 4096, &mapAe, full + stage, m0 + 32 * j, k0, mmask);
           } else if (p.a_3d && m0 + BM <= p.a_lim) {
             load3(sa, &mapA, k0, m0 / 32);
           } else if (p.a_mn) {  // 32-wide boxes: 2-D edge map (clipped at M)
@@ -578,7 +604,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 umma_tf32<CG>(tmem_d, da, db, idesc, (kb != kb0) || (sub != 0) || (kk != 0));
               }
             }
-            umma_commit<CG>(empty + stage);
+            if (CG == 1 && p.mcast > 1) umma_commit_mc(empty + stage, mmask);  // every producer of the panel
+            else umma_commit<CG>(empty + stage);
           }
           __syncwarp();
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -607,6 +634,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     for (; seg_next(p, cluster_id, cur, sg); ++it) {
       int mb, nb;
       tile_coords(sg.t, p.num_m, p.num_n, p.group_m, mb, nb);
+      if (p.mcast > 1) { mb = (sg.t / p.mcast) % p.num_m; nb = (sg.t / (p.mcast * p.num_m)) * p.mcast + sg.t % p.mcast; }
       const int split = sg.piece;
       const bool partial = !sg.full;
       const int q_ = warp & 3;
@@ -915,7 +943,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
   if (warp >= 2 && lane == 0) tma_store_wait_all();
   tc_fence_before();
-  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
+  if (CG == 2 || p.mcast > 1) cluster_sync(); else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
     if constexpr (CG == 1)
@@ -1240,10 +1268,24 @@ int gemm_tc(const G& g, void* ws, size_t wsb, cudaStream_t st) {
   }
   const int units = sm_count() / cg;
   const int work = p.num_tiles * p.splits;
-  const int nclusters = p.streamk ? units : (work < units ? work : units);
-  p.nclusters = nclusters;
+  int nclusters = p.streamk ? units : (work < units ? work : units);
   p.promo = g.promo > 0 && g.promo < p.num_kb ? g.promo : 0;
   p.promo_first = p.promo ? (g.promo_first > 0 && g.promo_first < p.num_kb ? g.promo_first : 0) : 0;
+  // A-panel multicast (single-CTA tiles in one wave with an MN-major A: the
+  // M = 784 weight gradient G8, 7 x 16 tiles): clusters of 4 CTAs along N
+  // share one A panel, each loading one of its four 32-row atoms and
+  // multicasting it -- per-SM operand bytes per k-block 48 -> 36 KB
+  static const bool no_mc = getenv("TX_GEMM_NO_MCAST") != nullptr;
+  p.mcast = 1;
+  const int mcs = 4;
+  if (cg == 1 && a_mn && p.splits == 1 && !p.streamk && !p.colsum && !p.promo && !no_mc &&
+      p.num_tiles <= units && p.num_n % mcs == 0 && p.num_m >= 2) {
+    if (!a_3d || g.M % 32 == 0) rc = make_map(&mae, g.A, g.M, g.K, g.sak, 32, 32, true);  // per-atom 2-D boxes
+    if (rc) return rc;
+    p.mcast = mcs;
+    nclusters = p.num_tiles;  // one tile per CTA: a cluster's CTAs walk the same A panel in lockstep
+  }
+  p.nclusters = nclusters;
   const int pr = p.promo ? 1 : 0;
   auto k1 = p.promo ? tc_gemm_kernel<1, true> : tc_gemm_kernel<1, false>;
   auto k2 = p.promo ? tc_gemm_kernel<2, true> : tc_gemm_kernel<2, false>;
@@ -1252,7 +1294,25 @@ int gemm_tc(const G& g, void* ws, size_t wsb, cudaStream_t st) {
       TX_CUDA(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<1>::SMEM));
       g_attr_set[pr][1] = true;
     }
-    ::tx::launch(k1, dim3(nclusters), dim3(NUM_THREADS), Cfg<1>::SMEM, st, ma, mb, mc, mx, mae, mbe, mp, p);
+    if (p.mcast > 1) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(nclusters, 1, 1);
+      cfg.blockDim = dim3(NUM_THREADS, 1, 1);
+      cfg.dynamicSmemBytes = Cfg<1>::SMEM;
+      cfg.stream = st;
+      cudaLaunchAttribute attr[2];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = (unsigned)p.mcast;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[1].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = pdl_enabled() ? 2 : 1;
+      TX_CUDA(cudaLaunchKernelEx(&cfg, k1, ma, mb, mc, mx, mae, mbe, mp, p));
+    } else {
+      ::tx::launch(k1, dim3(nclusters), dim3(NUM_THREADS), Cfg<1>::SMEM, st, ma, mb, mc, mx, mae, mbe, mp, p);
+    }
   } else {
     if (!g_attr_set[pr][2]) {
       TX_CUDA(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<2>::SMEM));
