@@ -36,6 +36,11 @@ def main():
         va, vb = T.matrix("a", dtype=f32), T.matrix("b", dtype=f32)
         for mode in ("auto", "3xtf32", "simt"):
             T.compile([va, vb], T.dot(va, vb), gemm_mode=mode, cuda_graph=False)(A, B)
+    # r02b A-panel multicast (single-CTA tiles, MN-major A, 4-CTA clusters along N)
+    At = rng.standard_normal((256, 200)).astype(np.float32)
+    Bm = rng.standard_normal((256, 1024)).astype(np.float32)
+    va, vb = T.matrix("a", dtype=f32), T.matrix("b", dtype=f32)
+    T.compile([va, vb], T.dot(T.transpose(va), vb), cuda_graph=False)(At, Bm)
     # r02 small-M kernel: every B layout, the cluster split of K (DSMEM reduction), an epilogue
     for (M, N, K, tb) in ((20, 200, 800, False), (7, 96, 1000, True), (20, 800, 200, False)):
         A = rng.standard_normal((M, K)).astype(np.float32)
