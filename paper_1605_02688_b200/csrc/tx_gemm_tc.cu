@@ -506,7 +506,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       while (seg_next(p, cluster_id, cur, sg)) {
         int mb, nb;
         tile_coords(sg.t, p.num_m, p.num_n, p.group_m, mb, nb);
-      if (p.mcast > 1) { mb = (sg.t / p.mcast) % p.num_m; nb = (sg.t / (p.mcast * p.num_m)) * p.mcast + sg.t % p.mcast; }
         if (p.mcast > 1) { mb = (sg.t / p.mcast) % p.num_m; nb = (sg.t / (p.mcast * p.num_m)) * p.mcast + sg.t % p.mcast; }
         const int kb0 = sg.kb0, kb1 = sg.kb1;
         const int m0 = mb * BM * CG + (int)rank * BM;   // this CTA's rows
