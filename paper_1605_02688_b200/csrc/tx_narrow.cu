@@ -222,7 +222,14 @@ __global__ void __launch_bounds__(256) narrow_grad_finalize(const float* __restr
   const int k = e < HK1 ? (int)(e / H) : NK;
   const bool live = e < HK1 && (k < NK || db);
   float v = 0.f;
-  if (live) {
+  if (live && S <= 128) {  // every slab of this warp in flight at once (same summation order as below)
+    float q[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) q[u] = w + 8 * u < S ? __ldcs(P + (int64_t)(w + 8 * u) * HK1 + e) : 0.f;
+#pragma unroll
+    for (int u = 0; u < 16; ++u)
+      if (w + 8 * u < S) v += q[u];
+  } else if (live) {
     int s = w;
     for (; s + 24 < S; s += 32) {
       const float q0 = __ldcs(P + (int64_t)s * HK1 + e), q1 = __ldcs(P + (int64_t)(s + 8) * HK1 + e);
@@ -254,7 +261,14 @@ __global__ void __launch_bounds__(256) colsum_finalize(const float* __restrict__
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t j = blockIdx.x * 32LL + lane;
   float v = 0.f;
-  if (j < H) {
+  if (j < H && S <= 256) {  // every block of this warp in flight at once (same summation order as below)
+    float q[32];
+#pragma unroll
+    for (int u = 0; u < 32; ++u) q[u] = w + 8 * u < S ? __ldcs(P + (int64_t)(w + 8 * u) * H + j) : 0.f;
+#pragma unroll
+    for (int u = 0; u < 32; ++u)
+      if (w + 8 * u < S) v += q[u];
+  } else if (j < H) {
     int s = w;
     for (; s + 24 < S; s += 32) {
       const float q0 = __ldcs(P + (int64_t)s * H + j), q1 = __ldcs(P + (int64_t)(s + 8) * H + j);
