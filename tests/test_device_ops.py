@@ -605,3 +605,25 @@ def test_dot_add_aux_bias_epilogue_bit_exact(M, N, K, rng):
     u = T.compile([vx, vw, vg, vb], expr, exclude=("fuse_gemm_epilogue",))
     assert "dot+add_aux_bias" not in [getattr(n.op, "display_name", n.op.name) for n in u.order]
     np.testing.assert_array_equal(f(x, W, g, b), u(x, W, g, b))
+
+
+@pytest.mark.parametrize("M,N,K", [(784, 3072, 512), (1000, 3072, 256), (784, 4096, 1024)])
+def test_gemm_a_panel_multicast(M, N, K, rng):
+    """Single-CTA one-wave products with an MN-major A (xᵀ·dz, the MLP's
+    weight gradient) run with the A panel multicast across 4-CTA clusters
+    along N (ragged last M tile included), plain and with the fused SGD
+    epilogue: within the TF32 bound of the float64 product.  (75-148 output
+    tiles: one wave and no split-K, the multicast condition.)"""
+    a = rng.standard_normal((K, M)).astype(np.float32)     # A = aᵀ (MN-major)
+    b = rng.standard_normal((K, N)).astype(np.float32)
+    w = rng.standard_normal((M, N)).astype(np.float32)
+    va, vb = T.matrix("a", dtype="float32"), T.matrix("b", dtype="float32")
+    got = T.compile([va, vb], T.dot(T.transpose(va), vb))(a, b)
+    A, B = a.T.astype(np.float64), b.astype(np.float64)
+    want, bound = A @ B, np.abs(A) @ np.abs(B)
+    assert np.all(np.abs(got - want) <= 2.0 ** -9 * bound + 1e-6)
+    W = T.shared(w.copy(), name="W")
+    f = T.compile([va, vb], [], updates=[(W, W - 0.5 * T.dot(T.transpose(va), vb))])
+    f(a, b)
+    upd = W.get_value()
+    assert np.all(np.abs(upd - (w - 0.5 * want)) <= 0.5 * 2.0 ** -9 * bound + 1e-5)
