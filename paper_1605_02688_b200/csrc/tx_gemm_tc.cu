@@ -1276,7 +1276,7 @@ int gemm_tc(const G& g, void* ws, size_t wsb, cudaStream_t st) {
   // multicasting it -- per-SM operand bytes per k-block 48 -> 36 KB
   static const bool no_mc = getenv("TX_GEMM_NO_MCAST") != nullptr;
   p.mcast = 1;
-  const int mcs = 4;
+  static const int mcs = getenv("TX_GEMM_MCAST_N") ? atoi(getenv("TX_GEMM_MCAST_N")) : 4;  // cluster size (A/B)
   if (cg == 1 && a_mn && p.splits == 1 && !p.streamk && !p.colsum && !p.promo && !no_mc &&
       p.num_tiles <= units && p.num_n % mcs == 0 && p.num_m >= 2) {
     if (!a_3d || g.M % 32 == 0) rc = make_map(&mae, g.A, g.M, g.K, g.sak, 32, 32, true);  // per-atom 2-D boxes
